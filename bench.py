@@ -1,0 +1,343 @@
+"""Benchmark of the synchronous data-parallel SGD step (BASELINE.json metric:
+train samples/sec, device-timed, max over ranks).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--precision tf32|fp32]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+    python bench.py --impl reference     # the CPU oracle on the host cores (reference arm)
+
+One "step" = one pass of the whole hot path over one global batch: forward,
+softmax-CE, backward, flat-buffer allreduce-sum (NCCL, bucketed, overlapped),
+x 1/P and the fused momentum update.  Strong scaling:
+the global batch B is fixed and split over the N ranks.
+Inputs are seeded synthetic data shaped like the paper's workloads (mtx_synth),
+resident in HBM before the timed region.  L2 is flushed (a 256 MiB write)
+before every timed step and the flush is outside the events.  Prints ONE JSON
+line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import re
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}
+TF32_PER_BF16 = 1.1 / 2.25  # nominal dense ratio (B200_PROFILING.md table)
+FP32_FMA_PER_SM_CLK = 128  # CUDA cores per SM (4 SMSP x 32 lanes), 2 flop per FMA
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        d["_source"] = "measured"
+        return d
+    d = dict(PEAKS_FALLBACK)
+    d["_source"] = "fallback"
+    return d
+
+
+# ----------------------------------------------------------------------------- clocks sampler
+class Clocks:
+    """Samples SM clock and clock-event reasons through NVML every ~2 ms while the timed region runs."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.stop_ev = index, [], threading.Event()
+
+    def start(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.index]) if vis else self.index
+            self.h = N.nvmlDeviceGetHandleByIndex(idx)
+            self.N = N
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self.N = None
+            self.err = str(e)
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        time.sleep(0.01)
+
+    def _run(self):
+        N = self.N
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append((N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
+                                     N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def stop(self):
+        self.stop_ev.set()
+        if self.N is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled: " + getattr(self, "err", "")]}
+        self.t.join(1)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        busy = [s for s in self.samples if not (s[1] & 0x1)] or self.samples
+        reasons = set()
+        for _, r in busy:
+            for bit, name in self.REASONS.items():
+                if r & bit and bit != 0x1:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[0] for s in busy), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(busy)}
+
+
+# ----------------------------------------------------------------------------- roofline helpers
+def kernel_work(name: str):
+    """Algorithmic work per launch from the launch-site name: ('flop'|'byte', amount, bound)."""
+    m = re.match(r"(\w+)\[(.*)\]", name)
+    if not m:
+        return None
+    kind, args = m.group(1), dict(kv.split("=") for kv in m.group(2).split(","))
+    a = {k: int(v) for k, v in args.items()}
+    if kind.startswith("gemm"):
+        tensor = kind.startswith("gemm_tc")
+        return "flop", 2 * a["M"] * a["N"] * a["K"], "tensor" if tensor else "alu"
+    if kind == "avg_update":
+        return "byte", (20 if a["v"] else 12) * a["n"], "hbm"
+    if kind == "head_softmax_xent":  # read A rows, write dZ_{L-1} (and dZ_L, loss)
+        return "byte", 4 * a["rows"] * (a["d"] * (1 + a["dgrad"]) + a["C"] + 1), "hbm"
+    if kind == "splitk_reduce":
+        return "byte", 4 * a["M"] * a["N"] * (a["splits"] + 1), "hbm"
+    if kind == "loss_reduce":
+        return "byte", 4 * a["n"], "hbm"
+    return None
+
+
+def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int):
+    """Dominant kernel class (by total device time) -> achieved / peak."""
+    groups = {}
+    for name, (ms, cnt) in timing.items():
+        w = kernel_work(name)
+        base = name.split("[")[0]
+        g = groups.setdefault(base, {"ms": 0.0, "cnt": 0, "work": 0.0, "unit": None, "bound": None})
+        g["ms"] += ms
+        g["cnt"] += cnt
+        if w:
+            g["work"] += w[1] * cnt
+            g["unit"], g["bound"] = w[0], w[2]
+    total = sum(g["ms"] for g in groups.values())
+    top_name, top = max(groups.items(), key=lambda kv: kv[1]["ms"])
+    per_launch_s = top["ms"] / 1e3 / top["cnt"]
+    per_launch_work = top["work"] / top["cnt"]
+    if top["bound"] == "hbm":
+        achieved = per_launch_work / per_launch_s / 1e9
+        peak, unit = pk["hbm_gbs"], "GB/s"
+    elif top["bound"] == "tensor":
+        achieved = per_launch_work / per_launch_s / 1e12
+        peak, unit = pk["bf16_tflops_sustained"] * TF32_PER_BF16, "TFLOP/s"
+    else:  # fp32 CUDA-core FMA peak at the clock observed under load
+        achieved = per_launch_work / per_launch_s / 1e12
+        clk = sm_mhz or pk.get("sm_max_mhz", 1965.0)
+        peak, unit = 148 * FP32_FMA_PER_SM_CLK * 2 * clk * 1e6 / 1e12, "TFLOP/s"
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(top_name)
+    return {"kernel": top_name, "bound": top["bound"], "achieved": round(achieved, 3), "peak": round(peak, 1),
+            "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic,
+            "work_per_launch": per_launch_work, "launch_us": round(per_launch_s * 1e6, 3),
+            "share_of_kernel_time": round(top["ms"] / total, 3),
+            "breakdown_us_per_step": {k: round(g["ms"] * 1e3 / steps, 2) for k, g in
+                                      sorted(groups.items(), key=lambda kv: -kv[1]["ms"])}}
+
+
+# ----------------------------------------------------------------------------- CPU oracle baseline
+def cpu_oracle(cfg: dict, budget_s: float, X, y):
+    """The oracle as it stands (single-threaded C, f64) on a bounded sample: whole SGD steps of the
+    same global batch, P=1 (the sequential definition the DP step must equal)."""
+    import numpy as np
+
+    import oracle
+    net = oracle.Net.from_cfg(cfg)
+    w = oracle.init_params(net, 42).astype(np.float64)
+    v = np.zeros_like(w)
+    B = cfg["B"]
+    t0 = time.perf_counter()
+    steps = 0
+    while True:
+        g, _ = oracle.local_grad(net, w, X, y, B, steps, 0, 1)
+        oracle.avg_update(g, w, v, 1, cfg["lr"], cfg["mu"])
+        steps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(B * steps / dt, 3), "unit": "samples/s", "cores": 1, "kind": "oracle",
+            "sample": f"{steps} full SGD steps of {cfg['name']} (B={B}) in f64 on 1 host thread, {dt:.1f} s"}
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "tf32"])
+    ap.add_argument("--impl", default="mtx", choices=["mtx", "reference"])
+    ap.add_argument("--bucket-mb", type=float, default=1.0)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference", "timing rules: >= 3 warm-up steps"
+
+    import numpy as np
+
+    import mtx_synth as S
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = dict(S.CONFIGS[args.config])
+    cfg["name"] = args.config
+    metric = "train samples/sec (device-timed, max over ranks)"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        X, y = S.dataset(cfg, n=min(cfg["n"], 100_000))
+        cb = cpu_oracle(cfg, max(2.0, min(args.cpu_budget, 10.0)), X, y)
+        line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": "samples/s", "n_gpus": 0,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(cfg["B"] / cb["value"] * 1e3, 3),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": f"{args.config}: {desc(cfg)}", "global_batch": cfg["B"]},
+                "cpu_baseline": cb,
+                "e2e": {"value": cb["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1704_04560_b200 as P
+    from paper_1704_04560_b200 import mtx
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    tc_ok = "tcgen05" in mtx.mtx_build_info()
+    prec = {"fp32": P.MTX_FP32, "tf32": P.MTX_TF32}.get(args.precision, P.MTX_TF32 if tc_ok else P.MTX_FP32)
+    uid = P.nccl_uid_broadcast(rank, world)
+    X, y = S.dataset(cfg)
+    rep = P.Replica(cfg, rank=rank, world=world, uid=uid, device=local, precision=prec,
+                    bucket_bytes=int(args.bucket_mb * (1 << 20)))
+    rep.bcast()
+    rep.shard(X, y)
+    s = rep.stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        rep.step()
+    barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    for k in range(args.steps):
+        with torch.cuda.stream(s):
+            flush.fill_(k & 0xFF)  # evict L2 (126 MB) before every timed step; outside the events
+            ev[k][0].record(s)
+        rep.step()
+        with torch.cuda.stream(s):
+            ev[k][1].record(s)
+    barrier()
+    clk = clocks.stop()
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    loss = mtx.mtx_train_step(rep.ctx, rep.step_idx, True, rep.s)
+    rep.step_idx += 1
+    t_all = [t_ms]
+    if world > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64)
+        gathered = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(gathered, tt)
+        t_all = [float(g[0]) for g in gathered]
+    t_max = max(t_all)
+    value = cfg["B"] * args.steps / (t_max / 1e3)
+    launches = mtx.mtx_launches_per_step(rep.ctx)
+
+    # kernel timing pass (eager launches bracketed by CUDA events on the launching stream)
+    mtx.mtx_set_timing(rep.ctx, True)
+    mtx.mtx_read_timing(rep.ctx, reset=True)
+    for k in range(args.steps):
+        with torch.cuda.stream(s):
+            flush.fill_(k & 0xFF)
+        rep.step()
+    timing = mtx.mtx_read_timing(rep.ctx, reset=True)
+    mtx.mtx_set_timing(rep.ctx, False)
+    pk = peaks()
+    roof = roofline(timing, pk, clk.get("sm_mhz"), args.steps)
+    roof["peak_source"] = pk["_source"]
+
+    # end-to-end through the public API with HOST inputs: per step H2D of the rank's rows from
+    # pinned memory, the step, D2H of the loss (mtx_train_step_host)
+    n = cfg["n"]
+    d = X.reshape(n, -1).shape[1]
+    Xh = torch.from_numpy(np.concatenate([X.reshape(n, -1), X.reshape(n, -1)[: cfg["B"]]])).pin_memory()
+    yh = torch.from_numpy(np.concatenate([y, y[: cfg["B"]]])).pin_memory()
+    b = cfg["B"] // world
+    for k in range(3):
+        row0 = (k * cfg["B"]) % n + rank * b
+        rep.step_host(Xh[row0:].numpy(), yh[row0:].numpy())
+    barrier()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        row0 = (k * cfg["B"]) % n + rank * b
+        rep.step_host(Xh[row0:].numpy(), yh[row0:].numpy())
+    t_e2e = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([t_e2e], dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt[0])
+    e2e = {"value": round(cfg["B"] * args.steps / t_e2e, 1), "unit": "samples/s",
+           "h2d_bytes_per_step": b * (4 * d + 4), "d2h_bytes_per_step": 4}
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_oracle(cfg, args.cpu_budget, X[:100_000], y[:100_000])
+    if rank == 0:
+        line = {"metric": metric, "value": round(value, 1), "unit": "samples/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 5),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "tf32" if prec == P.MTX_TF32 else "f32", "data": "synthetic",
+                "config": {"workload": f"{args.config}: {desc(cfg)}", "global_batch": cfg["B"],
+                           "local_batch": cfg["B"] // world, "parallelism": f"dp{world}",
+                           "bucket_mb": args.bucket_mb, "l2": "flushed (256 MiB write) before every timed step",
+                           "engine": mtx.mtx_build_info()},
+                "per_rank_ms": [round(t, 3) for t in t_all], "final_loss": loss,
+                "gpu_launches": launches * args.steps, "launches_per_step": launches,
+                "clocks": clk, "roofline": roof, "cpu_baseline": cb, "e2e": e2e}
+        print(json.dumps(line), flush=True)
+    rep.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def desc(cfg):
+    if cfg["kind"] == "mlp":
+        return f"MLP {'-'.join(map(str, cfg['dims']))}, {cfg['data']}-shaped n={cfg['n']}, B={cfg['B']}, lr={cfg['lr']}, mu={cfg['mu']}"
+    return f"LeNet CNN {cfg['in_hwc']}, {cfg['data']}-shaped n={cfg['n']}, B={cfg['B']}, lr={cfg['lr']}, mu={cfg['mu']}"
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,232 @@
+/*
+ * mtx.h -- C-ABI of the B200-native synchronous data-parallel SGD step of
+ * MaTEx-TensorFlow (Vishnu et al., arXiv 1704.04560).
+ *
+ * The paper adds two operators to a sequential training script -- a Global
+ * Broadcast of the model variables at the start of training and an
+ * MPI_Allreduce of the gradients after every batch -- so that P replicas run
+ * synchronous data-parallel SGD that is numerically equivalent to sequential
+ * SGD (Fig. 2).  This library is
+ * that step, one process per GPU:
+ *
+ *   mtx_init            context, NCCL communicator, seeded replica init
+ *   mtx_bcast_params    Global Broadcast of the flat parameter buffer
+ *   mtx_shard_data      registers the dataset; rank r reads its contiguous slice
+ *                       of each global batch ("automatically
+ *                       distributing datasets")
+ *   mtx_train_step      forward/backward on the local slice, allreduce-sum of the
+ *                       ONE flat gradient buffer, x 1/P, momentum update in the
+ *                       same pass
+ *   mtx_allreduce_avg   the averaging + update operator on caller buffers
+ *
+ * Conventions for every entry point:
+ *  - Returns mtx_status; MTX_OK == 0.  On failure mtx_last_error(ctx) holds a
+ *    one-line message.  CUDA or NCCL failures poison the context: every later
+ *    call except mtx_last_error/mtx_finalize returns MTX_ERR_STATE.
+ *  - "stream" arguments are cudaStream_t passed as void* (NULL = the context's
+ *    own internal stream).  The library orders its internal comm stream against
+ *    the caller's stream with events; calls are asynchronous w.r.t. the host
+ *    unless stated.
+ *  - Device pointers are BORROWED: the caller (PyTorch) owns the memory and must
+ *    keep it alive until mtx_finalize.  Host pointers are only read/written
+ *    during the call.
+ *  - Collective discipline: every rank calls mtx_bcast_params,
+ *    mtx_train_step and mtx_allreduce_avg in the same order with the same
+ *    sizes.  Misuse hangs inside NCCL; it is documented, not detected.
+ *  - Layouts: all floating-point buffers are fp32, row-major.  Weights follow
+ *    the x.W + b convention: a dense layer's W is [d_in][d_out]; a conv
+ *    layer's W is [kh][kw][c_in][c_out]; activations are [rows][features],
+ *    images NHWC.  "Canonical order" of the parameters is W_1, b_1, W_2, b_2,
+ *    ... (conv layers first), unpadded.
+ */
+#ifndef MTX_H
+#define MTX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mtx_ctx mtx_ctx;
+
+typedef enum {
+    MTX_OK = 0,
+    MTX_ERR_INVALID_ARG = 1, /* bad rank/world/sizes, B mod P != 0, B > n, NULL where required */
+    MTX_ERR_STATE = 2,       /* call out of order or context poisoned by an earlier failure */
+    MTX_ERR_SHAPE = 3,       /* buffer/count does not match the model */
+    MTX_ERR_CUDA = 4,        /* CUDA runtime/driver error (message in mtx_last_error) */
+    MTX_ERR_NCCL = 5,        /* NCCL error (message in mtx_last_error) */
+    MTX_ERR_NUMERIC = 6,     /* non-finite averaged gradient seen */
+    MTX_ERR_PROTOCOL = 7,    /* model description differs across ranks */
+    MTX_ERR_OOM = 8,         /* workspace too small */
+    MTX_ERR_UNSUPPORTED = 9  /* valid request this build does not implement */
+} mtx_status;
+
+typedef enum { MTX_MLP = 0, MTX_CNN = 1 } mtx_model_kind;
+
+/* Arithmetic of the local forward/backward contractions (north_star tolerance tiers).
+ *  MTX_FP32: SIMT FFMA, fp32 products and sums (parity gate 1e-5 vs the f64 oracle).
+ *  MTX_TF32: tcgen05.mma kind::tf32 on the 5th-gen tensor cores, operands fed by
+ *            TMA, fp32 accumulation in TMEM (parity gate 1e-3).
+ * Reductions across ranks, the average and the update are fp32 in both. */
+typedef enum { MTX_FP32 = 0, MTX_TF32 = 1 } mtx_precision;
+
+/* How the gradient allreduce-sum is computed (reading A2).
+ *  MTX_REDUCE_NCCL:    ncclAllReduce(sum) -- NCCL's order (ring/tree/NVLS).
+ *  MTX_REDUCE_ORDERED: ncclAllGather + an ascending-rank left fold kernel; bit-exact
+ *                      with the oracle's fold (test mode, P x the gradient memory). */
+typedef enum { MTX_REDUCE_NCCL = 0, MTX_REDUCE_ORDERED = 1 } mtx_reduce_mode;
+
+typedef struct {
+    int32_t kind;            /* mtx_model_kind */
+    /* MLP: widths d_0 .. d_L (n_dims = L + 1 >= 2); hidden layers use ReLU,
+       the last layer feeds mean softmax cross-entropy. */
+    int32_t n_dims;
+    const int32_t *dims;
+    /* CNN (LeNet-style): NHWC input in_h x in_w x in_c; n_conv valid/stride-1
+       conv layers conv_k[i] x conv_k[i] -> conv_c[i] channels, each followed by
+       bias, ReLU and 2x2/2 max-pool; then n_fc dense layers fc_dims[] (the last
+       is the class count). */
+    int32_t in_h, in_w, in_c;
+    int32_t n_conv;
+    const int32_t *conv_k;
+    const int32_t *conv_c;
+    int32_t n_fc;
+    const int32_t *fc_dims;
+    int64_t global_batch;    /* B; the local batch is b = B / world (B mod world == 0) */
+} mtx_model_desc;
+
+typedef struct {
+    float lr;                /* learning rate, constant */
+    float momentum;          /* mu in v <- mu v + g, w <- w - lr v (0 = plain SGD) */
+    int32_t precision;       /* mtx_precision */
+    int32_t reduce;          /* mtx_reduce_mode */
+    uint64_t bucket_bytes;   /* target allreduce bucket size; 0 = one bucket */
+    uint64_t init_seed;      /* rank r initialises with init_seed + r before the broadcast */
+} mtx_optim_desc;
+
+/* ---------------------------------------------------------------- bootstrap */
+
+/* NCCL unique id for mtx_init; rank 0 calls it and ships the 128 bytes to the
+ * other ranks over any side channel (the harness uses a torch gloo group). */
+mtx_status mtx_get_unique_id(uint8_t out[128]);
+
+/* Creates the per-rank context on CUDA device `device`: copies the model and
+ * optimiser descriptions, creates the NCCL communicator of `world` ranks (uid
+ * may be NULL when world == 1), and checks -- by an NCCL allgather of a 64-bit
+ * digest -- that every rank passed the same model/optimiser description
+ * (mismatch: MTX_ERR_PROTOCOL).  Errors: world < 1, rank outside
+ * [0, world), B mod world != 0, unsupported layer shapes -> MTX_ERR_INVALID_ARG. */
+mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t uid[128], int32_t device,
+                    const mtx_model_desc *model, const mtx_optim_desc *opt);
+
+/* Bytes of device workspace the context needs (parameters, velocity, the flat
+ * gradient buffer + loss slot, activations, scratch). */
+mtx_status mtx_workspace_bytes(const mtx_ctx *ctx, uint64_t *bytes);
+
+/* Lends the context a device buffer of >= mtx_workspace_bytes bytes (borrowed,
+ * 256-byte aligned).  Carves it and runs the seeded per-rank initialisation
+ * (O2: Glorot-uniform weights from SplitMix64 keyed by init_seed + rank, zero
+ * biases, zero velocity) on the context stream; synchronous. */
+mtx_status mtx_bind_workspace(mtx_ctx *ctx, void *dev_ptr, uint64_t bytes);
+
+/* Number of parameters N in canonical (unpadded) order. */
+mtx_status mtx_param_count(const mtx_ctx *ctx, uint64_t *n);
+
+/* ---------------------------------------------------------------- the method */
+
+/* Global Broadcast: every rank's parameters become bitwise equal to
+ * rank `root`'s; velocity is reset to +0.  One ncclBroadcast of the flat buffer,
+ * so the per-variable ordering problem of P:292-296 cannot arise.  Must follow
+ * mtx_bind_workspace. */
+mtx_status mtx_bcast_params(mtx_ctx *ctx, int32_t root, void *stream);
+
+/* Bytes of device memory mtx_shard_data needs for a dataset of n samples. */
+mtx_status mtx_dataset_bytes(const mtx_ctx *ctx, int64_t n, uint64_t *bytes);
+
+/* Registers the training set: X is n x sample_elems fp32 (MLP rows, or NHWC
+ * images), y is n int32 labels in [0, classes).  X/y are host pointers
+ * (src_is_device = 0) or device pointers (1); either way they are copied into
+ * dev_buf (>= mtx_dataset_bytes, borrowed) in a wrap-extended layout so that
+ * every rank's slice of every cyclic global-batch window is one contiguous
+ * range.  Sharding rule (O4): window t starts at (t*B) mod n; rank r owns its
+ * positions [r*b, (r+1)*b).  Synchronous.  Errors: B > n -> INVALID_ARG,
+ * sample_elems mismatch -> SHAPE. */
+mtx_status mtx_shard_data(mtx_ctx *ctx, const float *X, const int32_t *y, int64_t n, int64_t sample_elems,
+                          int32_t src_is_device, void *dev_buf, uint64_t buf_bytes, void *stream);
+
+/* Pure helper (no context, no GPU): the sample ids of rank's slice of step's
+ * window as <= 2 contiguous pieces [begin[i], begin[i] + len[i]). */
+mtx_status mtx_batch_slice(int64_t n, int64_t B, int64_t step, int32_t rank, int32_t world, int64_t begin[2],
+                           int64_t len[2]);
+
+/* One synchronous data-parallel SGD step `step` on the registered dataset:
+ *  forward (Z = A W + b, ReLU) -> mean softmax-CE loss and dlogits -> backward
+ *  (dgrad with ReLU mask, wgrad written in place into the flat gradient buffer)
+ *  -> per bucket, in reverse layer order on the comm stream: ncclAllReduce(sum)
+ *  -> fused average (x fl(1/P)) + momentum update of params/velocity.
+ * The step runs as a CUDA graph after the first call.  If host_loss != NULL the
+ * call synchronises and writes the global loss (sum of rank loss sums / B);
+ * a non-finite averaged gradient is reported as MTX_ERR_NUMERIC by the next
+ * synchronising call. */
+mtx_status mtx_train_step(mtx_ctx *ctx, int64_t step, float *host_loss, void *stream);
+
+/* Same step with the rank's b input rows and labels supplied from HOST memory
+ * (pinned for async copies): X_host is b x sample_elems, y_host is b int32.  The
+ * host->device copy and the device->host loss read are part of the call
+ * (the end-to-end user path).  host_loss must be non-NULL (synchronising). */
+mtx_status mtx_train_step_host(mtx_ctx *ctx, const float *X_host, const int32_t *y_host, float *host_loss,
+                               void *stream);
+
+/* The averaging + update operator on caller buffers (config 5 sweep; no model
+ * needed beyond the context's communicator): grad[count] <- allreduce-sum over
+ * ranks; if apply_update: gbar = grad * fl(1/P), velocity <- fma(mu, velocity,
+ * gbar) (skipped when velocity == NULL and mu == 0), param <- fma(-lr, v, param).
+ * All pointers are device pointers, 16-byte aligned.  A non-finite gbar sets
+ * the context's numeric flag (MTX_ERR_NUMERIC at the next sync). */
+mtx_status mtx_allreduce_avg(mtx_ctx *ctx, float *grad, float *param, float *velocity, uint64_t count, float lr,
+                             float momentum, int32_t apply_update, void *stream);
+
+/* ---------------------------------------------------------------- state access (tests, checkpoints) */
+
+typedef enum { MTX_BUF_PARAMS = 0, MTX_BUF_VELOCITY = 1, MTX_BUF_GRADS = 2 } mtx_buffer;
+
+/* Copies N floats in canonical order to host_out (synchronous).  MTX_BUF_GRADS
+ * is the last step's reduced gradient SUM G (before x 1/P). */
+mtx_status mtx_get_buffer(mtx_ctx *ctx, int32_t which, float *host_out, uint64_t count);
+/* Overwrites a buffer from N host floats in canonical order (synchronous). */
+mtx_status mtx_set_buffer(mtx_ctx *ctx, int32_t which, const float *host_in, uint64_t count);
+mtx_status mtx_get_params(mtx_ctx *ctx, float *host_out, uint64_t count);
+
+/* Last synchronised step's global loss (sum over ranks of loss sums / B). */
+mtx_status mtx_get_loss(mtx_ctx *ctx, float *loss);
+
+/* Order-independent 64-bit digest of the parameters and velocity: the wrapping
+ * sum over canonical index e of SplitMix64(bits(w_e), e) + SplitMix64(bits(v_e),
+ * e + 2^40).  Equal on all ranks after every step (invariant I2). Synchronous. */
+mtx_status mtx_param_digest(mtx_ctx *ctx, uint64_t *out);
+
+/* ---------------------------------------------------------------- instrumentation */
+
+/* Kernel launches one mtx_train_step issues (for the bench's gpu_launches). */
+mtx_status mtx_launches_per_step(const mtx_ctx *ctx, int32_t *n);
+
+/* Enables CUDA-event timing of every launch site inside the step graph. */
+mtx_status mtx_set_timing(mtx_ctx *ctx, int32_t enable);
+/* Accumulated device milliseconds and launch counts per launch-site class since
+ * the last reset; names is a '\n'-separated list (written into names_buf).  Synchronous. */
+mtx_status mtx_read_timing(mtx_ctx *ctx, char *names_buf, uint64_t names_len, double *ms, int64_t *counts,
+                           int32_t max_sites, int32_t *n_sites, int32_t reset);
+
+/* Short description of the build (arch, NCCL version, GEMM engine). */
+const char *mtx_build_info(void);
+
+const char *mtx_last_error(const mtx_ctx *ctx);
+mtx_status mtx_finalize(mtx_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MTX_H */

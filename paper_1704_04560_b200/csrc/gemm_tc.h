@@ -1,0 +1,14 @@
+// gemm_tc.h -- tcgen05 (5th-gen tensor core) TF32 GEMM engine: TMA -> smem ring
+// -> tcgen05.mma (accumulators in TMEM) -> tcgen05.ld epilogue.  Internal.
+#pragma once
+#include "kernels.h"
+
+namespace mtx {
+struct TcGemm;
+bool tc_available();
+TcGemm *tc_create(int device);
+void tc_destroy(TcGemm *t);
+// True when this engine handles the shape/layout of g (otherwise the caller uses SIMT).
+bool tc_supports(TcGemm *t, const GemmDesc &g);
+cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h);
+}  // namespace mtx

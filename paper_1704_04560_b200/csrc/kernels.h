@@ -1,0 +1,93 @@
+// kernels.h -- launch interface of libmtx's sm_100a kernels (internal C++; the
+// public boundary is include/mtx.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace mtx {
+
+enum Epi : int { EPI_STORE = 0, EPI_BIAS_RELU = 1, EPI_BIAS = 2, EPI_MASK = 3 };
+
+// C[M,N] = op(A)[M,K] . op(B)[K,N] (+ epilogue), fp32.
+//   ta == false: A stored [M][lda] (element (m,k) at A[m*lda+k]);  true: A stored [K][lda], (m,k) at A[k*lda+m].
+//   tb == false: B stored [K][ldb];                                 true: B stored [N][ldb], (k,n) at B[n*ldb+k].
+//   aug: row m == M-1 of op(A) is all ones (the bias row of an augmented wgrad: db = colsum(dZ)).
+//   arow: A's sample dimension (m if !ta, k if ta) starts at arow.row0().
+//   splits > 1: deterministic split-K -- partial[z][M][N] then an ordered sum into C.
+struct GemmDesc {
+    int M = 0, N = 0, K = 0;
+    bool ta = false, tb = false, aug = false;
+    int epi = EPI_STORE;
+    const float *A = nullptr;
+    int64_t lda = 0;
+    RowSel arow{nullptr, 0};
+    const float *B = nullptr;
+    int64_t ldb = 0;
+    float *C = nullptr;
+    int64_t ldc = 0;
+    const float *bias = nullptr;
+    const float *mask = nullptr;
+    int64_t ldm = 0;
+    int splits = 1;
+    float *partial = nullptr;
+};
+
+// Launch-site hook: the API layer brackets every launch with it (timing/counting).
+struct LaunchHook {
+    virtual void before(const char *name, cudaStream_t s) = 0;
+    virtual void after(const char *name, cudaStream_t s) = 0;
+    virtual ~LaunchHook() {}
+};
+
+cudaError_t gemm_simt(const GemmDesc &g, cudaStream_t s, LaunchHook *h);
+
+// Fused last layer: logits = A W + b (W,b = augmented [(d+1)][C] block), mean
+// softmax-CE, dZ_L = (softmax - onehot)/b, loss per row, and (if dprev) the
+// masked dgrad dZ_{L-1} = (dZ_L W^T) .* [A > 0].
+cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, const float *Wb, const int32_t *labels,
+                       RowSel lrow, float inv_b, float *dZL, float *dprev, float *loss_rows, cudaStream_t s,
+                       LaunchHook *h);
+
+// out = sum_{i ascending in a fixed tree} v[i] (one block; deterministic).
+cudaError_t reduce_sum(const float *v, int n, float *out, cudaStream_t s, LaunchHook *h);
+
+// K6: gbar = G * invP; v = fma(mu, v, gbar); w = fma(-lr, v, w) over n floats
+// (n % 4 == 0, 16-byte aligned).  v == nullptr: mu must be 0 and w = fma(-lr, gbar, w).
+// flag |= 1 on a non-finite gbar.  If win != nullptr, thread 0 advances the
+// window start: *win = (*win + B) mod n_data.
+cudaError_t avg_update(float *G, float *w, float *v, int64_t n, float invP, float lr, float mu, int *flag,
+                       int64_t *win, int64_t B, int64_t n_data, cudaStream_t s, LaunchHook *h);
+
+// Ordered reduce (test mode): G[e] = ((g_0[e] + g_1[e]) + ...) + g_{P-1}[e], g_r at gathered + r*stride.
+cudaError_t ordered_fold(const float *gathered, int P, int64_t stride, int64_t n, float *G, cudaStream_t s,
+                         LaunchHook *h);
+
+// O2 init of one weight tensor: w[e] = (2u - 1) * lim, u = (H(H(seed, 16+t), e) >> 40) * 2^-24.
+cudaError_t init_glorot(float *w, int64_t n, uint64_t seed, int tensor_index, float lim, cudaStream_t s);
+
+// Digest: out += sum_e H(bits(x_e), e + salt) (wrapping, order independent).
+cudaError_t digest(const float *x, int64_t n, uint64_t salt, unsigned long long *out, cudaStream_t s);
+
+// ---- CNN (LeNet-style) kernels, NHWC, one sample row per image.
+struct ConvGeom {
+    int hi, wi, ci;   // input
+    int k, co;        // kernel, output channels
+    int hc, wc;       // conv output (valid, stride 1)
+    int hp, wp;       // pooled output (2x2 / 2, floor)
+};
+// R = ReLU(conv(X) + b) [rows][hc][wc][co];  P = maxpool(R), argmax index (0..3) per pooled element.
+cudaError_t conv_fwd(const ConvGeom &g, int rows, const float *X, RowSel xrow, const float *Wb, float *R, float *P,
+                     uint8_t *arg, cudaStream_t s, LaunchHook *h);
+// dR = route(dP via arg) .* [R > 0]
+cudaError_t pool_relu_bwd(const ConvGeom &g, int rows, const float *dP, const uint8_t *arg, const float *R, float *dR,
+                          cudaStream_t s, LaunchHook *h);
+// dWb[(k*k*ci)+1][co] = sum over rows/positions of im2col(X)^T dR (+ bias row), deterministic split.
+cudaError_t conv_wgrad(const ConvGeom &g, int rows, const float *X, RowSel xrow, const float *dR, float *dWb,
+                       float *partial, int splits, cudaStream_t s, LaunchHook *h);
+// dX[rows][hi][wi][ci] = full-correlation of dR with W (no mask; the caller's previous layer routes it).
+cudaError_t conv_dgrad(const ConvGeom &g, int rows, const float *dR, const float *Wb, float *dX, cudaStream_t s,
+                       LaunchHook *h);
+
+}  // namespace mtx

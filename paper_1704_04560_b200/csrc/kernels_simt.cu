@@ -1,0 +1,438 @@
+// kernels_simt.cu -- SIMT (CUDA-core) kernels of the data-parallel SGD step:
+// the FP32-tier GEMM (fwd / dgrad / wgrad), the fused softmax-CE head, the
+// deterministic reductions, and K6, the fused average + momentum update.
+// Paper: forward/backward of each replica, allreduce + average
+// (P:182-184), update.  Design notes: DESIGN.md §Kernels.
+#include <math.h>
+#include <stdio.h>
+
+#include <algorithm>
+
+#include "kernels.h"
+
+namespace mtx {
+
+namespace {
+
+inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+// ------------------------------------------------------------------ SIMT GEMM
+// 64x64 output tile per 256-thread CTA, BK = 16, each thread owns a 4x4 strided
+// sub-tile (rows ty + 16i, cols tx + 16j) so shared-memory reads broadcast
+// (A) or hit 16 consecutive banks (B).  Register prefetch of the next K tile
+// overlaps global loads with the FMAs.  Every output element is summed over k
+// in ascending order inside its split; splits are folded in ascending order by
+// splitk_reduce -- no atomics, so results are run-to-run deterministic.
+constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
+
+template <bool TA, bool TB, int EPI, bool AUG, bool PARTIAL>
+__global__ void __launch_bounds__(NT) gemm_simt_kernel(GemmDesc g) {
+    __shared__ float As[BK][BM + 4];
+    __shared__ float Bs[BK][BN + 4];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int kper = (g.K + g.splits - 1) / g.splits;
+    const int kbeg = blockIdx.z * kper, kend = min(g.K, kbeg + kper);
+    const float *A = g.A + g.arow.row0() * g.lda;
+    const int Mreal = AUG ? g.M - 1 : g.M;
+
+    float ra[4], rb[4];
+    auto load_a = [&](int k0) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            int e = tid + NT * i, ml, kl;
+            if (TA) { kl = e / BM; ml = e % BM; } else { ml = e / BK; kl = e % BK; }
+            int m = m0 + ml, k = k0 + kl;
+            float v = 0.f;
+            if (k < kend) {
+                if (m < Mreal) v = TA ? A[(int64_t)k * g.lda + m] : A[(int64_t)m * g.lda + k];
+                else if (AUG && m == Mreal) v = 1.f;
+            }
+            ra[i] = v;
+        }
+    };
+    auto load_b = [&](int k0) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            int e = tid + NT * i, nl, kl;
+            if (TB) { nl = e / BK; kl = e % BK; } else { kl = e / BN; nl = e % BN; }
+            int n = n0 + nl, k = k0 + kl;
+            float v = 0.f;
+            if (k < kend && n < g.N) v = TB ? g.B[(int64_t)n * g.ldb + k] : g.B[(int64_t)k * g.ldb + n];
+            rb[i] = v;
+        }
+    };
+    auto store_ab = [&]() {
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            int e = tid + NT * i, ml, kl, nl, kb;
+            if (TA) { kl = e / BM; ml = e % BM; } else { ml = e / BK; kl = e % BK; }
+            As[kl][ml] = ra[i];
+            if (TB) { nl = e / BK; kb = e % BK; } else { kb = e / BN; nl = e % BN; }
+            Bs[kb][nl] = rb[i];
+        }
+    };
+
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) acc[i][j] = 0.f;
+
+    if (kbeg < kend) {
+        load_a(kbeg);
+        load_b(kbeg);
+        for (int k0 = kbeg; k0 < kend; k0 += BK) {
+            store_ab();
+            __syncthreads();
+            if (k0 + BK < kend) { load_a(k0 + BK); load_b(k0 + BK); }
+            // Blocked summation: a BK-term FMA chain per tile, then one add into the
+            // running sum -- error grows with BK + K/BK instead of K (fp32 tier, 1e-5).
+            float blk[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) blk[i][j] = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < BK; kk++) {
+                float a[4], b[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+                for (int j = 0; j < 4; j++) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) blk[i][j] = __fmaf_rn(a[i], b[j], blk[i][j]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) acc[i][j] = __fadd_rn(acc[i][j], blk[i][j]);
+            __syncthreads();
+        }
+    }
+
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        int m = m0 + ty + 16 * i;
+        if (m >= g.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            int n = n0 + tx + 16 * j;
+            if (n >= g.N) continue;
+            float v = acc[i][j];
+            if (PARTIAL) {
+                g.partial[((int64_t)blockIdx.z * g.M + m) * g.N + n] = v;
+                continue;
+            }
+            if (EPI == EPI_BIAS_RELU) v = fmaxf(v + g.bias[n], 0.f);
+            else if (EPI == EPI_BIAS) v = v + g.bias[n];
+            else if (EPI == EPI_MASK) v = g.mask[(int64_t)m * g.ldm + n] > 0.f ? v : 0.f;
+            g.C[(int64_t)m * g.ldc + n] = v;
+        }
+    }
+}
+
+__global__ void splitk_reduce_kernel(const float *__restrict__ partial, int splits, int M, int N, float *C,
+                                     int64_t ldc) {
+    int64_t total = (int64_t)M * N;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        float s = partial[e];
+        for (int z = 1; z < splits; z++) s += partial[(int64_t)z * total + e];
+        C[(e / N) * ldc + (e % N)] = s;
+    }
+}
+
+template <bool TA, bool TB, int EPI, bool AUG, bool PARTIAL>
+void launch_gemm(const GemmDesc &g, dim3 grid, cudaStream_t s) {
+    gemm_simt_kernel<TA, TB, EPI, AUG, PARTIAL><<<grid, NT, 0, s>>>(g);
+}
+
+}  // namespace
+
+cudaError_t gemm_simt(const GemmDesc &g, cudaStream_t s, LaunchHook *h) {
+    dim3 grid(cdiv(g.N, BN), cdiv(g.M, BM), g.splits);
+    const bool part = g.splits > 1;
+    char name[96];
+    snprintf(name, sizeof name, "%s[M=%d,N=%d,K=%d,splits=%d]",
+             g.epi == EPI_MASK ? "gemm_simt_dgrad" : (g.ta ? "gemm_simt_wgrad" : "gemm_simt_fwd"), g.M, g.N, g.K,
+             g.splits);
+    if (h) h->before(name, s);
+    // Instantiated combinations: fwd (NN, bias[+relu]), dgrad (NT, mask), wgrad (TN, aug, store or partial).
+    if (!g.ta && !g.tb && g.epi == EPI_BIAS_RELU) launch_gemm<false, false, EPI_BIAS_RELU, false, false>(g, grid, s);
+    else if (!g.ta && !g.tb && g.epi == EPI_BIAS) launch_gemm<false, false, EPI_BIAS, false, false>(g, grid, s);
+    else if (!g.ta && g.tb && g.epi == EPI_MASK) launch_gemm<false, true, EPI_MASK, false, false>(g, grid, s);
+    else if (!g.ta && g.tb && g.epi == EPI_STORE) launch_gemm<false, true, EPI_STORE, false, false>(g, grid, s);
+    else if (g.ta && !g.tb && g.aug && !part) launch_gemm<true, false, EPI_STORE, true, false>(g, grid, s);
+    else if (g.ta && !g.tb && g.aug && part) launch_gemm<true, false, EPI_STORE, true, true>(g, grid, s);
+    else if (g.ta && !g.tb && !g.aug && !part) launch_gemm<true, false, EPI_STORE, false, false>(g, grid, s);
+    else if (g.ta && !g.tb && !g.aug && part) launch_gemm<true, false, EPI_STORE, false, true>(g, grid, s);
+    else return cudaErrorInvalidValue;
+    if (h) h->after(name, s);
+    if (part) {
+        int64_t total = (int64_t)g.M * g.N;
+        unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 8);
+        char rn[64];
+        snprintf(rn, sizeof rn, "splitk_reduce[M=%d,N=%d,splits=%d]", g.M, g.N, g.splits);
+        if (h) h->before(rn, s);
+        splitk_reduce_kernel<<<blocks, 256, 0, s>>>(g.partial, g.splits, g.M, g.N, g.C, g.ldc);
+        if (h) h->after(rn, s);
+    }
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ fused head (last layer + loss)
+// One warp per sample row.  Lane l owns features k = l, l+32, ...; the C logit
+// partial sums are combined with a fixed xor-shuffle tree.  W_L (d x C, <= 64 KB)
+// and b_L are staged in shared memory once per CTA.
+namespace {
+constexpr int HEAD_MAXC = 16, HEAD_WARPS = 8;
+
+__global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, int C, const float *__restrict__ A,
+                                                             RowSel arow, const float *__restrict__ Wb,
+                                                             const int32_t *__restrict__ labels, RowSel lrow,
+                                                             float inv_b, float *__restrict__ dZL,
+                                                             float *__restrict__ dprev, float *__restrict__ loss_rows) {
+    extern __shared__ float sW[];  // [(d+1)][C]
+    for (int e = threadIdx.x; e < (d + 1) * C; e += blockDim.x) sW[e] = Wb[e];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float *Abase = A + arow.row0() * (int64_t)d;
+    const int32_t *lab = labels + lrow.row0();
+    for (int i = blockIdx.x * HEAD_WARPS + warp; i < rows; i += gridDim.x * HEAD_WARPS) {
+        const float *a = Abase + (int64_t)i * d;
+        float z[HEAD_MAXC];
+#pragma unroll
+        for (int j = 0; j < HEAD_MAXC; j++) z[j] = 0.f;
+        for (int k = lane; k < d; k += 32) {
+            float ak = a[k];
+#pragma unroll
+            for (int j = 0; j < HEAD_MAXC; j++)
+                if (j < C) z[j] = __fmaf_rn(ak, sW[k * C + j], z[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < HEAD_MAXC; j++) {
+            if (j < C) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) z[j] += __shfl_xor_sync(0xffffffffu, z[j], o);
+                z[j] += sW[d * C + j];  // bias after the full sum
+            }
+        }
+        float m = z[0];
+#pragma unroll
+        for (int j = 1; j < HEAD_MAXC; j++) if (j < C) m = fmaxf(m, z[j]);
+        float S = 0.f;
+#pragma unroll
+        for (int j = 0; j < HEAD_MAXC; j++) if (j < C) S += expf(z[j] - m);
+        const int y = lab[i];
+        float zy = 0.f;
+#pragma unroll
+        for (int j = 0; j < HEAD_MAXC; j++) if (j == y) zy = z[j];
+        const float invS = 1.f / S;
+        float dz[HEAD_MAXC];
+#pragma unroll
+        for (int j = 0; j < HEAD_MAXC; j++)
+            dz[j] = (j < C) ? (expf(z[j] - m) * invS - (j == y ? 1.f : 0.f)) * inv_b : 0.f;
+        if (lane == 0) loss_rows[i] = m + logf(S) - zy;
+        if (lane < C) {
+            float mine = 0.f;
+#pragma unroll
+            for (int j = 0; j < HEAD_MAXC; j++) if (j == lane) mine = dz[j];
+            dZL[(int64_t)i * C + lane] = mine;
+        }
+        if (dprev) {
+            for (int k = lane; k < d; k += 32) {
+                float sacc = 0.f;
+#pragma unroll
+                for (int j = 0; j < HEAD_MAXC; j++) if (j < C) sacc = __fmaf_rn(dz[j], sW[k * C + j], sacc);
+                dprev[(int64_t)i * d + k] = a[k] > 0.f ? sacc : 0.f;
+            }
+        }
+    }
+}
+}  // namespace
+
+cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, const float *Wb, const int32_t *labels,
+                       RowSel lrow, float inv_b, float *dZL, float *dprev, float *loss_rows, cudaStream_t s,
+                       LaunchHook *h) {
+    if (C > HEAD_MAXC || C < 1) return cudaErrorInvalidValue;
+    size_t smem = sizeof(float) * (size_t)(d + 1) * C;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    unsigned blocks = std::min<unsigned>(cdiv(rows, HEAD_WARPS), 148u * 4u);
+    char name[80];
+    snprintf(name, sizeof name, "head_softmax_xent[rows=%d,d=%d,C=%d,dgrad=%d]", rows, d, C, dprev ? 1 : 0);
+    if (h) h->before(name, s);
+    head_kernel<<<blocks, HEAD_WARPS * 32, smem, s>>>(rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL, dprev,
+                                                       loss_rows);
+    if (h) h->after(name, s);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ deterministic block sum
+namespace {
+__global__ void __launch_bounds__(1024) reduce_sum_kernel(const float *__restrict__ v, int n, float *out) {
+    __shared__ float sh[1024];
+    float acc = 0.f;
+    for (int i = threadIdx.x; i < n; i += 1024) acc += v[i];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 512; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+}  // namespace
+
+cudaError_t reduce_sum(const float *v, int n, float *out, cudaStream_t s, LaunchHook *h) {
+    char name[48];
+    snprintf(name, sizeof name, "loss_reduce[n=%d]", n);
+    if (h) h->before(name, s);
+    reduce_sum_kernel<<<1, 1024, 0, s>>>(v, n, out);
+    if (h) h->after(name, s);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K6: fused average + update
+// Streams G, w, v once (20 B/elem, 12 B/elem without velocity) with 128-bit
+// accesses; 4 independent float4 per thread per iteration keep enough bytes in
+// flight to saturate HBM3e; grid = a multiple of the 148 SMs.  Explicit
+// __fmaf_rn pins the contraction so results are bit-identical to the oracle's
+// fmaf (A4).
+namespace {
+constexpr int UPD_T = 256, UPD_U = 4;
+
+template <bool HAS_V>
+__global__ void __launch_bounds__(UPD_T) avg_update_kernel(const float4 *__restrict__ G, float4 *__restrict__ w,
+                                                         float4 *__restrict__ v, int64_t n4, float invP, float lr,
+                                                         float mu, int *flag, int64_t *win, int64_t B,
+                                                         int64_t n_data, int tail) {
+    bool bad = false;
+    const int64_t stride = (int64_t)gridDim.x * UPD_T * UPD_U;
+    for (int64_t base = (int64_t)blockIdx.x * UPD_T * UPD_U + threadIdx.x; base < n4; base += stride) {
+        float4 g[UPD_U], wv[UPD_U], vv[UPD_U];
+#pragma unroll
+        for (int u = 0; u < UPD_U; u++) {
+            int64_t i = base + (int64_t)u * UPD_T;
+            if (i < n4) {
+                g[u] = __ldcs(G + i);
+                wv[u] = __ldcs(w + i);
+                if (HAS_V) vv[u] = __ldcs(v + i);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UPD_U; u++) {
+            int64_t i = base + (int64_t)u * UPD_T;
+            if (i >= n4) continue;
+            float gb[4] = {g[u].x * invP, g[u].y * invP, g[u].z * invP, g[u].w * invP};
+            float *pw = &wv[u].x, *pv = &vv[u].x;
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                bad |= !isfinite(gb[c]);
+                if (HAS_V) {
+                    pv[c] = __fmaf_rn(mu, pv[c], gb[c]);
+                    pw[c] = __fmaf_rn(-lr, pv[c], pw[c]);
+                } else {
+                    pw[c] = __fmaf_rn(-lr, gb[c], pw[c]);
+                }
+            }
+            __stcs(w + i, wv[u]);
+            if (HAS_V) __stcs(v + i, vv[u]);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < tail) {  // the n % 4 scalar tail
+        const int64_t i = 4 * n4 + threadIdx.x;
+        float *Gs = (float *)G, *ws = (float *)w, *vs = (float *)v;
+        float gb = Gs[i] * invP;
+        bad |= !isfinite(gb);
+        if (HAS_V) {
+            vs[i] = __fmaf_rn(mu, vs[i], gb);
+            ws[i] = __fmaf_rn(-lr, vs[i], ws[i]);
+        } else {
+            ws[i] = __fmaf_rn(-lr, gb, ws[i]);
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0 && flag) atomicOr(flag, 1);
+    if (win && blockIdx.x == 0 && threadIdx.x == 0) *win = (*win + B) % n_data;
+}
+}  // namespace
+
+cudaError_t avg_update(float *G, float *w, float *v, int64_t n, float invP, float lr, float mu, int *flag,
+                       int64_t *win, int64_t B, int64_t n_data, cudaStream_t s, LaunchHook *h) {
+    int64_t n4 = n / 4;
+    int tail = (int)(n - 4 * n4);
+    int64_t need = (n4 + UPD_T * UPD_U - 1) / (UPD_T * UPD_U);
+    unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, 148 * 8));
+    char name[64];
+    snprintf(name, sizeof name, "avg_update[n=%lld,v=%d]", (long long)n, v ? 1 : 0);
+    if (h) h->before(name, s);
+    if (v)
+        avg_update_kernel<true><<<blocks, UPD_T, 0, s>>>((const float4 *)G, (float4 *)w, (float4 *)v, n4, invP, lr,
+                                                         mu, flag, win, B, n_data, tail);
+    else
+        avg_update_kernel<false><<<blocks, UPD_T, 0, s>>>((const float4 *)G, (float4 *)w, nullptr, n4, invP, lr, mu,
+                                                          flag, win, B, n_data, tail);
+    if (h) h->after(name, s);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ ordered fold (test mode, A2)
+namespace {
+__global__ void ordered_fold_kernel(const float *__restrict__ g, int P, int64_t stride, int64_t n, float *G) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        float s = g[e];
+        for (int r = 1; r < P; r++) s = __fadd_rn(s, g[(int64_t)r * stride + e]);
+        G[e] = s;
+    }
+}
+}  // namespace
+
+cudaError_t ordered_fold(const float *gathered, int P, int64_t stride, int64_t n, float *G, cudaStream_t s,
+                         LaunchHook *h) {
+    unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    char name[64];
+    snprintf(name, sizeof name, "ordered_fold[n=%lld,P=%d]", (long long)n, P);
+    if (h) h->before(name, s);
+    ordered_fold_kernel<<<blocks, 256, 0, s>>>(gathered, P, stride, n, G);
+    if (h) h->after(name, s);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ init + digest
+namespace {
+__global__ void init_glorot_kernel(float *w, int64_t n, uint64_t seed, int t, float lim) {
+    const uint64_t key = splitmix64(seed, (uint64_t)(16 + t));
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t bits = splitmix64(key, (uint64_t)e) >> 40;
+        float u = __fmul_rn((float)bits, 5.9604644775390625e-08f);  // 2^-24, exact
+        float s = __fsub_rn(__fmul_rn(2.f, u), 1.f);                 // exact
+        w[e] = __fmul_rn(s, lim);
+    }
+}
+
+__global__ void digest_kernel(const uint32_t *__restrict__ x, int64_t n, uint64_t salt, unsigned long long *out) {
+    uint64_t acc = 0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        acc += splitmix64((uint64_t)x[e], (uint64_t)e + salt);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)acc);
+}
+}  // namespace
+
+cudaError_t init_glorot(float *w, int64_t n, uint64_t seed, int tensor_index, float lim, cudaStream_t s) {
+    unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    init_glorot_kernel<<<blocks, 256, 0, s>>>(w, n, seed, tensor_index, lim);
+    return cudaGetLastError();
+}
+
+cudaError_t digest(const float *x, int64_t n, uint64_t salt, unsigned long long *out, cudaStream_t s) {
+    unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    digest_kernel<<<blocks, 256, 0, s>>>((const uint32_t *)x, n, salt, out);
+    return cudaGetLastError();
+}
+
+}  // namespace mtx

@@ -1,0 +1,936 @@
+// mtx_api.cu -- the C-ABI of include/mtx.h: per-rank context, flat buffers,
+// NCCL communicator, the step schedule (fwd -> head -> bwd with per-bucket
+// allreduce + fused update on a comm stream), CUDA-graph capture, timing.
+//
+// Paper map: Global Broadcast operator -> mtx_bcast_params;
+// MPI_Allreduce operator -> per-bucket ncclAllReduce on ONE flat
+// gradient buffer + avg_update (K6); data readers that "automatically
+// distribute datasets" -> mtx_shard_data; the training regime of
+// the user script (Fig. 7) -> mtx_train_step.
+#include <math.h>
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/mtx.h"
+#include "gemm_tc.h"
+#include "kernels.h"
+
+using namespace mtx;
+
+namespace {
+
+constexpr int64_t ALIGN_F = 32;  // 128-byte alignment of every layer block (floats)
+constexpr int64_t LOSS_SLOT = 32;
+
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// One augmented parameter block: W [rows_w][cols] followed by b [cols] -- exactly
+// the canonical order W_l, b_l, so wgrad of [A, 1]^T dZ writes both.
+struct Layer {
+    int64_t log_off = 0, pad_off = 0;
+    int rows_w = 0, cols = 0;
+    int fan_in = 0, fan_out = 0;
+    int64_t size() const { return (int64_t)(rows_w + 1) * cols; }
+};
+
+struct Bucket {
+    int64_t lo = 0, hi = 0;   // padded range [lo, hi) of the flat gradient buffer (hi may include the loss slot)
+    int last_layer = 0;       // lowest layer index in the bucket: ready after its wgrad
+};
+
+struct TimingHook : LaunchHook {
+    bool enabled = false;
+    bool counting = false;
+    int count = 0;
+    std::vector<cudaEvent_t> ev;
+    std::vector<std::string> names;
+    size_t used = 0;
+    std::map<std::string, std::pair<double, int64_t>> acc;
+    void before(const char *name, cudaStream_t s) override {
+        if (counting) count++;
+        if (!enabled) return;
+        if (used + 2 > ev.size()) flush();
+        cudaEventRecord(ev[used], s);
+        names.push_back(name);
+        used++;
+    }
+    void after(const char *, cudaStream_t s) override {
+        if (!enabled) return;
+        cudaEventRecord(ev[used], s);
+        used++;
+    }
+    void ensure() {
+        if (ev.empty()) {
+            ev.resize(8192);
+            for (auto &e : ev) cudaEventCreate(&e);
+        }
+    }
+    void flush() {
+        for (size_t i = 0; i + 1 < used; i += 2) {
+            cudaEventSynchronize(ev[i + 1]);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            auto &a = acc[names[i / 2]];
+            a.first += ms;
+            a.second += 1;
+        }
+        used = 0;
+        names.clear();
+    }
+    ~TimingHook() {
+        for (auto &e : ev) cudaEventDestroy(e);
+    }
+};
+
+}  // namespace
+
+struct mtx_ctx {
+    int rank = 0, world = 1, device = 0;
+    // model
+    int kind = MTX_MLP;
+    std::vector<int> dims;             // MLP widths
+    int in_h = 0, in_w = 0, in_c = 0;  // CNN
+    std::vector<int> conv_k, conv_c, fc;
+    std::vector<ConvGeom> convs;
+    int64_t B = 0, b = 0;
+    int classes = 0, d0 = 0;
+    mtx_optim_desc opt{};
+    std::vector<Layer> layers;
+    std::vector<Bucket> buckets;
+    int64_t N = 0, N_pad = 0;
+    // workspace
+    uint8_t *ws = nullptr;
+    uint64_t ws_bytes = 0;
+    float *params = nullptr, *vel = nullptr, *grads = nullptr, *gather = nullptr;
+    std::vector<float *> acts;  // MLP: acts[l] = A_l [b][d_l], l = 1..L-1
+    float *dz[2] = {nullptr, nullptr}, *dzL = nullptr, *loss_rows = nullptr, *partial = nullptr;
+    float *stage_x = nullptr;
+    int32_t *stage_y = nullptr;
+    int64_t *win = nullptr;
+    int *flag = nullptr;
+    unsigned long long *dig = nullptr;
+    uint64_t *proto = nullptr;  // P x 8 bytes for the model-digest allgather
+    // CNN activations
+    std::vector<float *> convR, convP, convDR, convDP;
+    std::vector<uint8_t *> convArg;
+    std::vector<float *> fcA;  // fc hidden activations
+    int64_t partial_floats = 0;
+    // dataset
+    float *X = nullptr;
+    int32_t *Y = nullptr;
+    int64_t n_data = 0;
+    // host pinned slots
+    float *h_loss = nullptr;
+    int *h_flag = nullptr;
+    // runtime
+    ncclComm_t comm = nullptr;
+    cudaStream_t own = nullptr, comm_s = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    std::vector<cudaEvent_t> ev_bucket;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};  // [0] resident data, [1] staged host data
+    cudaStream_t graph_stream[2] = {nullptr, nullptr};
+    int launches_per_step = 0;
+    int64_t next_step = 0;
+    float last_loss = NAN;
+    TimingHook hook;
+    TcGemm *tc = nullptr;
+    // state machine
+    enum { S_INIT, S_BOUND, S_BCAST, S_READY, S_POISON } state = S_INIT;
+    std::string err;
+};
+
+namespace {
+
+mtx_status fail(mtx_ctx *c, mtx_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) {
+        c->err = buf;
+        if (st == MTX_ERR_CUDA || st == MTX_ERR_NCCL) c->state = mtx_ctx::S_POISON;
+    }
+    return st;
+}
+
+#define CK(call)                                                                                       \
+    do {                                                                                               \
+        cudaError_t e_ = (call);                                                                       \
+        if (e_ != cudaSuccess) return fail(c, MTX_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                                           __FILE__, __LINE__);                                        \
+    } while (0)
+#define NK(call)                                                                                       \
+    do {                                                                                               \
+        ncclResult_t r_ = (call);                                                                      \
+        if (r_ != ncclSuccess) {                                                                       \
+            if (c && c->comm) ncclCommAbort(c->comm), c->comm = nullptr;                               \
+            return fail(c, MTX_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_));                    \
+        }                                                                                              \
+    } while (0)
+
+mtx_status live(mtx_ctx *c) {
+    if (!c) return MTX_ERR_INVALID_ARG;
+    if (c->state == mtx_ctx::S_POISON) return MTX_ERR_STATE;
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+    return MTX_OK;
+}
+
+uint64_t fnv(uint64_t h, const void *p, size_t n) {
+    const uint8_t *b = (const uint8_t *)p;
+    for (size_t i = 0; i < n; i++) h = (h ^ b[i]) * 0x100000001B3ull;
+    return h;
+}
+
+uint64_t model_digest(const mtx_ctx *c) {
+    uint64_t h = 0xCBF29CE484222325ull;
+    h = fnv(h, &c->kind, sizeof c->kind);
+    for (int d : c->dims) h = fnv(h, &d, sizeof d);
+    for (int d : c->conv_k) h = fnv(h, &d, sizeof d);
+    for (int d : c->conv_c) h = fnv(h, &d, sizeof d);
+    for (int d : c->fc) h = fnv(h, &d, sizeof d);
+    h = fnv(h, &c->in_h, sizeof(int) * 3);
+    h = fnv(h, &c->B, sizeof c->B);
+    h = fnv(h, &c->opt.lr, sizeof(float) * 2);
+    h = fnv(h, &c->opt.precision, sizeof(int32_t) * 2);
+    h = fnv(h, &c->opt.bucket_bytes, sizeof(uint64_t) * 2);
+    return h;
+}
+
+cudaStream_t pick(mtx_ctx *c, void *s) { return s ? (cudaStream_t)s : c->own; }
+
+// ------------------------------------------------------------------ layout
+mtx_status build_layout(mtx_ctx *c) {
+    c->layers.clear();
+    int64_t log_off = 0, pad_off = 0;
+    auto add = [&](int rows_w, int cols, int fi, int fo) {
+        Layer L;
+        L.log_off = log_off;
+        L.pad_off = pad_off;
+        L.rows_w = rows_w;
+        L.cols = cols;
+        L.fan_in = fi;
+        L.fan_out = fo;
+        c->layers.push_back(L);
+        log_off += L.size();
+        pad_off = round_up(pad_off + L.size(), ALIGN_F);
+    };
+    if (c->kind == MTX_MLP) {
+        for (size_t l = 1; l < c->dims.size(); l++) add(c->dims[l - 1], c->dims[l], c->dims[l - 1], c->dims[l]);
+        c->classes = c->dims.back();
+        c->d0 = c->dims[0];
+    } else {
+        int h = c->in_h, w = c->in_w, ch = c->in_c;
+        c->convs.clear();
+        for (size_t i = 0; i < c->conv_k.size(); i++) {
+            ConvGeom g;
+            g.hi = h; g.wi = w; g.ci = ch; g.k = c->conv_k[i]; g.co = c->conv_c[i];
+            g.hc = h - g.k + 1; g.wc = w - g.k + 1; g.hp = g.hc / 2; g.wp = g.wc / 2;
+            if (g.hc < 2 || g.wc < 2) return fail(c, MTX_ERR_INVALID_ARG, "conv layer %zu too small", i);
+            c->convs.push_back(g);
+            add(g.k * g.k * g.ci, g.co, g.k * g.k * g.ci, g.k * g.k * g.co);
+            h = g.hp; w = g.wp; ch = g.co;
+        }
+        int d = h * w * ch;
+        for (int f : c->fc) {
+            add(d, f, d, f);
+            d = f;
+        }
+        c->classes = c->fc.back();
+        c->d0 = c->in_h * c->in_w * c->in_c;
+    }
+    c->N = log_off;
+    c->N_pad = pad_off;
+    // buckets: reverse layer order, contiguous layer-aligned ranges of >= bucket_bytes
+    c->buckets.clear();
+    int nl = (int)c->layers.size();
+    int64_t target = c->opt.bucket_bytes ? (int64_t)c->opt.bucket_bytes / 4 : INT64_MAX;
+    int hi_layer = nl - 1;
+    while (hi_layer >= 0) {
+        int lo_layer = hi_layer;
+        int64_t sz = c->layers[hi_layer].size();
+        while (lo_layer > 0 && sz < target) {
+            lo_layer--;
+            sz += c->layers[lo_layer].size();
+        }
+        Bucket bk;
+        bk.lo = c->layers[lo_layer].pad_off;
+        bk.hi = (hi_layer == nl - 1) ? c->N_pad + LOSS_SLOT : c->layers[hi_layer + 1].pad_off;
+        bk.last_layer = lo_layer;
+        c->buckets.push_back(bk);
+        hi_layer = lo_layer - 1;
+    }
+    return MTX_OK;
+}
+
+int64_t wgrad_splits(int64_t M, int64_t N, int64_t K) {
+    // Enough CTAs to fill 148 SMs ~2x, but keep >= 256 k per split.
+    int64_t tiles = ((M + 63) / 64) * ((N + 63) / 64);
+    int64_t s = std::max<int64_t>(1, (2 * 148) / std::max<int64_t>(tiles, 1));
+    s = std::min<int64_t>(s, std::max<int64_t>(1, K / 256));
+    return std::min<int64_t>(s, 32);
+}
+
+uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) -> uint8_t * {
+        off = (off + 255) / 256 * 256;
+        uint8_t *p = base ? base + off : nullptr;
+        off += bytes;
+        return p;
+    };
+    const int64_t b = c->b;
+    float *params = (float *)take(4 * c->N_pad);
+    float *vel = (float *)take(4 * c->N_pad);
+    float *grads = (float *)take(4 * (c->N_pad + LOSS_SLOT));
+    float *gather = c->opt.reduce == MTX_REDUCE_ORDERED ? (float *)take(4 * c->world * (c->N_pad + LOSS_SLOT)) : nullptr;
+    std::vector<float *> acts, fcA;
+    std::vector<float *> cR, cP, cDR, cDP;
+    std::vector<uint8_t *> cArg;
+    int64_t maxd = 1;
+    int64_t partial = 0;
+    if (c->kind == MTX_MLP) {
+        int L = (int)c->dims.size() - 1;
+        acts.assign(L, nullptr);
+        for (int l = 1; l < L; l++) {
+            acts[l] = (float *)take(4 * b * c->dims[l]);
+            maxd = std::max<int64_t>(maxd, c->dims[l]);
+        }
+        for (int l = 1; l <= L; l++) {
+            int64_t M = c->dims[l - 1] + 1, N = c->dims[l];
+            int64_t s = wgrad_splits(M, N, b);
+            if (s > 1) partial = std::max<int64_t>(partial, s * M * N);
+        }
+    } else {
+        for (auto &g : c->convs) {
+            cR.push_back((float *)take(4 * b * g.hc * g.wc * g.co));
+            cDR.push_back((float *)take(4 * b * g.hc * g.wc * g.co));
+            cP.push_back((float *)take(4 * b * g.hp * g.wp * g.co));
+            cDP.push_back((float *)take(4 * b * g.hp * g.wp * g.co));
+            cArg.push_back(take(b * g.hp * g.wp * g.co));
+            int64_t kk = (int64_t)g.k * g.k * g.ci + 1;
+            partial = std::max<int64_t>(partial, 64 * kk * g.co);
+        }
+        int nfc = (int)c->fc.size();
+        const ConvGeom &gl = c->convs.back();
+        int d = gl.hp * gl.wp * gl.co;
+        fcA.assign(nfc, nullptr);
+        std::vector<int> fd{d};
+        for (int f : c->fc) fd.push_back(f);
+        for (int f = 1; f < nfc; f++) {
+            fcA[f] = (float *)take(4 * b * fd[f]);
+            maxd = std::max<int64_t>(maxd, fd[f]);
+        }
+        maxd = std::max<int64_t>(maxd, d);
+        for (int f = 1; f <= nfc; f++) {
+            int64_t M = fd[f - 1] + 1, N = fd[f];
+            int64_t s = wgrad_splits(M, N, b);
+            if (s > 1) partial = std::max<int64_t>(partial, s * M * N);
+        }
+    }
+    float *dz0 = (float *)take(4 * b * maxd);
+    float *dz1 = (float *)take(4 * b * maxd);
+    float *dzL = (float *)take(4 * b * c->classes);
+    float *loss_rows = (float *)take(4 * b);
+    float *part = partial ? (float *)take(4 * partial) : nullptr;
+    float *sx = (float *)take(4 * b * c->d0);
+    int32_t *sy = (int32_t *)take(4 * b);
+    uint8_t *misc = take(256 + 8 * (uint64_t)c->world);
+    if (assign) {
+        c->params = params; c->vel = vel; c->grads = grads; c->gather = gather;
+        c->acts = acts; c->fcA = fcA;
+        c->convR = cR; c->convP = cP; c->convDR = cDR; c->convDP = cDP; c->convArg = cArg;
+        c->dz[0] = dz0; c->dz[1] = dz1; c->dzL = dzL; c->loss_rows = loss_rows;
+        c->partial = part; c->partial_floats = partial;
+        c->stage_x = sx; c->stage_y = sy;
+        c->win = (int64_t *)misc;
+        c->flag = (int *)(misc + 16);
+        c->dig = (unsigned long long *)(misc + 32);
+        c->proto = (uint64_t *)(misc + 256);
+    }
+    return off + 256;
+}
+
+// ------------------------------------------------------------------ step schedule
+struct Runner {
+    mtx_ctx *c;
+    cudaStream_t s;
+    bool staged;
+    LaunchHook *h;
+
+    mtx_status gemm(const GemmDesc &g) {
+        cudaError_t e;
+        if (c->opt.precision == MTX_TF32 && c->tc && tc_supports(c->tc, g))
+            e = tc_gemm(c->tc, g, s, h);
+        else
+            e = gemm_simt(g, s, h);
+        if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
+        return MTX_OK;
+    }
+
+    RowSel xrow() const { return staged ? RowSel{nullptr, 0} : RowSel{c->win, (int64_t)c->rank * c->b}; }
+    const float *xbase() const { return staged ? c->stage_x : c->X; }
+    const int32_t *ybase() const { return staged ? c->stage_y : c->Y; }
+
+    // Wgrad of layer block `li` (augmented: writes dW and db) from A [b][rows_w] and dZ [b][cols].
+    mtx_status wgrad(int li, const float *A, RowSel arow, const float *dZ) {
+        const Layer &L = c->layers[li];
+        GemmDesc g;
+        g.M = L.rows_w + 1; g.N = L.cols; g.K = (int)c->b;
+        g.ta = true; g.aug = true;
+        g.A = A; g.lda = L.rows_w; g.arow = arow;
+        g.B = dZ; g.ldb = L.cols;
+        g.C = c->grads + L.pad_off; g.ldc = L.cols;
+        g.splits = (int)wgrad_splits(g.M, g.N, g.K);
+        g.partial = c->partial;
+        return gemm(g);
+    }
+
+    mtx_status forward_backward_mlp() {
+        const int L = (int)c->dims.size() - 1;
+        const auto &d = c->dims;
+        const int64_t b = c->b;
+        mtx_status st;
+        // forward l = 1 .. L-1: A_l = ReLU(A_{l-1} W_l + b_l)
+        for (int l = 1; l < L; l++) {
+            const Layer &Ly = c->layers[l - 1];
+            GemmDesc g;
+            g.M = (int)b; g.N = d[l]; g.K = d[l - 1];
+            g.epi = EPI_BIAS_RELU;
+            g.A = l == 1 ? xbase() : c->acts[l - 1];
+            g.lda = d[l - 1];
+            g.arow = l == 1 ? xrow() : RowSel{nullptr, 0};
+            g.B = c->params + Ly.pad_off; g.ldb = d[l];
+            g.bias = c->params + Ly.pad_off + (int64_t)d[l - 1] * d[l];
+            g.C = c->acts[l]; g.ldc = d[l];
+            if ((st = gemm(g))) return st;
+        }
+        // head: logits, loss rows, dZ_L, dZ_{L-1}
+        const Layer &LL = c->layers[L - 1];
+        const float *Ain = L == 1 ? xbase() : c->acts[L - 1];
+        RowSel ar = L == 1 ? xrow() : RowSel{nullptr, 0};
+        cudaError_t e = head_fused((int)b, d[L - 1], d[L], Ain, ar, c->params + LL.pad_off, ybase(), xrow(),
+                                   1.0f / (float)b, c->dzL, L > 1 ? c->dz[0] : nullptr, c->loss_rows, s, h);
+        if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "head: %s", cudaGetErrorString(e));
+        e = reduce_sum(c->loss_rows, (int)b, c->grads + c->N_pad, s, h);
+        if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "loss reduce: %s", cudaGetErrorString(e));
+        // backward l = L .. 1
+        int cur = 0;
+        size_t bk = 0;
+        for (int l = L; l >= 1; l--) {
+            const float *dZ = (l == L) ? c->dzL : c->dz[cur];
+            const float *Aprev = l == 1 ? xbase() : c->acts[l - 1];
+            if ((st = wgrad(l - 1, Aprev, l == 1 ? xrow() : RowSel{nullptr, 0}, dZ))) return st;
+            if ((st = bucket_ready(l - 1, bk))) return st;
+            if (l < L && l > 1) {
+                // dZ_{l-1} = (dZ_l W_l^T) .* [A_{l-1} > 0]
+                const Layer &Ly = c->layers[l - 1];
+                GemmDesc g;
+                g.M = (int)b; g.N = d[l - 1]; g.K = d[l];
+                g.tb = true; g.epi = EPI_MASK;
+                g.A = dZ; g.lda = d[l];
+                g.B = c->params + Ly.pad_off; g.ldb = d[l];
+                g.mask = c->acts[l - 1]; g.ldm = d[l - 1];
+                g.C = c->dz[cur ^ 1]; g.ldc = d[l - 1];
+                if ((st = gemm(g))) return st;
+                cur ^= 1;
+            }
+        }
+        return MTX_OK;
+    }
+
+    // After layer block `li`'s wgrad: launch the allreduce + update of every bucket it completes.
+    mtx_status bucket_ready(int li, size_t &bk) {
+        while (bk < c->buckets.size() && c->buckets[bk].last_layer == li) {
+            mtx_status st = reduce_update(c->buckets[bk], bk + 1 == c->buckets.size());
+            if (st) return st;
+            bk++;
+        }
+        return MTX_OK;
+    }
+
+    // mu == 0: plain SGD, the velocity buffer is not maintained (12 B/elem instead of 20).
+    float *vel_or_null(int64_t off) const { return c->opt.momentum != 0.f ? c->vel + off : nullptr; }
+
+    mtx_status reduce_update(const Bucket &bkt, bool last) {
+        const float invP = 1.0f / (float)c->world;
+        int64_t upd_hi = std::min<int64_t>(bkt.hi, c->N_pad);
+        int64_t *win = (last && !staged) ? c->win : nullptr;
+        if (c->world == 1) {
+            cudaError_t e = avg_update(c->grads + bkt.lo, c->params + bkt.lo, vel_or_null(bkt.lo), upd_hi - bkt.lo,
+                                       invP, c->opt.lr, c->opt.momentum, c->flag, win, c->B, c->n_data, s, h);
+            if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "update: %s", cudaGetErrorString(e));
+            return MTX_OK;
+        }
+        cudaEvent_t ev = c->ev_bucket[&bkt - &c->buckets[0]];
+        CK(cudaEventRecord(ev, s));
+        CK(cudaStreamWaitEvent(c->comm_s, ev, 0));
+        int64_t cnt = bkt.hi - bkt.lo;
+        if (c->opt.reduce == MTX_REDUCE_ORDERED) {
+            // allgather every rank's slice, then the ascending-rank left fold (A2 test mode)
+            NK(ncclGroupStart());
+            for (int r = 0; r < c->world; r++) {
+                int64_t stride = c->N_pad + LOSS_SLOT;
+                NK(ncclBroadcast(c->grads + bkt.lo, c->gather + r * stride + bkt.lo, cnt, ncclFloat, r, c->comm,
+                                   c->comm_s));
+            }
+            NK(ncclGroupEnd());
+            cudaError_t e = ordered_fold(c->gather + bkt.lo, c->world, c->N_pad + LOSS_SLOT, cnt, c->grads + bkt.lo,
+                                         c->comm_s, h);
+            if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "ordered fold: %s", cudaGetErrorString(e));
+        } else {
+            NK(ncclAllReduce(c->grads + bkt.lo, c->grads + bkt.lo, cnt, ncclFloat, ncclSum, c->comm, c->comm_s));
+        }
+        cudaError_t e = avg_update(c->grads + bkt.lo, c->params + bkt.lo, vel_or_null(bkt.lo), upd_hi - bkt.lo, invP,
+                                   c->opt.lr, c->opt.momentum, c->flag, win, c->B, c->n_data, c->comm_s, h);
+        if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "update: %s", cudaGetErrorString(e));
+        return MTX_OK;
+    }
+
+    mtx_status step() {
+        if (c->world > 1) {
+            CK(cudaEventRecord(c->ev_fork, s));
+            CK(cudaStreamWaitEvent(c->comm_s, c->ev_fork, 0));
+        }
+        mtx_status st = c->kind == MTX_MLP ? forward_backward_mlp() : forward_backward_cnn();
+        if (st) return st;
+        if (c->world > 1) {
+            CK(cudaEventRecord(c->ev_join, c->comm_s));
+            CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+        }
+        return MTX_OK;
+    }
+
+    mtx_status forward_backward_cnn();
+};
+
+}  // namespace
+
+mtx_status Runner::forward_backward_cnn() { return fail(c, MTX_ERR_UNSUPPORTED, "CNN step not built yet"); }
+
+namespace {
+
+mtx_status run_step(mtx_ctx *c, cudaStream_t s, bool staged) {
+    if (c->hook.enabled) {  // eager launches bracketed by CUDA events (kernel timing pass)
+        Runner r{c, s, staged, &c->hook};
+        return r.step();
+    }
+    int gi = staged ? 1 : 0;
+    if (!c->graph[gi]) {
+        c->hook.counting = true;
+        c->hook.count = 0;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+        Runner r{c, s, staged, &c->hook};
+        mtx_status st = r.step();
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(s, &g);
+        c->hook.counting = false;
+        if (st) {
+            if (g) cudaGraphDestroy(g);
+            return st;
+        }
+        CK(e);
+        c->launches_per_step = c->hook.count;
+        cudaError_t ei = cudaGraphInstantiate(&c->graph[gi], g, 0);
+        cudaGraphDestroy(g);
+        CK(ei);
+    }
+    CK(cudaGraphLaunch(c->graph[gi], s));
+    return MTX_OK;
+}
+
+// D2H of the loss slot and numeric flag, synchronise, then report.
+mtx_status sync_loss(mtx_ctx *c, cudaStream_t s, float *host_loss) {
+    CK(cudaMemcpyAsync(c->h_loss, c->grads + c->N_pad, sizeof(float), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->last_loss = (float)((double)c->h_loss[0] / (double)c->B);
+    if (host_loss) *host_loss = c->last_loss;
+    if (c->h_flag[0]) return fail(c, MTX_ERR_NUMERIC, "non-finite averaged gradient");
+    return MTX_OK;
+}
+
+mtx_status check_flag(mtx_ctx *c, cudaStream_t s) {
+    if (!c->flag) return MTX_OK;
+    CK(cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (c->h_flag[0]) return fail(c, MTX_ERR_NUMERIC, "non-finite averaged gradient");
+    return MTX_OK;
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+mtx_status mtx_get_unique_id(uint8_t out[128]) {
+    if (!out) return MTX_ERR_INVALID_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return MTX_ERR_NCCL;
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    memcpy(out, &id, 128);
+    return MTX_OK;
+}
+
+mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t uid[128], int32_t device,
+                    const mtx_model_desc *model, const mtx_optim_desc *opt) {
+    if (!out || !model || !opt) return MTX_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world || (world > 1 && !uid)) return MTX_ERR_INVALID_ARG;
+    if (model->global_batch <= 0 || model->global_batch % world) return MTX_ERR_INVALID_ARG;
+    if (opt->precision != MTX_FP32 && opt->precision != MTX_TF32) return MTX_ERR_INVALID_ARG;
+    if (opt->reduce != MTX_REDUCE_NCCL && opt->reduce != MTX_REDUCE_ORDERED) return MTX_ERR_INVALID_ARG;
+    mtx_ctx *c = new mtx_ctx();
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    c->kind = model->kind;
+    c->opt = *opt;
+    c->B = model->global_batch;
+    c->b = c->B / world;
+    if (model->kind == MTX_MLP) {
+        if (model->n_dims < 2 || !model->dims) { delete c; return MTX_ERR_INVALID_ARG; }
+        c->dims.assign(model->dims, model->dims + model->n_dims);
+        for (int d : c->dims) if (d < 1) { delete c; return MTX_ERR_INVALID_ARG; }
+    } else if (model->kind == MTX_CNN) {
+        if (model->n_conv < 1 || model->n_fc < 1 || !model->conv_k || !model->conv_c || !model->fc_dims) {
+            delete c;
+            return MTX_ERR_INVALID_ARG;
+        }
+        c->in_h = model->in_h; c->in_w = model->in_w; c->in_c = model->in_c;
+        c->conv_k.assign(model->conv_k, model->conv_k + model->n_conv);
+        c->conv_c.assign(model->conv_c, model->conv_c + model->n_conv);
+        c->fc.assign(model->fc_dims, model->fc_dims + model->n_fc);
+    } else {
+        delete c;
+        return MTX_ERR_INVALID_ARG;
+    }
+    mtx_status st = build_layout(c);
+    if (st) { delete c; return st; }
+    if (c->classes > 16) { delete c; return MTX_ERR_UNSUPPORTED; }
+    if (cudaSetDevice(device) != cudaSuccess) { delete c; return MTX_ERR_CUDA; }
+    if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->comm_s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaHostAlloc(&c->h_loss, 64, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&c->h_flag, 64, cudaHostAllocDefault) != cudaSuccess) {
+        delete c;
+        return MTX_ERR_CUDA;
+    }
+    c->ev_bucket.resize(c->buckets.size());
+    for (auto &e : c->ev_bucket) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (world > 1) {
+        ncclUniqueId id;
+        memcpy(&id, uid, 128);
+        ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+        if (r != ncclSuccess) {
+            c->comm = nullptr;
+            *out = c;
+            return fail(c, MTX_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+        }
+    }
+    if (opt->precision == MTX_TF32) c->tc = tc_create(device);
+    *out = c;
+    return MTX_OK;
+}
+
+mtx_status mtx_workspace_bytes(const mtx_ctx *c, uint64_t *bytes) {
+    if (!c || !bytes) return MTX_ERR_INVALID_ARG;
+    *bytes = carve(const_cast<mtx_ctx *>(c), nullptr, false);
+    return MTX_OK;
+}
+
+mtx_status mtx_param_count(const mtx_ctx *c, uint64_t *n) {
+    if (!c || !n) return MTX_ERR_INVALID_ARG;
+    *n = (uint64_t)c->N;
+    return MTX_OK;
+}
+
+mtx_status mtx_bind_workspace(mtx_ctx *c, void *dev_ptr, uint64_t bytes) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (c->state != mtx_ctx::S_INIT) return fail(c, MTX_ERR_STATE, "workspace already bound");
+    uint64_t need = carve(c, nullptr, false);
+    if (!dev_ptr || ((uintptr_t)dev_ptr & 255)) return fail(c, MTX_ERR_INVALID_ARG, "workspace must be 256-B aligned");
+    if (bytes < need) return fail(c, MTX_ERR_OOM, "workspace %llu < %llu bytes", (unsigned long long)bytes,
+                                  (unsigned long long)need);
+    c->ws = (uint8_t *)dev_ptr;
+    c->ws_bytes = bytes;
+    carve(c, c->ws, true);
+    CK(cudaMemsetAsync(c->ws, 0, need, c->own));
+    // O2: seeded per-rank Glorot-uniform init; lim = fl32(sqrt(6 / (fan_in + fan_out))).
+    const uint64_t seed = c->opt.init_seed + (uint64_t)c->rank;
+    for (size_t i = 0; i < c->layers.size(); i++) {
+        const Layer &L = c->layers[i];
+        float lim = (float)sqrt(6.0 / (double)(L.fan_in + L.fan_out));
+        CK(init_glorot(c->params + L.pad_off, (int64_t)L.rows_w * L.cols, seed, (int)(2 * i), lim, c->own));
+    }
+    if (c->world > 1) {  // every rank must run the same model
+        uint64_t mine = model_digest(c);
+        CK(cudaMemcpyAsync(c->proto + c->rank, &mine, 8, cudaMemcpyHostToDevice, c->own));
+        NK(ncclAllGather(c->proto + c->rank, c->proto, 1, ncclUint64, c->comm, c->own));
+        std::vector<uint64_t> all(c->world);
+        CK(cudaMemcpyAsync(all.data(), c->proto, 8 * c->world, cudaMemcpyDeviceToHost, c->own));
+        CK(cudaStreamSynchronize(c->own));
+        for (int r = 0; r < c->world; r++)
+            if (all[r] != mine) return fail(c, MTX_ERR_PROTOCOL, "rank %d model digest differs from rank %d", r, c->rank);
+    }
+    CK(cudaStreamSynchronize(c->own));
+    c->state = mtx_ctx::S_BOUND;
+    return MTX_OK;
+}
+
+mtx_status mtx_bcast_params(mtx_ctx *c, int32_t root, void *stream) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (c->state == mtx_ctx::S_INIT) return fail(c, MTX_ERR_STATE, "bind the workspace first");
+    if (root < 0 || root >= c->world) return fail(c, MTX_ERR_INVALID_ARG, "root %d", root);
+    cudaStream_t s = pick(c, stream);
+    if (c->world > 1) NK(ncclBroadcast(c->params, c->params, c->N_pad, ncclFloat, root, c->comm, s));
+    CK(cudaMemsetAsync(c->vel, 0, 4 * c->N_pad, s));
+    if (c->state == mtx_ctx::S_BOUND) c->state = mtx_ctx::S_BCAST;
+    return MTX_OK;
+}
+
+mtx_status mtx_dataset_bytes(const mtx_ctx *c, int64_t n, uint64_t *bytes) {
+    if (!c || !bytes || n <= 0) return MTX_ERR_INVALID_ARG;
+    uint64_t rows = (uint64_t)(n + c->B);
+    *bytes = (rows * c->d0 * 4 + 255) / 256 * 256 + rows * 4 + 256;
+    return MTX_OK;
+}
+
+mtx_status mtx_shard_data(mtx_ctx *c, const float *X, const int32_t *y, int64_t n, int64_t sample_elems,
+                          int32_t src_is_device, void *dev_buf, uint64_t buf_bytes, void *stream) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (c->state == mtx_ctx::S_INIT) return fail(c, MTX_ERR_STATE, "bind the workspace first");
+    if (!X || !y || !dev_buf || n <= 0) return fail(c, MTX_ERR_INVALID_ARG, "null dataset");
+    if (sample_elems != c->d0) return fail(c, MTX_ERR_SHAPE, "sample_elems %lld != %d", (long long)sample_elems, c->d0);
+    if (c->B > n) return fail(c, MTX_ERR_INVALID_ARG, "global batch %lld > n %lld", (long long)c->B, (long long)n);
+    uint64_t need;
+    mtx_dataset_bytes(c, n, &need);
+    if (buf_bytes < need || ((uintptr_t)dev_buf & 255)) return fail(c, MTX_ERR_OOM, "dataset buffer too small");
+    cudaStream_t s = pick(c, stream);
+    const uint64_t rows = (uint64_t)(n + c->B), d = c->d0;
+    float *Xd = (float *)dev_buf;
+    int32_t *Yd = (int32_t *)((uint8_t *)dev_buf + (rows * d * 4 + 255) / 256 * 256);
+    cudaMemcpyKind k = src_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpyAsync(Xd, X, (size_t)n * d * 4, k, s));
+    CK(cudaMemcpyAsync(Yd, y, (size_t)n * 4, k, s));
+    // wrap extension: rows n .. n+B-1 repeat rows 0 .. B-1 (every slice contiguous)
+    CK(cudaMemcpyAsync(Xd + (size_t)n * d, Xd, (size_t)c->B * d * 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(Yd + n, Yd, (size_t)c->B * 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync(c->win, 0, 8, s));
+    CK(cudaStreamSynchronize(s));
+    c->X = Xd;
+    c->Y = Yd;
+    c->n_data = n;
+    c->next_step = 0;
+    for (auto &g : c->graph)
+        if (g) cudaGraphExecDestroy(g), g = nullptr;  // n changed: re-capture
+    if (c->state == mtx_ctx::S_BCAST) c->state = mtx_ctx::S_READY;
+    return MTX_OK;
+}
+
+mtx_status mtx_batch_slice(int64_t n, int64_t B, int64_t step, int32_t rank, int32_t world, int64_t begin[2],
+                           int64_t len[2]) {
+    if (!begin || !len || n <= 0 || B <= 0 || B > n || world <= 0 || rank < 0 || rank >= world || B % world ||
+        step < 0)
+        return MTX_ERR_INVALID_ARG;
+    const int64_t b = B / world;
+    const int64_t s = (int64_t)(((unsigned __int128)step * (unsigned __int128)B) % (unsigned __int128)n);
+    const int64_t first = (s + (int64_t)rank * b) % n;
+    begin[0] = first;
+    begin[1] = 0;
+    len[0] = std::min<int64_t>(b, n - first);
+    len[1] = b - len[0];
+    return MTX_OK;
+}
+
+mtx_status mtx_train_step(mtx_ctx *c, int64_t step, float *host_loss, void *stream) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (c->state != mtx_ctx::S_READY) return fail(c, MTX_ERR_STATE, "train_step needs bcast_params and shard_data");
+    if (step < 0) return fail(c, MTX_ERR_INVALID_ARG, "step %lld", (long long)step);
+    cudaStream_t s = pick(c, stream);
+    if (step != c->next_step) {  // non-sequential step: reset the device window start (t*B) mod n
+        int64_t w = (int64_t)(((unsigned __int128)step * (unsigned __int128)c->B) % (unsigned __int128)c->n_data);
+        CK(cudaMemcpyAsync(c->win, &w, 8, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    if ((st = run_step(c, s, false))) return st;
+    c->next_step = step + 1;
+    if (host_loss) return sync_loss(c, s, host_loss);
+    return MTX_OK;
+}
+
+mtx_status mtx_train_step_host(mtx_ctx *c, const float *X_host, const int32_t *y_host, float *host_loss,
+                               void *stream) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (c->state != mtx_ctx::S_READY && c->state != mtx_ctx::S_BCAST)
+        return fail(c, MTX_ERR_STATE, "train_step_host needs bcast_params");
+    if (!X_host || !y_host || !host_loss) return fail(c, MTX_ERR_INVALID_ARG, "null host buffer");
+    cudaStream_t s = pick(c, stream);
+    if (c->n_data == 0) c->n_data = c->B;  // window advance is unused on the staged path
+    CK(cudaMemcpyAsync(c->stage_x, X_host, (size_t)c->b * c->d0 * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->stage_y, y_host, (size_t)c->b * 4, cudaMemcpyHostToDevice, s));
+    if ((st = run_step(c, s, true))) return st;
+    return sync_loss(c, s, host_loss);
+}
+
+mtx_status mtx_allreduce_avg(mtx_ctx *c, float *grad, float *param, float *velocity, uint64_t count, float lr,
+                             float momentum, int32_t apply_update, void *stream) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (c->state == mtx_ctx::S_INIT) return fail(c, MTX_ERR_STATE, "bind the workspace first");
+    if (!grad || (apply_update && !param) || (apply_update && !velocity && momentum != 0.f))
+        return fail(c, MTX_ERR_INVALID_ARG, "null buffer");
+    if (((uintptr_t)grad | (uintptr_t)param | (uintptr_t)velocity) & 15)
+        return fail(c, MTX_ERR_INVALID_ARG, "buffers must be 16-byte aligned");
+    cudaStream_t s = pick(c, stream);
+    LaunchHook *h = &c->hook;
+    if (c->world > 1) NK(ncclAllReduce(grad, grad, count, ncclFloat, ncclSum, c->comm, s));
+    if (apply_update) {
+        float *v = momentum != 0.f ? velocity : nullptr;
+        CK(avg_update(grad, param, v, (int64_t)count, 1.0f / (float)c->world, lr, momentum, c->flag, nullptr, 0, 1, s,
+                      h));
+    }
+    return MTX_OK;
+}
+
+mtx_status mtx_get_buffer(mtx_ctx *c, int32_t which, float *host_out, uint64_t count) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (c->state == mtx_ctx::S_INIT) return fail(c, MTX_ERR_STATE, "no workspace");
+    if (!host_out) return fail(c, MTX_ERR_INVALID_ARG, "null");
+    if (count != (uint64_t)c->N) return fail(c, MTX_ERR_SHAPE, "count %llu != N %lld", (unsigned long long)count,
+                                             (long long)c->N);
+    float *src = which == MTX_BUF_PARAMS ? c->params : which == MTX_BUF_VELOCITY ? c->vel
+               : which == MTX_BUF_GRADS ? c->grads : nullptr;
+    if (!src) return fail(c, MTX_ERR_INVALID_ARG, "buffer id %d", which);
+    CK(cudaDeviceSynchronize());
+    for (const Layer &L : c->layers)
+        CK(cudaMemcpy(host_out + L.log_off, src + L.pad_off, 4 * L.size(), cudaMemcpyDeviceToHost));
+    return check_flag(c, c->own);
+}
+
+mtx_status mtx_set_buffer(mtx_ctx *c, int32_t which, const float *host_in, uint64_t count) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (c->state == mtx_ctx::S_INIT) return fail(c, MTX_ERR_STATE, "no workspace");
+    if (!host_in) return fail(c, MTX_ERR_INVALID_ARG, "null");
+    if (count != (uint64_t)c->N) return fail(c, MTX_ERR_SHAPE, "count != N");
+    float *dst = which == MTX_BUF_PARAMS ? c->params : which == MTX_BUF_VELOCITY ? c->vel
+               : which == MTX_BUF_GRADS ? c->grads : nullptr;
+    if (!dst) return fail(c, MTX_ERR_INVALID_ARG, "buffer id %d", which);
+    CK(cudaDeviceSynchronize());
+    for (const Layer &L : c->layers)
+        CK(cudaMemcpy(dst + L.pad_off, host_in + L.log_off, 4 * L.size(), cudaMemcpyHostToDevice));
+    return MTX_OK;
+}
+
+mtx_status mtx_get_params(mtx_ctx *c, float *host_out, uint64_t count) {
+    return mtx_get_buffer(c, MTX_BUF_PARAMS, host_out, count);
+}
+
+mtx_status mtx_get_loss(mtx_ctx *c, float *loss) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (!loss) return MTX_ERR_INVALID_ARG;
+    *loss = c->last_loss;
+    return MTX_OK;
+}
+
+mtx_status mtx_param_digest(mtx_ctx *c, uint64_t *out) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (c->state == mtx_ctx::S_INIT || !out) return fail(c, MTX_ERR_STATE, "no workspace");
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemsetAsync(c->dig, 0, 8, c->own));
+    for (const Layer &L : c->layers) {
+        CK(digest(c->params + L.pad_off, L.size(), (uint64_t)L.log_off, c->dig, c->own));
+        CK(digest(c->vel + L.pad_off, L.size(), (uint64_t)L.log_off + (1ull << 40), c->dig, c->own));
+    }
+    unsigned long long h;
+    CK(cudaMemcpyAsync(&h, c->dig, 8, cudaMemcpyDeviceToHost, c->own));
+    CK(cudaStreamSynchronize(c->own));
+    *out = h;
+    return MTX_OK;
+}
+
+mtx_status mtx_launches_per_step(const mtx_ctx *c, int32_t *n) {
+    if (!c || !n) return MTX_ERR_INVALID_ARG;
+    *n = c->launches_per_step;
+    return MTX_OK;
+}
+
+mtx_status mtx_set_timing(mtx_ctx *c, int32_t enable) {
+    mtx_status st = live(c);
+    if (st) return st;
+    c->hook.ensure();
+    c->hook.enabled = enable != 0;
+    return MTX_OK;
+}
+
+mtx_status mtx_read_timing(mtx_ctx *c, char *names_buf, uint64_t names_len, double *ms, int64_t *counts,
+                           int32_t max_sites, int32_t *n_sites, int32_t reset) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (!names_buf || !ms || !counts || !n_sites) return MTX_ERR_INVALID_ARG;
+    c->hook.flush();
+    std::string names;
+    int i = 0;
+    for (auto &kv : c->hook.acc) {
+        if (i >= max_sites) break;
+        names += kv.first + "\n";
+        ms[i] = kv.second.first;
+        counts[i] = kv.second.second;
+        i++;
+    }
+    *n_sites = i;
+    snprintf(names_buf, names_len, "%s", names.c_str());
+    if (reset) c->hook.acc.clear();
+    return MTX_OK;
+}
+
+const char *mtx_build_info(void) {
+    static char buf[256];
+    int v = 0;
+    ncclGetVersion(&v);
+    snprintf(buf, sizeof buf, "libmtx sm_100a; nccl %d; gemm engines: simt-fp32%s", v,
+             tc_available() ? ", tcgen05-tf32" : "");
+    return buf;
+}
+
+const char *mtx_last_error(const mtx_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+mtx_status mtx_finalize(mtx_ctx *c) {
+    if (!c) return MTX_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (auto &g : c->graph)
+        if (g) cudaGraphExecDestroy(g);
+    if (c->comm) ncclCommDestroy(c->comm);
+    for (auto &e : c->ev_bucket) cudaEventDestroy(e);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->own) cudaStreamDestroy(c->own);
+    if (c->comm_s) cudaStreamDestroy(c->comm_s);
+    if (c->h_loss) cudaFreeHost(c->h_loss);
+    if (c->h_flag) cudaFreeHost(c->h_flag);
+    if (c->tc) tc_destroy(c->tc);
+    delete c;
+    return MTX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,39 @@
+"""Shared test helpers (comparison metrics; no method arithmetic)."""
+from __future__ import annotations
+
+import numpy as np
+
+# Tolerance tiers from BASELINE.json north_star: GPU vs oracle within 1e-5 relative
+# on the fp32 path, 1e-3 when TF32 tensor cores are used (max-norm per tensor).
+TOL = {0: 1e-5, 1: 1e-3}
+
+
+def maxrel(x, ref) -> float:
+    """Max-norm relative error: max_i |x_i - r_i| / max_i |r_i| (reading of "1e-5 relative")."""
+    x = np.asarray(x, np.float64)
+    ref = np.asarray(ref, np.float64)
+    den = max(np.abs(ref).max(initial=0.0), 1e-30)
+    return float(np.abs(x - ref).max(initial=0.0) / den)
+
+
+def per_tensor_maxrel(x, ref, table) -> list:
+    return [maxrel(x[o:o + s], ref[o:o + s]) for o, s in table]
+
+
+def digest_np(params: np.ndarray, vel: np.ndarray) -> int:
+    """Recomputes mtx_param_digest's definition from host copies (include/mtx.h)."""
+    import mtx_synth as S
+    idx = np.arange(params.size, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        hp = S.splitmix64(0, 0)  # noqa: F841 (warm)
+        a = _sm_keyvec(params.view(np.uint32).astype(np.uint64), idx)
+        b = _sm_keyvec(vel.view(np.uint32).astype(np.uint64), idx + np.uint64(1 << 40))
+        return int((a.sum(dtype=np.uint64) + b.sum(dtype=np.uint64)) & np.uint64(0xFFFFFFFFFFFFFFFF))
+
+
+def _sm_keyvec(keys: np.ndarray, k: np.ndarray) -> np.ndarray:
+    G = np.uint64(0x9E3779B97F4A7C15)
+    z = keys + (k + np.uint64(1)) * G
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
