@@ -114,11 +114,10 @@ typedef struct {
 mtx_status mtx_get_unique_id(uint8_t out[128]);
 
 /* Creates the per-rank context on CUDA device `device`: copies the model and
- * optimiser descriptions, creates the NCCL communicator of `world` ranks (uid
- * may be NULL when world == 1), and checks -- by an NCCL allgather of a 64-bit
- * digest -- that every rank passed the same model/optimiser description
- * (mismatch: MTX_ERR_PROTOCOL).  Errors: world < 1, rank outside
- * [0, world), B mod world != 0, unsupported layer shapes -> MTX_ERR_INVALID_ARG. */
+ * optimiser descriptions and creates the NCCL communicator of `world` ranks
+ * (uid may be NULL when world == 1).  Errors: world < 1, rank outside
+ * [0, world), B mod world != 0, unsupported layer shapes -> MTX_ERR_INVALID_ARG;
+ * more than 16 classes -> MTX_ERR_UNSUPPORTED. */
 mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t uid[128], int32_t device,
                     const mtx_model_desc *model, const mtx_optim_desc *opt);
 
@@ -127,9 +126,11 @@ mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t ui
 mtx_status mtx_workspace_bytes(const mtx_ctx *ctx, uint64_t *bytes);
 
 /* Lends the context a device buffer of >= mtx_workspace_bytes bytes (borrowed,
- * 256-byte aligned).  Carves it and runs the seeded per-rank initialisation
- * (O2: Glorot-uniform weights from SplitMix64 keyed by init_seed + rank, zero
- * biases, zero velocity) on the context stream; synchronous. */
+ * 256-byte aligned).  Carves it, runs the seeded per-rank initialisation (O2:
+ * Glorot-uniform weights from SplitMix64 keyed by init_seed + rank, zero
+ * biases, zero velocity) and -- collective when world > 1 -- checks by an NCCL
+ * allgather of a 64-bit digest that every rank passed the same model/optimiser
+ * description (mismatch: MTX_ERR_PROTOCOL).  Synchronous. */
 mtx_status mtx_bind_workspace(mtx_ctx *ctx, void *dev_ptr, uint64_t bytes);
 
 /* Number of parameters N in canonical (unpadded) order. */
@@ -219,6 +220,17 @@ mtx_status mtx_set_timing(mtx_ctx *ctx, int32_t enable);
  * the last reset; names is a '\n'-separated list (written into names_buf).  Synchronous. */
 mtx_status mtx_read_timing(mtx_ctx *ctx, char *names_buf, uint64_t names_len, double *ms, int64_t *counts,
                            int32_t max_sites, int32_t *n_sites, int32_t reset);
+
+/* Diagnostic: one local contraction through a chosen engine (0 = SIMT fp32, 1 =
+ * tcgen05 TF32), exactly as the step issues it -- C[M,N] = op(A) op(B) with
+ * epilogue epi (0 store, 1 +bias then ReLU, 2 +bias, 3 x [mask > 0]); ta/tb as
+ * in the step's forward (0,0), dgrad (0,1) and wgrad (1,0) layouts.  Device
+ * pointers, row-major fp32, leading dimensions in elements.  Used by the
+ * kernel-level parity tests; MTX_ERR_UNSUPPORTED if the engine cannot take the
+ * shape/layout. */
+mtx_status mtx_debug_gemm(mtx_ctx *ctx, int32_t engine, int32_t M, int32_t N, int32_t K, int32_t ta, int32_t tb,
+                          int32_t epi, const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc,
+                          const float *bias, const float *mask, int64_t ldm, void *stream);
 
 /* Short description of the build (arch, NCCL version, GEMM engine). */
 const char *mtx_build_info(void);

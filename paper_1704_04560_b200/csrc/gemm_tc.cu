@@ -1,11 +1,448 @@
-// gemm_tc.cu -- placeholder until the tcgen05 engine lands (see gemm_tc.h).
+// gemm_tc.cu -- the TF32 tensor-core GEMM engine of the local forward/backward
+// (the dense contractions of each replica's step; SURVEY.md
+// §8(a) a4/a6/a7).  sm_100a only: 5th-gen tensor cores through tcgen05.
+//
+//   * persistent CTAs (<= one per SM), static round-robin over (m, n, k-split) tiles
+//   * warp 0: TMA producer -- cp.async.bulk.tensor (SWIZZLE_128B) into a STAGES-deep
+//     shared-memory ring, completion on mbarriers (expect_tx)
+//   * warp 1: MMA issuer -- one elected thread issues tcgen05.mma.cta_group::1.kind::tf32
+//     (M = 128, N = BN, K = 8 per instruction) into a TMEM accumulator; tcgen05.commit
+//     frees the smem slot and, after the last k-block, signals the epilogue
+//   * warp 2: TMEM allocator (2 accumulators x BN columns -> epilogue/mainloop overlap)
+//   * warps 4-7: epilogue -- tcgen05.ld 32x32b (one accumulator row per thread), fused
+//     bias + ReLU (forward), ReLU mask (dgrad) or plain/partial store (wgrad)
+//
+// Operands are read in place from the row-major activation/weight/gradient
+// buffers: K-major (rows contiguous in K) or MN-major (contiguous in M/N) via the
+// UMMA shared-memory descriptor's major bit, so forward, dgrad and wgrad need no
+// transposes.  Accumulation is fp32 in TMEM; fp32 operands are consumed as TF32.
+#include <cuda.h>
+#include <stdio.h>
+
+#include <algorithm>
+
 #include "gemm_tc.h"
 
 namespace mtx {
-struct TcGemm {};
-bool tc_available() { return false; }
-TcGemm *tc_create(int) { return nullptr; }
+namespace {
+
+constexpr int BM = 128, BK = 32, NTHREADS = 256, STAGES = 4;
+constexpr uint32_t TILE_A_BYTES = BM * BK * 4;  // 16 KB
+
+template <int BN>
+struct SmemLayout {
+    static constexpr uint32_t A_BYTES = TILE_A_BYTES;
+    static constexpr uint32_t B_BYTES = BN * BK * 4;
+    static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr uint32_t TOTAL = BAR_OFF + 256 + 1024;  // barriers + tmem slot + 1024-B alignment slack
+    static constexpr uint32_t TMEM_COLS = 2 * BN;            // double-buffered accumulator
+};
+
+struct TcParams {
+    CUtensorMap ta;
+    CUtensorMap tb;
+    int M, N, K;
+    int a_mn, b_mn;      // operand majorness (1 = MN-major)
+    int tiles_m, tiles_n, splits, kb_total, kb_per_split;
+    int epi;
+    const float *bias;
+    const float *mask;
+    int64_t ldm;
+    float *C;
+    int64_t ldc;
+    float *partial;
+    const int64_t *a_win;  // dataset operand: sample-dimension offset read on the device
+    int64_t a_base;
+};
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            dst),
+        "l"((uint64_t)map), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+            d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+#define TMEM_LD32(taddr, r)                                                                                      \
+    asm volatile(                                                                                                \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                            \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),          \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),    \
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),  \
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])   \
+        : "r"(taddr))
+
+// UMMA shared-memory descriptor, version 1 (sm_100).  Verified on B200 with tools/tc_probe.cu:
+//   K-major : SWIZZLE_128B (type 2) -- 8-row x 128-B atoms (16-B chunks XOR row%8) stacked along
+//             M/N at SBO = 1024 B; LBO unused.  k-step of 8 tf32 = +32 B inside the row.
+//   MN-major: SWIZZLE_128B_BASE32B (type 1, the only MN-major layout tf32 accepts) -- 128-B rows
+//             of 32 M/N elements, 32-B chunks XOR row%4; 4-row K groups at SBO = 512 B, 32-element
+//             M/N groups at LBO = BK * 128 B.  k-step of 8 = +1024 B.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                              uint32_t layout_type) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // version
+    d |= (uint64_t)layout_type << 61;
+    return d;
+}
+
+// Instruction descriptor: D fp32, A/B tf32, majors, N>>3, M>>4 (kind::tf32, dense).
+__host__ __device__ constexpr uint32_t instr_desc(int M, int N, int a_mn, int b_mn) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
+    using L = SmemLayout<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    // SWIZZLE_128B atoms need 1024-B aligned stage buffers
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const uint32_t sbase = smem_u32(smem);
+    uint64_t *bars = (uint64_t *)(smem + L::BAR_OFF);
+    // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]
+    const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * STAGES, tfull0 = empty0 + 8 * STAGES,
+                   tempty0 = tfull0 + 16;
+    uint32_t *tmem_slot = (uint32_t *)(smem + L::BAR_OFF + 128);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&p.ta) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&p.tb) : "memory");
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; a++) {
+            mbar_init(tfull0 + 8 * a, 1);
+            mbar_init(tempty0 + 8 * a, 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(L::TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int tiles_mn = p.tiles_m * p.tiles_n;
+    const int total = tiles_mn * p.splits;
+
+    if (warp == 0) {
+        // ================= TMA producer
+        if (lane == 0) {
+            const int64_t row0 = p.a_win ? (*p.a_win + p.a_base) : 0;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int z = t / tiles_mn, r = t % tiles_mn;
+                const int m0 = (r % p.tiles_m) * BM, n0 = (r / p.tiles_m) * BN;
+                const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+                for (int kb = kb0; kb < kb1; kb++) {
+                    mbar_wait(empty0 + 8 * stage, phase ^ 1);
+                    const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::A_BYTES;
+                    const uint32_t fb = full0 + 8 * stage;
+                    mbar_expect_tx(fb, L::STAGE_BYTES);
+                    const int k0 = kb * BK;
+                    if (!p.a_mn) {
+                        tma_load_2d(sa, &p.ta, fb, k0, (int)(row0 + m0));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BM / 32; j++) tma_load_2d(sa + j * 4096, &p.ta, fb, m0 + 32 * j, (int)(row0 + k0));
+                    }
+                    if (!p.b_mn) {
+                        tma_load_2d(sb, &p.tb, fb, k0, n0);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BN / 32; j++) tma_load_2d(sb + j * 4096, &p.tb, fb, n0 + 32 * j, k0);
+                    }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer (single thread)
+        if (lane == 0) {
+            const uint32_t idesc = instr_desc(BM, BN, p.a_mn, p.b_mn);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int z = t / tiles_mn;
+                const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+                mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = kb0; kb < kb1; kb++) {
+                    mbar_wait(full0 + 8 * stage, phase);
+                    tc_fence_after();
+                    const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 8; kk++) {
+                        // K-major: advance 8 elements = 32 B inside the 128-B swizzled row;
+                        // MN-major: advance one 8-row K group = 1024 B.
+                        const uint64_t ad = p.a_mn ? smem_desc(sa + kk * 1024, BK * 128, 512, 1)
+                                                   : smem_desc(sa + kk * 32, 16, 1024, 2);
+                        const uint64_t bd = p.b_mn ? smem_desc(sb + kk * 1024, BK * 128, 512, 1)
+                                                   : smem_desc(sb + kk * 32, 16, 1024, 2);
+                        umma_tf32(d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(empty0 + 8 * stage);  // frees the smem slot when these MMAs retire
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                umma_commit(tfull0 + 8 * acc);  // accumulator ready for the epilogue
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (warp >= 4) {
+        // ================= epilogue: TMEM -> registers -> global
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            const int z = t / tiles_mn, r = t % tiles_mn;
+            const int m0 = (r % p.tiles_m) * BM, n0 = (r / p.tiles_m) * BN;
+            mbar_wait(tfull0 + 8 * acc, acc_phase);
+            tc_fence_after();
+            const int m = m0 + 32 * q + lane;
+            const bool row_ok = m < p.M;
+            float *dst_row = p.splits > 1 ? p.partial + ((int64_t)z * p.M + m) * p.N : p.C + (int64_t)m * p.ldc;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; c++) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(32 * q) << 16) + 32 * c;
+                TMEM_LD32(taddr, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (!row_ok) continue;
+                const int nb = n0 + 32 * c;
+#pragma unroll
+                for (int g4 = 0; g4 < 8; g4++) {
+                    const int n = nb + 4 * g4;
+                    if (n >= p.N) break;
+                    float o[4] = {__uint_as_float(v[4 * g4]), __uint_as_float(v[4 * g4 + 1]),
+                                  __uint_as_float(v[4 * g4 + 2]), __uint_as_float(v[4 * g4 + 3])};
+                    if (p.splits == 1) {
+                        if (p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) {
+#pragma unroll
+                            for (int e = 0; e < 4; e++)
+                                if (n + e < p.N) {
+                                    o[e] += p.bias[n + e];
+                                    if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e], 0.f);
+                                }
+                        } else if (p.epi == EPI_MASK) {
+#pragma unroll
+                            for (int e = 0; e < 4; e++)
+                                if (n + e < p.N && !(p.mask[(int64_t)m * p.ldm + n + e] > 0.f)) o[e] = 0.f;
+                        }
+                    }
+                    if (n + 3 < p.N) {
+                        *(float4 *)(dst_row + n) = make_float4(o[0], o[1], o[2], o[3]);
+                    } else {
+                        for (int e = 0; e < 4 && n + e < p.N; e++) dst_row[n + e] = o[e];
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(L::TMEM_COLS)
+                     : "memory");
+    }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// Row-major fp32 matrix [rows][cols] (row pitch ld elements), box = 32 cols x box_rows.
+// K-major operands use the 128-B swizzle (16-B atoms), MN-major ones the 128-B swizzle with
+// 32-B atoms, matching the UMMA descriptors above.
+bool make_map(EncodeTiled enc, CUtensorMap *m, const float *ptr, int64_t rows, int64_t cols, int64_t ld,
+              int box_rows, bool mn_major) {
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)ptr, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+struct TcGemm {
+    EncodeTiled encode = nullptr;
+    int sms = 148;
+    bool attr_set[2] = {false, false};
+};
+
+bool tc_available() { return true; }
+
+TcGemm *tc_create(int device) {
+    TcGemm *t = new TcGemm();
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+        q != cudaDriverEntryPointSuccess) {
+        delete t;
+        return nullptr;
+    }
+    t->encode = (EncodeTiled)fn;
+    cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, device);
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    if (major != 10) {  // tcgen05 exists on sm_100 only
+        delete t;
+        return nullptr;
+    }
+    return t;
+}
+
 void tc_destroy(TcGemm *t) { delete t; }
-bool tc_supports(TcGemm *, const GemmDesc &) { return false; }
-cudaError_t tc_gemm(TcGemm *, const GemmDesc &, cudaStream_t, LaunchHook *) { return cudaErrorNotSupported; }
+
+static bool al16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+bool tc_supports(TcGemm *t, const GemmDesc &g) {
+    if (!t) return false;
+    const int M = g.aug ? g.M - 1 : g.M;
+    if (M < 1 || g.N < 16 || g.K < 1) return false;
+    if (g.lda % 4 || g.ldb % 4 || g.ldc % 4 || !al16(g.A) || !al16(g.B) || !al16(g.C)) return false;
+    if (g.epi == EPI_MASK && (g.ldm % 4 || !al16(g.mask))) return false;
+    // dataset operand with the sample dimension along K: its k-blocks must not run into the next rank's rows
+    if (g.ta && g.arow.win && g.K % BK) return false;
+    if (g.arow.win && g.a_rows_total <= 0) return false;
+    return true;
+}
+
+cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h) {
+    const int M = g.aug ? g.M - 1 : g.M;  // the bias row of an augmented wgrad is a column sum (SIMT, below)
+    const int N = g.N, K = g.K;
+    constexpr int BN = 128;
+    TcParams p{};
+    p.M = M; p.N = N; p.K = K;
+    p.a_mn = g.ta ? 1 : 0;
+    p.b_mn = g.tb ? 0 : 1;  // B stored [K][N] (tb == false) is MN-major
+    // operand A: K-major [M rows][K] or MN-major stored [K rows][M]; the dataset operand's tensor map
+    // spans the whole wrap-extended buffer (rows are offset on the device by a_win + a_base).
+    const int64_t a_rows_total = g.a_rows_total;
+    bool ok;
+    if (!g.ta) ok = make_map(t->encode, &p.ta, g.A, g.arow.win ? a_rows_total : M, K, g.lda, BM, false);
+    else ok = make_map(t->encode, &p.ta, g.A, g.arow.win ? a_rows_total : K, M, g.lda, BK, true);
+    if (!ok) return cudaErrorInvalidValue;
+    if (g.tb) ok = make_map(t->encode, &p.tb, g.B, N, K, g.ldb, BN, false);  // [N][K], K-major
+    else ok = make_map(t->encode, &p.tb, g.B, K, N, g.ldb, BK, true);         // [K][N], MN-major
+    if (!ok) return cudaErrorInvalidValue;
+    p.a_win = g.arow.win;
+    p.a_base = g.arow.base;
+    p.tiles_m = (M + BM - 1) / BM;
+    p.tiles_n = (N + BN - 1) / BN;
+    p.kb_total = (K + BK - 1) / BK;
+    const int tiles = p.tiles_m * p.tiles_n;
+    int splits = 1;
+    if (g.epi == EPI_STORE && g.partial && tiles < t->sms && N % 4 == 0) {  // wgrad: split K to fill the SMs (deterministic fold)
+        splits = std::min(t->sms / tiles, std::max(1, p.kb_total / 4));
+        while (splits > 1 && (int64_t)splits * M * N > g.partial_cap) splits--;
+    }
+    p.kb_per_split = (p.kb_total + splits - 1) / splits;
+    splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+    p.splits = splits;
+    p.epi = g.epi;
+    p.bias = g.bias;
+    p.mask = g.mask;
+    p.ldm = g.ldm;
+    p.C = g.C;
+    p.ldc = g.ldc;
+    p.partial = g.partial;
+    const int total = tiles * splits;
+    const int grid = std::min(total, t->sms);
+    constexpr uint32_t smem = SmemLayout<BN>::TOTAL;
+    if (!t->attr_set[0]) {
+        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        t->attr_set[0] = true;
+    }
+    const char *kind = g.epi == EPI_MASK ? "gemm_tc_dgrad" : (g.ta ? "gemm_tc_wgrad" : "gemm_tc_fwd");
+    char name[96];
+    snprintf(name, sizeof name, "%s[M=%d,N=%d,K=%d,splits=%d]", kind, M, N, K, splits);
+    if (h) h->before(name, s);
+    tc_gemm_kernel<BN><<<grid, NTHREADS, smem, s>>>(p);
+    if (h) h->after(name, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (splits > 1) {
+        e = splitk_reduce(g.partial, splits, M, N, g.C, g.ldc, s, h);
+        if (e != cudaSuccess) return e;
+    }
+    if (g.aug) {  // bias gradient row: db[n] = sum_k B[k][n]  (ones row of the augmented A)
+        GemmDesc cs;
+        cs.M = 1; cs.N = N; cs.K = K;
+        cs.ta = true; cs.aug = true;
+        cs.A = g.A; cs.lda = g.lda;
+        cs.B = g.B; cs.ldb = g.ldb;
+        cs.C = g.C + (int64_t)M * g.ldc; cs.ldc = g.ldc;
+        int64_t tiles_cs = (N + 63) / 64;
+        cs.splits = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(296 / tiles_cs, K / 256),
+                                                                 g.partial_cap / std::max(1, N)));
+        cs.partial = g.partial;
+        e = gemm_simt(cs, s, h);  // partial is free again: the fold above precedes it in stream order
+    }
+    return e;
+}
+
 }  // namespace mtx

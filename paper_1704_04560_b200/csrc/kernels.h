@@ -32,6 +32,8 @@ struct GemmDesc {
     int64_t ldm = 0;
     int splits = 1;
     float *partial = nullptr;
+    int64_t partial_cap = 0;  // floats available at partial (engines may choose their own split count)
+    int64_t a_rows_total = 0; // rows of the buffer behind A when arow.win is set (wrap-extended dataset)
 };
 
 // Launch-site hook: the API layer brackets every launch with it (timing/counting).
@@ -42,6 +44,10 @@ struct LaunchHook {
 };
 
 cudaError_t gemm_simt(const GemmDesc &g, cudaStream_t s, LaunchHook *h);
+
+// C[m][n] = sum_{z ascending} partial[z][m][n]  (deterministic split-K fold)
+cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float *C, int64_t ldc, cudaStream_t s,
+                          LaunchHook *h);
 
 // Fused last layer: logits = A W + b (W,b = augmented [(d+1)][C] block), mean
 // softmax-CE, dZ_L = (softmax - onehot)/b, loss per row, and (if dprev) the

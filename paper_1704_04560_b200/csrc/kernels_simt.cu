@@ -170,15 +170,19 @@ cudaError_t gemm_simt(const GemmDesc &g, cudaStream_t s, LaunchHook *h) {
     else if (g.ta && !g.tb && !g.aug && part) launch_gemm<true, false, EPI_STORE, false, true>(g, grid, s);
     else return cudaErrorInvalidValue;
     if (h) h->after(name, s);
-    if (part) {
-        int64_t total = (int64_t)g.M * g.N;
-        unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 8);
-        char rn[64];
-        snprintf(rn, sizeof rn, "splitk_reduce[M=%d,N=%d,splits=%d]", g.M, g.N, g.splits);
-        if (h) h->before(rn, s);
-        splitk_reduce_kernel<<<blocks, 256, 0, s>>>(g.partial, g.splits, g.M, g.N, g.C, g.ldc);
-        if (h) h->after(rn, s);
-    }
+    if (part) return splitk_reduce(g.partial, g.splits, g.M, g.N, g.C, g.ldc, s, h);
+    return cudaGetLastError();
+}
+
+cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float *C, int64_t ldc, cudaStream_t s,
+                          LaunchHook *h) {
+    int64_t total = (int64_t)M * N;
+    unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8));
+    char rn[64];
+    snprintf(rn, sizeof rn, "splitk_reduce[M=%d,N=%d,splits=%d]", M, N, splits);
+    if (h) h->before(rn, s);
+    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(partial, splits, M, N, C, ldc);
+    if (h) h->after(rn, s);
     return cudaGetLastError();
 }
 

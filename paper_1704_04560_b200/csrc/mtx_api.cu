@@ -366,7 +366,10 @@ struct Runner {
     bool staged;
     LaunchHook *h;
 
-    mtx_status gemm(const GemmDesc &g) {
+    mtx_status gemm(GemmDesc g) {
+        g.partial = c->partial;
+        g.partial_cap = c->partial_floats;
+        if (g.arow.win) g.a_rows_total = c->n_data + c->B;
         cudaError_t e;
         if (c->opt.precision == MTX_TF32 && c->tc && tc_supports(c->tc, g))
             e = tc_gemm(c->tc, g, s, h);
@@ -422,14 +425,12 @@ struct Runner {
         if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "head: %s", cudaGetErrorString(e));
         e = reduce_sum(c->loss_rows, (int)b, c->grads + c->N_pad, s, h);
         if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "loss reduce: %s", cudaGetErrorString(e));
-        // backward l = L .. 1
+        // backward l = L .. 1.  dgrad(l) reads W_l, so it is issued before wgrad(l) completes the
+        // bucket holding W_l: the bucket's update (comm stream) may then overwrite W_l safely.
         int cur = 0;
         size_t bk = 0;
         for (int l = L; l >= 1; l--) {
             const float *dZ = (l == L) ? c->dzL : c->dz[cur];
-            const float *Aprev = l == 1 ? xbase() : c->acts[l - 1];
-            if ((st = wgrad(l - 1, Aprev, l == 1 ? xrow() : RowSel{nullptr, 0}, dZ))) return st;
-            if ((st = bucket_ready(l - 1, bk))) return st;
             if (l < L && l > 1) {
                 // dZ_{l-1} = (dZ_l W_l^T) .* [A_{l-1} > 0]
                 const Layer &Ly = c->layers[l - 1];
@@ -441,8 +442,11 @@ struct Runner {
                 g.mask = c->acts[l - 1]; g.ldm = d[l - 1];
                 g.C = c->dz[cur ^ 1]; g.ldc = d[l - 1];
                 if ((st = gemm(g))) return st;
-                cur ^= 1;
             }
+            const float *Aprev = l == 1 ? xbase() : c->acts[l - 1];
+            if ((st = wgrad(l - 1, Aprev, l == 1 ? xrow() : RowSel{nullptr, 0}, dZ))) return st;
+            if ((st = bucket_ready(l - 1, bk))) return st;
+            if (l < L && l > 1) cur ^= 1;
         }
         return MTX_OK;
     }
@@ -900,6 +904,34 @@ mtx_status mtx_read_timing(mtx_ctx *c, char *names_buf, uint64_t names_len, doub
     *n_sites = i;
     snprintf(names_buf, names_len, "%s", names.c_str());
     if (reset) c->hook.acc.clear();
+    return MTX_OK;
+}
+
+mtx_status mtx_debug_gemm(mtx_ctx *c, int32_t engine, int32_t M, int32_t N, int32_t K, int32_t ta, int32_t tb,
+                          int32_t epi, const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc,
+                          const float *bias, const float *mask, int64_t ldm, void *stream) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (c->state == mtx_ctx::S_INIT) return fail(c, MTX_ERR_STATE, "bind the workspace first");
+    if (M < 1 || N < 1 || K < 1 || !A || !B || !C || epi < 0 || epi > 3) return fail(c, MTX_ERR_INVALID_ARG, "bad gemm");
+    GemmDesc g;
+    g.M = M; g.N = N; g.K = K;
+    g.ta = ta != 0; g.tb = tb != 0; g.epi = epi;
+    g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
+    g.bias = bias; g.mask = mask; g.ldm = ldm;
+    g.partial = c->partial;
+    g.partial_cap = c->partial_floats;
+    cudaStream_t s = pick(c, stream);
+    cudaError_t e;
+    if (engine == 1) {
+        if (!c->tc) c->tc = tc_create(c->device);
+        if (!tc_supports(c->tc, g)) return fail(c, MTX_ERR_UNSUPPORTED, "tcgen05 engine: unsupported shape/layout");
+        e = tc_gemm(c->tc, g, s, &c->hook);
+    } else {
+        if (g.ta && g.epi != EPI_STORE) return fail(c, MTX_ERR_UNSUPPORTED, "simt: wgrad layout takes no epilogue");
+        e = gemm_simt(g, s, &c->hook);
+    }
+    CK(e);
     return MTX_OK;
 }
 

@@ -72,6 +72,8 @@ def _load():
         "mtx_set_timing": [vp, C.c_int32],
         "mtx_read_timing": [vp, C.c_char_p, C.c_uint64, C.POINTER(C.c_double), i64, C.c_int32, i32, C.c_int32],
         "mtx_finalize": [vp],
+        "mtx_debug_gemm": [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp,
+                           C.c_int64, vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_int64, vp],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -222,6 +224,16 @@ def mtx_read_timing(ctx, reset: bool = True) -> dict:
     _check(_lib.mtx_read_timing(ctx, names, 8192, ms, cnt, 64, C.byref(n), int(reset)), ctx, "mtx_read_timing")
     keys = names.value.decode().split("\n")[: n.value]
     return {k: (ms[i], cnt[i]) for i, k in enumerate(keys)}
+
+
+def mtx_debug_gemm(ctx, engine, M, N, K, ta, tb, epi, A, lda, B, ldb, C, ldc, bias=None, mask=None, ldm=0,
+                   stream=None):
+    _check(_lib.mtx_debug_gemm(ctx, engine, M, N, K, ta, tb, epi, C_ptr(A), lda, C_ptr(B), ldb, C_ptr(C), ldc,
+                               C_ptr(bias), C_ptr(mask), ldm, C_ptr(stream)), ctx, "mtx_debug_gemm")
+
+
+def C_ptr(x):
+    return C.c_void_p(x)
 
 
 def mtx_last_error(ctx) -> str:

@@ -1,0 +1,145 @@
+"""Multi-rank GPU parity worker, launched by tests/test_multigpu.py under torchrun
+(one process per GPU, NCCL data path, gloo for the uid and result exchange).
+
+Checks, per rank, against the oracle's DP(P) simulation:
+  * Global Broadcast: before it, replicas initialised with init_seed + r differ
+    (negative control); after it, every rank's parameters are bitwise rank
+    0's oracle init.
+  * Replica identity I2: the parameter/velocity digest is equal on all ranks after
+    every step.
+  * I1 across implementations: GPU DP(P) losses and weights vs oracle DP(P) within
+    the tier tolerance; the reduced gradient G vs the oracle's fold.
+  * The averaging operator on dyadic gradients is bit-exact vs the oracle (any
+    summation order is exact on those inputs, A2).
+  * MTX_REDUCE_ORDERED reproduces the NCCL result bitwise at P = 2 (addition commutes).
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import traceback
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import mtx_synth as S  # noqa: E402
+import oracle  # noqa: E402
+import paper_1704_04560_b200 as P  # noqa: E402
+from paper_1704_04560_b200 import mtx  # noqa: E402
+from tests._util import TOL, maxrel, per_tensor_maxrel  # noqa: E402
+
+
+def allgather_obj(x):
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, x)
+    return out
+
+
+def check(cond, msg):
+    if not cond:
+        raise AssertionError(msg)
+
+
+def run_model(rank, world, cfg, X, y, steps, precision, reduce=P.MTX_REDUCE_NCCL, bucket=256 << 10):
+    uid = P.nccl_uid_broadcast(rank, world)
+    r = P.Replica(cfg, rank=rank, world=world, uid=uid, device=rank, precision=precision, reduce=reduce,
+                  bucket_bytes=bucket)
+    try:
+        d0 = allgather_obj(r.digest())
+        check(len(set(d0)) == world, "replicas should differ before the broadcast (distinct init seeds)")
+        r.bcast()
+        net = oracle.Net.from_cfg(cfg)
+        w0 = r.get()
+        check(np.array_equal(w0.view(np.uint32), oracle.init_params(net, 42).view(np.uint32)),
+              f"rank {rank}: params after broadcast != oracle rank-0 init")
+        r.shard(X, y)
+        out = []
+        for t in range(steps):
+            loss = r.step(want_loss=True)
+            dg = allgather_obj(r.digest())
+            check(len(set(dg)) == 1, f"step {t}: replica digests differ {dg}")
+            out.append((loss, r.get(P.MTX_BUF_GRADS), r.get(P.MTX_BUF_PARAMS)))
+        return out
+    finally:
+        r.close()
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(rank)
+    report = {"rank": rank, "world": world, "checks": []}
+    try:
+        # ---- averaging operator on dyadic gradients: bit-exact vs oracle fold + update
+        cfg_tiny = dict(S.CONFIGS["cfg1"], B=4 * world)
+        uid = P.nccl_uid_broadcast(rank, world)
+        r = P.Replica(cfg_tiny, rank=rank, world=world, uid=uid, device=rank)
+        for n in (1000, (1 << 20) + 3, 61_100_840 // 16):
+            g_all = np.stack([S.cfg5_grad_dyadic(1, q, n) for q in range(world)])
+            w = S.cfg5_params(1, n)
+            v = S.cfg5_velocity(1, n)
+            Gd = torch.from_numpy(g_all[rank].copy()).cuda()
+            wd = torch.from_numpy(w.copy()).cuda()
+            vd = torch.from_numpy(v.copy()).cuda()
+            torch.cuda.synchronize()
+            mtx.mtx_allreduce_avg(r.ctx, Gd.data_ptr(), wd.data_ptr(), vd.data_ptr(), n, 0.01, 0.9, 1, r.s)
+            r.sync()
+            G = oracle.fold(g_all)
+            wo, vo = w.copy(), v.copy()
+            oracle.avg_update(G, wo, vo, world, 0.01, 0.9)
+            check(np.array_equal(Gd.cpu().numpy().view(np.uint32), G.view(np.uint32)), f"allreduce n={n}")
+            check(np.array_equal(wd.cpu().numpy().view(np.uint32), wo.view(np.uint32)), f"update w n={n}")
+            check(np.array_equal(vd.cpu().numpy().view(np.uint32), vo.view(np.uint32)), f"update v n={n}")
+        r.close()
+        report["checks"].append("allreduce_avg dyadic bit-exact")
+
+        # ---- the training step, DP(P) vs oracle DP(P)
+        precisions = [P.MTX_FP32] + ([P.MTX_TF32] if "tcgen05" in mtx.mtx_build_info() else [])
+        for prec in precisions:
+            tol = TOL[prec]
+            for name, B, steps in (("cfg1", 64, 5), ("cfg2", 512, 3)):
+                cfg = dict(S.CONFIGS[name], B=B)
+                X, y = S.mnist_like(1, 1000 if name == "cfg1" else 4096)
+                gpu = run_model(rank, world, cfg, X, y, steps, prec)
+                recs, w_ref, _ = oracle.train(oracle.Net.from_cfg(cfg), X, y, B, world, steps, cfg["lr"], cfg["mu"],
+                                              42, keep_grads=True)
+                tab = oracle.tensor_table(oracle.Net.from_cfg(cfg))
+                for t, (rec, (loss, G, _)) in enumerate(zip(recs, gpu)):
+                    check(abs(loss - rec.loss) <= tol * abs(rec.loss), f"{name} step {t} loss {loss} vs {rec.loss}")
+                    e = max(per_tensor_maxrel(G, rec.G, tab))
+                    check(e <= 5 * tol, f"{name} step {t} G err {e}")
+                e = maxrel(gpu[-1][2], w_ref)
+                check(e <= tol, f"{name} weights err {e}")
+                report["checks"].append(f"{name} DP({world}) prec={prec} vs oracle ok")
+        # ---- ORDERED reduce reproduces NCCL at P = 2
+        if world == 2:
+            cfg = dict(S.CONFIGS["cfg1"], B=64)
+            X, y = S.mnist_like(1, 1000)
+            a = run_model(rank, world, cfg, X, y, 2, P.MTX_FP32, P.MTX_REDUCE_NCCL)
+            b = run_model(rank, world, cfg, X, y, 2, P.MTX_FP32, P.MTX_REDUCE_ORDERED)
+            for (la, Ga, wa), (lb, Gb, wb) in zip(a, b):
+                check(np.array_equal(Ga.view(np.uint32), Gb.view(np.uint32)), "ORDERED != NCCL G at P=2")
+                check(np.array_equal(wa.view(np.uint32), wb.view(np.uint32)), "ORDERED != NCCL w at P=2")
+            report["checks"].append("ordered == nccl at P=2")
+        report["ok"] = True
+    except Exception:  # noqa: BLE001
+        report["ok"] = False
+        report["error"] = traceback.format_exc()
+    reports = allgather_obj(report)
+    if rank == 0:
+        path = os.environ.get("MTX_MP_REPORT")
+        if path:
+            json.dump(reports, open(path, "w"), indent=1)
+        print(json.dumps(reports, indent=1))
+    dist.destroy_process_group()
+    sys.exit(0 if all(r["ok"] for r in reports) else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,76 @@
+"""Kernel-level parity of the local contractions (both engines) against the
+definition C = op(A) op(B) (+ epilogue) computed in float64 by numpy, for the
+three layouts the step issues: forward (A, B row-major), dgrad (B transposed)
+and wgrad (A transposed), with ragged edges and several tiles."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import mtx_synth as S  # noqa: E402
+import paper_1704_04560_b200 as P  # noqa: E402
+from paper_1704_04560_b200 import mtx  # noqa: E402
+from tests._util import maxrel  # noqa: E402
+
+TC = "tcgen05" in mtx.mtx_build_info()
+
+
+@pytest.fixture(scope="module")
+def rep():
+    r = P.Replica(dict(S.CONFIGS["cfg4"], B=1024), precision=P.MTX_TF32 if TC else P.MTX_FP32)
+    yield r
+    r.close()
+
+
+SHAPES = [  # (M, N, K) incl. the step's shapes: cfg4 fwd/dgrad/wgrad, cfg2, K = 28, ragged M/N/K
+    (1024, 1024, 1024), (512, 512, 784), (8192, 1024, 28), (28, 1024, 2048), (300, 200, 100), (128, 64, 96),
+    (1000, 384, 520),
+]
+
+
+def _run(rep, engine, M, N, K, ta, tb, epi, rng):
+    A = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+    bias = rng.standard_normal(N).astype(np.float32)
+    mask = np.maximum(rng.standard_normal((M, N)), 0).astype(np.float32)
+    d = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    Ad, Bd, bd, md = d(A), d(B), d(bias), d(mask)
+    Cd = torch.full((M, N), np.nan, device="cuda")
+    torch.cuda.synchronize()
+    mtx.mtx_debug_gemm(rep.ctx, engine, M, N, K, ta, tb, epi, Ad.data_ptr(), M if ta else K, Bd.data_ptr(),
+                       K if tb else N, Cd.data_ptr(), N, bd.data_ptr(), md.data_ptr(), N, rep.s)
+    rep.sync()
+    a = A.T.astype(np.float64) if ta else A.astype(np.float64)
+    b = B.T.astype(np.float64) if tb else B.astype(np.float64)
+    ref = a @ b
+    if epi == 1:
+        ref = np.maximum(ref + bias, 0)
+    elif epi == 2:
+        ref = ref + bias
+    elif epi == 3:
+        ref = np.where(mask > 0, ref, 0)
+    return Cd.cpu().numpy(), ref
+
+
+@pytest.mark.parametrize("engine", [0, 1] if TC else [0])
+@pytest.mark.parametrize("layout", [(0, 0, 1), (0, 0, 2), (0, 1, 3), (1, 0, 0)])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_gemm_layouts(rep, engine, layout, shape):
+    ta, tb, epi = layout
+    M, N, K = shape
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    try:
+        C, ref = _run(rep, engine, M, N, K, ta, tb, epi, rng)
+    except P.MtxError as e:
+        if e.status == 9 and engine == 1:
+            pytest.skip("tcgen05 engine does not take this layout")
+        raise
+    assert not np.isnan(C).any()
+    # fp32 tier: blocked fp32 sums; tf32 tier: 10-bit operand mantissas, fp32 accumulation
+    tol = 1e-5 if engine == 0 else 2e-3
+    assert maxrel(C, ref) <= tol * max(1.0, np.sqrt(K / 1024)), maxrel(C, ref)

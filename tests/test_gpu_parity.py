@@ -94,8 +94,8 @@ def test_init_bit_exact(name):
 
 
 # ----------------------------------------------------------------------------- one-step and trajectory parity
-def _gpu_run(cfg, X, y, steps, precision, start=None, start_step=0):
-    r = make(cfg, precision=precision)
+def _gpu_run(cfg, X, y, steps, precision, start=None, start_step=0, **kw):
+    r = make(cfg, precision=precision, **kw)
     try:
         r.bcast()
         if start is not None:
@@ -111,11 +111,11 @@ def _gpu_run(cfg, X, y, steps, precision, start=None, start_step=0):
         r.close()
 
 
-def _check_step(cfg, X, y, precision, step, start):
+def _check_step(cfg, X, y, precision, step, start, **kw):
     """One step from identical params: G and the updated params vs the oracle (P = 1)."""
     net = oracle.Net.from_cfg(cfg)
     tab = oracle.tensor_table(net)
-    (loss, G, w1), = _gpu_run(cfg, X, y, 1, precision, start=start, start_step=step)
+    (loss, G, w1), = _gpu_run(cfg, X, y, 1, precision, start=start, start_step=step, **kw)
     g_ref, lsum = oracle.local_grad(net, start.astype(np.float64), X, y, cfg["B"], step, 0, 1)
     tol = TOL[precision]
     errs = per_tensor_maxrel(G, g_ref, tab)
@@ -159,6 +159,20 @@ def test_cfg2_one_step_and_wrap(precision):
     start = oracle.init_params(oracle.Net.from_cfg(cfg), 42)
     _check_step(cfg, X, y, precision, 0, start)
     _check_step(cfg, X, y, precision, 117, start)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_cfg2_small_buckets_two_steps(precision):
+    """Per-layer buckets: each bucket's update must not race the dgrad that still reads W_l."""
+    cfg = small_cfg("cfg2")
+    X, y = S.mnist_like(1, 4096)
+    net = oracle.Net.from_cfg(cfg)
+    recs, w_ref, _ = oracle.train(net, X, y, 512, 1, 2, cfg["lr"], cfg["mu"], 42, keep_grads=True)
+    gpu = _gpu_run(cfg, X, y, 2, precision, bucket_bytes=64 << 10)
+    tol = TOL[precision]
+    for rec, (loss, G, _) in zip(recs, gpu):
+        assert max(per_tensor_maxrel(G, rec.G, oracle.tensor_table(net))) <= 2 * tol
+    assert maxrel(gpu[-1][2], w_ref) <= tol
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
