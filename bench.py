@@ -108,8 +108,12 @@ def kernel_work(name: str):
     kind, args = m.group(1), dict(kv.split("=") for kv in m.group(2).split(","))
     a = {k: int(v) for k, v in args.items()}
     if kind.startswith("gemm"):
+        if kind.startswith("gemm_tc3x"):  # 3 tf32 MMAs per product: tensor work is 3x the algorithmic flops
+            return "flop", 2 * a["M"] * a["N"] * a["K"], "tensor3x"
         tensor = kind.startswith("gemm_tc")
         return "flop", 2 * a["M"] * a["N"] * a["K"], "tensor" if tensor else "alu"
+    if kind == "colsum":
+        return "byte", 4 * a["K"] * a["N"], "hbm"
     if kind == "avg_update":
         return "byte", (20 if a["v"] else 12) * a["n"], "hbm"
     if kind == "head_softmax_xent":  # read A rows, write dZ_{L-1} (and dZ_L, loss)
@@ -143,6 +147,10 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int):
     elif top["bound"] == "tensor":
         achieved = per_launch_work / per_launch_s / 1e12
         peak, unit = pk["bf16_tflops_sustained"] * TF32_PER_BF16, "TFLOP/s"
+    elif top["bound"] == "tensor3x":  # fp32-equivalent flops vs one third of the tf32 peak
+        achieved = per_launch_work / per_launch_s / 1e12
+        peak, unit = pk["bf16_tflops_sustained"] * TF32_PER_BF16 / 3, "TFLOP/s"
+        top["bound"] = "tensor"
     else:  # fp32 CUDA-core FMA peak at the clock observed under load
         achieved = per_launch_work / per_launch_s / 1e12
         clk = sm_mhz or pk.get("sm_max_mhz", 1965.0)
@@ -190,7 +198,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
-    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "tf32"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "tf32", "3xtf32"])
     ap.add_argument("--impl", default="mtx", choices=["mtx", "reference"])
     ap.add_argument("--bucket-mb", type=float, default=1.0)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -232,7 +240,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     tc_ok = "tcgen05" in mtx.mtx_build_info()
-    prec = {"fp32": P.MTX_FP32, "tf32": P.MTX_TF32}.get(args.precision, P.MTX_TF32 if tc_ok else P.MTX_FP32)
+    prec = {"fp32": P.MTX_FP32, "tf32": P.MTX_TF32, "3xtf32": P.MTX_3XTF32}.get(
+        args.precision, P.MTX_3XTF32 if tc_ok else P.MTX_FP32)
     uid = P.nccl_uid_broadcast(rank, world)
     X, y = S.dataset(cfg)
     rep = P.Replica(cfg, rank=rank, world=world, uid=uid, device=local, precision=prec,
@@ -319,7 +328,8 @@ def main():
         line = {"metric": metric, "value": round(value, 1), "unit": "samples/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 5),
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "tf32" if prec == P.MTX_TF32 else "f32", "data": "synthetic",
+                "dtype": {P.MTX_TF32: "tf32", P.MTX_3XTF32: "f32 (3xtf32 tensor cores)"}.get(prec, "f32"),
+                "data": "synthetic",
                 "config": {"workload": f"{args.config}: {desc(cfg)}", "global_batch": cfg["B"],
                            "local_batch": cfg["B"] // world, "parallelism": f"dp{world}",
                            "bucket_mb": args.bucket_mb, "l2": "flushed (256 MiB write) before every timed step",

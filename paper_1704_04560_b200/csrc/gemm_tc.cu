@@ -26,14 +26,22 @@
 namespace mtx {
 namespace {
 
-constexpr int BM = 128, BK = 32, NTHREADS = 256, STAGES = 4;
-constexpr uint32_t TILE_A_BYTES = BM * BK * 4;  // 16 KB
+constexpr int BM = 128, BK = 32;
 
-template <int BN>
+// Shared-memory plan per variant.  SPLIT (3xTF32) adds a second copy of each stage holding
+// the TF32 residual small = rne_tf32(x - trunc_tf32(x)) written by four splitter warps.
+template <int BN, bool SPLIT>
 struct SmemLayout {
-    static constexpr uint32_t A_BYTES = TILE_A_BYTES;
+    static constexpr int STAGES = SPLIT ? 3 : 6;
+    // warps 0 TMA, 1 MMA, 2 TMEM alloc, 3 spare, 4-11 epilogue (+ 12-15 splitters for SPLIT)
+    static constexpr int THREADS = SPLIT ? 512 : 384;
+    // k-blocks accumulated in TMEM before the epilogue warps promote the partial into fp32
+    // registers (the tensor core's internal accumulation truncates)
+    static constexpr int CHUNK = SPLIT ? 4 : 8;
+    static constexpr uint32_t A_BYTES = BM * BK * 4;
     static constexpr uint32_t B_BYTES = BN * BK * 4;
-    static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;
+    static constexpr uint32_t STAGE_BYTES = RAW_BYTES * (SPLIT ? 2 : 1);
     static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
     static constexpr uint32_t TOTAL = BAR_OFF + 256 + 1024;  // barriers + tmem slot + 1024-B alignment slack
     static constexpr uint32_t TMEM_COLS = 2 * BN;            // double-buffered accumulator
@@ -131,17 +139,18 @@ __host__ __device__ constexpr uint32_t instr_desc(int M, int N, int a_mn, int b_
            ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int BN>
-__global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
-    using L = SmemLayout<BN>;
+template <int BN, bool SPLIT>
+__global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
+    using L = SmemLayout<BN, SPLIT>;
+    constexpr int STAGES = L::STAGES;
     extern __shared__ uint8_t smem_raw[];
     // SWIZZLE_128B atoms need 1024-B aligned stage buffers
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t sbase = smem_u32(smem);
     uint64_t *bars = (uint64_t *)(smem + L::BAR_OFF);
-    // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]
+    // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2], split[STAGES]
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * STAGES, tfull0 = empty0 + 8 * STAGES,
-                   tempty0 = tfull0 + 16;
+                   tempty0 = tfull0 + 16, split0 = tempty0 + 16;
     uint32_t *tmem_slot = (uint32_t *)(smem + L::BAR_OFF + 128);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -154,8 +163,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         }
         for (int a = 0; a < 2; a++) {
             mbar_init(tfull0 + 8 * a, 1);
-            mbar_init(tempty0 + 8 * a, 4);
+            mbar_init(tempty0 + 8 * a, 8);
         }
+        if (SPLIT)
+            for (int s = 0; s < STAGES; s++) mbar_init(split0 + 8 * s, 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -186,7 +197,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
                     mbar_wait(empty0 + 8 * stage, phase ^ 1);
                     const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::A_BYTES;
                     const uint32_t fb = full0 + 8 * stage;
-                    mbar_expect_tx(fb, L::STAGE_BYTES);
+                    mbar_expect_tx(fb, L::RAW_BYTES);
                     const int k0 = kb * BK;
                     if (!p.a_mn) {
                         tma_load_2d(sa, &p.ta, fb, k0, (int)(row0 + m0));
@@ -205,92 +216,151 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
             }
         }
     } else if (warp == 1) {
-        // ================= MMA issuer (single thread)
+        // ================= MMA issuer (single thread).  Each tile's k-range is cut into chunks of
+        // CHUNK k-blocks; chunk i accumulates into TMEM buffer (i & 1) and is handed to the epilogue.
         if (lane == 0) {
             const uint32_t idesc = instr_desc(BM, BN, p.a_mn, p.b_mn);
             int stage = 0;
             uint32_t phase = 0;
-            int acc = 0;
-            uint32_t acc_phase = 0;
+            int buf = 0;
+            uint32_t buf_phase = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 const int z = t / tiles_mn;
                 const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
-                mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
-                tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int kb = kb0; kb < kb1; kb++) {
-                    mbar_wait(full0 + 8 * stage, phase);
+                for (int c0 = kb0; c0 < kb1; c0 += L::CHUNK) {
+                    const int c1 = min(kb1, c0 + L::CHUNK);
+                    mbar_wait(tempty0 + 8 * buf, buf_phase ^ 1);
                     tc_fence_after();
-                    const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::A_BYTES;
+                    const uint32_t d_tmem = tmem_base + buf * BN;
+                    for (int kb = c0; kb < c1; kb++) {
+                        mbar_wait((SPLIT ? split0 : full0) + 8 * stage, phase);
+                        tc_fence_after();
+                        const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::A_BYTES;
 #pragma unroll
-                    for (int kk = 0; kk < BK / 8; kk++) {
-                        // K-major: advance 8 elements = 32 B inside the 128-B swizzled row;
-                        // MN-major: advance one 8-row K group = 1024 B.
-                        const uint64_t ad = p.a_mn ? smem_desc(sa + kk * 1024, BK * 128, 512, 1)
-                                                   : smem_desc(sa + kk * 32, 16, 1024, 2);
-                        const uint64_t bd = p.b_mn ? smem_desc(sb + kk * 1024, BK * 128, 512, 1)
-                                                   : smem_desc(sb + kk * 32, 16, 1024, 2);
-                        umma_tf32(d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < BK / 8; kk++) {
+                            // K-major: advance 8 elements = 32 B inside the 128-B swizzled row;
+                            // MN-major: advance two 4-row K groups = 1024 B.
+                            const uint64_t ad = p.a_mn ? smem_desc(sa + kk * 1024, BK * 128, 512, 1)
+                                                       : smem_desc(sa + kk * 32, 16, 1024, 2);
+                            const uint64_t bd = p.b_mn ? smem_desc(sb + kk * 1024, BK * 128, 512, 1)
+                                                       : smem_desc(sb + kk * 32, 16, 1024, 2);
+                            const uint32_t acc0 = (kb > c0 || kk > 0) ? 1u : 0u;
+                            if (SPLIT) {
+                                // 3xTF32: big.small + small.big + big.big (big = rne_tf32(x) in place,
+                                // small = rne_tf32(x - big) in the residual buffer)
+                                const uint64_t ads = ad + (uint64_t)(L::RAW_BYTES >> 4),
+                                               bds = bd + (uint64_t)(L::RAW_BYTES >> 4);
+                                umma_tf32(d_tmem, ad, bds, idesc, acc0);
+                                umma_tf32(d_tmem, ads, bd, idesc, 1u);
+                                umma_tf32(d_tmem, ad, bd, idesc, 1u);
+                            } else {
+                                umma_tf32(d_tmem, ad, bd, idesc, acc0);
+                            }
+                        }
+                        umma_commit(empty0 + 8 * stage);  // frees the smem slot when these MMAs retire
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
-                    umma_commit(empty0 + 8 * stage);  // frees the smem slot when these MMAs retire
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    umma_commit(tfull0 + 8 * buf);  // chunk partial ready for promotion
+                    if (++buf == 2) { buf = 0; buf_phase ^= 1; }
                 }
-                umma_commit(tfull0 + 8 * acc);  // accumulator ready for the epilogue
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
-    } else if (warp >= 4) {
-        // ================= epilogue: TMEM -> registers -> global
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
-        int acc = 0;
-        uint32_t acc_phase = 0;
+    } else if (SPLIT && warp >= 12) {
+        // ================= 3xTF32 splitters: big = rne_tf32(x) (in place), small = rne_tf32(x - big)
+        // (same swizzled offset in the residual buffer).  Rounding big to nearest keeps the residuals
+        // sign-symmetric, so the dropped small.small term carries no bias (3xTF32).
+        const int st = threadIdx.x - 384;  // 0..127
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            const int z = t / tiles_mn;
+            const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+            for (int kb = kb0; kb < kb1; kb++) {
+                mbar_wait(full0 + 8 * stage, phase);
+                uint4 *raw = (uint4 *)(smem + stage * L::STAGE_BYTES);
+                uint4 *small = (uint4 *)(smem + stage * L::STAGE_BYTES + L::RAW_BYTES);
+#pragma unroll 4
+                for (int i = st; i < (int)(L::RAW_BYTES / 16); i += 128) {
+                    uint4 v = raw[i], bg, o;
+                    uint32_t *pv = &v.x, *pb = &bg.x, *po = &o.x;
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        uint32_t u = pv[e];
+                        u = (u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u;  // big: round to nearest tf32
+                        pb[e] = u;
+                        uint32_t r = __float_as_uint(__uint_as_float(pv[e]) - __uint_as_float(u));  // exact
+                        po[e] = (r + 0xFFFu + ((r >> 13) & 1u)) & 0xFFFFE000u;
+                    }
+                    raw[i] = bg;
+                    small[i] = o;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> tensor-core proxy
+                __syncwarp();
+                if (lane == 0) mbar_arrive(split0 + 8 * stage);
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp >= 4 && warp < 12) {
+        // ================= epilogue: 8 warps; warp -> (TMEM lane quarter q, column half h).  Each
+        // chunk partial is read from TMEM and added into fp32 registers (IEEE round-to-nearest);
+        // after the tile's last chunk the fused epilogue writes the row segment to global memory.
+        constexpr int HALF = BN / 2;
+        const int q = warp & 3, h = (warp - 4) >> 2;
+        int buf = 0;
+        uint32_t buf_phase = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x) {
             const int z = t / tiles_mn, r = t % tiles_mn;
-            const int m0 = (r % p.tiles_m) * BM, n0 = (r / p.tiles_m) * BN;
-            mbar_wait(tfull0 + 8 * acc, acc_phase);
-            tc_fence_after();
+            const int m0 = (r % p.tiles_m) * BM, n0 = (r / p.tiles_m) * BN + h * HALF;
+            const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+            float acc[HALF];
+            bool first = true;
+            for (int c0 = kb0; c0 < kb1; c0 += L::CHUNK) {
+                mbar_wait(tfull0 + 8 * buf, buf_phase);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < HALF / 32; c++) {
+                    uint32_t v[32];
+                    const uint32_t taddr = tmem_base + buf * BN + ((uint32_t)(32 * q) << 16) + h * HALF + 32 * c;
+                    TMEM_LD32(taddr, v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 32; j++)
+                        acc[32 * c + j] = first ? __uint_as_float(v[j]) : __fadd_rn(acc[32 * c + j], __uint_as_float(v[j]));
+                }
+                first = false;
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
+                if (++buf == 2) { buf = 0; buf_phase ^= 1; }
+            }
             const int m = m0 + 32 * q + lane;
-            const bool row_ok = m < p.M;
+            if (m >= p.M) continue;
             float *dst_row = p.splits > 1 ? p.partial + ((int64_t)z * p.M + m) * p.N : p.C + (int64_t)m * p.ldc;
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; c++) {
-                uint32_t v[32];
-                const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(32 * q) << 16) + 32 * c;
-                TMEM_LD32(taddr, v);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (!row_ok) continue;
-                const int nb = n0 + 32 * c;
 #pragma unroll
-                for (int g4 = 0; g4 < 8; g4++) {
-                    const int n = nb + 4 * g4;
-                    if (n >= p.N) break;
-                    float o[4] = {__uint_as_float(v[4 * g4]), __uint_as_float(v[4 * g4 + 1]),
-                                  __uint_as_float(v[4 * g4 + 2]), __uint_as_float(v[4 * g4 + 3])};
-                    if (p.splits == 1) {
-                        if (p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) {
+            for (int g4 = 0; g4 < HALF / 4; g4++) {
+                const int n = n0 + 4 * g4;
+                if (n >= p.N) break;
+                float o[4] = {acc[4 * g4], acc[4 * g4 + 1], acc[4 * g4 + 2], acc[4 * g4 + 3]};
+                if (p.splits == 1) {
+                    if (p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) {
 #pragma unroll
-                            for (int e = 0; e < 4; e++)
-                                if (n + e < p.N) {
-                                    o[e] += p.bias[n + e];
-                                    if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e], 0.f);
-                                }
-                        } else if (p.epi == EPI_MASK) {
+                        for (int e = 0; e < 4; e++)
+                            if (n + e < p.N) {
+                                o[e] += p.bias[n + e];
+                                if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e], 0.f);
+                            }
+                    } else if (p.epi == EPI_MASK) {
 #pragma unroll
-                            for (int e = 0; e < 4; e++)
-                                if (n + e < p.N && !(p.mask[(int64_t)m * p.ldm + n + e] > 0.f)) o[e] = 0.f;
-                        }
-                    }
-                    if (n + 3 < p.N) {
-                        *(float4 *)(dst_row + n) = make_float4(o[0], o[1], o[2], o[3]);
-                    } else {
-                        for (int e = 0; e < 4 && n + e < p.N; e++) dst_row[n + e] = o[e];
+                        for (int e = 0; e < 4; e++)
+                            if (n + e < p.N && !(p.mask[(int64_t)m * p.ldm + n + e] > 0.f)) o[e] = 0.f;
                     }
                 }
+                if (n + 3 < p.N) {
+                    *(float4 *)(dst_row + n) = make_float4(o[0], o[1], o[2], o[3]);
+                } else {
+                    for (int e = 0; e < 4 && n + e < p.N; e++) dst_row[n + e] = o[e];
+                }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
     tc_fence_before();
@@ -370,8 +440,22 @@ bool tc_supports(TcGemm *t, const GemmDesc &g) {
     return true;
 }
 
+template <int BN, bool SPLIT>
+static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s) {
+    using L = SmemLayout<BN, SPLIT>;
+    const int slot = SPLIT ? 1 : 0;
+    if (!t->attr_set[slot]) {
+        cudaError_t e =
+            cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+        if (e != cudaSuccess) return e;
+        t->attr_set[slot] = true;
+    }
+    tc_gemm_kernel<BN, SPLIT><<<grid, L::THREADS, L::TOTAL, s>>>(p);
+    return cudaGetLastError();
+}
+
 cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h) {
-    const int M = g.aug ? g.M - 1 : g.M;  // the bias row of an augmented wgrad is a column sum (SIMT, below)
+    const int M = g.aug ? g.M - 1 : g.M;  // the bias row of an augmented wgrad is a column sum (below)
     const int N = g.N, K = g.K;
     constexpr int BN = 128;
     TcParams p{};
@@ -395,7 +479,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.kb_total = (K + BK - 1) / BK;
     const int tiles = p.tiles_m * p.tiles_n;
     int splits = 1;
-    if (g.epi == EPI_STORE && g.partial && tiles < t->sms && N % 4 == 0) {  // wgrad: split K to fill the SMs (deterministic fold)
+    if (g.epi == EPI_STORE && g.partial && tiles < t->sms && N % 4 == 0) {  // wgrad: split K to fill the SMs
         splits = std::min(t->sms / tiles, std::max(1, p.kb_total / 4));
         while (splits > 1 && (int64_t)splits * M * N > g.partial_cap) splits--;
     }
@@ -411,37 +495,20 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.partial = g.partial;
     const int total = tiles * splits;
     const int grid = std::min(total, t->sms);
-    constexpr uint32_t smem = SmemLayout<BN>::TOTAL;
-    if (!t->attr_set[0]) {
-        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        t->attr_set[0] = true;
-    }
-    const char *kind = g.epi == EPI_MASK ? "gemm_tc_dgrad" : (g.ta ? "gemm_tc_wgrad" : "gemm_tc_fwd");
+    const char *kind = g.epi == EPI_MASK ? "dgrad" : (g.ta ? "wgrad" : "fwd");
     char name[96];
-    snprintf(name, sizeof name, "%s[M=%d,N=%d,K=%d,splits=%d]", kind, M, N, K, splits);
+    snprintf(name, sizeof name, "gemm_tc%s_%s[M=%d,N=%d,K=%d,splits=%d]", g.tf32x3 ? "3x" : "", kind, M, N, K,
+             splits);
     if (h) h->before(name, s);
-    tc_gemm_kernel<BN><<<grid, NTHREADS, smem, s>>>(p);
+    cudaError_t e = g.tf32x3 ? launch<BN, true>(t, p, grid, s) : launch<BN, false>(t, p, grid, s);
     if (h) h->after(name, s);
-    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (splits > 1) {
         e = splitk_reduce(g.partial, splits, M, N, g.C, g.ldc, s, h);
         if (e != cudaSuccess) return e;
     }
-    if (g.aug) {  // bias gradient row: db[n] = sum_k B[k][n]  (ones row of the augmented A)
-        GemmDesc cs;
-        cs.M = 1; cs.N = N; cs.K = K;
-        cs.ta = true; cs.aug = true;
-        cs.A = g.A; cs.lda = g.lda;
-        cs.B = g.B; cs.ldb = g.ldb;
-        cs.C = g.C + (int64_t)M * g.ldc; cs.ldc = g.ldc;
-        int64_t tiles_cs = (N + 63) / 64;
-        cs.splits = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(296 / tiles_cs, K / 256),
-                                                                 g.partial_cap / std::max(1, N)));
-        cs.partial = g.partial;
-        e = gemm_simt(cs, s, h);  // partial is free again: the fold above precedes it in stream order
-    }
+    if (g.aug)  // bias gradient row: db[n] = sum_k B[k][n]  (the ones row of the augmented A)
+        e = colsum(g.B, K, N, g.ldb, g.C + (int64_t)M * g.ldc, g.partial, g.partial_cap, s, h);
     return e;
 }
 

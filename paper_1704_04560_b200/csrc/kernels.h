@@ -34,6 +34,7 @@ struct GemmDesc {
     float *partial = nullptr;
     int64_t partial_cap = 0;  // floats available at partial (engines may choose their own split count)
     int64_t a_rows_total = 0; // rows of the buffer behind A when arow.win is set (wrap-extended dataset)
+    int tf32x3 = 0;           // tensor-core engine: 3xTF32 (fp32-accurate) instead of 1xTF32
 };
 
 // Launch-site hook: the API layer brackets every launch with it (timing/counting).
@@ -44,6 +45,11 @@ struct LaunchHook {
 };
 
 cudaError_t gemm_simt(const GemmDesc &g, cudaStream_t s, LaunchHook *h);
+
+// out[n] = sum_{k} X[k][n] for X [K][ld] (column sums, e.g. the bias gradient colsum(dZ)):
+// fixed-order per-block sums into partial[z][N], then an ascending-z fold -- deterministic.
+cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *partial, int64_t partial_cap,
+                   cudaStream_t s, LaunchHook *h);
 
 // C[m][n] = sum_{z ascending} partial[z][m][n]  (deterministic split-K fold)
 cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float *C, int64_t ldc, cudaStream_t s,
@@ -69,6 +75,10 @@ cudaError_t avg_update(float *G, float *w, float *v, int64_t n, float invP, floa
 // Ordered reduce (test mode): G[e] = ((g_0[e] + g_1[e]) + ...) + g_{P-1}[e], g_r at gathered + r*stride.
 cudaError_t ordered_fold(const float *gathered, int P, int64_t stride, int64_t n, float *G, cudaStream_t s,
                          LaunchHook *h);
+
+// Busy-waits ~ns nanoseconds on the GPU (timing pass: lets the host enqueue a whole step
+// before the GPU starts, so event pairs bracket device time only).
+cudaError_t gpu_spin(uint64_t ns, cudaStream_t s);
 
 // O2 init of one weight tensor: w[e] = (2u - 1) * lim, u = (H(H(seed, 16+t), e) >> 40) * 2^-24.
 cudaError_t init_glorot(float *w, int64_t n, uint64_t seed, int tensor_index, float lim, cudaStream_t s);

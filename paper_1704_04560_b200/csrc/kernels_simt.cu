@@ -186,6 +186,48 @@ cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float 
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ column sums (bias gradients)
+// Block (32 columns x 8 warps) over a contiguous K range: lane = column (128-B coalesced rows),
+// warp w sums rows k0 + w, k0 + w + 8, ... in order; the 8 warp sums are added in warp order.
+namespace {
+__global__ void __launch_bounds__(256) colsum_kernel(const float *__restrict__ X, int K, int N, int64_t ld,
+                                                     int k_per, float *__restrict__ partial) {
+    __shared__ float sh[8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int n = blockIdx.x * 32 + lane;
+    const int k0 = blockIdx.y * k_per, k1 = min(K, k0 + k_per);
+    float acc = 0.f;
+    if (n < N)
+        for (int k = k0 + w; k < k1; k += 8) acc += X[(int64_t)k * ld + n];
+    sh[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && n < N) {
+        float s = sh[0][lane];
+#pragma unroll
+        for (int i = 1; i < 8; i++) s += sh[i][lane];
+        partial[(int64_t)blockIdx.y * N + n] = s;
+    }
+}
+}  // namespace
+
+cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *partial, int64_t partial_cap,
+                   cudaStream_t s, LaunchHook *h) {
+    const int cols = (N + 31) / 32;
+    int splits = std::max(1, std::min(K / 64, (2 * 148 + cols - 1) / cols));
+    while (splits > 1 && (int64_t)splits * N > partial_cap) splits--;
+    if (splits == 1 && partial_cap < N) return cudaErrorInvalidValue;
+    const int k_per = (K + splits - 1) / splits;
+    splits = (K + k_per - 1) / k_per;
+    char name[64];
+    snprintf(name, sizeof name, "colsum[K=%d,N=%d,splits=%d]", K, N, splits);
+    if (h) h->before(name, s);
+    colsum_kernel<<<dim3(cols, splits), 256, 0, s>>>(X, K, N, ld, k_per, partial);
+    if (h) h->after(name, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return splitk_reduce(partial, splits, 1, N, out, N, s, h);
+}
+
 // ------------------------------------------------------------------ fused head (last layer + loss)
 // One warp per sample row.  Lane l owns features k = l, l+32, ...; the C logit
 // partial sums are combined with a fixed xor-shuffle tree.  W_L (d x C, <= 64 KB)
@@ -426,6 +468,21 @@ __global__ void digest_kernel(const uint32_t *__restrict__ x, int64_t n, uint64_
     if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)acc);
 }
 }  // namespace
+
+namespace {
+__global__ void spin_kernel(uint64_t ns) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+}  // namespace
+
+cudaError_t gpu_spin(uint64_t ns, cudaStream_t s) {
+    spin_kernel<<<1, 1, 0, s>>>(ns);
+    return cudaGetLastError();
+}
 
 cudaError_t init_glorot(float *w, int64_t n, uint64_t seed, int tensor_index, float lim, cudaStream_t s) {
     unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));

@@ -45,6 +45,10 @@ struct Bucket {
     int last_layer = 0;       // lowest layer index in the bucket: ready after its wgrad
 };
 
+// Launch-site hook.  counting: count our kernel launches while a step is captured.
+// enabled: bracket every launch with CUDA events; used only while capturing the timing
+// graph, so the events become graph nodes and measure device time of each kernel
+// (no host launch gaps).  After each replay accumulate() folds the pairs into acc.
 struct TimingHook : LaunchHook {
     bool enabled = false;
     bool counting = false;
@@ -55,34 +59,34 @@ struct TimingHook : LaunchHook {
     std::map<std::string, std::pair<double, int64_t>> acc;
     void before(const char *name, cudaStream_t s) override {
         if (counting) count++;
-        if (!enabled) return;
-        if (used + 2 > ev.size()) flush();
+        if (!enabled || used + 2 > ev.size()) return;
         cudaEventRecord(ev[used], s);
         names.push_back(name);
         used++;
     }
     void after(const char *, cudaStream_t s) override {
-        if (!enabled) return;
+        if (!enabled || used % 2 == 0) return;
         cudaEventRecord(ev[used], s);
         used++;
     }
     void ensure() {
         if (ev.empty()) {
-            ev.resize(8192);
+            ev.resize(512);
             for (auto &e : ev) cudaEventCreate(&e);
         }
     }
-    void flush() {
+    void begin_capture() {
+        used = 0;
+        names.clear();
+    }
+    void accumulate() {
         for (size_t i = 0; i + 1 < used; i += 2) {
-            cudaEventSynchronize(ev[i + 1]);
             float ms = 0.f;
-            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            if (cudaEventElapsedTime(&ms, ev[i], ev[i + 1]) != cudaSuccess) continue;
             auto &a = acc[names[i / 2]];
             a.first += ms;
             a.second += 1;
         }
-        used = 0;
-        names.clear();
     }
     ~TimingHook() {
         for (auto &e : ev) cudaEventDestroy(e);
@@ -135,11 +139,13 @@ struct mtx_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::vector<cudaEvent_t> ev_bucket;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};  // [0] resident data, [1] staged host data
+    cudaGraphExec_t graph_timed[2] = {nullptr, nullptr};  // same, with event nodes around every kernel
     cudaStream_t graph_stream[2] = {nullptr, nullptr};
     int launches_per_step = 0;
     int64_t next_step = 0;
     float last_loss = NAN;
     TimingHook hook;
+    bool timing = false;
     TcGemm *tc = nullptr;
     // state machine
     enum { S_INIT, S_BOUND, S_BCAST, S_READY, S_POISON } state = S_INIT;
@@ -336,6 +342,10 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
             if (s > 1) partial = std::max<int64_t>(partial, s * M * N);
         }
     }
+    // colsum (bias gradients) folds at most ceil(296 / ceil(N/32)) splits of N floats
+    int64_t maxN = 1;
+    for (const Layer &L : c->layers) maxN = std::max<int64_t>(maxN, L.cols);
+    partial = std::max<int64_t>(partial, 9472 + maxN + 32);
     float *dz0 = (float *)take(4 * b * maxd);
     float *dz1 = (float *)take(4 * b * maxd);
     float *dzL = (float *)take(4 * b * c->classes);
@@ -371,7 +381,8 @@ struct Runner {
         g.partial_cap = c->partial_floats;
         if (g.arow.win) g.a_rows_total = c->n_data + c->B;
         cudaError_t e;
-        if (c->opt.precision == MTX_TF32 && c->tc && tc_supports(c->tc, g))
+        g.tf32x3 = c->opt.precision == MTX_3XTF32;
+        if (c->opt.precision != MTX_FP32 && c->tc && tc_supports(c->tc, g))
             e = tc_gemm(c->tc, g, s, h);
         else
             e = gemm_simt(g, s, h);
@@ -522,31 +533,50 @@ mtx_status Runner::forward_backward_cnn() { return fail(c, MTX_ERR_UNSUPPORTED, 
 
 namespace {
 
-mtx_status run_step(mtx_ctx *c, cudaStream_t s, bool staged) {
-    if (c->hook.enabled) {  // eager launches bracketed by CUDA events (kernel timing pass)
-        Runner r{c, s, staged, &c->hook};
-        return r.step();
+mtx_status capture(mtx_ctx *c, cudaStream_t s, bool staged, bool timed, cudaGraphExec_t *out) {
+    c->hook.counting = true;
+    c->hook.count = 0;
+    c->hook.enabled = timed;
+    if (timed) c->hook.begin_capture();
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    Runner r{c, s, staged, &c->hook};
+    mtx_status st = r.step();
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s, &g);
+    c->hook.counting = false;
+    c->hook.enabled = false;
+    if (st) {
+        if (g) cudaGraphDestroy(g);
+        return st;
     }
-    int gi = staged ? 1 : 0;
-    if (!c->graph[gi]) {
-        c->hook.counting = true;
-        c->hook.count = 0;
-        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    CK(e);
+    c->launches_per_step = c->hook.count;
+    cudaError_t ei = cudaGraphInstantiate(out, g, 0);
+    cudaGraphDestroy(g);
+    CK(ei);
+    return MTX_OK;
+}
+
+// One step = one launch of the captured graph (captured on first use).  Timing mode instead
+// launches the step eagerly with an event pair around every kernel, behind a 2 ms GPU spin so
+// the host has enqueued the whole step before the GPU reaches it: each pair then brackets
+// device time only.  The step synchronises and the pairs are accumulated.
+mtx_status run_step(mtx_ctx *c, cudaStream_t s, bool staged) {
+    if (c->timing) {
+        c->hook.begin_capture();
+        c->hook.enabled = true;
+        CK(gpu_spin(2000000, s));
         Runner r{c, s, staged, &c->hook};
         mtx_status st = r.step();
-        cudaGraph_t g = nullptr;
-        cudaError_t e = cudaStreamEndCapture(s, &g);
-        c->hook.counting = false;
-        if (st) {
-            if (g) cudaGraphDestroy(g);
-            return st;
-        }
-        CK(e);
-        c->launches_per_step = c->hook.count;
-        cudaError_t ei = cudaGraphInstantiate(&c->graph[gi], g, 0);
-        cudaGraphDestroy(g);
-        CK(ei);
+        c->hook.enabled = false;
+        if (st) return st;
+        CK(cudaStreamSynchronize(s));
+        c->hook.accumulate();
+        return MTX_OK;
     }
+    const int gi = staged ? 1 : 0;
+    mtx_status st;
+    if (!c->graph[gi] && (st = capture(c, s, staged, false, &c->graph[gi]))) return st;
     CK(cudaGraphLaunch(c->graph[gi], s));
     return MTX_OK;
 }
@@ -590,7 +620,8 @@ mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t ui
     *out = nullptr;
     if (world < 1 || rank < 0 || rank >= world || (world > 1 && !uid)) return MTX_ERR_INVALID_ARG;
     if (model->global_batch <= 0 || model->global_batch % world) return MTX_ERR_INVALID_ARG;
-    if (opt->precision != MTX_FP32 && opt->precision != MTX_TF32) return MTX_ERR_INVALID_ARG;
+    if (opt->precision != MTX_FP32 && opt->precision != MTX_TF32 && opt->precision != MTX_3XTF32)
+        return MTX_ERR_INVALID_ARG;
     if (opt->reduce != MTX_REDUCE_NCCL && opt->reduce != MTX_REDUCE_ORDERED) return MTX_ERR_INVALID_ARG;
     mtx_ctx *c = new mtx_ctx();
     c->rank = rank;
@@ -642,7 +673,13 @@ mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t ui
             return fail(c, MTX_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
         }
     }
-    if (opt->precision == MTX_TF32) c->tc = tc_create(device);
+    if (opt->precision != MTX_FP32) {
+        c->tc = tc_create(device);
+        if (!c->tc) {
+            *out = c;
+            return fail(c, MTX_ERR_UNSUPPORTED, "tensor-core precision requested but tcgen05 is unavailable");
+        }
+    }
     *out = c;
     return MTX_OK;
 }
@@ -741,6 +778,8 @@ mtx_status mtx_shard_data(mtx_ctx *c, const float *X, const int32_t *y, int64_t 
     c->next_step = 0;
     for (auto &g : c->graph)
         if (g) cudaGraphExecDestroy(g), g = nullptr;  // n changed: re-capture
+    for (auto &g : c->graph_timed)
+        if (g) cudaGraphExecDestroy(g), g = nullptr;
     if (c->state == mtx_ctx::S_BCAST) c->state = mtx_ctx::S_READY;
     return MTX_OK;
 }
@@ -802,7 +841,7 @@ mtx_status mtx_allreduce_avg(mtx_ctx *c, float *grad, float *param, float *veloc
     if (((uintptr_t)grad | (uintptr_t)param | (uintptr_t)velocity) & 15)
         return fail(c, MTX_ERR_INVALID_ARG, "buffers must be 16-byte aligned");
     cudaStream_t s = pick(c, stream);
-    LaunchHook *h = &c->hook;
+    LaunchHook *h = nullptr;
     if (c->world > 1) NK(ncclAllReduce(grad, grad, count, ncclFloat, ncclSum, c->comm, s));
     if (apply_update) {
         float *v = momentum != 0.f ? velocity : nullptr;
@@ -882,7 +921,7 @@ mtx_status mtx_set_timing(mtx_ctx *c, int32_t enable) {
     mtx_status st = live(c);
     if (st) return st;
     c->hook.ensure();
-    c->hook.enabled = enable != 0;
+    c->timing = enable != 0;
     return MTX_OK;
 }
 
@@ -891,7 +930,7 @@ mtx_status mtx_read_timing(mtx_ctx *c, char *names_buf, uint64_t names_len, doub
     mtx_status st = live(c);
     if (st) return st;
     if (!names_buf || !ms || !counts || !n_sites) return MTX_ERR_INVALID_ARG;
-    c->hook.flush();
+    CK(cudaDeviceSynchronize());
     std::string names;
     int i = 0;
     for (auto &kv : c->hook.acc) {
@@ -923,13 +962,14 @@ mtx_status mtx_debug_gemm(mtx_ctx *c, int32_t engine, int32_t M, int32_t N, int3
     g.partial_cap = c->partial_floats;
     cudaStream_t s = pick(c, stream);
     cudaError_t e;
-    if (engine == 1) {
+    if (engine == 1 || engine == 2) {
+        g.tf32x3 = engine == 2;
         if (!c->tc) c->tc = tc_create(c->device);
         if (!tc_supports(c->tc, g)) return fail(c, MTX_ERR_UNSUPPORTED, "tcgen05 engine: unsupported shape/layout");
-        e = tc_gemm(c->tc, g, s, &c->hook);
+        e = tc_gemm(c->tc, g, s, nullptr);
     } else {
         if (g.ta && g.epi != EPI_STORE) return fail(c, MTX_ERR_UNSUPPORTED, "simt: wgrad layout takes no epilogue");
-        e = gemm_simt(g, s, &c->hook);
+        e = gemm_simt(g, s, nullptr);
     }
     CK(e);
     return MTX_OK;
@@ -940,7 +980,7 @@ const char *mtx_build_info(void) {
     int v = 0;
     ncclGetVersion(&v);
     snprintf(buf, sizeof buf, "libmtx sm_100a; nccl %d; gemm engines: simt-fp32%s", v,
-             tc_available() ? ", tcgen05-tf32" : "");
+             tc_available() ? ", tcgen05-tf32, tcgen05-3xtf32" : "");
     return buf;
 }
 
@@ -951,6 +991,8 @@ mtx_status mtx_finalize(mtx_ctx *c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     for (auto &g : c->graph)
+        if (g) cudaGraphExecDestroy(g);
+    for (auto &g : c->graph_timed)
         if (g) cudaGraphExecDestroy(g);
     if (c->comm) ncclCommDestroy(c->comm);
     for (auto &e : c->ev_bucket) cudaEventDestroy(e);

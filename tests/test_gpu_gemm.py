@@ -57,7 +57,7 @@ def _run(rep, engine, M, N, K, ta, tb, epi, rng):
     return Cd.cpu().numpy(), ref
 
 
-@pytest.mark.parametrize("engine", [0, 1] if TC else [0])
+@pytest.mark.parametrize("engine", [0, 1, 2] if TC else [0])
 @pytest.mark.parametrize("layout", [(0, 0, 1), (0, 0, 2), (0, 1, 3), (1, 0, 0)])
 @pytest.mark.parametrize("shape", SHAPES)
 def test_gemm_layouts(rep, engine, layout, shape):
@@ -71,6 +71,6 @@ def test_gemm_layouts(rep, engine, layout, shape):
             pytest.skip("tcgen05 engine does not take this layout")
         raise
     assert not np.isnan(C).any()
-    # fp32 tier: blocked fp32 sums; tf32 tier: 10-bit operand mantissas, fp32 accumulation
-    tol = 1e-5 if engine == 0 else 2e-3
+    # fp32 tier (SIMT, 3xTF32): fp32 products/sums; tf32: truncated 10-bit operand mantissas
+    tol = 2e-3 if engine == 1 else 1e-5
     assert maxrel(C, ref) <= tol * max(1.0, np.sqrt(K / 1024)), maxrel(C, ref)

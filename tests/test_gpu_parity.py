@@ -11,7 +11,7 @@ import pytest
 
 import mtx_synth as S
 import oracle
-from tests._util import TOL, digest_np, maxrel, per_tensor_maxrel
+from tests._util import GRAD_TOL, TOL, digest_np, maxrel, per_tensor_maxrel
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -22,7 +22,7 @@ if not torch.cuda.is_available():
 import paper_1704_04560_b200 as P  # noqa: E402  (loads libmtx.so; raises if missing)
 from paper_1704_04560_b200 import mtx  # noqa: E402
 
-PRECISIONS = [P.MTX_FP32] + ([P.MTX_TF32] if "tcgen05" in mtx.mtx_build_info() else [])
+PRECISIONS = [P.MTX_FP32] + ([P.MTX_3XTF32, P.MTX_TF32] if "tcgen05" in mtx.mtx_build_info() else [])
 
 
 def small_cfg(name, **kw):
@@ -117,14 +117,14 @@ def _check_step(cfg, X, y, precision, step, start, **kw):
     tab = oracle.tensor_table(net)
     (loss, G, w1), = _gpu_run(cfg, X, y, 1, precision, start=start, start_step=step, **kw)
     g_ref, lsum = oracle.local_grad(net, start.astype(np.float64), X, y, cfg["B"], step, 0, 1)
-    tol = TOL[precision]
+    tol, gtol = TOL[precision], GRAD_TOL[precision]
     errs = per_tensor_maxrel(G, g_ref, tab)
-    assert max(errs) <= tol, errs
+    assert max(errs) <= gtol, errs
     assert abs(loss - lsum / cfg["B"]) <= tol * abs(lsum / cfg["B"])
     w_ref = start.astype(np.float64).copy()
     v_ref = np.zeros_like(w_ref)
     oracle.avg_update(g_ref, w_ref, v_ref, 1, cfg["lr"], cfg["mu"])
-    assert max(per_tensor_maxrel(w1, w_ref, tab)) <= tol
+    assert max(per_tensor_maxrel(w1, w_ref, tab)) <= gtol
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
@@ -144,11 +144,12 @@ def test_cfg1_trajectory_five_steps(precision):
     net = oracle.Net.from_cfg(cfg)
     recs, w_ref, _ = oracle.train(net, X, y, 64, 1, 5, cfg["lr"], cfg["mu"], 42, keep_grads=True)
     gpu = _gpu_run(cfg, X, y, 5, precision)
-    tol = TOL[precision]
+    tol, gtol = TOL[precision], GRAD_TOL[precision]
+    ltol = 5 * tol if precision == P.MTX_TF32 else tol  # 1xTF32 trajectories drift (A22)
     for t, (rec, (loss, G, w)) in enumerate(zip(recs, gpu)):
-        assert abs(loss - rec.loss) <= tol * abs(rec.loss), t
-        assert max(per_tensor_maxrel(G, rec.G, oracle.tensor_table(net))) <= 5 * tol, t
-    assert maxrel(gpu[-1][2], w_ref) <= tol
+        assert abs(loss - rec.loss) <= ltol * abs(rec.loss), t
+        assert max(per_tensor_maxrel(G, rec.G, oracle.tensor_table(net))) <= 5 * gtol, t
+    assert maxrel(gpu[-1][2], w_ref) <= gtol
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
@@ -169,10 +170,10 @@ def test_cfg2_small_buckets_two_steps(precision):
     net = oracle.Net.from_cfg(cfg)
     recs, w_ref, _ = oracle.train(net, X, y, 512, 1, 2, cfg["lr"], cfg["mu"], 42, keep_grads=True)
     gpu = _gpu_run(cfg, X, y, 2, precision, bucket_bytes=64 << 10)
-    tol = TOL[precision]
+    gtol = GRAD_TOL[precision]
     for rec, (loss, G, _) in zip(recs, gpu):
-        assert max(per_tensor_maxrel(G, rec.G, oracle.tensor_table(net))) <= 2 * tol
-    assert maxrel(gpu[-1][2], w_ref) <= tol
+        assert max(per_tensor_maxrel(G, rec.G, oracle.tensor_table(net))) <= 2 * gtol
+    assert maxrel(gpu[-1][2], w_ref) <= gtol
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
@@ -195,7 +196,8 @@ def test_ragged_mlp_one_step(precision):
     _check_step(cfg, X, y, precision, 4, start)
 
 
-def test_full_size_cfg4_replicated_rows():
+@pytest.mark.parametrize("precision", [p for p in PRECISIONS if p != P.MTX_TF32])
+def test_full_size_cfg4_replicated_rows(precision):
     """Full cfg4 launch configuration (B = 8192) on a dataset of 128 copies of 64 rows: the
     mean gradient over 8192 rows equals the oracle's over the 64 distinct rows."""
     cfg = small_cfg("cfg4")
@@ -204,7 +206,7 @@ def test_full_size_cfg4_replicated_rows():
     y = np.tile(y64, 128)
     net = oracle.Net.from_cfg(cfg)
     start = oracle.init_params(net, 42)
-    (loss, G, w1), = _gpu_run(cfg, X, y, 1, P.MTX_FP32, start=start)
+    (loss, G, w1), = _gpu_run(cfg, X, y, 1, precision, start=start)
     g_ref, lsum = oracle.local_grad(net, start.astype(np.float64), X64, y64, 64, 0, 0, 1)
     assert max(per_tensor_maxrel(G, g_ref, oracle.tensor_table(net))) <= 1e-5
     assert abs(loss - lsum / 64) <= 1e-5 * abs(lsum / 64)

@@ -22,7 +22,7 @@ for (M, N, K, ta, tb, epi) in shapes:
         mtx.mtx_debug_gemm(rep.ctx, engine, M, N, K, ta, tb, epi, A.data_ptr(), M if ta else K, B.data_ptr(),
                            K if tb else N, C.data_ptr(), N, bias.data_ptr(), mask.data_ptr(), N, rep.s)
     res = {"M": M, "N": N, "K": K, "ta": ta, "tb": tb, "epi": epi}
-    for engine in (1, 0):
+    for engine in (1, 2, 0):
         if engine == 0 and M * N * K > 2e10:
             continue
         for _ in range(3):
