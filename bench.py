@@ -125,7 +125,7 @@ def kernel_work(name: str):
     return None
 
 
-def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int):
+def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: str):
     """Dominant kernel class (by total device time) -> achieved / peak."""
     groups = {}
     for name, (ms, cnt) in timing.items():
@@ -155,10 +155,16 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int):
         achieved = per_launch_work / per_launch_s / 1e12
         clk = sm_mhz or pk.get("sm_max_mhz", 1965.0)
         peak, unit = 148 * FP32_FMA_PER_SM_CLK * 2 * clk * 1e6 / 1e12, "TFLOP/s"
+    # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
+    # (profiles/ncu_traffic.json, written by tools/ncu_summary.py), averaged over its captured launches
+    ncu_kernel = {"gemm_tc3x": "tc_gemm_kernel<128, 1>", "gemm_tc": "tc_gemm_kernel<128, 0>",
+                  "avg_update": "avg_update_kernel<1>", "head_softmax_xent": "head_kernel",
+                  "colsum": "colsum_kernel", "splitk_reduce": "splitk_reduce_kernel"}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(top_name)
+    key = next((v for k, v in ncu_kernel.items() if top_name.startswith(k)), None)
+    if os.path.exists(tp) and key:
+        traffic = json.load(open(tp)).get(f"{config}:{key}")
     return {"kernel": top_name, "bound": top["bound"], "achieved": round(achieved, 3), "peak": round(peak, 1),
             "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic,
             "work_per_launch": per_launch_work, "launch_us": round(per_launch_s * 1e6, 3),
@@ -295,7 +301,7 @@ def main():
     timing = mtx.mtx_read_timing(rep.ctx, reset=True)
     mtx.mtx_set_timing(rep.ctx, False)
     pk = peaks()
-    roof = roofline(timing, pk, clk.get("sm_mhz"), args.steps)
+    roof = roofline(timing, pk, clk.get("sm_mhz"), args.steps, args.config)
     roof["peak_source"] = pk["_source"]
 
     # end-to-end through the public API with HOST inputs: per step H2D of the rank's rows from
