@@ -323,7 +323,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
             cDP.push_back((float *)take(4 * b * g.hp * g.wp * g.co));
             cArg.push_back(take(b * g.hp * g.wp * g.co));
             int64_t kk = (int64_t)g.k * g.k * g.ci + 1;
-            partial = std::max<int64_t>(partial, 64 * kk * g.co);
+            partial = std::max<int64_t>(partial, 296 * kk * g.co);  // conv_wgrad block partials
         }
         int nfc = (int)c->fc.size();
         const ConvGeom &gl = c->convs.back();
@@ -529,7 +529,85 @@ struct Runner {
 
 }  // namespace
 
-mtx_status Runner::forward_backward_cnn() { return fail(c, MTX_ERR_UNSUPPORTED, "CNN step not built yet"); }
+// LeNet-style step: conv(+bias+ReLU+pool) stack -> flatten (NHWC order = the pooled layout,
+// reading A7) -> fc layers -> fused head; backward mirrors it.  The head's / first fc dgrad's
+// ReLU-style mask on the flattened pool output is [P > 0], which equals routing through the
+// argmax and masking by [R > 0] (P is the max of post-ReLU values), so the pool backward
+// sees the same dP either way.
+mtx_status Runner::forward_backward_cnn() {
+    const int NC = (int)c->convs.size(), NF = (int)c->fc.size();
+    const int64_t b = c->b;
+    std::vector<int> fd{c->convs.back().hp * c->convs.back().wp * c->convs.back().co};
+    for (int f : c->fc) fd.push_back(f);
+    mtx_status st;
+    cudaError_t e;
+    for (int ci = 0; ci < NC; ci++) {
+        const float *in = ci == 0 ? xbase() : c->convP[ci - 1];
+        RowSel row = ci == 0 ? xrow() : RowSel{nullptr, 0};
+        e = conv_fwd(c->convs[ci], (int)b, in, row, c->params + c->layers[ci].pad_off, c->convR[ci], c->convP[ci],
+                     c->convArg[ci], s, h);
+        if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "conv_fwd: %s", cudaGetErrorString(e));
+    }
+    const float *flat = c->convP[NC - 1];
+    auto fc_in = [&](int f) -> const float * { return f == 1 ? flat : c->fcA[f - 1]; };
+    for (int f = 1; f < NF; f++) {
+        const Layer &Ly = c->layers[NC + f - 1];
+        GemmDesc g;
+        g.M = (int)b; g.N = fd[f]; g.K = fd[f - 1];
+        g.epi = EPI_BIAS_RELU;
+        g.A = fc_in(f); g.lda = fd[f - 1];
+        g.B = c->params + Ly.pad_off; g.ldb = fd[f];
+        g.bias = c->params + Ly.pad_off + (int64_t)fd[f - 1] * fd[f];
+        g.C = c->fcA[f]; g.ldc = fd[f];
+        if ((st = gemm(g))) return st;
+    }
+    float *head_dprev = NF > 1 ? c->dz[0] : c->convDP[NC - 1];
+    e = head_fused((int)b, fd[NF - 1], fd[NF], fc_in(NF), RowSel{nullptr, 0}, c->params + c->layers[NC + NF - 1].pad_off,
+                   ybase(), xrow(), 1.0f / (float)b, c->dzL, head_dprev, c->loss_rows, s, h);
+    if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "head: %s", cudaGetErrorString(e));
+    e = reduce_sum(c->loss_rows, (int)b, c->grads + c->N_pad, s, h);
+    if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "loss reduce: %s", cudaGetErrorString(e));
+    int cur = 0;
+    size_t bk = 0;
+    for (int f = NF; f >= 1; f--) {
+        const float *dZ = (f == NF) ? c->dzL : c->dz[cur];
+        if (f < NF) {
+            // dgrad into the previous activation (ReLU mask), or into the pool output (mask [P > 0])
+            const Layer &Ly = c->layers[NC + f - 1];
+            GemmDesc g;
+            g.M = (int)b; g.N = fd[f - 1]; g.K = fd[f];
+            g.tb = true; g.epi = EPI_MASK;
+            g.A = dZ; g.lda = fd[f];
+            g.B = c->params + Ly.pad_off; g.ldb = fd[f];
+            g.mask = fc_in(f); g.ldm = fd[f - 1];
+            g.C = f == 1 ? c->convDP[NC - 1] : c->dz[cur ^ 1]; g.ldc = fd[f - 1];
+            if ((st = gemm(g))) return st;
+        }
+        if ((st = wgrad(NC + f - 1, fc_in(f), RowSel{nullptr, 0}, dZ))) return st;
+        if ((st = bucket_ready(NC + f - 1, bk))) return st;
+        if (f < NF && f > 1) cur ^= 1;
+    }
+    for (int ci = NC - 1; ci >= 0; ci--) {
+        const ConvGeom &g = c->convs[ci];
+        e = pool_relu_bwd(g, (int)b, c->convDP[ci], c->convArg[ci], c->convR[ci], c->convDR[ci], s, h);
+        if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "pool_relu_bwd: %s", cudaGetErrorString(e));
+        if (ci > 0) {
+            e = conv_dgrad(g, (int)b, c->convDR[ci], c->params + c->layers[ci].pad_off, c->convDP[ci - 1], s, h);
+            if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "conv_dgrad: %s", cudaGetErrorString(e));
+        }
+        const float *in = ci == 0 ? xbase() : c->convP[ci - 1];
+        RowSel row = ci == 0 ? xrow() : RowSel{nullptr, 0};
+        const int64_t npos = b * g.hc * g.wc;
+        const int E = g.k * g.k * g.ci + 1;
+        int splits = (int)std::max<int64_t>(1, std::min<int64_t>(296, npos / 256));
+        splits = (int)std::min<int64_t>(splits, c->partial_floats / ((int64_t)E * g.co));
+        e = conv_wgrad(g, (int)b, in, row, c->convDR[ci], c->grads + c->layers[ci].pad_off, c->partial,
+                       std::max(1, splits), s, h);
+        if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "conv_wgrad: %s", cudaGetErrorString(e));
+        if ((st = bucket_ready(ci, bk))) return st;
+    }
+    return MTX_OK;
+}
 
 namespace {
 

@@ -103,9 +103,12 @@ def main():
         precisions = [P.MTX_FP32] + ([P.MTX_3XTF32, P.MTX_TF32] if "tcgen05" in mtx.mtx_build_info() else [])
         for prec in precisions:
             tol, gtol = TOL[prec], GRAD_TOL[prec]
-            for name, B, steps in (("cfg1", 64, 5), ("cfg2", 512, 3)):
+            for name, B, steps in (("cfg1", 64, 5), ("cfg2", 512, 3), ("cfg3", 64, 2)):
                 cfg = dict(S.CONFIGS[name], B=B)
-                X, y = S.mnist_like(1, 1000 if name == "cfg1" else 4096)
+                if name == "cfg3":
+                    X, y = S.cifar_like(1, 300)
+                else:
+                    X, y = S.mnist_like(1, 1000 if name == "cfg1" else 4096)
                 gpu = run_model(rank, world, cfg, X, y, steps, prec)
                 recs, w_ref, _ = oracle.train(oracle.Net.from_cfg(cfg), X, y, B, world, steps, cfg["lr"], cfg["mu"],
                                               42, keep_grads=True)

@@ -197,6 +197,29 @@ def test_ragged_mlp_one_step(precision):
 
 
 @pytest.mark.parametrize("precision", [p for p in PRECISIONS if p != P.MTX_TF32])
+def test_cnn_lenet_one_step(precision):
+    """configs[2] model (LeNet on CIFAR-shaped NHWC 32x32x3) at a batch the oracle finishes in seconds;
+    step 3 wraps the window (n = 200, B = 64)."""
+    cfg = small_cfg("cfg3", B=64, n=200)
+    X, y = S.cifar_like(1, 200)
+    start = oracle.init_params(oracle.Net.from_cfg(cfg), 42)
+    _check_step(cfg, X, y, precision, 0, start)
+    _check_step(cfg, X, y, precision, 3, start)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_cnn_mini_one_step(precision):
+    """Odd geometry: two conv stages (3x3 then 2x2, odd spatial sizes so pooling drops edges)."""
+    cfg = dict(kind="cnn", in_hwc=(13, 13, 2), conv=[(3, 5), (2, 7)], fc=[9, 4], data="cifar", n=100, B=30,
+               lr=0.05, mu=0.9)
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((100, 13, 13, 2)).astype(np.float32)
+    y = rng.integers(0, 4, 100).astype(np.int32)
+    start = oracle.init_params(oracle.Net.from_cfg(cfg), 42)
+    _check_step(cfg, X, y, precision, 1, start)
+
+
+@pytest.mark.parametrize("precision", [p for p in PRECISIONS if p != P.MTX_TF32])
 def test_full_size_cfg4_replicated_rows(precision):
     """Full cfg4 launch configuration (B = 8192) on a dataset of 128 copies of 64 rows: the
     mean gradient over 8192 rows equals the oracle's over the 64 distinct rows."""
