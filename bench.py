@@ -236,6 +236,9 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
+    # stdout must carry exactly one JSON line: keep NCCL's version banner off it
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+        os.environ["NCCL_DEBUG"] = "WARN"
     import torch
     import torch.distributed as dist
 
