@@ -114,6 +114,10 @@ def kernel_work(name: str):
         return "flop", 2 * a["M"] * a["N"] * a["K"], "tensor" if tensor else "alu"
     if kind == "colsum":
         return "byte", 4 * a["K"] * a["N"], "hbm"
+    if kind == "wgrad_narrow":  # streams A [K x (M-1)] once; dZ is tiny
+        return "byte", 4 * a["K"] * (a["M"] - 1 + a["N"]), "hbm"
+    if kind.startswith("conv_") or kind == "pool_relu_bwd":
+        return None
     if kind == "avg_update":
         return "byte", (20 if a["v"] else 12) * a["n"], "hbm"
     if kind == "head_softmax_xent":  # read A rows, write dZ_{L-1} (and dZ_L, loss)

@@ -404,6 +404,15 @@ struct TcGemm {
 
 bool tc_available() { return true; }
 
+int tc_choose_splits(int sms, int M, int N, int K) {
+    const int tiles = ((M + BM - 1) / BM) * ((N + 127) / 128);
+    const int kb = (K + BK - 1) / BK;
+    if (tiles * 2 > sms) return 1;
+    int s = std::min(sms / tiles, std::max(1, kb / 3));  // >= 3 k-blocks per split
+    const int per = (kb + s - 1) / s;
+    return (kb + per - 1) / per;
+}
+
 TcGemm *tc_create(int device) {
     TcGemm *t = new TcGemm();
     cudaDriverEntryPointQueryResult q;
@@ -479,8 +488,8 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.kb_total = (K + BK - 1) / BK;
     const int tiles = p.tiles_m * p.tiles_n;
     int splits = 1;
-    if (g.epi == EPI_STORE && g.partial && tiles < t->sms && N % 4 == 0) {  // wgrad: split K to fill the SMs
-        splits = std::min(t->sms / tiles, std::max(1, p.kb_total / 4));
+    if (g.partial && N % 4 == 0) {  // few output tiles: split K to fill the SMs (deterministic fold)
+        splits = tc_choose_splits(t->sms, M, N, K);
         while (splits > 1 && (int64_t)splits * M * N > g.partial_cap) splits--;
     }
     p.kb_per_split = (p.kb_total + splits - 1) / splits;
@@ -503,8 +512,8 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     cudaError_t e = g.tf32x3 ? launch<BN, true>(t, p, grid, s) : launch<BN, false>(t, p, grid, s);
     if (h) h->after(name, s);
     if (e != cudaSuccess) return e;
-    if (splits > 1) {
-        e = splitk_reduce(g.partial, splits, M, N, g.C, g.ldc, s, h);
+    if (splits > 1) {  // fold in ascending split order and apply the epilogue once
+        e = splitk_reduce(g.partial, splits, M, N, g.C, g.ldc, s, h, g.epi, g.bias, g.mask, g.ldm);
         if (e != cudaSuccess) return e;
     }
     if (g.aug)  // bias gradient row: db[n] = sum_k B[k][n]  (the ones row of the augmented A)

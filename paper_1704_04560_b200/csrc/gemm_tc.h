@@ -6,6 +6,8 @@
 namespace mtx {
 struct TcGemm;
 bool tc_available();
+// Split-K factor the engine uses for an M x N x K GEMM when the partial buffer allows it.
+int tc_choose_splits(int sms, int M, int N, int K);
 TcGemm *tc_create(int device);
 void tc_destroy(TcGemm *t);
 // True when this engine handles the shape/layout of g (otherwise the caller uses SIMT).

@@ -51,16 +51,25 @@ cudaError_t gemm_simt(const GemmDesc &g, cudaStream_t s, LaunchHook *h);
 cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *partial, int64_t partial_cap,
                    cudaStream_t s, LaunchHook *h);
 
-// C[m][n] = sum_{z ascending} partial[z][m][n]  (deterministic split-K fold)
+// C[m][n] = epi(sum_{z ascending} partial[z][m][n])  (deterministic split-K fold + GEMM epilogue)
 cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float *C, int64_t ldc, cudaStream_t s,
-                          LaunchHook *h);
+                          LaunchHook *h, int epi = EPI_STORE, const float *bias = nullptr,
+                          const float *mask = nullptr, int64_t ldm = 0);
+
+// Narrow weight gradient (N <= 16, e.g. the classifier layer): dWb[k][j] = sum_i A[i][k] dZ[i][j]
+// for k < K_in, plus (aug) the bias row dWb[K_in][j] = sum_i dZ[i][j].  Thread per k, rows split
+// over blocks, blocked fp32 sums, ascending fold.  A's row offset: arow (dataset operand).
+cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *dZ, int rows, int K_in, int N,
+                         float *dWb, float *partial, int64_t partial_cap, cudaStream_t s, LaunchHook *h);
 
 // Fused last layer: logits = A W + b (W,b = augmented [(d+1)][C] block), mean
-// softmax-CE, dZ_L = (softmax - onehot)/b, loss per row, and (if dprev) the
-// masked dgrad dZ_{L-1} = (dZ_L W^T) .* [A > 0].
+// softmax-CE, dZ_L = (softmax - onehot)/b, loss per row, (if dprev) the masked
+// dgrad dZ_{L-1} = (dZ_L W^T) .* [A > 0], and the local loss sum into *loss_out
+// (per-block partials folded in block order by the last block; ticket must be 0
+// on entry and is re-armed on exit; loss_part holds >= 1024 floats).
 cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, const float *Wb, const int32_t *labels,
-                       RowSel lrow, float inv_b, float *dZL, float *dprev, float *loss_rows, cudaStream_t s,
-                       LaunchHook *h);
+                       RowSel lrow, float inv_b, float *dZL, float *dprev, float *loss_rows, float *loss_part,
+                       unsigned *ticket, float *loss_out, cudaStream_t s, LaunchHook *h);
 
 // out = sum_{i ascending in a fixed tree} v[i] (one block; deterministic).
 cudaError_t reduce_sum(const float *v, int n, float *out, cudaStream_t s, LaunchHook *h);

@@ -134,13 +134,20 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(GemmDesc g) {
     }
 }
 
+// Deterministic split-K fold (ascending z) with the GEMM epilogue applied after the sum:
+// bias (+ReLU) for forward GEMMs, the ReLU mask for dgrad, plain store otherwise.
 __global__ void splitk_reduce_kernel(const float *__restrict__ partial, int splits, int M, int N, float *C,
-                                     int64_t ldc) {
+                                     int64_t ldc, int epi, const float *__restrict__ bias,
+                                     const float *__restrict__ mask, int64_t ldm) {
     int64_t total = (int64_t)M * N;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         float s = partial[e];
         for (int z = 1; z < splits; z++) s += partial[(int64_t)z * total + e];
-        C[(e / N) * ldc + (e % N)] = s;
+        const int64_t m = e / N, n = e % N;
+        if (epi == EPI_BIAS_RELU) s = fmaxf(s + bias[n], 0.f);
+        else if (epi == EPI_BIAS) s = s + bias[n];
+        else if (epi == EPI_MASK) s = mask[m * ldm + n] > 0.f ? s : 0.f;
+        C[m * ldc + n] = s;
     }
 }
 
@@ -175,15 +182,72 @@ cudaError_t gemm_simt(const GemmDesc &g, cudaStream_t s, LaunchHook *h) {
 }
 
 cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float *C, int64_t ldc, cudaStream_t s,
-                          LaunchHook *h) {
+                          LaunchHook *h, int epi, const float *bias, const float *mask, int64_t ldm) {
     int64_t total = (int64_t)M * N;
     unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8));
-    char rn[64];
-    snprintf(rn, sizeof rn, "splitk_reduce[M=%d,N=%d,splits=%d]", M, N, splits);
+    char rn[80];
+    snprintf(rn, sizeof rn, "splitk_reduce[M=%d,N=%d,splits=%d,epi=%d]", M, N, splits, epi);
     if (h) h->before(rn, s);
-    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(partial, splits, M, N, C, ldc);
+    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(partial, splits, M, N, C, ldc, epi, bias, mask, ldm);
     if (h) h->after(rn, s);
     return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ narrow weight gradient (N <= 16)
+namespace {
+constexpr int NW_T = 128, NW_ROWS = 32, NW_MAXN = 16;
+__global__ void __launch_bounds__(NW_T) wgrad_narrow_kernel(const float *__restrict__ A, int64_t lda, RowSel arow,
+                                                          const float *__restrict__ dZ, int rows, int K_in, int N,
+                                                          int rows_per, float *__restrict__ partial) {
+    __shared__ float sdz[NW_ROWS][NW_MAXN];
+    const int k = blockIdx.x * NW_T + threadIdx.x;
+    const int r0 = blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
+    const float *Ab = A + arow.row0() * lda;
+    float acc[NW_MAXN];
+#pragma unroll
+    for (int j = 0; j < NW_MAXN; j++) acc[j] = 0.f;
+    for (int i0 = r0; i0 < r1; i0 += NW_ROWS) {
+        const int nr = min(NW_ROWS, r1 - i0);
+        for (int e = threadIdx.x; e < NW_ROWS * NW_MAXN; e += NW_T) {
+            const int i = e / NW_MAXN, j = e % NW_MAXN;
+            sdz[i][j] = (i < nr && j < N) ? dZ[(int64_t)(i0 + i) * N + j] : 0.f;
+        }
+        __syncthreads();
+        if (k <= K_in) {
+            float t[NW_MAXN];
+#pragma unroll
+            for (int j = 0; j < NW_MAXN; j++) t[j] = 0.f;
+            for (int i = 0; i < nr; i++) {
+                const float a = k < K_in ? Ab[(int64_t)(i0 + i) * lda + k] : 1.f;  // k == K_in: bias row
+#pragma unroll
+                for (int j = 0; j < NW_MAXN; j++) t[j] = __fmaf_rn(a, sdz[i][j], t[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < NW_MAXN; j++) acc[j] = __fadd_rn(acc[j], t[j]);  // blocked summation
+        }
+        __syncthreads();
+    }
+    if (k <= K_in)
+        for (int j = 0; j < N; j++) partial[((int64_t)blockIdx.y * (K_in + 1) + k) * N + j] = acc[j];
+}
+}  // namespace
+
+cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *dZ, int rows, int K_in, int N,
+                         float *dWb, float *partial, int64_t partial_cap, cudaStream_t s, LaunchHook *h) {
+    if (N > NW_MAXN) return cudaErrorInvalidValue;
+    const int kb = (K_in + 1 + NW_T - 1) / NW_T;
+    int splits = std::max(1, std::min((2 * 148 + kb - 1) / kb, (rows + 63) / 64));
+    while (splits > 1 && (int64_t)splits * (K_in + 1) * N > partial_cap) splits--;
+    const int rows_per = (rows + splits - 1) / splits;
+    splits = (rows + rows_per - 1) / rows_per;
+    char name[80];
+    snprintf(name, sizeof name, "wgrad_narrow[M=%d,N=%d,K=%d,splits=%d]", K_in + 1, N, rows, splits);
+    if (h) h->before(name, s);
+    wgrad_narrow_kernel<<<dim3(kb, splits), NW_T, 0, s>>>(A, lda, arow, dZ, rows, K_in, N, rows_per, partial);
+    if (h) h->after(name, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return splitk_reduce(partial, splits, K_in + 1, N, dWb, N, s, h);
 }
 
 // ------------------------------------------------------------------ column sums (bias gradients)
@@ -239,7 +303,12 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
                                                              RowSel arow, const float *__restrict__ Wb,
                                                              const int32_t *__restrict__ labels, RowSel lrow,
                                                              float inv_b, float *__restrict__ dZL,
-                                                             float *__restrict__ dprev, float *__restrict__ loss_rows) {
+                                                             float *__restrict__ dprev, float *__restrict__ loss_rows,
+                                                             float *__restrict__ loss_part, unsigned *ticket,
+                                                             float *__restrict__ loss_out) {
+    __shared__ float swl[HEAD_WARPS];
+    __shared__ bool last;
+    float wloss = 0.f;  // this warp's rows, in row order
     extern __shared__ float sW[];  // [(d+1)][C]
     for (int e = threadIdx.x; e < (d + 1) * C; e += blockDim.x) sW[e] = Wb[e];
     __syncthreads();
@@ -280,7 +349,9 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
 #pragma unroll
         for (int j = 0; j < HEAD_MAXC; j++)
             dz[j] = (j < C) ? (expf(z[j] - m) * invS - (j == y ? 1.f : 0.f)) * inv_b : 0.f;
-        if (lane == 0) loss_rows[i] = m + logf(S) - zy;
+        const float li = m + logf(S) - zy;
+        if (lane == 0) loss_rows[i] = li;
+        wloss += li;
         if (lane < C) {
             float mine = 0.f;
 #pragma unroll
@@ -296,12 +367,31 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
             }
         }
     }
+    // loss: warp sums -> block sum (warp order) -> per-block partial; the last block folds the
+    // partials in block order into the loss slot (deterministic, no float atomics)
+    if (lane == 0) swl[warp] = wloss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float bsum = 0.f;
+        for (int w = 0; w < HEAD_WARPS; w++) bsum += swl[w];
+        loss_part[blockIdx.x] = bsum;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        float tot = 0.f;
+        for (unsigned bidx = 0; bidx < gridDim.x; bidx++) tot += ((volatile float *)loss_part)[bidx];
+        *loss_out = tot;
+        *ticket = 0u;  // re-armed for the next step
+    }
 }
 }  // namespace
 
 cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, const float *Wb, const int32_t *labels,
-                       RowSel lrow, float inv_b, float *dZL, float *dprev, float *loss_rows, cudaStream_t s,
-                       LaunchHook *h) {
+                       RowSel lrow, float inv_b, float *dZL, float *dprev, float *loss_rows, float *loss_part,
+                       unsigned *ticket, float *loss_out, cudaStream_t s, LaunchHook *h) {
     if (C > HEAD_MAXC || C < 1) return cudaErrorInvalidValue;
     size_t smem = sizeof(float) * (size_t)(d + 1) * C;
     if (smem > 48 * 1024) {
@@ -313,7 +403,7 @@ cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, cons
     snprintf(name, sizeof name, "head_softmax_xent[rows=%d,d=%d,C=%d,dgrad=%d]", rows, d, C, dprev ? 1 : 0);
     if (h) h->before(name, s);
     head_kernel<<<blocks, HEAD_WARPS * 32, smem, s>>>(rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL, dprev,
-                                                       loss_rows);
+                                                       loss_rows, loss_part, ticket, loss_out);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }

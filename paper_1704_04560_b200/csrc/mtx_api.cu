@@ -120,6 +120,8 @@ struct mtx_ctx {
     int64_t *win = nullptr;
     int *flag = nullptr;
     unsigned long long *dig = nullptr;
+    float *loss_part = nullptr;
+    unsigned *ticket = nullptr;
     uint64_t *proto = nullptr;  // P x 8 bytes for the model-digest allgather
     // CNN activations
     std::vector<float *> convR, convP, convDR, convDP;
@@ -314,6 +316,12 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
             int64_t M = c->dims[l - 1] + 1, N = c->dims[l];
             int64_t s = wgrad_splits(M, N, b);
             if (s > 1) partial = std::max<int64_t>(partial, s * M * N);
+            if (c->opt.precision != MTX_FP32) {  // tensor-core engine: split-K of wgrad, fwd and dgrad
+                partial = std::max<int64_t>(partial, (int64_t)tc_choose_splits(148, (int)M - 1, (int)N, (int)b) * (M - 1) * N);
+                partial = std::max<int64_t>(partial, (int64_t)tc_choose_splits(148, (int)b, (int)N, (int)(M - 1)) * b * N);
+                partial = std::max<int64_t>(partial, (int64_t)tc_choose_splits(148, (int)b, (int)(M - 1), (int)N) * b * (M - 1));
+            }
+            if (N <= 16) partial = std::max<int64_t>(partial, 296 * M * N);  // wgrad_narrow
         }
     } else {
         for (auto &g : c->convs) {
@@ -340,6 +348,12 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
             int64_t M = fd[f - 1] + 1, N = fd[f];
             int64_t s = wgrad_splits(M, N, b);
             if (s > 1) partial = std::max<int64_t>(partial, s * M * N);
+            if (c->opt.precision != MTX_FP32) {
+                partial = std::max<int64_t>(partial, (int64_t)tc_choose_splits(148, (int)M - 1, (int)N, (int)b) * (M - 1) * N);
+                partial = std::max<int64_t>(partial, (int64_t)tc_choose_splits(148, (int)b, (int)N, (int)(M - 1)) * b * N);
+                partial = std::max<int64_t>(partial, (int64_t)tc_choose_splits(148, (int)b, (int)(M - 1), (int)N) * b * (M - 1));
+            }
+            if (N <= 16) partial = std::max<int64_t>(partial, 296 * M * N);
         }
     }
     // colsum (bias gradients) folds at most ceil(296 / ceil(N/32)) splits of N floats
@@ -353,6 +367,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     float *part = partial ? (float *)take(4 * partial) : nullptr;
     float *sx = (float *)take(4 * b * c->d0);
     int32_t *sy = (int32_t *)take(4 * b);
+    float *loss_part = (float *)take(4 * 1024);
     uint8_t *misc = take(256 + 8 * (uint64_t)c->world);
     if (assign) {
         c->params = params; c->vel = vel; c->grads = grads; c->gather = gather;
@@ -361,6 +376,8 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         c->dz[0] = dz0; c->dz[1] = dz1; c->dzL = dzL; c->loss_rows = loss_rows;
         c->partial = part; c->partial_floats = partial;
         c->stage_x = sx; c->stage_y = sy;
+        c->loss_part = loss_part;
+        c->ticket = (unsigned *)(misc + 48);
         c->win = (int64_t *)misc;
         c->flag = (int *)(misc + 16);
         c->dig = (unsigned long long *)(misc + 32);
@@ -397,6 +414,12 @@ struct Runner {
     // Wgrad of layer block `li` (augmented: writes dW and db) from A [b][rows_w] and dZ [b][cols].
     mtx_status wgrad(int li, const float *A, RowSel arow, const float *dZ) {
         const Layer &L = c->layers[li];
+        if (L.cols <= 16) {  // classifier-width layers: thread-per-input-feature kernel, bias row included
+            cudaError_t e = wgrad_narrow(A, L.rows_w, arow, dZ, (int)c->b, L.rows_w, L.cols, c->grads + L.pad_off,
+                                         c->partial, c->partial_floats, s, h);
+            if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "wgrad_narrow: %s", cudaGetErrorString(e));
+            return MTX_OK;
+        }
         GemmDesc g;
         g.M = L.rows_w + 1; g.N = L.cols; g.K = (int)c->b;
         g.ta = true; g.aug = true;
@@ -404,7 +427,6 @@ struct Runner {
         g.B = dZ; g.ldb = L.cols;
         g.C = c->grads + L.pad_off; g.ldc = L.cols;
         g.splits = (int)wgrad_splits(g.M, g.N, g.K);
-        g.partial = c->partial;
         return gemm(g);
     }
 
@@ -432,10 +454,9 @@ struct Runner {
         const float *Ain = L == 1 ? xbase() : c->acts[L - 1];
         RowSel ar = L == 1 ? xrow() : RowSel{nullptr, 0};
         cudaError_t e = head_fused((int)b, d[L - 1], d[L], Ain, ar, c->params + LL.pad_off, ybase(), xrow(),
-                                   1.0f / (float)b, c->dzL, L > 1 ? c->dz[0] : nullptr, c->loss_rows, s, h);
+                                   1.0f / (float)b, c->dzL, L > 1 ? c->dz[0] : nullptr, c->loss_rows, c->loss_part,
+                                   c->ticket, c->grads + c->N_pad, s, h);
         if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "head: %s", cudaGetErrorString(e));
-        e = reduce_sum(c->loss_rows, (int)b, c->grads + c->N_pad, s, h);
-        if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "loss reduce: %s", cudaGetErrorString(e));
         // backward l = L .. 1.  dgrad(l) reads W_l, so it is issued before wgrad(l) completes the
         // bucket holding W_l: the bucket's update (comm stream) may then overwrite W_l safely.
         int cur = 0;
@@ -563,10 +584,9 @@ mtx_status Runner::forward_backward_cnn() {
     }
     float *head_dprev = NF > 1 ? c->dz[0] : c->convDP[NC - 1];
     e = head_fused((int)b, fd[NF - 1], fd[NF], fc_in(NF), RowSel{nullptr, 0}, c->params + c->layers[NC + NF - 1].pad_off,
-                   ybase(), xrow(), 1.0f / (float)b, c->dzL, head_dprev, c->loss_rows, s, h);
+                   ybase(), xrow(), 1.0f / (float)b, c->dzL, head_dprev, c->loss_rows, c->loss_part, c->ticket,
+                   c->grads + c->N_pad, s, h);
     if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "head: %s", cudaGetErrorString(e));
-    e = reduce_sum(c->loss_rows, (int)b, c->grads + c->N_pad, s, h);
-    if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "loss reduce: %s", cudaGetErrorString(e));
     int cur = 0;
     size_t bk = 0;
     for (int f = NF; f >= 1; f--) {
