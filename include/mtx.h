@@ -220,11 +220,11 @@ mtx_status mtx_param_digest(mtx_ctx *ctx, uint64_t *out);
 /* Kernel launches one mtx_train_step issues (for the bench's gpu_launches). */
 mtx_status mtx_launches_per_step(const mtx_ctx *ctx, int32_t *n);
 
-/* Enables CUDA-event timing of every launch site: the step is then launched
- * eagerly with an event pair around every kernel, queued behind a short GPU spin
- * so the pairs bracket device time only (no host launch gaps); each
+/* Enables CUDA-event timing of every launch site: the step then runs as a second
+ * captured graph with an event-record node (cudaEventRecordExternal) around every
+ * kernel, so each pair measures device time inside the replayed graph; each
  * mtx_train_step synchronises to accumulate them.  Disable to return to the
- * captured-graph step. */
+ * plain graph. */
 mtx_status mtx_set_timing(mtx_ctx *ctx, int32_t enable);
 /* Accumulated device milliseconds and launch counts per launch-site class since
  * the last reset; names is a '\n'-separated list (written into names_buf).  Synchronous. */

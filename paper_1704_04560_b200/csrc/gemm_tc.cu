@@ -18,6 +18,7 @@
 // transposes.  Accumulation is fp32 in TMEM; fp32 operands are consumed as TF32.
 #include <cuda.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -62,6 +63,7 @@ struct TcParams {
     float *partial;
     const int64_t *a_win;  // dataset operand: sample-dimension offset read on the device
     int64_t a_base;
+    unsigned *counters;    // split-K: one arrival counter per output tile (zero between launches)
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -152,6 +154,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * STAGES, tfull0 = empty0 + 8 * STAGES,
                    tempty0 = tfull0 + 16, split0 = tempty0 + 16;
     uint32_t *tmem_slot = (uint32_t *)(smem + L::BAR_OFF + 128);
+    volatile int *fix_flag = (volatile int *)(smem + L::BAR_OFF + 136);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (warp == 0 && lane == 0) {
@@ -334,26 +337,63 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                 if (++buf == 2) { buf = 0; buf_phase ^= 1; }
             }
             const int m = m0 + 32 * q + lane;
+            if (p.splits > 1) {
+                // split-K: write this split's partial, then the last CTA to arrive for the tile folds
+                // all partials in ascending split order and applies the epilogue (deterministic)
+                if (m < p.M) {
+                    float *prow = p.partial + ((int64_t)z * p.M + m) * p.N;
+#pragma unroll
+                    for (int g4 = 0; g4 < HALF / 4; g4++) {
+                        const int n = n0 + 4 * g4;
+                        if (n + 3 < p.N) *(float4 *)(prow + n) = make_float4(acc[4 * g4], acc[4 * g4 + 1], acc[4 * g4 + 2], acc[4 * g4 + 3]);
+                        else for (int e = 0; e < 4 && n + e < p.N; e++) prow[n + e] = acc[4 * g4 + e];
+                    }
+                }
+                if (!p.counters) continue;  // folded by a separate kernel
+                __threadfence();
+                asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps
+                if (threadIdx.x == 128) *fix_flag = atomicAdd(p.counters + r, 1u) == (unsigned)(p.splits - 1);
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (!*fix_flag) continue;
+                __threadfence();
+                if (m < p.M) {
+#pragma unroll
+                    for (int g4 = 0; g4 < HALF / 4; g4++) {
+                        const int n = n0 + 4 * g4;
+                        if (n >= p.N) break;
+                        float o[4] = {0.f, 0.f, 0.f, 0.f};
+                        for (int zz = 0; zz < p.splits; zz++) {
+                            const float *src = p.partial + ((int64_t)zz * p.M + m) * p.N + n;
+                            if (n + 3 < p.N) {
+                                const float4 v = __ldcg((const float4 *)src);
+                                o[0] += v.x; o[1] += v.y; o[2] += v.z; o[3] += v.w;
+                            } else {
+                                for (int e = 0; e < 4 && n + e < p.N; e++) o[e] += __ldcg(src + e);
+                            }
+                        }
+                        acc[4 * g4] = o[0]; acc[4 * g4 + 1] = o[1]; acc[4 * g4 + 2] = o[2]; acc[4 * g4 + 3] = o[3];
+                    }
+                }
+                if (threadIdx.x == 128) p.counters[r] = 0u;  // re-armed for the next launch
+            }
             if (m >= p.M) continue;
-            float *dst_row = p.splits > 1 ? p.partial + ((int64_t)z * p.M + m) * p.N : p.C + (int64_t)m * p.ldc;
+            float *dst_row = p.C + (int64_t)m * p.ldc;
 #pragma unroll
             for (int g4 = 0; g4 < HALF / 4; g4++) {
                 const int n = n0 + 4 * g4;
                 if (n >= p.N) break;
                 float o[4] = {acc[4 * g4], acc[4 * g4 + 1], acc[4 * g4 + 2], acc[4 * g4 + 3]};
-                if (p.splits == 1) {
-                    if (p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) {
+                if (p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) {
 #pragma unroll
-                        for (int e = 0; e < 4; e++)
-                            if (n + e < p.N) {
-                                o[e] += p.bias[n + e];
-                                if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e], 0.f);
-                            }
-                    } else if (p.epi == EPI_MASK) {
+                    for (int e = 0; e < 4; e++)
+                        if (n + e < p.N) {
+                            o[e] += p.bias[n + e];
+                            if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e], 0.f);
+                        }
+                } else if (p.epi == EPI_MASK) {
 #pragma unroll
-                        for (int e = 0; e < 4; e++)
-                            if (n + e < p.N && !(p.mask[(int64_t)m * p.ldm + n + e] > 0.f)) o[e] = 0.f;
-                    }
+                    for (int e = 0; e < 4; e++)
+                        if (n + e < p.N && !(p.mask[(int64_t)m * p.ldm + n + e] > 0.f)) o[e] = 0.f;
                 }
                 if (n + 3 < p.N) {
                     *(float4 *)(dst_row + n) = make_float4(o[0], o[1], o[2], o[3]);
@@ -400,6 +440,7 @@ struct TcGemm {
     EncodeTiled encode = nullptr;
     int sms = 148;
     bool attr_set[2] = {false, false};
+    bool fixup = false;  // split-K: fold in the last CTA per tile (measured slower on cfg2; MTX_TC_FIXUP=1)
 };
 
 bool tc_available() { return true; }
@@ -423,6 +464,7 @@ TcGemm *tc_create(int device) {
         return nullptr;
     }
     t->encode = (EncodeTiled)fn;
+    if (const char *k = getenv("MTX_TC_FIXUP")) t->fixup = atoi(k) != 0;  // development A/B knob
     cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, device);
     int major = 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
@@ -488,7 +530,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.kb_total = (K + BK - 1) / BK;
     const int tiles = p.tiles_m * p.tiles_n;
     int splits = 1;
-    if (g.partial && N % 4 == 0) {  // few output tiles: split K to fill the SMs (deterministic fold)
+    if (g.partial && N % 4 == 0) {  // few output tiles: split K to fill the SMs
         splits = tc_choose_splits(t->sms, M, N, K);
         while (splits > 1 && (int64_t)splits * M * N > g.partial_cap) splits--;
     }
@@ -502,6 +544,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.C = g.C;
     p.ldc = g.ldc;
     p.partial = g.partial;
+    p.counters = t->fixup ? g.counters : nullptr;
     const int total = tiles * splits;
     const int grid = std::min(total, t->sms);
     const char *kind = g.epi == EPI_MASK ? "dgrad" : (g.ta ? "wgrad" : "fwd");
@@ -512,7 +555,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     cudaError_t e = g.tf32x3 ? launch<BN, true>(t, p, grid, s) : launch<BN, false>(t, p, grid, s);
     if (h) h->after(name, s);
     if (e != cudaSuccess) return e;
-    if (splits > 1) {  // fold in ascending split order and apply the epilogue once
+    if (splits > 1 && !p.counters) {  // no in-kernel fixup: fold with the epilogue in a separate kernel
         e = splitk_reduce(g.partial, splits, M, N, g.C, g.ldc, s, h, g.epi, g.bias, g.mask, g.ldm);
         if (e != cudaSuccess) return e;
     }

@@ -35,6 +35,7 @@ struct GemmDesc {
     int64_t partial_cap = 0;  // floats available at partial (engines may choose their own split count)
     int64_t a_rows_total = 0; // rows of the buffer behind A when arow.win is set (wrap-extended dataset)
     int tf32x3 = 0;           // tensor-core engine: 3xTF32 (fp32-accurate) instead of 1xTF32
+    unsigned *counters = nullptr;  // tensor-core split-K fixup: >= 256 per-tile counters, zeroed
 };
 
 // Launch-site hook: the API layer brackets every launch with it (timing/counting).

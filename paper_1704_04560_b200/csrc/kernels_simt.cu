@@ -217,18 +217,26 @@ __global__ void __launch_bounds__(NW_T) wgrad_narrow_kernel(const float *__restr
             float t[NW_MAXN];
 #pragma unroll
             for (int j = 0; j < NW_MAXN; j++) t[j] = 0.f;
-            for (int i = 0; i < nr; i++) {
-                const float a = k < K_in ? Ab[(int64_t)(i0 + i) * lda + k] : 1.f;  // k == K_in: bias row
+            for (int ib = 0; ib < nr; ib += 8) {
+                float a8[8];
 #pragma unroll
-                for (int j = 0; j < NW_MAXN; j++) t[j] = __fmaf_rn(a, sdz[i][j], t[j]);
+                for (int u = 0; u < 8; u++)  // k == K_in: the bias row (a = 1)
+                    a8[u] = (ib + u < nr) ? (k < K_in ? __ldg(Ab + (int64_t)(i0 + ib + u) * lda + k) : 1.f) : 0.f;
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+#pragma unroll
+                    for (int j = 0; j < NW_MAXN; j++) t[j] = __fmaf_rn(a8[u], sdz[ib + u][j], t[j]);
             }
 #pragma unroll
             for (int j = 0; j < NW_MAXN; j++) acc[j] = __fadd_rn(acc[j], t[j]);  // blocked summation
         }
         __syncthreads();
     }
-    if (k <= K_in)
-        for (int j = 0; j < N; j++) partial[((int64_t)blockIdx.y * (K_in + 1) + k) * N + j] = acc[j];
+    if (k <= K_in) {
+#pragma unroll
+        for (int j = 0; j < NW_MAXN; j++)
+            if (j < N) partial[((int64_t)blockIdx.y * (K_in + 1) + k) * N + j] = acc[j];
+    }
 }
 }  // namespace
 
@@ -236,7 +244,7 @@ cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *
                          float *dWb, float *partial, int64_t partial_cap, cudaStream_t s, LaunchHook *h) {
     if (N > NW_MAXN) return cudaErrorInvalidValue;
     const int kb = (K_in + 1 + NW_T - 1) / NW_T;
-    int splits = std::max(1, std::min((2 * 148 + kb - 1) / kb, (rows + 63) / 64));
+    int splits = std::max(1, std::min((4 * 148 + kb - 1) / kb, (rows + 31) / 32));
     while (splits > 1 && (int64_t)splits * (K_in + 1) * N > partial_cap) splits--;
     const int rows_per = (rows + splits - 1) / splits;
     splits = (rows + rows_per - 1) / rows_per;
@@ -297,8 +305,11 @@ cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *
 // partial sums are combined with a fixed xor-shuffle tree.  W_L (d x C, <= 64 KB)
 // and b_L are staged in shared memory once per CTA.
 namespace {
-constexpr int HEAD_MAXC = 16, HEAD_WARPS = 8;
+constexpr int HEAD_WARPS = 8;
 
+// NV = float4 groups per lane (d <= 128 * NV): lane owns features 4*lane + 128*t .. +3, loaded as
+// float4 with all of the row's loads in flight before the FMAs.
+template <int NV, bool VEC, int HEAD_MAXC>
 __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, int C, const float *__restrict__ A,
                                                              RowSel arow, const float *__restrict__ Wb,
                                                              const int32_t *__restrict__ labels, RowSel lrow,
@@ -306,26 +317,43 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
                                                              float *__restrict__ dprev, float *__restrict__ loss_rows,
                                                              float *__restrict__ loss_part, unsigned *ticket,
                                                              float *__restrict__ loss_out) {
+    extern __shared__ float sW[];  // [(d+1)][C]
     __shared__ float swl[HEAD_WARPS];
     __shared__ bool last;
-    float wloss = 0.f;  // this warp's rows, in row order
-    extern __shared__ float sW[];  // [(d+1)][C]
     for (int e = threadIdx.x; e < (d + 1) * C; e += blockDim.x) sW[e] = Wb[e];
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float *Abase = A + arow.row0() * (int64_t)d;
     const int32_t *lab = labels + lrow.row0();
+    float wloss = 0.f;  // this warp's rows, in row order
     for (int i = blockIdx.x * HEAD_WARPS + warp; i < rows; i += gridDim.x * HEAD_WARPS) {
         const float *a = Abase + (int64_t)i * d;
+        float av[NV][4];
+#pragma unroll
+        for (int t = 0; t < NV; t++) {
+            const int k = 4 * lane + 128 * t;
+            if (VEC && k + 3 < d) {
+                const float4 v = __ldg((const float4 *)(a + k));
+                av[t][0] = v.x; av[t][1] = v.y; av[t][2] = v.z; av[t][3] = v.w;
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; u++) av[t][u] = (k + u < d) ? __ldg(a + k + u) : 0.f;
+            }
+        }
         float z[HEAD_MAXC];
 #pragma unroll
         for (int j = 0; j < HEAD_MAXC; j++) z[j] = 0.f;
-        for (int k = lane; k < d; k += 32) {
-            float ak = a[k];
 #pragma unroll
-            for (int j = 0; j < HEAD_MAXC; j++)
-                if (j < C) z[j] = __fmaf_rn(ak, sW[k * C + j], z[j]);
-        }
+        for (int t = 0; t < NV; t++)
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int k = 4 * lane + 128 * t + u;
+                if (k < d) {
+#pragma unroll
+                    for (int j = 0; j < HEAD_MAXC; j++)
+                        if (j < C) z[j] = __fmaf_rn(av[t][u], sW[k * C + j], z[j]);
+                }
+            }
 #pragma unroll
         for (int j = 0; j < HEAD_MAXC; j++) {
             if (j < C) {
@@ -359,11 +387,25 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
             dZL[(int64_t)i * C + lane] = mine;
         }
         if (dprev) {
-            for (int k = lane; k < d; k += 32) {
-                float sacc = 0.f;
 #pragma unroll
-                for (int j = 0; j < HEAD_MAXC; j++) if (j < C) sacc = __fmaf_rn(dz[j], sW[k * C + j], sacc);
-                dprev[(int64_t)i * d + k] = a[k] > 0.f ? sacc : 0.f;
+            for (int t = 0; t < NV; t++) {
+                const int k = 4 * lane + 128 * t;
+                float o[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    float sacc = 0.f;
+                    if (k + u < d) {
+#pragma unroll
+                        for (int j = 0; j < HEAD_MAXC; j++) if (j < C) sacc = __fmaf_rn(dz[j], sW[(k + u) * C + j], sacc);
+                    }
+                    o[u] = av[t][u] > 0.f ? sacc : 0.f;
+                }
+                if (VEC && k + 3 < d) {
+                    *(float4 *)(dprev + (int64_t)i * d + k) = make_float4(o[0], o[1], o[2], o[3]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; u++) if (k + u < d) dprev[(int64_t)i * d + k + u] = o[u];
+                }
             }
         }
     }
@@ -387,25 +429,54 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
         *ticket = 0u;  // re-armed for the next step
     }
 }
+
+template <int NV, bool VEC, int CM>
+cudaError_t launch_head(unsigned blocks, size_t smem, cudaStream_t s, int rows, int d, int C, const float *A, RowSel arow,
+                        const float *Wb, const int32_t *labels, RowSel lrow, float inv_b, float *dZL, float *dprev,
+                        float *loss_rows, float *loss_part, unsigned *ticket, float *loss_out) {
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(head_kernel<NV, VEC, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    head_kernel<NV, VEC, CM><<<blocks, HEAD_WARPS * 32, smem, s>>>(rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL, dprev,
+                                                               loss_rows, loss_part, ticket, loss_out);
+    return cudaGetLastError();
+}
 }  // namespace
 
 cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, const float *Wb, const int32_t *labels,
                        RowSel lrow, float inv_b, float *dZL, float *dprev, float *loss_rows, float *loss_part,
                        unsigned *ticket, float *loss_out, cudaStream_t s, LaunchHook *h) {
-    if (C > HEAD_MAXC || C < 1) return cudaErrorInvalidValue;
-    size_t smem = sizeof(float) * (size_t)(d + 1) * C;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    unsigned blocks = std::min<unsigned>(cdiv(rows, HEAD_WARPS), 148u * 4u);
+    if (C > 16 || C < 1 || d > 1024) return cudaErrorInvalidValue;
+    const size_t smem = sizeof(float) * (size_t)(d + 1) * C;
+    // enough rows per block that the block count stays <= 1024 (loss partial slots)
+    const unsigned blocks = std::min<unsigned>(cdiv(rows, HEAD_WARPS), 1024u);
+    const bool vec = (d % 4 == 0) && ((uintptr_t)A % 16 == 0) && (dprev == nullptr || (uintptr_t)dprev % 16 == 0);
     char name[80];
     snprintf(name, sizeof name, "head_softmax_xent[rows=%d,d=%d,C=%d,dgrad=%d]", rows, d, C, dprev ? 1 : 0);
     if (h) h->before(name, s);
-    head_kernel<<<blocks, HEAD_WARPS * 32, smem, s>>>(rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL, dprev,
-                                                       loss_rows, loss_part, ticket, loss_out);
+    cudaError_t e;
+#define HEAD_CASE3(NVv, CMv)                                                                                   \
+    e = vec ? launch_head<NVv, true, CMv>(blocks, smem, s, rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL, dprev, \
+                                          loss_rows, loss_part, ticket, loss_out)                              \
+            : launch_head<NVv, false, CMv>(blocks, smem, s, rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL,     \
+                                           dprev, loss_rows, loss_part, ticket, loss_out)
+#define HEAD_CASE(NVv)             \
+    if (C <= 2) {                  \
+        HEAD_CASE3(NVv, 2);        \
+    } else if (C <= 4) {           \
+        HEAD_CASE3(NVv, 4);        \
+    } else {                       \
+        HEAD_CASE3(NVv, 16);       \
+    }
+    if (d <= 128) { HEAD_CASE(1); }
+    else if (d <= 256) { HEAD_CASE(2); }
+    else if (d <= 512) { HEAD_CASE(4); }
+    else { HEAD_CASE(8); }
+#undef HEAD_CASE
+#undef HEAD_CASE3
     if (h) h->after(name, s);
-    return cudaGetLastError();
+    return e;
 }
 
 // ------------------------------------------------------------------ deterministic block sum

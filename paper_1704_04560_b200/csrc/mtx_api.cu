@@ -60,13 +60,15 @@ struct TimingHook : LaunchHook {
     void before(const char *name, cudaStream_t s) override {
         if (counting) count++;
         if (!enabled || used + 2 > ev.size()) return;
-        cudaEventRecord(ev[used], s);
+        // External records become event-record nodes of the captured graph (a plain record
+        // inside a capture is only a dependency marker), so the pairs time device execution.
+        cudaEventRecordWithFlags(ev[used], s, cudaEventRecordExternal);
         names.push_back(name);
         used++;
     }
     void after(const char *, cudaStream_t s) override {
         if (!enabled || used % 2 == 0) return;
-        cudaEventRecord(ev[used], s);
+        cudaEventRecordWithFlags(ev[used], s, cudaEventRecordExternal);
         used++;
     }
     void ensure() {
@@ -122,6 +124,7 @@ struct mtx_ctx {
     unsigned long long *dig = nullptr;
     float *loss_part = nullptr;
     unsigned *ticket = nullptr;
+    unsigned *counters = nullptr;  // tensor-core split-K tile counters
     uint64_t *proto = nullptr;  // P x 8 bytes for the model-digest allgather
     // CNN activations
     std::vector<float *> convR, convP, convDR, convDP;
@@ -321,7 +324,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
                 partial = std::max<int64_t>(partial, (int64_t)tc_choose_splits(148, (int)b, (int)N, (int)(M - 1)) * b * N);
                 partial = std::max<int64_t>(partial, (int64_t)tc_choose_splits(148, (int)b, (int)(M - 1), (int)N) * b * (M - 1));
             }
-            if (N <= 16) partial = std::max<int64_t>(partial, 296 * M * N);  // wgrad_narrow
+            if (N <= 16) partial = std::max<int64_t>(partial, 600 * M * N);  // wgrad_narrow
         }
     } else {
         for (auto &g : c->convs) {
@@ -353,7 +356,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
                 partial = std::max<int64_t>(partial, (int64_t)tc_choose_splits(148, (int)b, (int)N, (int)(M - 1)) * b * N);
                 partial = std::max<int64_t>(partial, (int64_t)tc_choose_splits(148, (int)b, (int)(M - 1), (int)N) * b * (M - 1));
             }
-            if (N <= 16) partial = std::max<int64_t>(partial, 296 * M * N);
+            if (N <= 16) partial = std::max<int64_t>(partial, 600 * M * N);
         }
     }
     // colsum (bias gradients) folds at most ceil(296 / ceil(N/32)) splits of N floats
@@ -368,6 +371,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     float *sx = (float *)take(4 * b * c->d0);
     int32_t *sy = (int32_t *)take(4 * b);
     float *loss_part = (float *)take(4 * 1024);
+    unsigned *counters = (unsigned *)take(4 * 256);
     uint8_t *misc = take(256 + 8 * (uint64_t)c->world);
     if (assign) {
         c->params = params; c->vel = vel; c->grads = grads; c->gather = gather;
@@ -377,6 +381,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         c->partial = part; c->partial_floats = partial;
         c->stage_x = sx; c->stage_y = sy;
         c->loss_part = loss_part;
+        c->counters = counters;
         c->ticket = (unsigned *)(misc + 48);
         c->win = (int64_t *)misc;
         c->flag = (int *)(misc + 16);
@@ -396,6 +401,7 @@ struct Runner {
     mtx_status gemm(GemmDesc g) {
         g.partial = c->partial;
         g.partial_cap = c->partial_floats;
+        g.counters = c->counters;
         if (g.arow.win) g.a_rows_total = c->n_data + c->B;
         cudaError_t e;
         g.tf32x3 = c->opt.precision == MTX_3XTF32;
@@ -655,27 +661,21 @@ mtx_status capture(mtx_ctx *c, cudaStream_t s, bool staged, bool timed, cudaGrap
     return MTX_OK;
 }
 
-// One step = one launch of the captured graph (captured on first use).  Timing mode instead
-// launches the step eagerly with an event pair around every kernel, behind a 2 ms GPU spin so
-// the host has enqueued the whole step before the GPU reaches it: each pair then brackets
-// device time only.  The step synchronises and the pairs are accumulated.
+// One step = one launch of the captured graph (captured on first use).  Timing mode runs a
+// second captured graph whose every kernel is bracketed by event-record nodes
+// (cudaEventRecordExternal), so each pair measures device time inside the replayed graph;
+// the step then synchronises and the pairs are accumulated.
 mtx_status run_step(mtx_ctx *c, cudaStream_t s, bool staged) {
-    if (c->timing) {
-        c->hook.begin_capture();
-        c->hook.enabled = true;
-        CK(gpu_spin(2000000, s));
-        Runner r{c, s, staged, &c->hook};
-        mtx_status st = r.step();
-        c->hook.enabled = false;
-        if (st) return st;
+    const int gi = staged ? 1 : 0;
+    const bool timed = c->timing;
+    cudaGraphExec_t *slot = timed ? &c->graph_timed[gi] : &c->graph[gi];
+    mtx_status st;
+    if (!*slot && (st = capture(c, s, staged, timed, slot))) return st;
+    CK(cudaGraphLaunch(*slot, s));
+    if (timed) {
         CK(cudaStreamSynchronize(s));
         c->hook.accumulate();
-        return MTX_OK;
     }
-    const int gi = staged ? 1 : 0;
-    mtx_status st;
-    if (!c->graph[gi] && (st = capture(c, s, staged, false, &c->graph[gi]))) return st;
-    CK(cudaGraphLaunch(c->graph[gi], s));
     return MTX_OK;
 }
 
@@ -1058,6 +1058,7 @@ mtx_status mtx_debug_gemm(mtx_ctx *c, int32_t engine, int32_t M, int32_t N, int3
     g.bias = bias; g.mask = mask; g.ldm = ldm;
     g.partial = c->partial;
     g.partial_cap = c->partial_floats;
+    g.counters = c->counters;
     cudaStream_t s = pick(c, stream);
     cudaError_t e;
     if (engine == 1 || engine == 2) {
