@@ -139,15 +139,45 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(GemmDesc g) {
 __global__ void splitk_reduce_kernel(const float *__restrict__ partial, int splits, int M, int N, float *C,
                                      int64_t ldc, int epi, const float *__restrict__ bias,
                                      const float *__restrict__ mask, int64_t ldm) {
-    int64_t total = (int64_t)M * N;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        float s = partial[e];
-        for (int z = 1; z < splits; z++) s += partial[(int64_t)z * total + e];
-        const int64_t m = e / N, n = e % N;
-        if (epi == EPI_BIAS_RELU) s = fmaxf(s + bias[n], 0.f);
-        else if (epi == EPI_BIAS) s = s + bias[n];
-        else if (epi == EPI_MASK) s = mask[m * ldm + n] > 0.f ? s : 0.f;
-        C[m * ldc + n] = s;
+    const int64_t total = (int64_t)M * N;
+    // 4 consecutive elements per thread (float4 when the row holds them), splits loaded 8 at a time
+    const int64_t n4 = (total + 3) / 4;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n4; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e0 = 4 * q;
+        const bool vec = (N % 4 == 0) && (e0 + 3 < total);
+        float s[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int z0 = 0; z0 < splits; z0 += 8) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                if (z0 + u >= splits) break;
+                const float *src = partial + (int64_t)(z0 + u) * total + e0;
+                if (vec) {
+                    v[u] = __ldcg((const float4 *)src);
+                } else {
+                    v[u].x = __ldcg(src);
+                    v[u].y = e0 + 1 < total ? __ldcg(src + 1) : 0.f;
+                    v[u].z = e0 + 2 < total ? __ldcg(src + 2) : 0.f;
+                    v[u].w = e0 + 3 < total ? __ldcg(src + 3) : 0.f;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {  // ascending split order
+                if (z0 + u >= splits) break;
+                s[0] += v[u].x; s[1] += v[u].y; s[2] += v[u].z; s[3] += v[u].w;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const int64_t e = e0 + c;
+            if (e >= total) break;
+            const int64_t m = e / N, n = e % N;
+            float r = s[c];
+            if (epi == EPI_BIAS_RELU) r = fmaxf(r + bias[n], 0.f);
+            else if (epi == EPI_BIAS) r = r + bias[n];
+            else if (epi == EPI_MASK) r = mask[m * ldm + n] > 0.f ? r : 0.f;
+            C[m * ldc + n] = r;
+        }
     }
 }
 
@@ -184,7 +214,7 @@ cudaError_t gemm_simt(const GemmDesc &g, cudaStream_t s, LaunchHook *h) {
 cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float *C, int64_t ldc, cudaStream_t s,
                           LaunchHook *h, int epi, const float *bias, const float *mask, int64_t ldm) {
     int64_t total = (int64_t)M * N;
-    unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8));
+    unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total / 4 + 255) / 256, 148 * 8));
     char rn[80];
     snprintf(rn, sizeof rn, "splitk_reduce[M=%d,N=%d,splits=%d,epi=%d]", M, N, splits, epi);
     if (h) h->before(rn, s);
@@ -259,41 +289,64 @@ cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *
 }
 
 // ------------------------------------------------------------------ column sums (bias gradients)
-// Block (32 columns x 8 warps) over a contiguous K range: lane = column (128-B coalesced rows),
-// warp w sums rows k0 + w, k0 + w + 8, ... in order; the 8 warp sums are added in warp order.
+// Block = 8 warps over a contiguous K range; lane owns 4 consecutive columns (float4 loads, 128 B
+// per warp per row when 16-B aligned); warp w sums rows k0 + w, k0 + w + 8, ... in order (4 rows in
+// flight); the 8 warp sums are added in warp order; per-block partials are folded in block order.
 namespace {
+template <bool VEC>
 __global__ void __launch_bounds__(256) colsum_kernel(const float *__restrict__ X, int K, int N, int64_t ld,
                                                      int k_per, float *__restrict__ partial) {
-    __shared__ float sh[8][33];
+    __shared__ float4 sh[8][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int n = blockIdx.x * 32 + lane;
+    const int n = blockIdx.x * 128 + 4 * lane;
     const int k0 = blockIdx.y * k_per, k1 = min(K, k0 + k_per);
-    float acc = 0.f;
-    if (n < N)
-        for (int k = k0 + w; k < k1; k += 8) acc += X[(int64_t)k * ld + n];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto load = [&](int k) -> float4 {
+        const float *src = X + (int64_t)k * ld + n;
+        if (VEC && n + 3 < N) return __ldg((const float4 *)src);
+        return make_float4(n < N ? src[0] : 0.f, n + 1 < N ? src[1] : 0.f, n + 2 < N ? src[2] : 0.f,
+                           n + 3 < N ? src[3] : 0.f);
+    };
+    for (int k = k0 + w; k < k1; k += 32) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) v[u] = (k + 8 * u < k1) ? load(k + 8 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+        }
+    }
     sh[w][lane] = acc;
     __syncthreads();
-    if (w == 0 && n < N) {
-        float s = sh[0][lane];
+    if (w == 0) {
+        float4 s = sh[0][lane];
 #pragma unroll
-        for (int i = 1; i < 8; i++) s += sh[i][lane];
-        partial[(int64_t)blockIdx.y * N + n] = s;
+        for (int i = 1; i < 8; i++) {
+            s.x += sh[i][lane].x; s.y += sh[i][lane].y; s.z += sh[i][lane].z; s.w += sh[i][lane].w;
+        }
+        float *dst = partial + (int64_t)blockIdx.y * N + n;
+        if (n < N) dst[0] = s.x;
+        if (n + 1 < N) dst[1] = s.y;
+        if (n + 2 < N) dst[2] = s.z;
+        if (n + 3 < N) dst[3] = s.w;
     }
 }
 }  // namespace
 
 cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *partial, int64_t partial_cap,
                    cudaStream_t s, LaunchHook *h) {
-    const int cols = (N + 31) / 32;
-    int splits = std::max(1, std::min(K / 64, (2 * 148 + cols - 1) / cols));
+    const int cols = (N + 127) / 128;
+    int splits = std::max(1, std::min((K + 63) / 64, (2 * 148 + cols - 1) / cols));
     while (splits > 1 && (int64_t)splits * N > partial_cap) splits--;
     if (splits == 1 && partial_cap < N) return cudaErrorInvalidValue;
     const int k_per = (K + splits - 1) / splits;
     splits = (K + k_per - 1) / k_per;
+    const bool vec = (ld % 4 == 0) && ((uintptr_t)X % 16 == 0);
     char name[64];
     snprintf(name, sizeof name, "colsum[K=%d,N=%d,splits=%d]", K, N, splits);
     if (h) h->before(name, s);
-    colsum_kernel<<<dim3(cols, splits), 256, 0, s>>>(X, K, N, ld, k_per, partial);
+    if (vec) colsum_kernel<true><<<dim3(cols, splits), 256, 0, s>>>(X, K, N, ld, k_per, partial);
+    else colsum_kernel<false><<<dim3(cols, splits), 256, 0, s>>>(X, K, N, ld, k_per, partial);
     if (h) h->after(name, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -317,10 +370,24 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
                                                              float *__restrict__ dprev, float *__restrict__ loss_rows,
                                                              float *__restrict__ loss_part, unsigned *ticket,
                                                              float *__restrict__ loss_out) {
-    extern __shared__ float sW[];  // [(d+1)][C]
+    extern __shared__ __align__(16) float sW[];  // [(d+1)][C]
     __shared__ float swl[HEAD_WARPS];
     __shared__ bool last;
-    for (int e = threadIdx.x; e < (d + 1) * C; e += blockDim.x) sW[e] = Wb[e];
+    {   // stage W_L and b_L: float4 loads, 4 in flight per thread (the block is 16-B aligned)
+        const int n = (d + 1) * C, n4 = n / 4;
+        const float4 *W4 = (const float4 *)Wb;
+        float4 *s4 = (float4 *)sW;
+        for (int e = threadIdx.x; e < n4; e += 4 * blockDim.x) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (e + u * (int)blockDim.x < n4) v[u] = __ldg(W4 + e + u * blockDim.x);
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (e + u * (int)blockDim.x < n4) s4[e + u * blockDim.x] = v[u];
+        }
+        for (int e = 4 * n4 + threadIdx.x; e < n; e += blockDim.x) sW[e] = Wb[e];
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float *Abase = A + arow.row0() * (int64_t)d;
@@ -421,12 +488,21 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
         last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (last) {  // all partials loaded in parallel, then a fixed-shape tree: deterministic
         __threadfence();
-        float tot = 0.f;
-        for (unsigned bidx = 0; bidx < gridDim.x; bidx++) tot += ((volatile float *)loss_part)[bidx];
-        *loss_out = tot;
-        *ticket = 0u;  // re-armed for the next step
+        __shared__ float red[HEAD_WARPS * 32];
+        float v = 0.f;
+        for (unsigned bidx = threadIdx.x; bidx < gridDim.x; bidx += blockDim.x) v += __ldcg(loss_part + bidx);
+        red[threadIdx.x] = v;
+        __syncthreads();
+        for (int off = HEAD_WARPS * 16; off > 0; off >>= 1) {
+            if ((int)threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            *loss_out = red[0];
+            *ticket = 0u;  // re-armed for the next step
+        }
     }
 }
 
