@@ -130,7 +130,14 @@ def kernel_work(name: str):
 
 
 def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: str):
-    """Dominant kernel class (by total device time) -> achieved / peak."""
+    """Dominant kernel class (by total device time) -> achieved / peak.
+
+    Each kernel's event pair inside the timing graph also spans the graph's per-node launch
+    latency; the timing graph brackets an empty kernel the same way ("launch_overhead") and that
+    per-launch overhead is subtracted from every launch (clamped at 10% of the raw time)."""
+    cal = timing.pop("launch_overhead[calibration]", None)
+    over_ms = cal[0] / cal[1] if cal and cal[1] else 0.0
+    timing = {k: (max(ms - over_ms * cnt, 0.1 * ms), cnt) for k, (ms, cnt) in timing.items()}
     groups = {}
     for name, (ms, cnt) in timing.items():
         w = kernel_work(name)
@@ -173,6 +180,7 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
             "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic,
             "work_per_launch": per_launch_work, "launch_us": round(per_launch_s * 1e6, 3),
             "share_of_kernel_time": round(top["ms"] / total, 3),
+            "launch_overhead_us_subtracted": round(over_ms * 1e3, 3),
             "breakdown_us_per_step": {k: round(g["ms"] * 1e3 / steps, 2) for k, g in
                                       sorted(groups.items(), key=lambda kv: -kv[1]["ms"])}}
 

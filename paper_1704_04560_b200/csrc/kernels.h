@@ -89,6 +89,8 @@ cudaError_t ordered_fold(const float *gathered, int P, int64_t stride, int64_t n
 // Busy-waits ~ns nanoseconds on the GPU (timing pass: lets the host enqueue a whole step
 // before the GPU starts, so event pairs bracket device time only).
 cudaError_t gpu_spin(uint64_t ns, cudaStream_t s);
+// An empty kernel bracketed like every other launch site: the timing graph's per-launch overhead.
+cudaError_t empty_launch(cudaStream_t s, LaunchHook *h);
 
 // O2 init of one weight tensor: w[e] = (2u - 1) * lim, u = (H(H(seed, 16+t), e) >> 40) * 2^-24.
 cudaError_t init_glorot(float *w, int64_t n, uint64_t seed, int tensor_index, float lim, cudaStream_t s);

@@ -370,23 +370,29 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
                                                              float *__restrict__ dprev, float *__restrict__ loss_rows,
                                                              float *__restrict__ loss_part, unsigned *ticket,
                                                              float *__restrict__ loss_out) {
-    extern __shared__ __align__(16) float sW[];  // [(d+1)][C]
+    // W_L staged TRANSPOSED: sWt[j][k], row pitch dp = round_up(d + 1, 4) (k == d: bias), so a lane
+    // reads the weights of its 4 consecutive features as one conflict-free 128-bit load
+    extern __shared__ __align__(16) float sWt[];
     __shared__ float swl[HEAD_WARPS];
     __shared__ bool last;
-    {   // stage W_L and b_L: float4 loads, 4 in flight per thread (the block is 16-B aligned)
-        const int n = (d + 1) * C, n4 = n / 4;
-        const float4 *W4 = (const float4 *)Wb;
-        float4 *s4 = (float4 *)sW;
-        for (int e = threadIdx.x; e < n4; e += 4 * blockDim.x) {
-            float4 v[4];
+    const int dp = (d + 1 + 3) & ~3;
+    {
+        const int n = (d + 1) * C;
+        for (int e0 = threadIdx.x; e0 < n; e0 += 4 * blockDim.x) {
+            float v[4];
 #pragma unroll
-            for (int u = 0; u < 4; u++)
-                if (e + u * (int)blockDim.x < n4) v[u] = __ldg(W4 + e + u * blockDim.x);
+            for (int u = 0; u < 4; u++) {
+                const int e = e0 + u * blockDim.x;
+                v[u] = e < n ? __ldg(Wb + e) : 0.f;
+            }
 #pragma unroll
-            for (int u = 0; u < 4; u++)
-                if (e + u * (int)blockDim.x < n4) s4[e + u * blockDim.x] = v[u];
+            for (int u = 0; u < 4; u++) {
+                const int e = e0 + u * blockDim.x;
+                if (e < n) sWt[(e % C) * dp + e / C] = v[u];
+            }
         }
-        for (int e = 4 * n4 + threadIdx.x; e < n; e += blockDim.x) sW[e] = Wb[e];
+        const int pad = dp - d - 1;  // zero the row padding: it meets zero features in 128-bit reads
+        for (int e = threadIdx.x; e < C * pad; e += blockDim.x) sWt[(e / pad) * dp + d + 1 + e % pad] = 0.f;
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -411,22 +417,26 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
 #pragma unroll
         for (int j = 0; j < HEAD_MAXC; j++) z[j] = 0.f;
 #pragma unroll
-        for (int t = 0; t < NV; t++)
+        for (int t = 0; t < NV; t++) {
+            const int k = 4 * lane + 128 * t;
+            if (k < d) {
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int k = 4 * lane + 128 * t + u;
-                if (k < d) {
-#pragma unroll
-                    for (int j = 0; j < HEAD_MAXC; j++)
-                        if (j < C) z[j] = __fmaf_rn(av[t][u], sW[k * C + j], z[j]);
-                }
+                for (int j = 0; j < HEAD_MAXC; j++)
+                    if (j < C) {
+                        const float4 w = *(const float4 *)(sWt + j * dp + k);  // features k..k+3 (zero-padded)
+                        z[j] = __fmaf_rn(av[t][0], w.x, z[j]);
+                        z[j] = __fmaf_rn(av[t][1], w.y, z[j]);
+                        z[j] = __fmaf_rn(av[t][2], w.z, z[j]);
+                        z[j] = __fmaf_rn(av[t][3], w.w, z[j]);
+                    }
             }
+        }
 #pragma unroll
         for (int j = 0; j < HEAD_MAXC; j++) {
             if (j < C) {
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) z[j] += __shfl_xor_sync(0xffffffffu, z[j], o);
-                z[j] += sW[d * C + j];  // bias after the full sum
+                z[j] += sWt[j * dp + d];  // bias after the full sum
             }
         }
         float m = z[0];
@@ -457,16 +467,19 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
 #pragma unroll
             for (int t = 0; t < NV; t++) {
                 const int k = 4 * lane + 128 * t;
-                float o[4];
+                if (k >= d) continue;
+                float o[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    float sacc = 0.f;
-                    if (k + u < d) {
-#pragma unroll
-                        for (int j = 0; j < HEAD_MAXC; j++) if (j < C) sacc = __fmaf_rn(dz[j], sW[(k + u) * C + j], sacc);
+                for (int j = 0; j < HEAD_MAXC; j++)
+                    if (j < C) {
+                        const float4 w = *(const float4 *)(sWt + j * dp + k);
+                        o[0] = __fmaf_rn(dz[j], w.x, o[0]);
+                        o[1] = __fmaf_rn(dz[j], w.y, o[1]);
+                        o[2] = __fmaf_rn(dz[j], w.z, o[2]);
+                        o[3] = __fmaf_rn(dz[j], w.w, o[3]);
                     }
-                    o[u] = av[t][u] > 0.f ? sacc : 0.f;
-                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) o[u] = av[t][u] > 0.f ? o[u] : 0.f;
                 if (VEC && k + 3 < d) {
                     *(float4 *)(dprev + (int64_t)i * d + k) = make_float4(o[0], o[1], o[2], o[3]);
                 } else {
@@ -524,7 +537,7 @@ cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, cons
                        RowSel lrow, float inv_b, float *dZL, float *dprev, float *loss_rows, float *loss_part,
                        unsigned *ticket, float *loss_out, cudaStream_t s, LaunchHook *h) {
     if (C > 16 || C < 1 || d > 1024) return cudaErrorInvalidValue;
-    const size_t smem = sizeof(float) * (size_t)(d + 1) * C;
+    const size_t smem = sizeof(float) * (size_t)((d + 1 + 3) & ~3) * C;
     // enough rows per block that the block count stays <= 1024 (loss partial slots)
     const unsigned blocks = std::min<unsigned>(cdiv(rows, HEAD_WARPS), 1024u);
     const bool vec = (d % 4 == 0) && ((uintptr_t)A % 16 == 0) && (dprev == nullptr || (uintptr_t)dprev % 16 == 0);
@@ -707,6 +720,7 @@ __global__ void digest_kernel(const uint32_t *__restrict__ x, int64_t n, uint64_
 }  // namespace
 
 namespace {
+__global__ void empty_kernel() {}
 __global__ void spin_kernel(uint64_t ns) {
     uint64_t t0, t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -715,6 +729,13 @@ __global__ void spin_kernel(uint64_t ns) {
     } while (t - t0 < ns);
 }
 }  // namespace
+
+cudaError_t empty_launch(cudaStream_t s, LaunchHook *h) {
+    if (h) h->before("launch_overhead[calibration]", s);
+    empty_kernel<<<1, 32, 0, s>>>();
+    if (h) h->after("launch_overhead[calibration]", s);
+    return cudaGetLastError();
+}
 
 cudaError_t gpu_spin(uint64_t ns, cudaStream_t s) {
     spin_kernel<<<1, 1, 0, s>>>(ns);
