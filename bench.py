@@ -219,6 +219,9 @@ def main():
     ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "tf32", "3xtf32"])
     ap.add_argument("--impl", default="mtx", choices=["mtx", "reference"])
     ap.add_argument("--bucket-mb", type=float, default=1.0)
+    ap.add_argument("--reduce", default="fused", choices=["nccl", "ordered", "fused"],
+                    help="gradient allreduce (N > 1): NCCL per bucket, ORDERED test mode, or the averaging "
+                         "operator fused with its collective over NVLink peer memory")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -265,8 +268,9 @@ def main():
         args.precision, P.MTX_3XTF32 if tc_ok else P.MTX_FP32)
     uid = P.nccl_uid_broadcast(rank, world)
     X, y = S.dataset(cfg)
+    reduce = {"nccl": P.MTX_REDUCE_NCCL, "ordered": P.MTX_REDUCE_ORDERED, "fused": P.MTX_REDUCE_FUSED}[args.reduce]
     rep = P.Replica(cfg, rank=rank, world=world, uid=uid, device=local, precision=prec,
-                    bucket_bytes=int(args.bucket_mb * (1 << 20)))
+                    bucket_bytes=int(args.bucket_mb * (1 << 20)), reduce=reduce if world > 1 else P.MTX_REDUCE_NCCL)
     rep.bcast()
     rep.shard(X, y)
     s = rep.stream
@@ -353,7 +357,8 @@ def main():
                 "data": "synthetic",
                 "config": {"workload": f"{args.config}: {desc(cfg)}", "global_batch": cfg["B"],
                            "local_batch": cfg["B"] // world, "parallelism": f"dp{world}",
-                           "bucket_mb": args.bucket_mb, "l2": "flushed (256 MiB write) before every timed step",
+                           "bucket_mb": args.bucket_mb, "reduce": args.reduce if world > 1 else "none (P=1)",
+                           "l2": "flushed (256 MiB write) before every timed step",
                            "engine": mtx.mtx_build_info()},
                 "per_rank_ms": [round(t, 3) for t in t_all], "final_loss": loss,
                 "gpu_launches": launches * args.steps, "launches_per_step": launches,

@@ -80,10 +80,17 @@ typedef enum { MTX_MLP = 0, MTX_CNN = 1 } mtx_model_kind;
 typedef enum { MTX_FP32 = 0, MTX_TF32 = 1, MTX_3XTF32 = 2 } mtx_precision;
 
 /* How the gradient allreduce-sum is computed (reading A2).
- *  MTX_REDUCE_NCCL:    ncclAllReduce(sum) -- NCCL's order (ring/tree/NVLS).
+ *  MTX_REDUCE_NCCL:    ncclAllReduce(sum) per bucket on a comm stream -- NCCL's order
+ *                      (ring/tree/NVLS) -- then the fused average + update kernel.
  *  MTX_REDUCE_ORDERED: ncclAllGather + an ascending-rank left fold kernel; bit-exact
- *                      with the oracle's fold (test mode, P x the gradient memory). */
-typedef enum { MTX_REDUCE_NCCL = 0, MTX_REDUCE_ORDERED = 1 } mtx_reduce_mode;
+ *                      with the oracle's fold (test mode, P x the gradient memory).
+ *  MTX_REDUCE_FUSED:   the averaging operator fused with its collective over NVLink peer
+ *                      memory (CUDA IPC mappings exchanged at bind time, world <= 8 on one
+ *                      node): rank r pulls every rank's gradient on its 1/P slice, folds them
+ *                      in ascending rank order (bit-exact with ORDERED), applies x fl(1/P) and
+ *                      the momentum update, and stores w, v, G into every replica; two
+ *                      cross-GPU flag barriers (10 s timeout -> MTX_ERR_NCCL) bracket it. */
+typedef enum { MTX_REDUCE_NCCL = 0, MTX_REDUCE_ORDERED = 1, MTX_REDUCE_FUSED = 2 } mtx_reduce_mode;
 
 typedef struct {
     int32_t kind;            /* mtx_model_kind */
@@ -195,6 +202,13 @@ mtx_status mtx_train_step_host(mtx_ctx *ctx, const float *X_host, const int32_t 
  * the context's numeric flag (MTX_ERR_NUMERIC at the next sync). */
 mtx_status mtx_allreduce_avg(mtx_ctx *ctx, float *grad, float *param, float *velocity, uint64_t count, float lr,
                              float momentum, int32_t apply_update, void *stream);
+
+/* The MPI_Allreduce operator of P:298-306 on the gradient buffer as it stands (e.g. written by
+ * mtx_set_buffer(MTX_BUF_GRADS) from a user's own backward pass): exactly the reduction path
+ * mtx_train_step uses (per-bucket NCCL, ORDERED or FUSED), x fl(1/P), momentum update of the
+ * parameters/velocity; G stays in the gradient buffer (SPEC's sync_gradients + apply_update,
+ * S:258-275).  Collective; synchronous; MTX_ERR_NUMERIC on a non-finite average. */
+mtx_status mtx_sync_update(mtx_ctx *ctx, void *stream);
 
 /* ---------------------------------------------------------------- state access (tests, checkpoints) */
 

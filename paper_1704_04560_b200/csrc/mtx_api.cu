@@ -8,6 +8,7 @@
 // distribute datasets" -> mtx_shard_data; the training regime of
 // the user script (Fig. 7) -> mtx_train_step.
 #include <math.h>
+#include <cuda.h>
 #include <nccl.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -21,6 +22,7 @@
 #include "../../include/mtx.h"
 #include "gemm_tc.h"
 #include "kernels.h"
+#include "p2p_fused.h"
 
 using namespace mtx;
 
@@ -125,6 +127,11 @@ struct mtx_ctx {
     float *loss_part = nullptr;
     unsigned *ticket = nullptr;
     unsigned *counters = nullptr;  // tensor-core split-K tile counters
+    // MTX_REDUCE_FUSED: peer mappings of every rank's workspace
+    PeerPtrs pp{};
+    std::vector<void *> ipc_opened;
+    uint64_t *epoch = nullptr, *flags = nullptr;
+    bool fused = false;
     uint64_t *proto = nullptr;  // P x 8 bytes for the model-digest allgather
     // CNN activations
     std::vector<float *> convR, convP, convDR, convDP;
@@ -372,7 +379,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     int32_t *sy = (int32_t *)take(4 * b);
     float *loss_part = (float *)take(4 * 1024);
     unsigned *counters = (unsigned *)take(4 * 256);
-    uint8_t *misc = take(256 + 8 * (uint64_t)c->world);
+    uint8_t *misc = take(512 + 128 * (uint64_t)c->world);
     if (assign) {
         c->params = params; c->vel = vel; c->grads = grads; c->gather = gather;
         c->acts = acts; c->fcA = fcA;
@@ -386,7 +393,9 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         c->win = (int64_t *)misc;
         c->flag = (int *)(misc + 16);
         c->dig = (unsigned long long *)(misc + 32);
-        c->proto = (uint64_t *)(misc + 256);
+        c->epoch = (uint64_t *)(misc + 64);
+        c->flags = (uint64_t *)(misc + 128);  // MAX_PEERS epochs
+        c->proto = (uint64_t *)(misc + 512);  // world x 128 B: model digests / IPC handle records
     }
     return off + 256;
 }
@@ -504,6 +513,17 @@ struct Runner {
 
     mtx_status reduce_update(const Bucket &bkt, bool last) {
         const float invP = 1.0f / (float)c->world;
+        if (c->fused) {  // one fused collective + update over the whole buffer after the last wgrad
+            if (!last) return MTX_OK;
+            int64_t *win = staged ? nullptr : c->win;
+            cudaError_t e = peer_barrier(c->pp, c->world, c->rank, c->epoch, c->flag, s, h);
+            if (e == cudaSuccess)
+                e = fused_avg_update(c->pp, c->world, c->rank, c->N_pad, c->opt.lr, c->opt.momentum,
+                                     c->opt.momentum != 0.f, c->flag, win, c->B, c->n_data, s, h);
+            if (e == cudaSuccess) e = peer_barrier(c->pp, c->world, c->rank, c->epoch, c->flag, s, h);
+            if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "fused update: %s", cudaGetErrorString(e));
+            return MTX_OK;
+        }
         int64_t upd_hi = std::min<int64_t>(bkt.hi, c->N_pad);
         int64_t *win = (last && !staged) ? c->win : nullptr;
         if (c->world == 1) {
@@ -534,6 +554,23 @@ struct Runner {
         cudaError_t e = avg_update(c->grads + bkt.lo, c->params + bkt.lo, vel_or_null(bkt.lo), upd_hi - bkt.lo, invP,
                                    c->opt.lr, c->opt.momentum, c->flag, win, c->B, c->n_data, c->comm_s, h);
         if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "update: %s", cudaGetErrorString(e));
+        return MTX_OK;
+    }
+
+    // Reduction + update of every bucket with no backward pass (mtx_sync_update).
+    mtx_status sync_update_only() {
+        if (c->world > 1) {
+            CK(cudaEventRecord(c->ev_fork, s));
+            CK(cudaStreamWaitEvent(c->comm_s, c->ev_fork, 0));
+        }
+        for (size_t i = 0; i < c->buckets.size(); i++) {
+            mtx_status st = reduce_update(c->buckets[i], i + 1 == c->buckets.size());
+            if (st) return st;
+        }
+        if (c->world > 1) {
+            CK(cudaEventRecord(c->ev_join, c->comm_s));
+            CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+        }
         return MTX_OK;
     }
 
@@ -686,11 +723,12 @@ mtx_status run_step(mtx_ctx *c, cudaStream_t s, bool staged) {
 
 // D2H of the loss slot and numeric flag, synchronise, then report.
 mtx_status sync_loss(mtx_ctx *c, cudaStream_t s, float *host_loss) {
-    CK(cudaMemcpyAsync(c->h_loss, c->grads + c->N_pad, sizeof(float), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->h_loss, c->grads + c->N_pad + (c->fused ? 1 : 0), sizeof(float), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     c->last_loss = (float)((double)c->h_loss[0] / (double)c->B);
     if (host_loss) *host_loss = c->last_loss;
+    if (c->h_flag[0] & 2) return fail(c, MTX_ERR_NCCL, "peer barrier timeout (a rank did not reach the step)");
     if (c->h_flag[0]) return fail(c, MTX_ERR_NUMERIC, "non-finite averaged gradient");
     return MTX_OK;
 }
@@ -699,11 +737,60 @@ mtx_status check_flag(mtx_ctx *c, cudaStream_t s) {
     if (!c->flag) return MTX_OK;
     CK(cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (c->h_flag[0] & 2) return fail(c, MTX_ERR_NCCL, "peer barrier timeout (a rank did not reach the step)");
     if (c->h_flag[0]) return fail(c, MTX_ERR_NUMERIC, "non-finite averaged gradient");
     return MTX_OK;
 }
 
 }  // namespace
+
+// MTX_REDUCE_FUSED: export this rank's workspace allocation as a CUDA IPC handle, allgather the
+// (handle, offset) records over NCCL, and map every peer's workspace.  All ranks carve identical
+// layouts, so a peer buffer is the peer's workspace base plus the local buffer's offset.
+typedef CUresult (*GetAddrRange)(CUdeviceptr *, size_t *, CUdeviceptr);
+
+mtx_status map_peers(mtx_ctx *c) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+        return fail(c, MTX_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (((GetAddrRange)fn)(&base, &size, (CUdeviceptr)c->ws) != CUDA_SUCCESS)
+        return fail(c, MTX_ERR_CUDA, "cuMemGetAddressRange failed");
+    struct Rec {
+        cudaIpcMemHandle_t h;
+        int64_t off;
+        uint8_t pad[128 - sizeof(cudaIpcMemHandle_t) - 8];
+    } mine{};
+    static_assert(sizeof(Rec) == 128, "record size");
+    CK(cudaIpcGetMemHandle(&mine.h, (void *)base));
+    mine.off = (int64_t)((uint8_t *)c->ws - (uint8_t *)base);
+    uint8_t *dev = (uint8_t *)c->proto;
+    CK(cudaMemcpyAsync(dev + 128 * c->rank, &mine, 128, cudaMemcpyHostToDevice, c->own));
+    NK(ncclAllGather(dev + 128 * c->rank, dev, 128, ncclUint8, c->comm, c->own));
+    std::vector<Rec> all(c->world);
+    CK(cudaMemcpyAsync(all.data(), dev, 128 * c->world, cudaMemcpyDeviceToHost, c->own));
+    CK(cudaStreamSynchronize(c->own));
+    auto rel = [&](void *p) { return (int64_t)((uint8_t *)p - c->ws); };
+    for (int r = 0; r < c->world; r++) {
+        uint8_t *ws_r;
+        if (r == c->rank) {
+            ws_r = c->ws;
+        } else {
+            void *p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, all[r].h, cudaIpcMemLazyEnablePeerAccess));
+            c->ipc_opened.push_back(p);
+            ws_r = (uint8_t *)p + all[r].off;
+        }
+        c->pp.g[r] = c->pp.G[r] = (float *)(ws_r + rel(c->grads));
+        c->pp.w[r] = (float *)(ws_r + rel(c->params));
+        c->pp.v[r] = (float *)(ws_r + rel(c->vel));
+        c->pp.flags[r] = (uint64_t *)(ws_r + rel(c->flags));
+    }
+    c->fused = true;
+    return MTX_OK;
+}
 
 // =================================================================== C-ABI
 extern "C" {
@@ -725,7 +812,9 @@ mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t ui
     if (model->global_batch <= 0 || model->global_batch % world) return MTX_ERR_INVALID_ARG;
     if (opt->precision != MTX_FP32 && opt->precision != MTX_TF32 && opt->precision != MTX_3XTF32)
         return MTX_ERR_INVALID_ARG;
-    if (opt->reduce != MTX_REDUCE_NCCL && opt->reduce != MTX_REDUCE_ORDERED) return MTX_ERR_INVALID_ARG;
+    if (opt->reduce != MTX_REDUCE_NCCL && opt->reduce != MTX_REDUCE_ORDERED && opt->reduce != MTX_REDUCE_FUSED)
+        return MTX_ERR_INVALID_ARG;
+    if (opt->reduce == MTX_REDUCE_FUSED && world > MAX_PEERS) return MTX_ERR_UNSUPPORTED;
     mtx_ctx *c = new mtx_ctx();
     c->rank = rank;
     c->world = world;
@@ -828,6 +917,7 @@ mtx_status mtx_bind_workspace(mtx_ctx *c, void *dev_ptr, uint64_t bytes) {
         for (int r = 0; r < c->world; r++)
             if (all[r] != mine) return fail(c, MTX_ERR_PROTOCOL, "rank %d model digest differs from rank %d", r, c->rank);
     }
+    if (c->world > 1 && c->opt.reduce == MTX_REDUCE_FUSED && (st = map_peers(c))) return st;
     CK(cudaStreamSynchronize(c->own));
     c->state = mtx_ctx::S_BOUND;
     return MTX_OK;
@@ -952,6 +1042,18 @@ mtx_status mtx_allreduce_avg(mtx_ctx *c, float *grad, float *param, float *veloc
                       h));
     }
     return MTX_OK;
+}
+
+mtx_status mtx_sync_update(mtx_ctx *c, void *stream) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (c->state == mtx_ctx::S_INIT) return fail(c, MTX_ERR_STATE, "bind the workspace first");
+    cudaStream_t s = pick(c, stream);
+    CK(cudaDeviceSynchronize());
+    // the window counter must not advance: staged = true keeps win untouched
+    Runner r{c, s, true, nullptr};
+    if ((st = r.sync_update_only())) return st;
+    return sync_loss(c, s, nullptr);
 }
 
 mtx_status mtx_get_buffer(mtx_ctx *c, int32_t which, float *host_out, uint64_t count) {
@@ -1098,6 +1200,7 @@ mtx_status mtx_finalize(mtx_ctx *c) {
         if (g) cudaGraphExecDestroy(g);
     for (auto &g : c->graph_timed)
         if (g) cudaGraphExecDestroy(g);
+    for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
     if (c->comm) ncclCommDestroy(c->comm);
     for (auto &e : c->ev_bucket) cudaEventDestroy(e);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);

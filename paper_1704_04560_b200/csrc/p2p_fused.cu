@@ -1,0 +1,146 @@
+// p2p_fused.cu -- the averaging operator fused with its collective over NVLink peer memory
+// ("MPI_Allreduce ... averaging gradients").
+//
+// Every rank maps every other rank's workspace (CUDA IPC, handles exchanged over NCCL at
+// bind time).  After the backward pass:
+//   peer_barrier   -- each rank signals "gradient ready" to all peers and waits for all of them
+//   fused_avg_update -- rank r owns slice S_r of the flat buffer: it loads g_0..g_{P-1} on S_r
+//                     (local + NVLink loads), folds them in ascending rank order (the oracle's
+//                     left fold, reading A2), ḡ = G·fl(1/P), v = fma(mu,v,ḡ), w = fma(-lr,v,w),
+//                     and stores w, v, G to its own buffers and to every peer (NVLink stores)
+//   peer_barrier   -- "my slice is published"; afterwards every replica holds identical w, v, G
+// Each element is computed by exactly one rank, so replicas are bit-identical, and the sum is
+// bit-exact with MTX_REDUCE_ORDERED and with the oracle's f32 fold of the same g_r.
+// Barriers spin on flags written by peers with a timeout: a missing peer sets an error bit
+// instead of hanging the GPU.
+#include <stdio.h>
+
+#include "p2p_fused.h"
+
+namespace mtx {
+namespace {
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void peer_barrier_kernel(PeerPtrs pp, int P, int rank, uint64_t *epoch_ctr, int *errflag,
+                                    uint64_t timeout_ns) {
+    __shared__ uint64_t epoch;
+    if (threadIdx.x == 0) {
+        epoch = *epoch_ctr + 1;
+        *epoch_ctr = epoch;
+    }
+    __syncthreads();
+    __threadfence_system();
+    const int q = threadIdx.x;
+    if (q < P) st_release_sys(pp.flags[q] + rank, epoch);  // "rank arrived" in q's flag array
+    if (q < P) {
+        const uint64_t *mine = pp.flags[rank] + q;
+        const uint64_t t0 = globaltimer();
+        while (ld_acquire_sys(mine) < epoch) {
+            if (globaltimer() - t0 > timeout_ns) {
+                atomicOr(errflag, 2);  // peer barrier timeout -> MTX_ERR_NCCL at the next sync
+                break;
+            }
+        }
+    }
+    __syncthreads();
+    __threadfence_system();
+}
+
+template <bool HAS_V>
+__global__ void __launch_bounds__(256) fused_avg_update_kernel(PeerPtrs pp, int P, int rank, int64_t lo4, int64_t hi4,
+                                                             float invP, float lr, float mu, int *flag, int64_t *win,
+                                                             int64_t B, int64_t n_data, int64_t loss_idx) {
+    bool bad = false;
+    for (int64_t i = lo4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float4 g[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+            if (q < P) g[q] = __ldcv((const float4 *)pp.g[q] + i);  // peer loads bypass stale caches
+        float4 G = g[0];
+#pragma unroll
+        for (int q = 1; q < 8; q++)
+            if (q < P) {  // ascending-rank left fold
+                G.x = __fadd_rn(G.x, g[q].x); G.y = __fadd_rn(G.y, g[q].y);
+                G.z = __fadd_rn(G.z, g[q].z); G.w = __fadd_rn(G.w, g[q].w);
+            }
+        const float4 w0 = ((const float4 *)pp.w[rank])[i];
+        float4 w = w0, v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (HAS_V) v = ((const float4 *)pp.v[rank])[i];
+        float gb[4] = {G.x * invP, G.y * invP, G.z * invP, G.w * invP};
+        float *pw = &w.x, *pv = &v.x;
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            bad |= !isfinite(gb[c]);
+            if (HAS_V) {
+                pv[c] = __fmaf_rn(mu, pv[c], gb[c]);
+                pw[c] = __fmaf_rn(-lr, pv[c], pw[c]);
+            } else {
+                pw[c] = __fmaf_rn(-lr, gb[c], pw[c]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+            if (q < P) {  // publish the owner's results to every replica (local store for q == rank)
+                __stcg((float4 *)pp.w[q] + i, w);
+                if (HAS_V) __stcg((float4 *)pp.v[q] + i, v);
+                __stcg((float4 *)pp.G[q] + i, G);
+            }
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // the loss slot: every rank folds all ranks' local loss sums itself (same order, same bits)
+        float L = __ldcv(pp.g[0] + loss_idx);
+        for (int q = 1; q < P; q++) L = __fadd_rn(L, __ldcv(pp.g[q] + loss_idx));
+        pp.G[rank][loss_idx + 1] = L;  // slot 0 keeps this rank's local sum (peers may still read it)
+        if (win) *win = (*win + B) % n_data;
+    }
+}
+
+}  // namespace
+
+cudaError_t peer_barrier(const PeerPtrs &pp, int P, int rank, uint64_t *epoch_ctr, int *errflag, cudaStream_t s,
+                         LaunchHook *h) {
+    char name[32];
+    snprintf(name, sizeof name, "peer_barrier[P=%d]", P);
+    if (h) h->before(name, s);
+    peer_barrier_kernel<<<1, 32, 0, s>>>(pp, P, rank, epoch_ctr, errflag, 10000000000ull);
+    if (h) h->after(name, s);
+    return cudaGetLastError();
+}
+
+cudaError_t fused_avg_update(const PeerPtrs &pp, int P, int rank, int64_t n_pad, float lr, float mu, bool has_v,
+                             int *flag, int64_t *win, int64_t B, int64_t n_data, cudaStream_t s, LaunchHook *h) {
+    if (P > 8 || n_pad % 4) return cudaErrorInvalidValue;
+    const int64_t n4 = n_pad / 4;
+    const int64_t lo4 = n4 * rank / P, hi4 = n4 * (rank + 1) / P;
+    const int64_t mine = hi4 - lo4;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((mine + 255) / 256, 148 * 4));
+    char name[96];
+    snprintf(name, sizeof name, "fused_avg_update[n=%lld,P=%d,v=%d]", (long long)n_pad, P, has_v ? 1 : 0);
+    if (h) h->before(name, s);
+    const float invP = 1.0f / (float)P;
+    if (has_v)
+        fused_avg_update_kernel<true><<<blocks, 256, 0, s>>>(pp, P, rank, lo4, hi4, invP, lr, mu, flag, win, B, n_data,
+                                                             n_pad);
+    else
+        fused_avg_update_kernel<false><<<blocks, 256, 0, s>>>(pp, P, rank, lo4, hi4, invP, lr, mu, flag, win, B,
+                                                              n_data, n_pad);
+    if (h) h->after(name, s);
+    return cudaGetLastError();
+}
+
+}  // namespace mtx

@@ -20,7 +20,7 @@ STATUS = ["MTX_OK", "MTX_ERR_INVALID_ARG", "MTX_ERR_STATE", "MTX_ERR_SHAPE", "MT
           "MTX_ERR_NUMERIC", "MTX_ERR_PROTOCOL", "MTX_ERR_OOM", "MTX_ERR_UNSUPPORTED"]
 MTX_MLP, MTX_CNN = 0, 1
 MTX_FP32, MTX_TF32, MTX_3XTF32 = 0, 1, 2
-MTX_REDUCE_NCCL, MTX_REDUCE_ORDERED = 0, 1
+MTX_REDUCE_NCCL, MTX_REDUCE_ORDERED, MTX_REDUCE_FUSED = 0, 1, 2
 MTX_BUF_PARAMS, MTX_BUF_VELOCITY, MTX_BUF_GRADS = 0, 1, 2
 
 
@@ -72,6 +72,7 @@ def _load():
         "mtx_set_timing": [vp, C.c_int32],
         "mtx_read_timing": [vp, C.c_char_p, C.c_uint64, C.POINTER(C.c_double), i64, C.c_int32, i32, C.c_int32],
         "mtx_finalize": [vp],
+        "mtx_sync_update": [vp, vp],
         "mtx_debug_gemm": [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp,
                            C.c_int64, vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_int64, vp],
     }
@@ -176,6 +177,10 @@ def mtx_allreduce_avg(ctx, grad: int, param: int | None, velocity: int | None, c
                       momentum: float, apply_update: int = 1, stream: int | None = None):
     _check(_lib.mtx_allreduce_avg(ctx, C.c_void_p(grad), C.c_void_p(param), C.c_void_p(velocity), count, lr,
                                   momentum, apply_update, C.c_void_p(stream)), ctx, "mtx_allreduce_avg")
+
+
+def mtx_sync_update(ctx, stream: int | None = None):
+    _check(_lib.mtx_sync_update(ctx, C.c_void_p(stream)), ctx, "mtx_sync_update")
 
 
 def mtx_get_buffer(ctx, which: int) -> np.ndarray:

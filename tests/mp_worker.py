@@ -121,6 +121,51 @@ def main():
                 e = maxrel(gpu[-1][2], w_ref)
                 check(e <= gtol, f"{name} weights err {e}")
                 report["checks"].append(f"{name} DP({world}) prec={prec} vs oracle ok")
+        # ---- the averaging operator on arbitrary fp32 gradients (mtx_sync_update): ORDERED and FUSED are
+        #      bit-exact with the oracle's f32 left fold + update; NCCL within the gamma_{P-1} bound
+        cfg = dict(S.CONFIGS["cfg2"], B=64 * world)
+        net = oracle.Net.from_cfg(cfg)
+        N = oracle.param_count(net)
+        rng = np.random.default_rng(123)
+        g_all = (rng.standard_normal((world, N)) * 10.0 ** rng.integers(-6, 0, (world, N))).astype(np.float32)
+        w0 = oracle.init_params(net, 42)
+        v0 = (rng.standard_normal(N) * 1e-3).astype(np.float32)
+        Gref = oracle.fold(g_all)
+        wref, vref = w0.copy(), v0.copy()
+        oracle.avg_update(Gref, wref, vref, world, cfg["lr"], cfg["mu"])
+        for mode in (P.MTX_REDUCE_ORDERED, P.MTX_REDUCE_FUSED, P.MTX_REDUCE_NCCL):
+            uid = P.nccl_uid_broadcast(rank, world)
+            r = P.Replica(cfg, rank=rank, world=world, uid=uid, device=rank, reduce=mode, bucket_bytes=1 << 20)
+            r.bcast()
+            r.set(P.MTX_BUF_PARAMS, w0)
+            r.set(P.MTX_BUF_VELOCITY, v0)
+            r.set(P.MTX_BUF_GRADS, g_all[rank])
+            mtx.mtx_sync_update(r.ctx, r.s)
+            G, wv, vv = r.get(P.MTX_BUF_GRADS), r.get(P.MTX_BUF_PARAMS), r.get(P.MTX_BUF_VELOCITY)
+            r.close()
+            if mode != P.MTX_REDUCE_NCCL or world == 2:
+                check(np.array_equal(G.view(np.uint32), Gref.view(np.uint32)), f"sync_update G mode {mode}")
+                check(np.array_equal(wv.view(np.uint32), wref.view(np.uint32)), f"sync_update w mode {mode}")
+                check(np.array_equal(vv.view(np.uint32), vref.view(np.uint32)), f"sync_update v mode {mode}")
+            else:
+                u = 2.0 ** -24
+                # both NCCL's order and the fold are within gamma_{P-1} sum|g| of the exact sum
+                bound = 2 * (world - 1) * u / (1 - (world - 1) * u) * np.abs(g_all.astype(np.float64)).sum(0)
+                check(np.all(np.abs(G.astype(np.float64) - Gref) <= bound + 1e-38), "NCCL G outside gamma bound")
+        report["checks"].append(f"sync_update ORDERED/FUSED bit-exact vs oracle fold at P={world}")
+
+        # ---- FUSED (NVLink peer-memory reduce + update) is bit-exact with ORDERED (same rank-ordered fold)
+        for prec in ([P.MTX_FP32, P.MTX_3XTF32] if "tcgen05" in mtx.mtx_build_info() else [P.MTX_FP32]):
+            for name, B, n in (("cfg1", 64, 1000), ("cfg2", 512, 4096)):
+                cfg = dict(S.CONFIGS[name], B=B)
+                X, y = S.mnist_like(1, n)
+                a = run_model(rank, world, cfg, X, y, 3, prec, P.MTX_REDUCE_ORDERED)
+                b = run_model(rank, world, cfg, X, y, 3, prec, P.MTX_REDUCE_FUSED)
+                for t, ((la, Ga, wa), (lb, Gb, wb)) in enumerate(zip(a, b)):
+                    check(np.array_equal(Ga.view(np.uint32), Gb.view(np.uint32)), f"FUSED != ORDERED G {name} step {t}")
+                    check(np.array_equal(wa.view(np.uint32), wb.view(np.uint32)), f"FUSED != ORDERED w {name} step {t}")
+                    check(la == lb, f"FUSED != ORDERED loss {name} step {t}: {la} {lb}")
+        report["checks"].append(f"fused == ordered bitwise at P={world}")
         # ---- ORDERED reduce reproduces NCCL at P = 2
         if world == 2:
             cfg = dict(S.CONFIGS["cfg1"], B=64)

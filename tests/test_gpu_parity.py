@@ -60,6 +60,31 @@ def test_fused_avg_update_bit_exact(n, mu):
         r.close()
 
 
+def test_sync_update_single_rank_bit_exact():
+    """mtx_sync_update at P = 1: G = the injected gradient; w, v bit-exact with the oracle's fp32 update."""
+    cfg = small_cfg("cfg2")
+    net = oracle.Net.from_cfg(cfg)
+    n = oracle.param_count(net)
+    rng = np.random.default_rng(9)
+    g = (rng.standard_normal(n) * 1e-2).astype(np.float32)
+    w0 = oracle.init_params(net, 42)
+    v0 = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    r = make(cfg, bucket_bytes=256 << 10)
+    try:
+        r.bcast()
+        r.set(P.MTX_BUF_PARAMS, w0)
+        r.set(P.MTX_BUF_VELOCITY, v0)
+        r.set(P.MTX_BUF_GRADS, g)
+        mtx.mtx_sync_update(r.ctx, r.s)
+        wo, vo = w0.copy(), v0.copy()
+        oracle.avg_update(g, wo, vo, 1, cfg["lr"], cfg["mu"])
+        assert np.array_equal(r.get(P.MTX_BUF_GRADS).view(np.uint32), g.view(np.uint32))
+        assert np.array_equal(r.get(P.MTX_BUF_PARAMS).view(np.uint32), wo.view(np.uint32))
+        assert np.array_equal(r.get(P.MTX_BUF_VELOCITY).view(np.uint32), vo.view(np.uint32))
+    finally:
+        r.close()
+
+
 def test_fused_update_flags_non_finite():
     r = make(small_cfg("cfg1", B=4, P=1))
     try:
