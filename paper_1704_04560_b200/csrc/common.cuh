@@ -2,6 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #define MTX_DEVI __device__ __forceinline__
 
@@ -26,5 +29,40 @@ struct RowSel {
     int64_t base;  // rank * b
     MTX_DEVI int64_t row0() const { return win ? (*win + base) : 0; }
 };
+
+// Programmatic dependent launch.  Every kernel of the step starts with pdl_wait()
+// (griddepcontrol.wait: returns once the preceding grid has completed and its memory is
+// visible; a no-op when the launch was not programmatic) and is launched with
+// launch_pdl(), so its launch and prologue overlap the predecessor's tail.
+// The trigger right after the wait lets the next kernel be launched as soon as every CTA of
+// this grid is running (its CTAs then park in their own wait until this grid completes).
+MTX_DEVI void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+    static const int on = [] {
+        const char *e = getenv("MTX_PDL");  // development A/B knob, default on
+        return e ? atoi(e) : 1;
+    }();
+    return on != 0;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace mtx

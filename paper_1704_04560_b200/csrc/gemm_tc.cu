@@ -118,6 +118,12 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])   \
         : "r"(taddr))
 
+#define TMEM_LD16(taddr, r)                                                                                      \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),   \
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) \
+                 : "r"(taddr))
+
 // UMMA shared-memory descriptor, version 1 (sm_100).  Verified on B200 with tools/tc_probe.cu:
 //   K-major : SWIZZLE_128B (type 2) -- 8-row x 128-B atoms (16-B chunks XOR row%8) stacked along
 //             M/N at SBO = 1024 B; LBO unused.  k-step of 8 tf32 = +32 B inside the row.
@@ -139,6 +145,50 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes,
 __host__ __device__ constexpr uint32_t instr_desc(int M, int N, int a_mn, int b_mn) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
            ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// Split-K fixup run by the last CTA of a tile (MTX_TC_FIXUP=1): fold all splits in ascending order,
+// coalesced -- the 256 epilogue threads sweep the 128 x BN tile row by row, one float4 each.
+// Kept out of line so its registers do not add to the epilogue's accumulator registers.
+template <int BN>
+__device__ __noinline__ void splitk_fixup(const TcParams &p, int r, int m0) {
+    {   // last CTA of the tile: fold all splits in ascending order, coalesced -- the 256
+        // epilogue threads sweep the 128 x BN tile row by row, one float4 each
+        const int et = threadIdx.x - 128;
+        const int mt0 = m0, nt0 = (r / p.tiles_m) * BN;
+        for (int idx = et; idx < BM * (BN / 4); idx += 256) {
+            const int mm = mt0 + idx / (BN / 4), nn = nt0 + 4 * (idx % (BN / 4));
+            if (mm >= p.M || nn >= p.N) continue;
+            const bool vec4 = nn + 3 < p.N;
+            float o[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int z0 = 0; z0 < p.splits; z0 += 4) {
+                float4 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    if (z0 + u >= p.splits) break;
+                    const float *src = p.partial + ((int64_t)(z0 + u) * p.M + mm) * p.N + nn;
+                    if (vec4) v[u] = __ldcg((const float4 *)src);
+                    else v[u] = make_float4(__ldcg(src), nn + 1 < p.N ? __ldcg(src + 1) : 0.f,
+                                            nn + 2 < p.N ? __ldcg(src + 2) : 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    if (z0 + u >= p.splits) break;
+                    o[0] += v[u].x; o[1] += v[u].y; o[2] += v[u].z; o[3] += v[u].w;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                if (nn + e >= p.N) break;
+                if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e] + p.bias[nn + e], 0.f);
+                else if (p.epi == EPI_BIAS) o[e] += p.bias[nn + e];
+                else if (p.epi == EPI_MASK && !(p.mask[(int64_t)mm * p.ldm + nn + e] > 0.f)) o[e] = 0.f;
+            }
+            float *dst = p.C + (int64_t)mm * p.ldc + nn;
+            if (vec4) *(float4 *)dst = make_float4(o[0], o[1], o[2], o[3]);
+            else for (int e = 0; e < 4 && nn + e < p.N; e++) dst[e] = o[e];
+        }
+    }
 }
 
 template <int BN, bool SPLIT>
@@ -182,6 +232,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // prologue above overlaps the previous kernel's tail (programmatic launch)
 
     const int tiles_mn = p.tiles_m * p.tiles_n;
     const int total = tiles_mn * p.splits;
@@ -320,15 +371,20 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
             for (int c0 = kb0; c0 < kb1; c0 += L::CHUNK) {
                 mbar_wait(tfull0 + 8 * buf, buf_phase);
                 tc_fence_after();
+                constexpr int CW = HALF >= 32 ? 32 : HALF;  // columns per tcgen05.ld
 #pragma unroll
-                for (int c = 0; c < HALF / 32; c++) {
-                    uint32_t v[32];
-                    const uint32_t taddr = tmem_base + buf * BN + ((uint32_t)(32 * q) << 16) + h * HALF + 32 * c;
-                    TMEM_LD32(taddr, v);
+                for (int c = 0; c < HALF / CW; c++) {
+                    uint32_t v[CW];
+                    const uint32_t taddr = tmem_base + buf * BN + ((uint32_t)(32 * q) << 16) + h * HALF + CW * c;
+                    if constexpr (CW == 32) {
+                        TMEM_LD32(taddr, v);
+                    } else {
+                        TMEM_LD16(taddr, v);
+                    }
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                    for (int j = 0; j < 32; j++)
-                        acc[32 * c + j] = first ? __uint_as_float(v[j]) : __fadd_rn(acc[32 * c + j], __uint_as_float(v[j]));
+                    for (int j = 0; j < CW; j++)
+                        acc[CW * c + j] = first ? __uint_as_float(v[j]) : __fadd_rn(acc[CW * c + j], __uint_as_float(v[j]));
                 }
                 first = false;
                 tc_fence_before();
@@ -356,25 +412,9 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                 asm volatile("bar.sync 1, 256;" ::: "memory");
                 if (!*fix_flag) continue;
                 __threadfence();
-                if (m < p.M) {
-#pragma unroll
-                    for (int g4 = 0; g4 < HALF / 4; g4++) {
-                        const int n = n0 + 4 * g4;
-                        if (n >= p.N) break;
-                        float o[4] = {0.f, 0.f, 0.f, 0.f};
-                        for (int zz = 0; zz < p.splits; zz++) {
-                            const float *src = p.partial + ((int64_t)zz * p.M + m) * p.N + n;
-                            if (n + 3 < p.N) {
-                                const float4 v = __ldcg((const float4 *)src);
-                                o[0] += v.x; o[1] += v.y; o[2] += v.z; o[3] += v.w;
-                            } else {
-                                for (int e = 0; e < 4 && n + e < p.N; e++) o[e] += __ldcg(src + e);
-                            }
-                        }
-                        acc[4 * g4] = o[0]; acc[4 * g4 + 1] = o[1]; acc[4 * g4 + 2] = o[2]; acc[4 * g4 + 3] = o[3];
-                    }
-                }
+                splitk_fixup<BN>(p, r, m0);
                 if (threadIdx.x == 128) p.counters[r] = 0u;  // re-armed for the next launch
+                continue;
             }
             if (m >= p.M) continue;
             float *dst_row = p.C + (int64_t)m * p.ldc;
@@ -439,20 +479,37 @@ bool make_map(EncodeTiled enc, CUtensorMap *m, const float *ptr, int64_t rows, i
 struct TcGemm {
     EncodeTiled encode = nullptr;
     int sms = 148;
-    bool attr_set[2] = {false, false};
-    bool fixup = false;  // split-K: fold in the last CTA per tile (measured slower on cfg2; MTX_TC_FIXUP=1)
+    bool attr_set[8] = {};
+    // split-K fold inside the kernel by the tile's last CTA (MTX_TC_FIXUP=1).  Off: a one-SM fold of
+    // splits x 64 KB is slower than the all-SM fold kernel on every measured shape.
+    bool fixup = false;
 };
 
 bool tc_available() { return true; }
 
-int tc_choose_splits(int sms, int M, int N, int K) {
-    const int tiles = ((M + BM - 1) / BM) * ((N + 127) / 128);
+// Tile plan: the widest N tile (128, 64, 32) that still gives >= sms/2 output tiles, then split K
+// only if the tile count is still below that (split-K costs a fold pass over the partials).
+TcPlan tc_plan(int sms, int M, int N, int K) {
+    TcPlan pl;
+    const int tm = (M + BM - 1) / BM;
+    const int kb_all = (K + BK - 1) / BK;
+    for (int bn : {128, 64, 32}) {
+        pl.bn = bn;
+        // long K: split-K of wide tiles keeps the per-flop smem traffic low and amortises its fold
+        if (tm * ((N + bn - 1) / bn) * 2 >= sms || kb_all >= 64) break;
+    }
+    const int tiles = tm * ((N + pl.bn - 1) / pl.bn);
     const int kb = (K + BK - 1) / BK;
-    if (tiles * 2 > sms) return 1;
-    int s = std::min(sms / tiles, std::max(1, kb / 3));  // >= 3 k-blocks per split
-    const int per = (kb + s - 1) / s;
-    return (kb + per - 1) / per;
+    pl.splits = 1;
+    if (tiles * 2 < sms) {
+        int s = std::min(sms / tiles, std::max(1, kb / 3));  // >= 3 k-blocks per split
+        const int per = (kb + s - 1) / s;
+        pl.splits = (kb + per - 1) / per;
+    }
+    return pl;
 }
+
+int tc_choose_splits(int sms, int M, int N, int K) { return tc_plan(sms, M, N, K).splits; }
 
 TcGemm *tc_create(int device) {
     TcGemm *t = new TcGemm();
@@ -494,21 +551,21 @@ bool tc_supports(TcGemm *t, const GemmDesc &g) {
 template <int BN, bool SPLIT>
 static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s) {
     using L = SmemLayout<BN, SPLIT>;
-    const int slot = SPLIT ? 1 : 0;
+    const int slot = (SPLIT ? 1 : 0) + 2 * (BN == 128 ? 0 : BN == 64 ? 1 : 2);
     if (!t->attr_set[slot]) {
         cudaError_t e =
             cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
         if (e != cudaSuccess) return e;
         t->attr_set[slot] = true;
     }
-    tc_gemm_kernel<BN, SPLIT><<<grid, L::THREADS, L::TOTAL, s>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(tc_gemm_kernel<BN, SPLIT>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
 }
 
 cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h) {
     const int M = g.aug ? g.M - 1 : g.M;  // the bias row of an augmented wgrad is a column sum (below)
     const int N = g.N, K = g.K;
-    constexpr int BN = 128;
+    const TcPlan plan = tc_plan(t->sms, M, N, K);
+    const int BN = plan.bn;
     TcParams p{};
     p.M = M; p.N = N; p.K = K;
     p.a_mn = g.ta ? 1 : 0;
@@ -531,7 +588,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     const int tiles = p.tiles_m * p.tiles_n;
     int splits = 1;
     if (g.partial && N % 4 == 0) {  // few output tiles: split K to fill the SMs
-        splits = tc_choose_splits(t->sms, M, N, K);
+        splits = plan.splits;
         while (splits > 1 && (int64_t)splits * M * N > g.partial_cap) splits--;
     }
     p.kb_per_split = (p.kb_total + splits - 1) / splits;
@@ -549,10 +606,13 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     const int grid = std::min(total, t->sms);
     const char *kind = g.epi == EPI_MASK ? "dgrad" : (g.ta ? "wgrad" : "fwd");
     char name[96];
-    snprintf(name, sizeof name, "gemm_tc%s_%s[M=%d,N=%d,K=%d,splits=%d]", g.tf32x3 ? "3x" : "", kind, M, N, K,
-             splits);
+    snprintf(name, sizeof name, "gemm_tc%s_%s[M=%d,N=%d,K=%d,splits=%d,bn=%d]", g.tf32x3 ? "3x" : "", kind, M, N, K,
+             splits, BN);
     if (h) h->before(name, s);
-    cudaError_t e = g.tf32x3 ? launch<BN, true>(t, p, grid, s) : launch<BN, false>(t, p, grid, s);
+    cudaError_t e;
+    if (BN == 128) e = g.tf32x3 ? launch<128, true>(t, p, grid, s) : launch<128, false>(t, p, grid, s);
+    else if (BN == 64) e = g.tf32x3 ? launch<64, true>(t, p, grid, s) : launch<64, false>(t, p, grid, s);
+    else e = g.tf32x3 ? launch<32, true>(t, p, grid, s) : launch<32, false>(t, p, grid, s);
     if (h) h->after(name, s);
     if (e != cudaSuccess) return e;
     if (splits > 1 && !p.counters) {  // no in-kernel fixup: fold with the epilogue in a separate kernel
@@ -560,7 +620,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
         if (e != cudaSuccess) return e;
     }
     if (g.aug)  // bias gradient row: db[n] = sum_k B[k][n]  (the ones row of the augmented A)
-        e = colsum(g.B, K, N, g.ldb, g.C + (int64_t)M * g.ldc, g.partial, g.partial_cap, s, h);
+        e = colsum(g.B, K, N, g.ldb, g.C + (int64_t)M * g.ldc, g.partial, g.partial_cap, g.counters + 255, s, h);
     return e;
 }
 

@@ -6,7 +6,13 @@
 namespace mtx {
 struct TcGemm;
 bool tc_available();
-// Split-K factor the engine uses for an M x N x K GEMM when the partial buffer allows it.
+// Tile width and split-K factor the engine uses for an M x N x K GEMM (splits if the partial
+// buffer allows it).
+struct TcPlan {
+    int bn = 128;
+    int splits = 1;
+};
+TcPlan tc_plan(int sms, int M, int N, int K);
 int tc_choose_splits(int sms, int M, int N, int K);
 TcGemm *tc_create(int device);
 void tc_destroy(TcGemm *t);

@@ -48,9 +48,10 @@ struct LaunchHook {
 cudaError_t gemm_simt(const GemmDesc &g, cudaStream_t s, LaunchHook *h);
 
 // out[n] = sum_{k} X[k][n] for X [K][ld] (column sums, e.g. the bias gradient colsum(dZ)):
-// fixed-order per-block sums into partial[z][N], then an ascending-z fold -- deterministic.
+// fixed-order per-block sums into partial[z][N]; the last block (ticket, zero on entry and
+// re-armed on exit) folds them in ascending z -- deterministic, one launch.
 cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *partial, int64_t partial_cap,
-                   cudaStream_t s, LaunchHook *h);
+                   unsigned *ticket, cudaStream_t s, LaunchHook *h);
 
 // C[m][n] = epi(sum_{z ascending} partial[z][m][n])  (deterministic split-K fold + GEMM epilogue)
 cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float *C, int64_t ldc, cudaStream_t s,
@@ -61,7 +62,8 @@ cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float 
 // for k < K_in, plus (aug) the bias row dWb[K_in][j] = sum_i dZ[i][j].  Thread per k, rows split
 // over blocks, blocked fp32 sums, ascending fold.  A's row offset: arow (dataset operand).
 cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *dZ, int rows, int K_in, int N,
-                         float *dWb, float *partial, int64_t partial_cap, cudaStream_t s, LaunchHook *h);
+                         float *dWb, float *partial, int64_t partial_cap, unsigned *ticket, cudaStream_t s,
+                         LaunchHook *h);
 
 // Fused last layer: logits = A W + b (W,b = augmented [(d+1)][C] block), mean
 // softmax-CE, dZ_L = (softmax - onehot)/b, loss per row, (if dprev) the masked

@@ -22,6 +22,7 @@ inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b);
 __global__ void __launch_bounds__(256) conv_fwd_kernel(ConvGeom g, int rows, const float *__restrict__ X, RowSel xrow,
                                                      const float *__restrict__ Wb, float *__restrict__ R,
                                                      float *__restrict__ P, uint8_t *__restrict__ arg) {
+    pdl_wait();
     extern __shared__ float sw[];  // (k*k*ci + 1) * co
     const int KK = g.k * g.k * g.ci;
     for (int e = threadIdx.x; e < (KK + 1) * g.co; e += blockDim.x) sw[e] = Wb[e];
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(256) conv_fwd_kernel(ConvGeom g, int rows, con
 __global__ void pool_relu_bwd_kernel(ConvGeom g, int rows, const float *__restrict__ dP,
                                      const uint8_t *__restrict__ arg, const float *__restrict__ R,
                                      float *__restrict__ dR) {
+    pdl_wait();
     const int64_t total = (int64_t)rows * g.hc * g.wc * g.co;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -95,6 +97,7 @@ constexpr int WG_T = 256, WG_POS = 32;
 __global__ void __launch_bounds__(WG_T) conv_wgrad_kernel(ConvGeom g, int rows, const float *__restrict__ X,
                                                         RowSel xrow, const float *__restrict__ dR, int64_t pos_per,
                                                         float *__restrict__ partial) {
+    pdl_wait();
     extern __shared__ float sm[];
     const int KK = g.k * g.k * g.ci, E = KK + 1;
     float *sp = sm;                 // [WG_POS][E]
@@ -155,6 +158,7 @@ __global__ void __launch_bounds__(WG_T) conv_wgrad_kernel(ConvGeom g, int rows, 
 // Input gradient (full correlation): dX[n][h][w][ci] = sum_{kh,kw,co} dR[n][h-kh][w-kw][co] W[kh][kw][ci][co].
 __global__ void __launch_bounds__(256) conv_dgrad_kernel(ConvGeom g, int rows, const float *__restrict__ dR,
                                                        const float *__restrict__ Wb, float *__restrict__ dX) {
+    pdl_wait();
     extern __shared__ float sw[];
     const int KK = g.k * g.k * g.ci;
     for (int e = threadIdx.x; e < KK * g.co; e += blockDim.x) sw[e] = Wb[e];
@@ -194,7 +198,7 @@ cudaError_t conv_fwd(const ConvGeom &g, int rows, const float *X, RowSel xrow, c
     char name[96];
     snprintf(name, sizeof name, "conv_fwd[rows=%d,hi=%d,ci=%d,k=%d,co=%d]", rows, g.hi, g.ci, g.k, g.co);
     if (h) h->before(name, s);
-    conv_fwd_kernel<<<blocks, 256, smem, s>>>(g, rows, X, xrow, Wb, R, P, arg);
+    launch_pdl(conv_fwd_kernel, dim3(blocks), dim3(256), smem, s, g, rows, X, xrow, Wb, R, P, arg);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }
@@ -206,7 +210,7 @@ cudaError_t pool_relu_bwd(const ConvGeom &g, int rows, const float *dP, const ui
     char name[80];
     snprintf(name, sizeof name, "pool_relu_bwd[n=%lld]", (long long)total);
     if (h) h->before(name, s);
-    pool_relu_bwd_kernel<<<blocks, 256, 0, s>>>(g, rows, dP, arg, R, dR);
+    launch_pdl(pool_relu_bwd_kernel, dim3(blocks), dim3(256), 0, s, g, rows, dP, arg, R, dR);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }
@@ -222,7 +226,7 @@ cudaError_t conv_wgrad(const ConvGeom &g, int rows, const float *X, RowSel xrow,
     char name[96];
     snprintf(name, sizeof name, "conv_wgrad[pos=%lld,E=%d,co=%d,splits=%d]", (long long)npos, E, g.co, splits);
     if (h) h->before(name, s);
-    conv_wgrad_kernel<<<splits, WG_T, smem, s>>>(g, rows, X, xrow, dR, pos_per, partial);
+    launch_pdl(conv_wgrad_kernel, dim3(splits), dim3(WG_T), smem, s, g, rows, X, xrow, dR, pos_per, partial);
     if (h) h->after(name, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -237,7 +241,7 @@ cudaError_t conv_dgrad(const ConvGeom &g, int rows, const float *dR, const float
     char name[80];
     snprintf(name, sizeof name, "conv_dgrad[n=%lld,k=%d,co=%d]", (long long)total, g.k, g.co);
     if (h) h->before(name, s);
-    conv_dgrad_kernel<<<blocks, 256, smem, s>>>(g, rows, dR, Wb, dX);
+    launch_pdl(conv_dgrad_kernel, dim3(blocks), dim3(256), smem, s, g, rows, dR, Wb, dX);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }

@@ -27,6 +27,7 @@ constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
 
 template <bool TA, bool TB, int EPI, bool AUG, bool PARTIAL>
 __global__ void __launch_bounds__(NT) gemm_simt_kernel(GemmDesc g) {
+    pdl_wait();
     __shared__ float As[BK][BM + 4];
     __shared__ float Bs[BK][BN + 4];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -139,6 +140,7 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(GemmDesc g) {
 __global__ void splitk_reduce_kernel(const float *__restrict__ partial, int splits, int M, int N, float *C,
                                      int64_t ldc, int epi, const float *__restrict__ bias,
                                      const float *__restrict__ mask, int64_t ldm) {
+    pdl_wait();
     const int64_t total = (int64_t)M * N;
     // 4 consecutive elements per thread (float4 when the row holds them), splits loaded 8 at a time
     const int64_t n4 = (total + 3) / 4;
@@ -183,7 +185,7 @@ __global__ void splitk_reduce_kernel(const float *__restrict__ partial, int spli
 
 template <bool TA, bool TB, int EPI, bool AUG, bool PARTIAL>
 void launch_gemm(const GemmDesc &g, dim3 grid, cudaStream_t s) {
-    gemm_simt_kernel<TA, TB, EPI, AUG, PARTIAL><<<grid, NT, 0, s>>>(g);
+    launch_pdl(gemm_simt_kernel<TA, TB, EPI, AUG, PARTIAL>, grid, dim3(NT), 0, s, g);
 }
 
 }  // namespace
@@ -218,7 +220,7 @@ cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float 
     char rn[80];
     snprintf(rn, sizeof rn, "splitk_reduce[M=%d,N=%d,splits=%d,epi=%d]", M, N, splits, epi);
     if (h) h->before(rn, s);
-    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(partial, splits, M, N, C, ldc, epi, bias, mask, ldm);
+    launch_pdl(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, s, partial, splits, M, N, C, ldc, epi, bias, mask, ldm);
     if (h) h->after(rn, s);
     return cudaGetLastError();
 }
@@ -228,7 +230,9 @@ namespace {
 constexpr int NW_T = 128, NW_ROWS = 32, NW_MAXN = 16;
 __global__ void __launch_bounds__(NW_T) wgrad_narrow_kernel(const float *__restrict__ A, int64_t lda, RowSel arow,
                                                           const float *__restrict__ dZ, int rows, int K_in, int N,
-                                                          int rows_per, float *__restrict__ partial) {
+                                                          int rows_per, float *__restrict__ partial, unsigned *ticket,
+                                                          float *__restrict__ dWb) {
+    pdl_wait();
     __shared__ float sdz[NW_ROWS][NW_MAXN];
     const int k = blockIdx.x * NW_T + threadIdx.x;
     const int r0 = blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
@@ -271,7 +275,8 @@ __global__ void __launch_bounds__(NW_T) wgrad_narrow_kernel(const float *__restr
 }  // namespace
 
 cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *dZ, int rows, int K_in, int N,
-                         float *dWb, float *partial, int64_t partial_cap, cudaStream_t s, LaunchHook *h) {
+                         float *dWb, float *partial, int64_t partial_cap, unsigned *ticket, cudaStream_t s,
+                         LaunchHook *h) {
     if (N > NW_MAXN) return cudaErrorInvalidValue;
     const int kb = (K_in + 1 + NW_T - 1) / NW_T;
     int splits = std::max(1, std::min((4 * 148 + kb - 1) / kb, (rows + 31) / 32));
@@ -281,11 +286,12 @@ cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *
     char name[80];
     snprintf(name, sizeof name, "wgrad_narrow[M=%d,N=%d,K=%d,splits=%d]", K_in + 1, N, rows, splits);
     if (h) h->before(name, s);
-    wgrad_narrow_kernel<<<dim3(kb, splits), NW_T, 0, s>>>(A, lda, arow, dZ, rows, K_in, N, rows_per, partial);
+    launch_pdl(wgrad_narrow_kernel, dim3(kb, splits), dim3(NW_T), 0, s, A, lda, arow, dZ, rows, K_in, N, rows_per,
+               partial, ticket, dWb);
     if (h) h->after(name, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return splitk_reduce(partial, splits, K_in + 1, N, dWb, N, s, h);
+    return splitk_reduce(partial, splits, K_in + 1, N, dWb, N, s, h);  // all-SM ascending fold
 }
 
 // ------------------------------------------------------------------ column sums (bias gradients)
@@ -295,8 +301,11 @@ cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *
 namespace {
 template <bool VEC>
 __global__ void __launch_bounds__(256) colsum_kernel(const float *__restrict__ X, int K, int N, int64_t ld,
-                                                     int k_per, float *__restrict__ partial) {
+                                                     int k_per, float *__restrict__ partial, unsigned *ticket,
+                                                     float *__restrict__ out) {
+    pdl_wait();
     __shared__ float4 sh[8][32];
+    __shared__ bool last;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int n = blockIdx.x * 128 + 4 * lane;
     const int k0 = blockIdx.y * k_per, k1 = min(K, k0 + k_per);
@@ -330,11 +339,24 @@ __global__ void __launch_bounds__(256) colsum_kernel(const float *__restrict__ X
         if (n + 2 < N) dst[2] = s.z;
         if (n + 3 < N) dst[3] = s.w;
     }
+    // the last block to finish folds the per-split partials in ascending split order
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int c = threadIdx.x; c < N; c += blockDim.x) {
+        float s = 0.f;
+        for (unsigned z = 0; z < gridDim.y; z++) s += __ldcg(partial + (int64_t)z * N + c);
+        out[c] = s;
+    }
+    if (threadIdx.x == 0) *ticket = 0u;
 }
 }  // namespace
 
 cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *partial, int64_t partial_cap,
-                   cudaStream_t s, LaunchHook *h) {
+                   unsigned *ticket, cudaStream_t s, LaunchHook *h) {
     const int cols = (N + 127) / 128;
     int splits = std::max(1, std::min((K + 63) / 64, (2 * 148 + cols - 1) / cols));
     while (splits > 1 && (int64_t)splits * N > partial_cap) splits--;
@@ -345,12 +367,10 @@ cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *
     char name[64];
     snprintf(name, sizeof name, "colsum[K=%d,N=%d,splits=%d]", K, N, splits);
     if (h) h->before(name, s);
-    if (vec) colsum_kernel<true><<<dim3(cols, splits), 256, 0, s>>>(X, K, N, ld, k_per, partial);
-    else colsum_kernel<false><<<dim3(cols, splits), 256, 0, s>>>(X, K, N, ld, k_per, partial);
+    if (vec) launch_pdl(colsum_kernel<true>, dim3(cols, splits), dim3(256), 0, s, X, K, N, ld, k_per, partial, ticket, out);
+    else launch_pdl(colsum_kernel<false>, dim3(cols, splits), dim3(256), 0, s, X, K, N, ld, k_per, partial, ticket, out);
     if (h) h->after(name, s);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    return splitk_reduce(partial, splits, 1, N, out, N, s, h);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ fused head (last layer + loss)
@@ -370,6 +390,7 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
                                                              float *__restrict__ dprev, float *__restrict__ loss_rows,
                                                              float *__restrict__ loss_part, unsigned *ticket,
                                                              float *__restrict__ loss_out) {
+    pdl_wait();
     // W_L staged TRANSPOSED: sWt[j][k], row pitch dp = round_up(d + 1, 4) (k == d: bias), so a lane
     // reads the weights of its 4 consecutive features as one conflict-free 128-bit load
     extern __shared__ __align__(16) float sWt[];
@@ -527,9 +548,8 @@ cudaError_t launch_head(unsigned blocks, size_t smem, cudaStream_t s, int rows, 
         cudaError_t e = cudaFuncSetAttribute(head_kernel<NV, VEC, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    head_kernel<NV, VEC, CM><<<blocks, HEAD_WARPS * 32, smem, s>>>(rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL, dprev,
-                                                               loss_rows, loss_part, ticket, loss_out);
-    return cudaGetLastError();
+    return launch_pdl(head_kernel<NV, VEC, CM>, dim3(blocks), dim3(HEAD_WARPS * 32), smem, s, rows, d, C, A, arow, Wb,
+                      labels, lrow, inv_b, dZL, dprev, loss_rows, loss_part, ticket, loss_out);
 }
 }  // namespace
 
@@ -571,6 +591,7 @@ cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, cons
 // ------------------------------------------------------------------ deterministic block sum
 namespace {
 __global__ void __launch_bounds__(1024) reduce_sum_kernel(const float *__restrict__ v, int n, float *out) {
+    pdl_wait();
     __shared__ float sh[1024];
     float acc = 0.f;
     for (int i = threadIdx.x; i < n; i += 1024) acc += v[i];
@@ -588,7 +609,7 @@ cudaError_t reduce_sum(const float *v, int n, float *out, cudaStream_t s, Launch
     char name[48];
     snprintf(name, sizeof name, "loss_reduce[n=%d]", n);
     if (h) h->before(name, s);
-    reduce_sum_kernel<<<1, 1024, 0, s>>>(v, n, out);
+    launch_pdl(reduce_sum_kernel, dim3(1), dim3(1024), 0, s, v, n, out);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }
@@ -607,6 +628,7 @@ __global__ void __launch_bounds__(UPD_T) avg_update_kernel(const float4 *__restr
                                                          float4 *__restrict__ v, int64_t n4, float invP, float lr,
                                                          float mu, int *flag, int64_t *win, int64_t B,
                                                          int64_t n_data, int tail) {
+    pdl_wait();
     bool bad = false;
     const int64_t stride = (int64_t)gridDim.x * UPD_T * UPD_U;
     for (int64_t base = (int64_t)blockIdx.x * UPD_T * UPD_U + threadIdx.x; base < n4; base += stride) {
@@ -667,11 +689,11 @@ cudaError_t avg_update(float *G, float *w, float *v, int64_t n, float invP, floa
     snprintf(name, sizeof name, "avg_update[n=%lld,v=%d]", (long long)n, v ? 1 : 0);
     if (h) h->before(name, s);
     if (v)
-        avg_update_kernel<true><<<blocks, UPD_T, 0, s>>>((const float4 *)G, (float4 *)w, (float4 *)v, n4, invP, lr,
-                                                         mu, flag, win, B, n_data, tail);
+        launch_pdl(avg_update_kernel<true>, dim3(blocks), dim3(UPD_T), 0, s, (const float4 *)G, (float4 *)w, (float4 *)v,
+                   n4, invP, lr, mu, flag, win, B, n_data, tail);
     else
-        avg_update_kernel<false><<<blocks, UPD_T, 0, s>>>((const float4 *)G, (float4 *)w, nullptr, n4, invP, lr, mu,
-                                                          flag, win, B, n_data, tail);
+        launch_pdl(avg_update_kernel<false>, dim3(blocks), dim3(UPD_T), 0, s, (const float4 *)G, (float4 *)w,
+                   (float4 *)nullptr, n4, invP, lr, mu, flag, win, B, n_data, tail);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }
@@ -679,6 +701,7 @@ cudaError_t avg_update(float *G, float *w, float *v, int64_t n, float invP, floa
 // ------------------------------------------------------------------ ordered fold (test mode, A2)
 namespace {
 __global__ void ordered_fold_kernel(const float *__restrict__ g, int P, int64_t stride, int64_t n, float *G) {
+    pdl_wait();
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
         float s = g[e];
         for (int r = 1; r < P; r++) s = __fadd_rn(s, g[(int64_t)r * stride + e]);
@@ -693,7 +716,7 @@ cudaError_t ordered_fold(const float *gathered, int P, int64_t stride, int64_t n
     char name[64];
     snprintf(name, sizeof name, "ordered_fold[n=%lld,P=%d]", (long long)n, P);
     if (h) h->before(name, s);
-    ordered_fold_kernel<<<blocks, 256, 0, s>>>(gathered, P, stride, n, G);
+    launch_pdl(ordered_fold_kernel, dim3(blocks), dim3(256), 0, s, gathered, P, stride, n, G);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }

@@ -270,7 +270,8 @@ mtx_status build_layout(mtx_ctx *c) {
     // buckets: reverse layer order, contiguous layer-aligned ranges of >= bucket_bytes
     c->buckets.clear();
     int nl = (int)c->layers.size();
-    int64_t target = c->opt.bucket_bytes ? (int64_t)c->opt.bucket_bytes / 4 : INT64_MAX;
+    // buckets only pay when a collective can overlap the backward: one bucket at P = 1
+    int64_t target = (c->opt.bucket_bytes && c->world > 1) ? (int64_t)c->opt.bucket_bytes / 4 : INT64_MAX;
     int hi_layer = nl - 1;
     while (hi_layer >= 0) {
         int lo_layer = hi_layer;
@@ -431,7 +432,7 @@ struct Runner {
         const Layer &L = c->layers[li];
         if (L.cols <= 16) {  // classifier-width layers: thread-per-input-feature kernel, bias row included
             cudaError_t e = wgrad_narrow(A, L.rows_w, arow, dZ, (int)c->b, L.rows_w, L.cols, c->grads + L.pad_off,
-                                         c->partial, c->partial_floats, s, h);
+                                         c->partial, c->partial_floats, c->counters + 254, s, h);
             if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "wgrad_narrow: %s", cudaGetErrorString(e));
             return MTX_OK;
         }

@@ -36,6 +36,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
 
 __global__ void peer_barrier_kernel(PeerPtrs pp, int P, int rank, uint64_t *epoch_ctr, int *errflag,
                                     uint64_t timeout_ns) {
+    pdl_wait();
     __shared__ uint64_t epoch;
     if (threadIdx.x == 0) {
         epoch = *epoch_ctr + 1;
@@ -63,6 +64,7 @@ template <bool HAS_V>
 __global__ void __launch_bounds__(256) fused_avg_update_kernel(PeerPtrs pp, int P, int rank, int64_t lo4, int64_t hi4,
                                                              float invP, float lr, float mu, int *flag, int64_t *win,
                                                              int64_t B, int64_t n_data, int64_t loss_idx) {
+    pdl_wait();
     bool bad = false;
     for (int64_t i = lo4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi4;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -117,7 +119,7 @@ cudaError_t peer_barrier(const PeerPtrs &pp, int P, int rank, uint64_t *epoch_ct
     char name[32];
     snprintf(name, sizeof name, "peer_barrier[P=%d]", P);
     if (h) h->before(name, s);
-    peer_barrier_kernel<<<1, 32, 0, s>>>(pp, P, rank, epoch_ctr, errflag, 10000000000ull);
+    launch_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, s, pp, P, rank, epoch_ctr, errflag, 10000000000ull);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }
@@ -134,11 +136,11 @@ cudaError_t fused_avg_update(const PeerPtrs &pp, int P, int rank, int64_t n_pad,
     if (h) h->before(name, s);
     const float invP = 1.0f / (float)P;
     if (has_v)
-        fused_avg_update_kernel<true><<<blocks, 256, 0, s>>>(pp, P, rank, lo4, hi4, invP, lr, mu, flag, win, B, n_data,
-                                                             n_pad);
+        launch_pdl(fused_avg_update_kernel<true>, dim3(blocks), dim3(256), 0, s, pp, P, rank, lo4, hi4, invP, lr, mu,
+                   flag, win, B, n_data, n_pad);
     else
-        fused_avg_update_kernel<false><<<blocks, 256, 0, s>>>(pp, P, rank, lo4, hi4, invP, lr, mu, flag, win, B,
-                                                              n_data, n_pad);
+        launch_pdl(fused_avg_update_kernel<false>, dim3(blocks), dim3(256), 0, s, pp, P, rank, lo4, hi4, invP, lr, mu,
+                   flag, win, B, n_data, n_pad);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }

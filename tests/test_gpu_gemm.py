@@ -29,7 +29,7 @@ def rep():
 
 SHAPES = [  # (M, N, K) incl. the step's shapes: cfg4 fwd/dgrad/wgrad, cfg2, K = 28, ragged M/N/K
     (1024, 1024, 1024), (512, 512, 784), (8192, 1024, 28), (28, 1024, 2048), (300, 200, 100), (128, 64, 96),
-    (1000, 384, 520),
+    (1000, 384, 520), (1024, 640, 256), (64, 784, 512),  # tcgen05 N-tile 64 / 32 plans
 ]
 
 

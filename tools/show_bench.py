@@ -7,4 +7,7 @@ for f in sys.argv[1:]:
     r = d["roofline"]
     print(f.split("/")[-1], d["value"], "samples/s", round(d["ms_per_step"] * 1000, 1), "us/step", d["launches_per_step"], "launches;",
           r["kernel"], r["achieved"], r["unit"], "frac", r["frac"], "| e2e", d["e2e"]["value"])
-    print("   ", {k: v for k, v in list(r["breakdown_us_per_step"].items())[:9]})
+    try:
+        print("   ", {k: v for k, v in list(r["breakdown_us_per_step"].items())[:9]})
+    except BrokenPipeError:
+        pass
