@@ -219,7 +219,7 @@ def main():
     ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "tf32", "3xtf32"])
     ap.add_argument("--impl", default="mtx", choices=["mtx", "reference"])
     ap.add_argument("--bucket-mb", type=float, default=1.0)
-    ap.add_argument("--reduce", default="fused", choices=["nccl", "ordered", "fused"],
+    ap.add_argument("--reduce", default="fused", choices=["nccl", "ordered", "fused", "layerwise", "zero1"],
                     help="gradient allreduce (N > 1): NCCL per bucket, ORDERED test mode, or the averaging "
                          "operator fused with its collective over NVLink peer memory")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -268,7 +268,8 @@ def main():
         args.precision, P.MTX_3XTF32 if tc_ok else P.MTX_FP32)
     uid = P.nccl_uid_broadcast(rank, world)
     X, y = S.dataset(cfg)
-    reduce = {"nccl": P.MTX_REDUCE_NCCL, "ordered": P.MTX_REDUCE_ORDERED, "fused": P.MTX_REDUCE_FUSED}[args.reduce]
+    reduce = {"nccl": P.MTX_REDUCE_NCCL, "ordered": P.MTX_REDUCE_ORDERED, "fused": P.MTX_REDUCE_FUSED,
+              "layerwise": P.MTX_REDUCE_LAYERWISE, "zero1": P.MTX_REDUCE_ZERO1}[args.reduce]
     rep = P.Replica(cfg, rank=rank, world=world, uid=uid, device=local, precision=prec,
                     bucket_bytes=int(args.bucket_mb * (1 << 20)), reduce=reduce if world > 1 else P.MTX_REDUCE_NCCL)
     rep.bcast()

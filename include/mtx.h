@@ -90,7 +90,20 @@ typedef enum { MTX_FP32 = 0, MTX_TF32 = 1, MTX_3XTF32 = 2 } mtx_precision;
  *                      in ascending rank order (bit-exact with ORDERED), applies x fl(1/P) and
  *                      the momentum update, and stores w, v, G into every replica; two
  *                      cross-GPU flag barriers (10 s timeout -> MTX_ERR_NCCL) bracket it. */
-typedef enum { MTX_REDUCE_NCCL = 0, MTX_REDUCE_ORDERED = 1, MTX_REDUCE_FUSED = 2 } mtx_reduce_mode;
+/*  MTX_REDUCE_LAYERWISE: the paper's own design ("an ordered list of reduction
+ *                      operators ... sequentially synchronizes each layer"): after the backward,
+ *                      one ncclAllReduce per variable (W_1, b_1, W_2, ...) in canonical order,
+ *                      then the fused update -- an ablation against the flat bucketed buffer.
+ *  MTX_REDUCE_ZERO1:   ncclReduceScatter of the flat buffer, the fused update of this rank's
+ *                      1/P shard only, ncclAllGather of the updated w and v (same bus bytes as
+ *                      an allreduce, 1/P of the update's HBM bytes). */
+typedef enum {
+    MTX_REDUCE_NCCL = 0,
+    MTX_REDUCE_ORDERED = 1,
+    MTX_REDUCE_FUSED = 2,
+    MTX_REDUCE_LAYERWISE = 3,
+    MTX_REDUCE_ZERO1 = 4
+} mtx_reduce_mode;
 
 typedef struct {
     int32_t kind;            /* mtx_model_kind */

@@ -12,7 +12,8 @@ import numpy as np
 
 from . import mtx
 from .mtx import (MTX_3XTF32, MTX_BUF_GRADS, MTX_BUF_PARAMS, MTX_BUF_VELOCITY, MTX_FP32,  # noqa: F401
-                  MTX_REDUCE_FUSED, MTX_REDUCE_NCCL, MTX_REDUCE_ORDERED, MTX_TF32, MtxError)
+                  MTX_REDUCE_FUSED, MTX_REDUCE_LAYERWISE, MTX_REDUCE_NCCL, MTX_REDUCE_ORDERED, MTX_REDUCE_ZERO1,
+                  MTX_TF32, MtxError)
 
 __all__ = ["mtx", "Replica", "MtxError", "nccl_uid_broadcast"]
 

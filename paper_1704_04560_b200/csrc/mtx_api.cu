@@ -266,7 +266,7 @@ mtx_status build_layout(mtx_ctx *c) {
         c->d0 = c->in_h * c->in_w * c->in_c;
     }
     c->N = log_off;
-    c->N_pad = pad_off;
+    c->N_pad = round_up(pad_off, ALIGN_F * std::max(1, c->world));  // equal 128-B aligned shards (ZeRO-1)
     // buckets: reverse layer order, contiguous layer-aligned ranges of >= bucket_bytes
     c->buckets.clear();
     int nl = (int)c->layers.size();
@@ -514,6 +514,45 @@ struct Runner {
 
     mtx_status reduce_update(const Bucket &bkt, bool last) {
         const float invP = 1.0f / (float)c->world;
+        if (c->world > 1 && c->opt.reduce == MTX_REDUCE_LAYERWISE) {
+            // paper-literal: after the backward, one allreduce per variable in canonical order
+            if (!last) return MTX_OK;
+            cudaEvent_t ev = c->ev_bucket[0];
+            CK(cudaEventRecord(ev, s));
+            CK(cudaStreamWaitEvent(c->comm_s, ev, 0));
+            for (const Layer &L : c->layers) {
+                const int64_t wsz = (int64_t)L.rows_w * L.cols;
+                NK(ncclAllReduce(c->grads + L.pad_off, c->grads + L.pad_off, wsz, ncclFloat, ncclSum, c->comm, c->comm_s));
+                NK(ncclAllReduce(c->grads + L.pad_off + wsz, c->grads + L.pad_off + wsz, L.cols, ncclFloat, ncclSum,
+                                 c->comm, c->comm_s));
+            }
+            NK(ncclAllReduce(c->grads + c->N_pad, c->grads + c->N_pad, 1, ncclFloat, ncclSum, c->comm, c->comm_s));
+            cudaError_t e = avg_update(c->grads, c->params, vel_or_null(0), c->N_pad, invP, c->opt.lr,
+                                       c->opt.momentum, c->flag, staged ? nullptr : c->win, c->B, c->n_data,
+                                       c->comm_s, h);
+            if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "update: %s", cudaGetErrorString(e));
+            return MTX_OK;
+        }
+        if (c->world > 1 && c->opt.reduce == MTX_REDUCE_ZERO1) {
+            // reduce-scatter -> update of this rank's shard -> all-gather of w (and v)
+            if (!last) return MTX_OK;
+            cudaEvent_t ev = c->ev_bucket[0];
+            CK(cudaEventRecord(ev, s));
+            CK(cudaStreamWaitEvent(c->comm_s, ev, 0));
+            const int64_t shard = c->N_pad / c->world, off = shard * c->rank;
+            NK(ncclReduceScatter(c->grads, c->grads + off, shard, ncclFloat, ncclSum, c->comm, c->comm_s));
+            NK(ncclAllReduce(c->grads + c->N_pad, c->grads + c->N_pad, 1, ncclFloat, ncclSum, c->comm, c->comm_s));
+            cudaError_t e = avg_update(c->grads + off, c->params + off, vel_or_null(off), shard, invP, c->opt.lr,
+                                       c->opt.momentum, c->flag, staged ? nullptr : c->win, c->B, c->n_data,
+                                       c->comm_s, h);
+            if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "update: %s", cudaGetErrorString(e));
+            NK(ncclGroupStart());
+            NK(ncclAllGather(c->params + off, c->params, shard, ncclFloat, c->comm, c->comm_s));
+            if (c->opt.momentum != 0.f) NK(ncclAllGather(c->vel + off, c->vel, shard, ncclFloat, c->comm, c->comm_s));
+            NK(ncclAllGather(c->grads + off, c->grads, shard, ncclFloat, c->comm, c->comm_s));  // G on every rank
+            NK(ncclGroupEnd());
+            return MTX_OK;
+        }
         if (c->fused) {  // one fused collective + update over the whole buffer after the last wgrad
             if (!last) return MTX_OK;
             int64_t *win = staged ? nullptr : c->win;
@@ -813,8 +852,7 @@ mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t ui
     if (model->global_batch <= 0 || model->global_batch % world) return MTX_ERR_INVALID_ARG;
     if (opt->precision != MTX_FP32 && opt->precision != MTX_TF32 && opt->precision != MTX_3XTF32)
         return MTX_ERR_INVALID_ARG;
-    if (opt->reduce != MTX_REDUCE_NCCL && opt->reduce != MTX_REDUCE_ORDERED && opt->reduce != MTX_REDUCE_FUSED)
-        return MTX_ERR_INVALID_ARG;
+    if (opt->reduce < MTX_REDUCE_NCCL || opt->reduce > MTX_REDUCE_ZERO1) return MTX_ERR_INVALID_ARG;
     if (opt->reduce == MTX_REDUCE_FUSED && world > MAX_PEERS) return MTX_ERR_UNSUPPORTED;
     mtx_ctx *c = new mtx_ctx();
     c->rank = rank;

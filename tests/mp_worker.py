@@ -133,7 +133,8 @@ def main():
         Gref = oracle.fold(g_all)
         wref, vref = w0.copy(), v0.copy()
         oracle.avg_update(Gref, wref, vref, world, cfg["lr"], cfg["mu"])
-        for mode in (P.MTX_REDUCE_ORDERED, P.MTX_REDUCE_FUSED, P.MTX_REDUCE_NCCL):
+        for mode in (P.MTX_REDUCE_ORDERED, P.MTX_REDUCE_FUSED, P.MTX_REDUCE_NCCL, P.MTX_REDUCE_LAYERWISE,
+                     P.MTX_REDUCE_ZERO1):
             uid = P.nccl_uid_broadcast(rank, world)
             r = P.Replica(cfg, rank=rank, world=world, uid=uid, device=rank, reduce=mode, bucket_bytes=1 << 20)
             r.bcast()
@@ -143,7 +144,7 @@ def main():
             mtx.mtx_sync_update(r.ctx, r.s)
             G, wv, vv = r.get(P.MTX_BUF_GRADS), r.get(P.MTX_BUF_PARAMS), r.get(P.MTX_BUF_VELOCITY)
             r.close()
-            if mode != P.MTX_REDUCE_NCCL or world == 2:
+            if mode in (P.MTX_REDUCE_ORDERED, P.MTX_REDUCE_FUSED) or world == 2:
                 check(np.array_equal(G.view(np.uint32), Gref.view(np.uint32)), f"sync_update G mode {mode}")
                 check(np.array_equal(wv.view(np.uint32), wref.view(np.uint32)), f"sync_update w mode {mode}")
                 check(np.array_equal(vv.view(np.uint32), vref.view(np.uint32)), f"sync_update v mode {mode}")
@@ -152,7 +153,21 @@ def main():
                 # both NCCL's order and the fold are within gamma_{P-1} sum|g| of the exact sum
                 bound = 2 * (world - 1) * u / (1 - (world - 1) * u) * np.abs(g_all.astype(np.float64)).sum(0)
                 check(np.all(np.abs(G.astype(np.float64) - Gref) <= bound + 1e-38), "NCCL G outside gamma bound")
-        report["checks"].append(f"sync_update ORDERED/FUSED bit-exact vs oracle fold at P={world}")
+        report["checks"].append(f"sync_update ORDERED/FUSED bit-exact vs oracle fold at P={world}; NCCL/LAYERWISE/ZERO1 "
+                                "bit-exact at P=2, within gamma bound otherwise")
+        # ---- the training step in LAYERWISE and ZERO1 modes (replica digests checked every step)
+        cfg = dict(S.CONFIGS["cfg2"], B=512)
+        X, y = S.mnist_like(1, 4096)
+        recs, w_ref, _ = oracle.train(oracle.Net.from_cfg(cfg), X, y, 512, world, 2, cfg["lr"], cfg["mu"], 42,
+                                      keep_grads=True)
+        for mode in (P.MTX_REDUCE_LAYERWISE, P.MTX_REDUCE_ZERO1):
+            gpu = run_model(rank, world, cfg, X, y, 2, P.MTX_FP32, mode)
+            for t, (rec, (loss, G, _)) in enumerate(zip(recs, gpu)):
+                check(abs(loss - rec.loss) <= 1e-5 * abs(rec.loss), f"mode {mode} step {t} loss")
+                e = max(per_tensor_maxrel(G, rec.G, oracle.tensor_table(oracle.Net.from_cfg(cfg))))
+                check(e <= 5e-5, f"mode {mode} step {t} G err {e}")
+            check(maxrel(gpu[-1][2], w_ref) <= 1e-5, f"mode {mode} weights")
+        report["checks"].append(f"layerwise and zero1 steps vs oracle at P={world}")
 
         # ---- FUSED (NVLink peer-memory reduce + update) is bit-exact with ORDERED (same rank-ordered fold)
         for prec in ([P.MTX_FP32, P.MTX_3XTF32] if "tcgen05" in mtx.mtx_build_info() else [P.MTX_FP32]):
