@@ -30,6 +30,16 @@ struct RowSel {
     MTX_DEVI int64_t row0() const { return win ? (*win + base) : 0; }
 };
 
+// 3xTF32 operand planes: hi = x rounded to nearest TF32, lo = (x - hi) rounded to nearest TF32
+// (x - hi is exact in fp32).  hi + lo represents x to ~2^-22 relative, and both round-to-nearest
+// parts are sign-symmetric, so the dropped lo.lo product carries no bias.
+MTX_DEVI uint32_t rne_tf32_bits(uint32_t u) { return (u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u; }
+MTX_DEVI void split_tf32(float x, float &hi, float &lo) {
+    const uint32_t h = rne_tf32_bits(__float_as_uint(x));
+    hi = __uint_as_float(h);
+    lo = __uint_as_float(rne_tf32_bits(__float_as_uint(x - hi)));
+}
+
 // Programmatic dependent launch.  Every kernel of the step starts with pdl_wait()
 // (griddepcontrol.wait: returns once the preceding grid has completed and its memory is
 // visible; a no-op when the launch was not programmatic) and is launched with

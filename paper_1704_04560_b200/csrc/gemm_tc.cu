@@ -29,13 +29,13 @@ namespace {
 
 constexpr int BM = 128, BK = 32;
 
-// Shared-memory plan per variant.  SPLIT (3xTF32) adds a second copy of each stage holding
-// the TF32 residual small = rne_tf32(x - trunc_tf32(x)) written by four splitter warps.
+// Shared-memory plan per variant.  SPLIT (3xTF32) stages two planes of each operand tile: hi =
+// rne_tf32(x) and lo = rne_tf32(x - hi), written once by the tensor's producer.
 template <int BN, bool SPLIT>
 struct SmemLayout {
     static constexpr int STAGES = SPLIT ? 3 : 6;
-    // warps 0 TMA, 1 MMA, 2 TMEM alloc, 3 spare, 4-11 epilogue (+ 12-15 splitters for SPLIT)
-    static constexpr int THREADS = SPLIT ? 512 : 384;
+    // warps 0 TMA, 1 MMA, 2 TMEM alloc, 3 spare, 4-11 epilogue
+    static constexpr int THREADS = 384;
     // k-blocks accumulated in TMEM before the epilogue warps promote the partial into fp32
     // registers (the tensor core's internal accumulation truncates)
     static constexpr int CHUNK = SPLIT ? 4 : 8;
@@ -49,8 +49,11 @@ struct SmemLayout {
 };
 
 struct TcParams {
-    CUtensorMap ta;
+    CUtensorMap ta;     // A (1xTF32) or A's hi plane (3xTF32)
     CUtensorMap tb;
+    CUtensorMap ta_lo;  // 3xTF32: lo planes
+    CUtensorMap tb_lo;
+    float *C_hi, *C_lo;  // optional hi/lo planes of the output (for the next 3xTF32 GEMM)
     int M, N, K;
     int a_mn, b_mn;      // operand majorness (1 = MN-major)
     int tiles_m, tiles_n, splits, kb_total, kb_per_split;
@@ -200,9 +203,9 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t sbase = smem_u32(smem);
     uint64_t *bars = (uint64_t *)(smem + L::BAR_OFF);
-    // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2], split[STAGES]
+    // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * STAGES, tfull0 = empty0 + 8 * STAGES,
-                   tempty0 = tfull0 + 16, split0 = tempty0 + 16;
+                   tempty0 = tfull0 + 16;
     uint32_t *tmem_slot = (uint32_t *)(smem + L::BAR_OFF + 128);
     volatile int *fix_flag = (volatile int *)(smem + L::BAR_OFF + 136);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -210,6 +213,10 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&p.ta) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&p.tb) : "memory");
+        if (SPLIT) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&p.ta_lo) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&p.tb_lo) : "memory");
+        }
         for (int s = 0; s < STAGES; s++) {
             mbar_init(full0 + 8 * s, 1);
             mbar_init(empty0 + 8 * s, 1);
@@ -218,8 +225,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
             mbar_init(tfull0 + 8 * a, 1);
             mbar_init(tempty0 + 8 * a, 8);
         }
-        if (SPLIT)
-            for (int s = 0; s < STAGES; s++) mbar_init(split0 + 8 * s, 4);
+
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -251,19 +257,24 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                     mbar_wait(empty0 + 8 * stage, phase ^ 1);
                     const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::A_BYTES;
                     const uint32_t fb = full0 + 8 * stage;
-                    mbar_expect_tx(fb, L::RAW_BYTES);
+                    mbar_expect_tx(fb, L::STAGE_BYTES);
                     const int k0 = kb * BK;
-                    if (!p.a_mn) {
-                        tma_load_2d(sa, &p.ta, fb, k0, (int)(row0 + m0));
-                    } else {
 #pragma unroll
-                        for (int j = 0; j < BM / 32; j++) tma_load_2d(sa + j * 4096, &p.ta, fb, m0 + 32 * j, (int)(row0 + k0));
-                    }
-                    if (!p.b_mn) {
-                        tma_load_2d(sb, &p.tb, fb, k0, n0);
-                    } else {
+                    for (int plane = 0; plane < (SPLIT ? 2 : 1); plane++) {  // hi into the raw region, lo after it
+                        const CUtensorMap *ma = plane ? &p.ta_lo : &p.ta, *mb = plane ? &p.tb_lo : &p.tb;
+                        const uint32_t pa = sa + plane * L::RAW_BYTES, pb = sb + plane * L::RAW_BYTES;
+                        if (!p.a_mn) {
+                            tma_load_2d(pa, ma, fb, k0, (int)(row0 + m0));
+                        } else {
 #pragma unroll
-                        for (int j = 0; j < BN / 32; j++) tma_load_2d(sb + j * 4096, &p.tb, fb, n0 + 32 * j, k0);
+                            for (int j = 0; j < BM / 32; j++) tma_load_2d(pa + j * 4096, ma, fb, m0 + 32 * j, (int)(row0 + k0));
+                        }
+                        if (!p.b_mn) {
+                            tma_load_2d(pb, mb, fb, k0, n0);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < BN / 32; j++) tma_load_2d(pb + j * 4096, mb, fb, n0 + 32 * j, k0);
+                        }
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -287,7 +298,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                     tc_fence_after();
                     const uint32_t d_tmem = tmem_base + buf * BN;
                     for (int kb = c0; kb < c1; kb++) {
-                        mbar_wait((SPLIT ? split0 : full0) + 8 * stage, phase);
+                        mbar_wait(full0 + 8 * stage, phase);
                         tc_fence_after();
                         const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::A_BYTES;
 #pragma unroll
@@ -300,8 +311,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                                                        : smem_desc(sb + kk * 32, 16, 1024, 2);
                             const uint32_t acc0 = (kb > c0 || kk > 0) ? 1u : 0u;
                             if (SPLIT) {
-                                // 3xTF32: big.small + small.big + big.big (big = rne_tf32(x) in place,
-                                // small = rne_tf32(x - big) in the residual buffer)
+                                // 3xTF32: hi.lo + lo.hi + hi.hi (hi = rne_tf32(x), lo = rne_tf32(x - hi))
                                 const uint64_t ads = ad + (uint64_t)(L::RAW_BYTES >> 4),
                                                bds = bd + (uint64_t)(L::RAW_BYTES >> 4);
                                 umma_tf32(d_tmem, ad, bds, idesc, acc0);
@@ -317,41 +327,6 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                     umma_commit(tfull0 + 8 * buf);  // chunk partial ready for promotion
                     if (++buf == 2) { buf = 0; buf_phase ^= 1; }
                 }
-            }
-        }
-    } else if (SPLIT && warp >= 12) {
-        // ================= 3xTF32 splitters: big = rne_tf32(x) (in place), small = rne_tf32(x - big)
-        // (same swizzled offset in the residual buffer).  Rounding big to nearest keeps the residuals
-        // sign-symmetric, so the dropped small.small term carries no bias (3xTF32).
-        const int st = threadIdx.x - 384;  // 0..127
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x) {
-            const int z = t / tiles_mn;
-            const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
-            for (int kb = kb0; kb < kb1; kb++) {
-                mbar_wait(full0 + 8 * stage, phase);
-                uint4 *raw = (uint4 *)(smem + stage * L::STAGE_BYTES);
-                uint4 *small = (uint4 *)(smem + stage * L::STAGE_BYTES + L::RAW_BYTES);
-#pragma unroll 4
-                for (int i = st; i < (int)(L::RAW_BYTES / 16); i += 128) {
-                    uint4 v = raw[i], bg, o;
-                    uint32_t *pv = &v.x, *pb = &bg.x, *po = &o.x;
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        uint32_t u = pv[e];
-                        u = (u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u;  // big: round to nearest tf32
-                        pb[e] = u;
-                        uint32_t r = __float_as_uint(__uint_as_float(pv[e]) - __uint_as_float(u));  // exact
-                        po[e] = (r + 0xFFFu + ((r >> 13) & 1u)) & 0xFFFFE000u;
-                    }
-                    raw[i] = bg;
-                    small[i] = o;
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> tensor-core proxy
-                __syncwarp();
-                if (lane == 0) mbar_arrive(split0 + 8 * stage);
-                if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }
     } else if (warp >= 4 && warp < 12) {
@@ -440,6 +415,21 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                 } else {
                     for (int e = 0; e < 4 && n + e < p.N; e++) dst_row[n + e] = o[e];
                 }
+                if (p.C_hi) {  // hi/lo planes for the consuming 3xTF32 GEMM
+                    float hi[4], lo[4];
+#pragma unroll
+                    for (int e = 0; e < 4; e++) split_tf32(o[e], hi[e], lo[e]);
+                    const int64_t off = (int64_t)m * p.ldc + n;
+                    if (n + 3 < p.N) {
+                        *(float4 *)(p.C_hi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                        *(float4 *)(p.C_lo + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+                    } else {
+                        for (int e = 0; e < 4 && n + e < p.N; e++) {
+                            p.C_hi[off + e] = hi[e];
+                            p.C_lo[off + e] = lo[e];
+                        }
+                    }
+                }
             }
         }
     }
@@ -505,6 +495,12 @@ TcPlan tc_plan(int sms, int M, int N, int K) {
         int s = std::min(sms / tiles, std::max(1, kb / 3));  // >= 3 k-blocks per split
         const int per = (kb + s - 1) / s;
         pl.splits = (kb + per - 1) / per;
+        // a split costs a fold launch over the partials: only worth it when it buys >= min_split x
+        static const int min_split = [] {
+            const char *e = getenv("MTX_TC_MINSPLIT");  // development knob
+            return e ? atoi(e) : 2;
+        }();
+        if (pl.splits < min_split) pl.splits = 1;
     }
     return pl;
 }
@@ -544,6 +540,7 @@ bool tc_supports(TcGemm *t, const GemmDesc &g) {
     if (g.epi == EPI_MASK && (g.ldm % 4 || !al16(g.mask))) return false;
     // dataset operand with the sample dimension along K: its k-blocks must not run into the next rank's rows
     if (g.ta && g.arow.win && g.K % BK) return false;
+    if (g.tf32x3 && !(g.A_hi && g.A_lo && g.B_hi && g.B_lo)) return false;  // 3xTF32 consumes producer planes
     if (g.arow.win && g.a_rows_total <= 0) return false;
     return true;
 }
@@ -574,12 +571,19 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     // spans the whole wrap-extended buffer (rows are offset on the device by a_win + a_base).
     const int64_t a_rows_total = g.a_rows_total;
     bool ok;
-    if (!g.ta) ok = make_map(t->encode, &p.ta, g.A, g.arow.win ? a_rows_total : M, K, g.lda, BM, false);
-    else ok = make_map(t->encode, &p.ta, g.A, g.arow.win ? a_rows_total : K, M, g.lda, BK, true);
+    auto map_a = [&](CUtensorMap *m, const float *ptr) {
+        return !g.ta ? make_map(t->encode, m, ptr, g.arow.win ? a_rows_total : M, K, g.lda, BM, false)
+                     : make_map(t->encode, m, ptr, g.arow.win ? a_rows_total : K, M, g.lda, BK, true);
+    };
+    auto map_b = [&](CUtensorMap *m, const float *ptr) {
+        return g.tb ? make_map(t->encode, m, ptr, N, K, g.ldb, BN, false)   // [N][K], K-major
+                    : make_map(t->encode, m, ptr, K, N, g.ldb, BK, true);   // [K][N], MN-major
+    };
+    if (g.tf32x3) ok = map_a(&p.ta, g.A_hi) && map_a(&p.ta_lo, g.A_lo) && map_b(&p.tb, g.B_hi) && map_b(&p.tb_lo, g.B_lo);
+    else ok = map_a(&p.ta, g.A) && map_b(&p.tb, g.B);
     if (!ok) return cudaErrorInvalidValue;
-    if (g.tb) ok = make_map(t->encode, &p.tb, g.B, N, K, g.ldb, BN, false);  // [N][K], K-major
-    else ok = make_map(t->encode, &p.tb, g.B, K, N, g.ldb, BK, true);         // [K][N], MN-major
-    if (!ok) return cudaErrorInvalidValue;
+    p.C_hi = g.C_hi;
+    p.C_lo = g.C_lo;
     p.a_win = g.arow.win;
     p.a_base = g.arow.base;
     p.tiles_m = (M + BM - 1) / BM;
@@ -601,7 +605,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.C = g.C;
     p.ldc = g.ldc;
     p.partial = g.partial;
-    p.counters = t->fixup ? g.counters : nullptr;
+    p.counters = (t->fixup && !g.C_hi) ? g.counters : nullptr;
     const int total = tiles * splits;
     const int grid = std::min(total, t->sms);
     const char *kind = g.epi == EPI_MASK ? "dgrad" : (g.ta ? "wgrad" : "fwd");
@@ -616,7 +620,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     if (h) h->after(name, s);
     if (e != cudaSuccess) return e;
     if (splits > 1 && !p.counters) {  // no in-kernel fixup: fold with the epilogue in a separate kernel
-        e = splitk_reduce(g.partial, splits, M, N, g.C, g.ldc, s, h, g.epi, g.bias, g.mask, g.ldm);
+        e = splitk_reduce(g.partial, splits, M, N, g.C, g.ldc, s, h, g.epi, g.bias, g.mask, g.ldm, g.C_hi, g.C_lo);
         if (e != cudaSuccess) return e;
     }
     if (g.aug)  // bias gradient row: db[n] = sum_k B[k][n]  (the ones row of the augmented A)

@@ -35,6 +35,10 @@ struct GemmDesc {
     int64_t partial_cap = 0;  // floats available at partial (engines may choose their own split count)
     int64_t a_rows_total = 0; // rows of the buffer behind A when arow.win is set (wrap-extended dataset)
     int tf32x3 = 0;           // tensor-core engine: 3xTF32 (fp32-accurate) instead of 1xTF32
+    // 3xTF32 operand planes (same layout as A / B; hi = rne_tf32(x), lo = rne_tf32(x - hi)) and
+    // optional planes of the output for the next 3xTF32 consumer
+    const float *A_hi = nullptr, *A_lo = nullptr, *B_hi = nullptr, *B_lo = nullptr;
+    float *C_hi = nullptr, *C_lo = nullptr;
     unsigned *counters = nullptr;  // tensor-core split-K fixup: >= 256 per-tile counters, zeroed
 };
 
@@ -56,7 +60,13 @@ cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *
 // C[m][n] = epi(sum_{z ascending} partial[z][m][n])  (deterministic split-K fold + GEMM epilogue)
 cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float *C, int64_t ldc, cudaStream_t s,
                           LaunchHook *h, int epi = EPI_STORE, const float *bias = nullptr,
-                          const float *mask = nullptr, int64_t ldm = 0);
+                          const float *mask = nullptr, int64_t ldm = 0, float *C_hi = nullptr,
+                          float *C_lo = nullptr);
+
+// hi/lo 3xTF32 planes of x[n] (n % 4 == 0, 16-B aligned; rows of x need not be contiguous: a
+// [rows][cols] block with leading dimension ld)
+cudaError_t split_planes(const float *x, int64_t rows, int64_t cols, int64_t ld, float *hi, float *lo, cudaStream_t s,
+                         LaunchHook *h);
 
 // Narrow weight gradient (N <= 16, e.g. the classifier layer): dWb[k][j] = sum_i A[i][k] dZ[i][j]
 // for k < K_in, plus (aug) the bias row dWb[K_in][j] = sum_i dZ[i][j].  Thread per k, rows split
@@ -69,10 +79,12 @@ cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *
 // softmax-CE, dZ_L = (softmax - onehot)/b, loss per row, (if dprev) the masked
 // dgrad dZ_{L-1} = (dZ_L W^T) .* [A > 0], and the local loss sum into *loss_out
 // (per-block partials folded in block order by the last block; ticket must be 0
-// on entry and is re-armed on exit; loss_part holds >= 1024 floats).
+// on entry and is re-armed on exit; loss_part holds >= 1024 floats).  dp_hi/dp_lo
+// (nullable): 3xTF32 planes of dprev for the consuming tensor-core GEMMs.
 cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, const float *Wb, const int32_t *labels,
-                       RowSel lrow, float inv_b, float *dZL, float *dprev, float *loss_rows, float *loss_part,
-                       unsigned *ticket, float *loss_out, cudaStream_t s, LaunchHook *h);
+                       RowSel lrow, float inv_b, float *dZL, float *dprev, float *dp_hi, float *dp_lo,
+                       float *loss_rows, float *loss_part, unsigned *ticket, float *loss_out, cudaStream_t s,
+                       LaunchHook *h);
 
 // out = sum_{i ascending in a fixed tree} v[i] (one block; deterministic).
 cudaError_t reduce_sum(const float *v, int n, float *out, cudaStream_t s, LaunchHook *h);

@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(GemmDesc g) {
 // bias (+ReLU) for forward GEMMs, the ReLU mask for dgrad, plain store otherwise.
 __global__ void splitk_reduce_kernel(const float *__restrict__ partial, int splits, int M, int N, float *C,
                                      int64_t ldc, int epi, const float *__restrict__ bias,
-                                     const float *__restrict__ mask, int64_t ldm) {
+                                     const float *__restrict__ mask, int64_t ldm, float *C_hi, float *C_lo) {
     pdl_wait();
     const int64_t total = (int64_t)M * N;
     // 4 consecutive elements per thread (float4 when the row holds them), splits loaded 8 at a time
@@ -179,6 +179,7 @@ __global__ void splitk_reduce_kernel(const float *__restrict__ partial, int spli
             else if (epi == EPI_BIAS) r = r + bias[n];
             else if (epi == EPI_MASK) r = mask[m * ldm + n] > 0.f ? r : 0.f;
             C[m * ldc + n] = r;
+            if (C_hi) split_tf32(r, C_hi[m * ldc + n], C_lo[m * ldc + n]);
         }
     }
 }
@@ -214,14 +215,49 @@ cudaError_t gemm_simt(const GemmDesc &g, cudaStream_t s, LaunchHook *h) {
 }
 
 cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float *C, int64_t ldc, cudaStream_t s,
-                          LaunchHook *h, int epi, const float *bias, const float *mask, int64_t ldm) {
+                          LaunchHook *h, int epi, const float *bias, const float *mask, int64_t ldm, float *C_hi,
+                          float *C_lo) {
     int64_t total = (int64_t)M * N;
     unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total / 4 + 255) / 256, 148 * 8));
     char rn[80];
     snprintf(rn, sizeof rn, "splitk_reduce[M=%d,N=%d,splits=%d,epi=%d]", M, N, splits, epi);
     if (h) h->before(rn, s);
-    launch_pdl(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, s, partial, splits, M, N, C, ldc, epi, bias, mask, ldm);
+    launch_pdl(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, s, partial, splits, M, N, C, ldc, epi, bias, mask, ldm,
+               C_hi, C_lo);
     if (h) h->after(rn, s);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ 3xTF32 operand planes
+namespace {
+__global__ void split_planes_kernel(const float *__restrict__ x, int64_t rows, int64_t cols, int64_t ld,
+                                    float *__restrict__ hi, float *__restrict__ lo) {
+    pdl_wait();
+    const int64_t c4 = cols / 4, total = rows * c4;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = q / c4, off = r * ld + 4 * (q % c4);
+        const float4 v = __ldg((const float4 *)(x + off));
+        float4 h, l;
+        split_tf32(v.x, h.x, l.x);
+        split_tf32(v.y, h.y, l.y);
+        split_tf32(v.z, h.z, l.z);
+        split_tf32(v.w, h.w, l.w);
+        *(float4 *)(hi + off) = h;
+        *(float4 *)(lo + off) = l;
+    }
+}
+}  // namespace
+
+cudaError_t split_planes(const float *x, int64_t rows, int64_t cols, int64_t ld, float *hi, float *lo, cudaStream_t s,
+                         LaunchHook *h) {
+    if (cols % 4 || ld % 4) return cudaErrorInvalidValue;
+    const int64_t total = rows * (cols / 4);
+    unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8));
+    char name[64];
+    snprintf(name, sizeof name, "split_planes[n=%lld]", (long long)(rows * cols));
+    if (h) h->before(name, s);
+    launch_pdl(split_planes_kernel, dim3(blocks), dim3(256), 0, s, x, rows, cols, ld, hi, lo);
+    if (h) h->after(name, s);
     return cudaGetLastError();
 }
 
@@ -387,7 +423,8 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
                                                              RowSel arow, const float *__restrict__ Wb,
                                                              const int32_t *__restrict__ labels, RowSel lrow,
                                                              float inv_b, float *__restrict__ dZL,
-                                                             float *__restrict__ dprev, float *__restrict__ loss_rows,
+                                                             float *__restrict__ dprev, float *__restrict__ dp_hi,
+                                                             float *__restrict__ dp_lo, float *__restrict__ loss_rows,
                                                              float *__restrict__ loss_part, unsigned *ticket,
                                                              float *__restrict__ loss_out) {
     pdl_wait();
@@ -501,11 +538,25 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
                     }
 #pragma unroll
                 for (int u = 0; u < 4; u++) o[u] = av[t][u] > 0.f ? o[u] : 0.f;
+                float oh[4], ol[4];
+                if (dp_hi) {
+#pragma unroll
+                    for (int u = 0; u < 4; u++) split_tf32(o[u], oh[u], ol[u]);
+                }
+                const int64_t off = (int64_t)i * d + k;
                 if (VEC && k + 3 < d) {
-                    *(float4 *)(dprev + (int64_t)i * d + k) = make_float4(o[0], o[1], o[2], o[3]);
+                    *(float4 *)(dprev + off) = make_float4(o[0], o[1], o[2], o[3]);
+                    if (dp_hi) {
+                        *(float4 *)(dp_hi + off) = make_float4(oh[0], oh[1], oh[2], oh[3]);
+                        *(float4 *)(dp_lo + off) = make_float4(ol[0], ol[1], ol[2], ol[3]);
+                    }
                 } else {
 #pragma unroll
-                    for (int u = 0; u < 4; u++) if (k + u < d) dprev[(int64_t)i * d + k + u] = o[u];
+                    for (int u = 0; u < 4; u++)
+                        if (k + u < d) {
+                            dprev[off + u] = o[u];
+                            if (dp_hi) { dp_hi[off + u] = oh[u]; dp_lo[off + u] = ol[u]; }
+                        }
                 }
             }
         }
@@ -543,33 +594,36 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
 template <int NV, bool VEC, int CM>
 cudaError_t launch_head(unsigned blocks, size_t smem, cudaStream_t s, int rows, int d, int C, const float *A, RowSel arow,
                         const float *Wb, const int32_t *labels, RowSel lrow, float inv_b, float *dZL, float *dprev,
-                        float *loss_rows, float *loss_part, unsigned *ticket, float *loss_out) {
+                        float *dp_hi, float *dp_lo, float *loss_rows, float *loss_part, unsigned *ticket,
+                        float *loss_out) {
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(head_kernel<NV, VEC, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     return launch_pdl(head_kernel<NV, VEC, CM>, dim3(blocks), dim3(HEAD_WARPS * 32), smem, s, rows, d, C, A, arow, Wb,
-                      labels, lrow, inv_b, dZL, dprev, loss_rows, loss_part, ticket, loss_out);
+                      labels, lrow, inv_b, dZL, dprev, dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out);
 }
 }  // namespace
 
 cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, const float *Wb, const int32_t *labels,
-                       RowSel lrow, float inv_b, float *dZL, float *dprev, float *loss_rows, float *loss_part,
-                       unsigned *ticket, float *loss_out, cudaStream_t s, LaunchHook *h) {
+                       RowSel lrow, float inv_b, float *dZL, float *dprev, float *dp_hi, float *dp_lo,
+                       float *loss_rows, float *loss_part, unsigned *ticket, float *loss_out, cudaStream_t s,
+                       LaunchHook *h) {
     if (C > 16 || C < 1 || d > 1024) return cudaErrorInvalidValue;
     const size_t smem = sizeof(float) * (size_t)((d + 1 + 3) & ~3) * C;
     // enough rows per block that the block count stays <= 1024 (loss partial slots)
     const unsigned blocks = std::min<unsigned>(cdiv(rows, HEAD_WARPS), 1024u);
-    const bool vec = (d % 4 == 0) && ((uintptr_t)A % 16 == 0) && (dprev == nullptr || (uintptr_t)dprev % 16 == 0);
+    const bool vec = (d % 4 == 0) && ((uintptr_t)A % 16 == 0) && (dprev == nullptr || (uintptr_t)dprev % 16 == 0) &&
+                     (dp_hi == nullptr || ((uintptr_t)dp_hi % 16 == 0 && (uintptr_t)dp_lo % 16 == 0));
     char name[80];
     snprintf(name, sizeof name, "head_softmax_xent[rows=%d,d=%d,C=%d,dgrad=%d]", rows, d, C, dprev ? 1 : 0);
     if (h) h->before(name, s);
     cudaError_t e;
 #define HEAD_CASE3(NVv, CMv)                                                                                   \
     e = vec ? launch_head<NVv, true, CMv>(blocks, smem, s, rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL, dprev, \
-                                          loss_rows, loss_part, ticket, loss_out)                              \
+                                          dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out)                \
             : launch_head<NVv, false, CMv>(blocks, smem, s, rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL,     \
-                                           dprev, loss_rows, loss_part, ticket, loss_out)
+                                           dprev, dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out)
 #define HEAD_CASE(NVv)             \
     if (C <= 2) {                  \
         HEAD_CASE3(NVv, 2);        \

@@ -118,6 +118,14 @@ struct mtx_ctx {
     uint64_t ws_bytes = 0;
     float *params = nullptr, *vel = nullptr, *grads = nullptr, *gather = nullptr;
     std::vector<float *> acts;  // MLP: acts[l] = A_l [b][d_l], l = 1..L-1
+    // 3xTF32: hi/lo planes of the buffers tensor-core GEMMs consume (registered ranges)
+    struct PlaneRange {
+        const float *base;
+        int64_t len;
+        float *hi, *lo;
+    };
+    std::vector<PlaneRange> planes;
+    float *params_hi = nullptr, *params_lo = nullptr, *stage_hi = nullptr, *stage_lo = nullptr;
     float *dz[2] = {nullptr, nullptr}, *dzL = nullptr, *loss_rows = nullptr, *partial = nullptr;
     float *stage_x = nullptr;
     int32_t *stage_y = nullptr;
@@ -307,7 +315,18 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         return p;
     };
     const int64_t b = c->b;
+    const bool x3 = c->opt.precision == MTX_3XTF32;
+    std::vector<mtx_ctx::PlaneRange> planes;
+    auto plane = [&](float *buf, int64_t len) {  // hi/lo planes next to a buffer (3xTF32 only)
+        if (!x3 || !base) {
+            if (x3) { take(4 * len); take(4 * len); }
+            return;
+        }
+        float *hi = (float *)take(4 * len), *lo = (float *)take(4 * len);
+        planes.push_back({buf, len, hi, lo});
+    };
     float *params = (float *)take(4 * c->N_pad);
+    plane(params, c->N_pad);
     float *vel = (float *)take(4 * c->N_pad);
     float *grads = (float *)take(4 * (c->N_pad + LOSS_SLOT));
     float *gather = c->opt.reduce == MTX_REDUCE_ORDERED ? (float *)take(4 * c->world * (c->N_pad + LOSS_SLOT)) : nullptr;
@@ -321,6 +340,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         acts.assign(L, nullptr);
         for (int l = 1; l < L; l++) {
             acts[l] = (float *)take(4 * b * c->dims[l]);
+            if (l < L - 1) plane(acts[l], b * c->dims[l]);  // A_{L-1} feeds only the SIMT head/narrow wgrad
             maxd = std::max<int64_t>(maxd, c->dims[l]);
         }
         for (int l = 1; l <= L; l++) {
@@ -350,8 +370,10 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         fcA.assign(nfc, nullptr);
         std::vector<int> fd{d};
         for (int f : c->fc) fd.push_back(f);
+        plane(cP.back(), b * d);  // the flattened conv output feeds fc1
         for (int f = 1; f < nfc; f++) {
             fcA[f] = (float *)take(4 * b * fd[f]);
+            if (f < nfc - 1) plane(fcA[f], b * fd[f]);
             maxd = std::max<int64_t>(maxd, fd[f]);
         }
         maxd = std::max<int64_t>(maxd, d);
@@ -372,11 +394,14 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     for (const Layer &L : c->layers) maxN = std::max<int64_t>(maxN, L.cols);
     partial = std::max<int64_t>(partial, 9472 + maxN + 32);
     float *dz0 = (float *)take(4 * b * maxd);
+    plane(dz0, b * maxd);
     float *dz1 = (float *)take(4 * b * maxd);
+    plane(dz1, b * maxd);
     float *dzL = (float *)take(4 * b * c->classes);
     float *loss_rows = (float *)take(4 * b);
     float *part = partial ? (float *)take(4 * partial) : nullptr;
     float *sx = (float *)take(4 * b * c->d0);
+    plane(sx, b * c->d0);
     int32_t *sy = (int32_t *)take(4 * b);
     float *loss_part = (float *)take(4 * 1024);
     unsigned *counters = (unsigned *)take(4 * 256);
@@ -388,6 +413,11 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         c->dz[0] = dz0; c->dz[1] = dz1; c->dzL = dzL; c->loss_rows = loss_rows;
         c->partial = part; c->partial_floats = partial;
         c->stage_x = sx; c->stage_y = sy;
+        c->planes = planes;
+        for (auto &pr : planes) {
+            if (pr.base == params) { c->params_hi = pr.hi; c->params_lo = pr.lo; }
+            if (pr.base == sx) { c->stage_hi = pr.hi; c->stage_lo = pr.lo; }
+        }
         c->loss_part = loss_part;
         c->counters = counters;
         c->ticket = (unsigned *)(misc + 48);
@@ -399,6 +429,17 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         c->proto = (uint64_t *)(misc + 512);  // world x 128 B: model digests / IPC handle records
     }
     return off + 256;
+}
+
+// hi/lo planes of the registered buffer containing p (same offset), or false
+bool plane_of(const mtx_ctx *c, const float *p, const float **hi, const float **lo) {
+    for (const auto &pr : c->planes)
+        if (p >= pr.base && p < pr.base + pr.len) {
+            *hi = pr.hi + (p - pr.base);
+            *lo = pr.lo + (p - pr.base);
+            return true;
+        }
+    return false;
 }
 
 // ------------------------------------------------------------------ step schedule
@@ -415,10 +456,21 @@ struct Runner {
         if (g.arow.win) g.a_rows_total = c->n_data + c->B;
         cudaError_t e;
         g.tf32x3 = c->opt.precision == MTX_3XTF32;
-        if (c->opt.precision != MTX_FP32 && c->tc && tc_supports(c->tc, g))
+        if (g.tf32x3) {  // operand planes from their producers, output planes for its consumers
+            plane_of(c, g.A, &g.A_hi, &g.A_lo);
+            plane_of(c, g.B, &g.B_hi, &g.B_lo);
+            const float *ch = nullptr, *cl = nullptr;
+            if (plane_of(c, g.C, &ch, &cl)) { g.C_hi = (float *)ch; g.C_lo = (float *)cl; }
+        }
+        if (c->opt.precision != MTX_FP32 && c->tc && tc_supports(c->tc, g)) {
             e = tc_gemm(c->tc, g, s, h);
-        else
+        } else {
             e = gemm_simt(g, s, h);
+            // SIMT produced a tensor a 3xTF32 GEMM will consume (rows that are not 16-B multiples
+            // cannot feed TMA: their consumers take the SIMT path too)
+            if (e == cudaSuccess && g.C_hi && g.N % 4 == 0 && g.ldc % 4 == 0)
+                e = split_planes(g.C, g.M, g.N, g.ldc, g.C_hi, g.C_lo, s, h);
+        }
         if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
         return MTX_OK;
     }
@@ -469,9 +521,11 @@ struct Runner {
         const Layer &LL = c->layers[L - 1];
         const float *Ain = L == 1 ? xbase() : c->acts[L - 1];
         RowSel ar = L == 1 ? xrow() : RowSel{nullptr, 0};
+        const float *dph = nullptr, *dpl = nullptr;
+        if (L > 1) plane_of(c, c->dz[0], &dph, &dpl);
         cudaError_t e = head_fused((int)b, d[L - 1], d[L], Ain, ar, c->params + LL.pad_off, ybase(), xrow(),
-                                   1.0f / (float)b, c->dzL, L > 1 ? c->dz[0] : nullptr, c->loss_rows, c->loss_part,
-                                   c->ticket, c->grads + c->N_pad, s, h);
+                                   1.0f / (float)b, c->dzL, L > 1 ? c->dz[0] : nullptr, (float *)dph, (float *)dpl,
+                                   c->loss_rows, c->loss_part, c->ticket, c->grads + c->N_pad, s, h);
         if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "head: %s", cudaGetErrorString(e));
         // backward l = L .. 1.  dgrad(l) reads W_l, so it is issued before wgrad(l) completes the
         // bucket holding W_l: the bucket's update (comm stream) may then overwrite W_l safely.
@@ -619,6 +673,11 @@ struct Runner {
             CK(cudaEventRecord(c->ev_fork, s));
             CK(cudaStreamWaitEvent(c->comm_s, c->ev_fork, 0));
         }
+        if (c->params_hi) {  // 3xTF32: planes of this step's parameters (and of a staged batch)
+            CK(split_planes(c->params, 1, c->N_pad, c->N_pad, c->params_hi, c->params_lo, s, h));
+            if (staged && c->stage_hi && c->d0 % 4 == 0)
+                CK(split_planes(c->stage_x, c->b, c->d0, c->d0, c->stage_hi, c->stage_lo, s, h));
+        }
         mtx_status st = c->kind == MTX_MLP ? forward_backward_mlp() : forward_backward_cnn();
         if (st) return st;
         if (c->world > 1) {
@@ -653,6 +712,13 @@ mtx_status Runner::forward_backward_cnn() {
         if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "conv_fwd: %s", cudaGetErrorString(e));
     }
     const float *flat = c->convP[NC - 1];
+    {
+        const float *fh = nullptr, *fl = nullptr;
+        if (plane_of(c, flat, &fh, &fl) && fd[0] % 4 == 0) {
+            e = split_planes(flat, b, fd[0], fd[0], (float *)fh, (float *)fl, s, h);
+            if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "split_planes: %s", cudaGetErrorString(e));
+        }
+    }
     auto fc_in = [&](int f) -> const float * { return f == 1 ? flat : c->fcA[f - 1]; };
     for (int f = 1; f < NF; f++) {
         const Layer &Ly = c->layers[NC + f - 1];
@@ -666,9 +732,11 @@ mtx_status Runner::forward_backward_cnn() {
         if ((st = gemm(g))) return st;
     }
     float *head_dprev = NF > 1 ? c->dz[0] : c->convDP[NC - 1];
+    const float *dph = nullptr, *dpl = nullptr;
+    if (NF > 1) plane_of(c, c->dz[0], &dph, &dpl);
     e = head_fused((int)b, fd[NF - 1], fd[NF], fc_in(NF), RowSel{nullptr, 0}, c->params + c->layers[NC + NF - 1].pad_off,
-                   ybase(), xrow(), 1.0f / (float)b, c->dzL, head_dprev, c->loss_rows, c->loss_part, c->ticket,
-                   c->grads + c->N_pad, s, h);
+                   ybase(), xrow(), 1.0f / (float)b, c->dzL, head_dprev, (float *)dph, (float *)dpl, c->loss_rows,
+                   c->loss_part, c->ticket, c->grads + c->N_pad, s, h);
     if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "head: %s", cudaGetErrorString(e));
     int cur = 0;
     size_t bk = 0;
@@ -977,7 +1045,9 @@ mtx_status mtx_bcast_params(mtx_ctx *c, int32_t root, void *stream) {
 mtx_status mtx_dataset_bytes(const mtx_ctx *c, int64_t n, uint64_t *bytes) {
     if (!c || !bytes || n <= 0) return MTX_ERR_INVALID_ARG;
     uint64_t rows = (uint64_t)(n + c->B);
-    *bytes = (rows * c->d0 * 4 + 255) / 256 * 256 + rows * 4 + 256;
+    const uint64_t xb = (rows * c->d0 * 4 + 255) / 256 * 256;
+    const int nx = c->opt.precision == MTX_3XTF32 ? 3 : 1;  // + hi/lo planes for the tensor cores
+    *bytes = nx * xb + rows * 4 + 256;
     return MTX_OK;
 }
 
@@ -994,8 +1064,10 @@ mtx_status mtx_shard_data(mtx_ctx *c, const float *X, const int32_t *y, int64_t 
     if (buf_bytes < need || ((uintptr_t)dev_buf & 255)) return fail(c, MTX_ERR_OOM, "dataset buffer too small");
     cudaStream_t s = pick(c, stream);
     const uint64_t rows = (uint64_t)(n + c->B), d = c->d0;
+    const uint64_t xb = (rows * d * 4 + 255) / 256 * 256;
+    const int nx = c->opt.precision == MTX_3XTF32 ? 3 : 1;
     float *Xd = (float *)dev_buf;
-    int32_t *Yd = (int32_t *)((uint8_t *)dev_buf + (rows * d * 4 + 255) / 256 * 256);
+    int32_t *Yd = (int32_t *)((uint8_t *)dev_buf + nx * xb);
     cudaMemcpyKind k = src_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     CK(cudaMemcpyAsync(Xd, X, (size_t)n * d * 4, k, s));
     CK(cudaMemcpyAsync(Yd, y, (size_t)n * 4, k, s));
@@ -1003,6 +1075,15 @@ mtx_status mtx_shard_data(mtx_ctx *c, const float *X, const int32_t *y, int64_t 
     CK(cudaMemcpyAsync(Xd + (size_t)n * d, Xd, (size_t)c->B * d * 4, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(Yd + n, Yd, (size_t)c->B * 4, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemsetAsync(c->win, 0, 8, s));
+    // drop planes of a previously registered dataset; add this one's (3xTF32, rows of 16-B multiples)
+    c->planes.erase(std::remove_if(c->planes.begin(), c->planes.end(),
+                                   [&](const mtx_ctx::PlaneRange &pr) { return pr.base == c->X && c->X; }),
+                    c->planes.end());
+    if (nx == 3 && d % 4 == 0) {
+        float *hi = (float *)((uint8_t *)dev_buf + xb), *lo = (float *)((uint8_t *)dev_buf + 2 * xb);
+        CK(split_planes(Xd, (int64_t)rows, (int64_t)d, (int64_t)d, hi, lo, s, nullptr));
+        c->planes.push_back({Xd, (int64_t)(rows * d), hi, lo});
+    }
     CK(cudaStreamSynchronize(s));
     c->X = Xd;
     c->Y = Yd;
@@ -1207,6 +1288,24 @@ mtx_status mtx_debug_gemm(mtx_ctx *c, int32_t engine, int32_t M, int32_t N, int3
     g.counters = c->counters;
     cudaStream_t s = pick(c, stream);
     cudaError_t e;
+    std::vector<void *> tmp;  // diagnostic path: temporary operand planes for engine 2
+    struct Free {
+        std::vector<void *> &v;
+        ~Free() {
+            for (void *p : v) cudaFree(p);
+        }
+    } freer{tmp};
+    if (engine == 2) {
+        const int64_t na = ta ? (int64_t)K * lda : (int64_t)M * lda, nb = tb ? (int64_t)N * ldb : (int64_t)K * ldb;
+        float *pl[4];
+        for (int i = 0; i < 4; i++) {
+            CK(cudaMalloc(&pl[i], 4 * (i < 2 ? na : nb)));
+            tmp.push_back(pl[i]);
+        }
+        CK(split_planes(A, 1, na, na, pl[0], pl[1], s, nullptr));
+        CK(split_planes(B, 1, nb, nb, pl[2], pl[3], s, nullptr));
+        g.A_hi = pl[0]; g.A_lo = pl[1]; g.B_hi = pl[2]; g.B_lo = pl[3];
+    }
     if (engine == 1 || engine == 2) {
         g.tf32x3 = engine == 2;
         if (!c->tc) c->tc = tc_create(c->device);
