@@ -8,9 +8,12 @@
 //   * warp 1: MMA issuer -- one elected thread issues tcgen05.mma.cta_group::1.kind::tf32
 //     (M = 128, N = BN, K = 8 per instruction) into a TMEM accumulator; tcgen05.commit
 //     frees the smem slot and, after the last k-block, signals the epilogue
-//   * warp 2: TMEM allocator (2 accumulators x BN columns -> epilogue/mainloop overlap)
-//   * warps 4-7: epilogue -- tcgen05.ld 32x32b (one accumulator row per thread), fused
-//     bias + ReLU (forward), ReLU mask (dgrad) or plain/partial store (wgrad)
+//   * warp 2: TMEM allocator (a ring of up to 4 accumulators x BN columns -> the MMA warp runs
+//     ahead of the epilogue)
+//   * warps 4-11: epilogue -- tcgen05.ld 32x32b (one accumulator row per thread) promoted into
+//     fp32 registers; the finished tile is staged through swizzled shared memory and written
+//     as whole row segments with the fused bias + ReLU (forward), ReLU mask (dgrad), hi/lo
+//     planes (3xTF32 consumers) or plain/partial store (wgrad)
 //
 // Operands are read in place from the row-major activation/weight/gradient
 // buffers: K-major (rows contiguous in K) or MN-major (contiguous in M/N) via the
@@ -33,7 +36,6 @@ constexpr int BM = 128, BK = 32;
 // rne_tf32(x) and lo = rne_tf32(x - hi), written once by the tensor's producer.
 template <int BN, bool SPLIT>
 struct SmemLayout {
-    static constexpr int STAGES = SPLIT ? 3 : 6;
     // warps 0 TMA, 1 MMA, 2 TMEM alloc, 3 spare, 4-11 epilogue
     static constexpr int THREADS = 384;
     // k-blocks accumulated in TMEM before the epilogue warps promote the partial into fp32
@@ -43,9 +45,18 @@ struct SmemLayout {
     static constexpr uint32_t B_BYTES = BN * BK * 4;
     static constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;
     static constexpr uint32_t STAGE_BYTES = RAW_BYTES * (SPLIT ? 2 : 1);
-    static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
+    // epilogue staging: one 32 x 32 fp32 sub-tile per epilogue warp (coalesced stores)
+    static constexpr uint32_t EPI_BYTES = 8 * 32 * 32 * 4;
+    static constexpr uint32_t SMEM_MAX = 232448;  // 227 KB opt-in per CTA
+    static constexpr int STAGES_FIT = (int)((SMEM_MAX - 256 - 1024 - EPI_BYTES) / STAGE_BYTES);
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;  // deepest ring that fits
+    static_assert(STAGES >= 2, "smem ring");
+    static constexpr uint32_t EPI_OFF = STAGES * STAGE_BYTES;
+    static constexpr uint32_t BAR_OFF = EPI_OFF + EPI_BYTES;
     static constexpr uint32_t TOTAL = BAR_OFF + 256 + 1024;  // barriers + tmem slot + 1024-B alignment slack
-    static constexpr uint32_t TMEM_COLS = 2 * BN;            // double-buffered accumulator
+    // TMEM accumulator ring: the MMA warp runs up to NBUF chunks ahead of the epilogue
+    static constexpr int NBUF = 512 / BN > 4 ? 4 : 512 / BN;
+    static constexpr uint32_t TMEM_COLS = NBUF * BN;
 };
 
 struct TcParams {
@@ -203,11 +214,12 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t sbase = smem_u32(smem);
     uint64_t *bars = (uint64_t *)(smem + L::BAR_OFF);
-    // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]
+    // bars: full[STAGES], empty[STAGES], tfull[NBUF], tempty[NBUF]  (<= 192 B)
+    constexpr int NBUF = L::NBUF;
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * STAGES, tfull0 = empty0 + 8 * STAGES,
-                   tempty0 = tfull0 + 16;
-    uint32_t *tmem_slot = (uint32_t *)(smem + L::BAR_OFF + 128);
-    volatile int *fix_flag = (volatile int *)(smem + L::BAR_OFF + 136);
+                   tempty0 = tfull0 + 8 * NBUF;
+    uint32_t *tmem_slot = (uint32_t *)(smem + L::BAR_OFF + 224);
+    volatile int *fix_flag = (volatile int *)(smem + L::BAR_OFF + 232);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (warp == 0 && lane == 0) {
@@ -221,7 +233,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
             mbar_init(full0 + 8 * s, 1);
             mbar_init(empty0 + 8 * s, 1);
         }
-        for (int a = 0; a < 2; a++) {
+        for (int a = 0; a < NBUF; a++) {
             mbar_init(tfull0 + 8 * a, 1);
             mbar_init(tempty0 + 8 * a, 8);
         }
@@ -325,7 +337,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                     umma_commit(tfull0 + 8 * buf);  // chunk partial ready for promotion
-                    if (++buf == 2) { buf = 0; buf_phase ^= 1; }
+                    if (++buf == NBUF) { buf = 0; buf_phase ^= 1; }
                 }
             }
         }
@@ -365,22 +377,82 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
-                if (++buf == 2) { buf = 0; buf_phase ^= 1; }
+                if (++buf == NBUF) { buf = 0; buf_phase ^= 1; }
             }
-            const int m = m0 + 32 * q + lane;
-            if (p.splits > 1) {
-                // split-K: write this split's partial, then the last CTA to arrive for the tile folds
-                // all partials in ascending split order and applies the epilogue (deterministic)
-                if (m < p.M) {
-                    float *prow = p.partial + ((int64_t)z * p.M + m) * p.N;
+            // ---- store: stage each 32-row x CW-column sub-tile in shared memory (lane = row, 16-B
+            // chunks XOR-swizzled: conflict-free both ways), then the warp writes whole row segments
+            // (CPR lanes per row, RPI rows per instruction) with the fused epilogue applied there.
+            constexpr int SW = HALF >= 32 ? 32 : HALF;  // staged columns
+            constexpr int CPR = SW / 4, RPI = 32 / CPR;
+            float *stg = (float *)(smem + L::EPI_OFF) + (warp - 4) * 32 * 32;
+            const int jj = lane % CPR, rl = lane / CPR;
+            auto swz = [](int row, int chunk) { return (chunk ^ (row / (8 / CPR))) & (CPR - 1); };
 #pragma unroll
-                    for (int g4 = 0; g4 < HALF / 4; g4++) {
-                        const int n = n0 + 4 * g4;
-                        if (n + 3 < p.N) *(float4 *)(prow + n) = make_float4(acc[4 * g4], acc[4 * g4 + 1], acc[4 * g4 + 2], acc[4 * g4 + 3]);
-                        else for (int e = 0; e < 4 && n + e < p.N; e++) prow[n + e] = acc[4 * g4 + e];
+            for (int c = 0; c < HALF / SW; c++) {
+#pragma unroll
+                for (int j = 0; j < CPR; j++)
+                    *(float4 *)(stg + lane * SW + 4 * swz(lane, j)) =
+                        make_float4(acc[SW * c + 4 * j], acc[SW * c + 4 * j + 1], acc[SW * c + 4 * j + 2],
+                                    acc[SW * c + 4 * j + 3]);
+                __syncwarp();
+                const int n = n0 + SW * c + 4 * jj;
+#pragma unroll 4
+                for (int it = 0; it < 32 / RPI; it++) {
+                    const int r = it * RPI + rl;
+                    const int m = m0 + 32 * q + r;
+                    const float4 sv = *(const float4 *)(stg + r * SW + 4 * swz(r, jj));
+                    if (m >= p.M || n >= p.N) continue;
+                    const bool vec4 = n + 3 < p.N;
+                    float o[4] = {sv.x, sv.y, sv.z, sv.w};
+                    if (p.splits > 1) {  // split-K partial (folded with the epilogue by splitk_reduce)
+                        float *dst = p.partial + ((int64_t)z * p.M + m) * p.N + n;
+                        if (vec4) *(float4 *)dst = sv;
+                        else for (int e = 0; e < 4 && n + e < p.N; e++) dst[e] = o[e];
+                        continue;
+                    }
+                    if (p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) {
+#pragma unroll
+                        for (int e = 0; e < 4; e++)
+                            if (n + e < p.N) {
+                                o[e] += __ldg(p.bias + n + e);
+                                if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e], 0.f);
+                            }
+                    } else if (p.epi == EPI_MASK) {
+                        const float *mk = p.mask + (int64_t)m * p.ldm + n;
+                        float mv[4];
+                        if (vec4) {
+                            const float4 t4 = __ldg((const float4 *)mk);
+                            mv[0] = t4.x; mv[1] = t4.y; mv[2] = t4.z; mv[3] = t4.w;
+                        } else {
+                            for (int e = 0; e < 4; e++) mv[e] = n + e < p.N ? mk[e] : 0.f;
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; e++)
+                            if (!(mv[e] > 0.f)) o[e] = 0.f;
+                    }
+                    const int64_t off = (int64_t)m * p.ldc + n;
+                    if (vec4) *(float4 *)(p.C + off) = make_float4(o[0], o[1], o[2], o[3]);
+                    else for (int e = 0; e < 4 && n + e < p.N; e++) p.C[off + e] = o[e];
+                    if (p.C_hi) {  // hi/lo planes for the consuming 3xTF32 GEMM
+                        float hi[4], lo[4];
+#pragma unroll
+                        for (int e = 0; e < 4; e++) split_tf32(o[e], hi[e], lo[e]);
+                        if (vec4) {
+                            *(float4 *)(p.C_hi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                            *(float4 *)(p.C_lo + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+                        } else {
+                            for (int e = 0; e < 4 && n + e < p.N; e++) {
+                                p.C_hi[off + e] = hi[e];
+                                p.C_lo[off + e] = lo[e];
+                            }
+                        }
                     }
                 }
-                if (!p.counters) continue;  // folded by a separate kernel
+                __syncwarp();
+            }
+            if (p.splits > 1 && p.counters) {
+                // in-kernel fixup (MTX_TC_FIXUP=1): the last CTA to arrive for the tile folds all
+                // partials in ascending split order and applies the epilogue (deterministic)
                 __threadfence();
                 asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps
                 if (threadIdx.x == 128) *fix_flag = atomicAdd(p.counters + r, 1u) == (unsigned)(p.splits - 1);
@@ -389,47 +461,6 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                 __threadfence();
                 splitk_fixup<BN>(p, r, m0);
                 if (threadIdx.x == 128) p.counters[r] = 0u;  // re-armed for the next launch
-                continue;
-            }
-            if (m >= p.M) continue;
-            float *dst_row = p.C + (int64_t)m * p.ldc;
-#pragma unroll
-            for (int g4 = 0; g4 < HALF / 4; g4++) {
-                const int n = n0 + 4 * g4;
-                if (n >= p.N) break;
-                float o[4] = {acc[4 * g4], acc[4 * g4 + 1], acc[4 * g4 + 2], acc[4 * g4 + 3]};
-                if (p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) {
-#pragma unroll
-                    for (int e = 0; e < 4; e++)
-                        if (n + e < p.N) {
-                            o[e] += p.bias[n + e];
-                            if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e], 0.f);
-                        }
-                } else if (p.epi == EPI_MASK) {
-#pragma unroll
-                    for (int e = 0; e < 4; e++)
-                        if (n + e < p.N && !(p.mask[(int64_t)m * p.ldm + n + e] > 0.f)) o[e] = 0.f;
-                }
-                if (n + 3 < p.N) {
-                    *(float4 *)(dst_row + n) = make_float4(o[0], o[1], o[2], o[3]);
-                } else {
-                    for (int e = 0; e < 4 && n + e < p.N; e++) dst_row[n + e] = o[e];
-                }
-                if (p.C_hi) {  // hi/lo planes for the consuming 3xTF32 GEMM
-                    float hi[4], lo[4];
-#pragma unroll
-                    for (int e = 0; e < 4; e++) split_tf32(o[e], hi[e], lo[e]);
-                    const int64_t off = (int64_t)m * p.ldc + n;
-                    if (n + 3 < p.N) {
-                        *(float4 *)(p.C_hi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-                        *(float4 *)(p.C_lo + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
-                    } else {
-                        for (int e = 0; e < 4 && n + e < p.N; e++) {
-                            p.C_hi[off + e] = hi[e];
-                            p.C_lo[off + e] = lo[e];
-                        }
-                    }
-                }
             }
         }
     }
