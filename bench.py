@@ -182,7 +182,10 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
             "share_of_kernel_time": round(top["ms"] / total, 3),
             "launch_overhead_us_subtracted": round(over_ms * 1e3, 3),
             "breakdown_us_per_step": {k: round(g["ms"] * 1e3 / steps, 2) for k, g in
-                                      sorted(groups.items(), key=lambda kv: -kv[1]["ms"])}}
+                                      sorted(groups.items(), key=lambda kv: -kv[1]["ms"])},
+            # every distinct launch of the step (name carries the shape / plan), overhead-corrected
+            "launches_us_per_step": {k: round(ms * 1e3 / steps, 2) for k, (ms, cnt) in
+                                     sorted(timing.items(), key=lambda kv: -kv[1][0])}}
 
 
 # ----------------------------------------------------------------------------- CPU oracle baseline

@@ -259,7 +259,9 @@ mtx_status mtx_read_timing(mtx_ctx *ctx, char *names_buf, uint64_t names_len, do
                            int32_t max_sites, int32_t *n_sites, int32_t reset);
 
 /* Diagnostic: one local contraction through a chosen engine (0 = SIMT fp32, 1 =
- * tcgen05 TF32, 2 = tcgen05 3xTF32), exactly as the step issues it -- C[M,N] = op(A) op(B) with
+ * tcgen05 TF32, 2 = tcgen05 3xTF32 -- A and B are split into hi/lo planes in library-owned
+ * scratch first; 3 = tcgen05 3xTF32 on the planes of the previous engine-2 call, which must
+ * have had the same A, B, shape and layout: times the contraction alone), exactly as the step issues it -- C[M,N] = op(A) op(B) with
  * epilogue epi (0 store, 1 +bias then ReLU, 2 +bias, 3 x [mask > 0]); ta/tb as
  * in the step's forward (0,0), dgrad (0,1) and wgrad (1,0) layouts.  Device
  * pointers, row-major fp32, leading dimensions in elements.  Used by the

@@ -169,7 +169,7 @@ __device__ __noinline__ void splitk_fixup(const TcParams &p, int r, int m0) {
     {   // last CTA of the tile: fold all splits in ascending order, coalesced -- the 256
         // epilogue threads sweep the 128 x BN tile row by row, one float4 each
         const int et = threadIdx.x - 128;
-        const int mt0 = m0, nt0 = (r / p.tiles_m) * BN;
+        const int mt0 = m0, nt0 = (r % p.tiles_n) * BN;
         for (int idx = et; idx < BM * (BN / 4); idx += 256) {
             const int mm = mt0 + idx / (BN / 4), nn = nt0 + 4 * (idx % (BN / 4));
             if (mm >= p.M || nn >= p.N) continue;
@@ -263,7 +263,9 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 const int z = t / tiles_mn, r = t % tiles_mn;
-                const int m0 = (r % p.tiles_m) * BM, n0 = (r / p.tiles_m) * BN;
+                // raster n-fastest: the CTAs sharing an A row-panel run together (A read from DRAM once,
+                // B -- the weights -- stays L2-resident)
+                const int m0 = (r / p.tiles_n) * BM, n0 = (r % p.tiles_n) * BN;
                 const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
                 for (int kb = kb0; kb < kb1; kb++) {
                     mbar_wait(empty0 + 8 * stage, phase ^ 1);
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
         uint32_t buf_phase = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x) {
             const int z = t / tiles_mn, r = t % tiles_mn;
-            const int m0 = (r % p.tiles_m) * BM, n0 = (r / p.tiles_m) * BN + h * HALF;
+            const int m0 = (r / p.tiles_n) * BM, n0 = (r % p.tiles_n) * BN + h * HALF;
             const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
             float acc[HALF];
             bool first = true;
@@ -508,31 +510,37 @@ struct TcGemm {
 
 bool tc_available() { return true; }
 
-// Tile plan: the widest N tile (128, 64, 32) that still gives >= sms/2 output tiles, then split K
-// only if the tile count is still below that (split-K costs a fold pass over the partials).
+// Tile plan, fitted to the plan sweep (tools/gemm_plan_sweep.py): problems whose
+// 128-wide tiles already cover half the SMs run unsplit 128-wide tiles; smaller ones take the widest
+// N tile (128, 64, 32) whose tiles x K-splits reach 3/4 of the SMs with >= 4 k-blocks per split
+// (wide tiles keep the operand re-reads from L2 low; splits fill the SMs, their fold is one light
+// launch).  Store-bound single-k-block GEMMs use 64-wide tiles.
 TcPlan tc_plan(int sms, int M, int N, int K) {
     TcPlan pl;
     const int tm = (M + BM - 1) / BM;
-    const int kb_all = (K + BK - 1) / BK;
-    for (int bn : {128, 64, 32}) {
-        pl.bn = bn;
-        // long K: split-K of wide tiles keeps the per-flop smem traffic low and amortises its fold
-        if (tm * ((N + bn - 1) / bn) * 2 >= sms || kb_all >= 64) break;
-    }
-    const int tiles = tm * ((N + pl.bn - 1) / pl.bn);
     const int kb = (K + BK - 1) / BK;
+    const int max_split = std::max(1, kb / 4);
+    pl.bn = 128;
     pl.splits = 1;
-    if (tiles * 2 < sms) {
-        int s = std::min(sms / tiles, std::max(1, kb / 3));  // >= 3 k-blocks per split
-        const int per = (kb + s - 1) / s;
+    if (tm * ((N + 127) / 128) * 2 >= sms) {
+        if (kb <= 2 && N >= 64) pl.bn = 64;
+    } else {
+        for (int bn : {128, 64, 32}) {
+            const int tiles = tm * ((N + bn - 1) / bn);
+            const int s = std::max(1, std::min(max_split, sms / tiles));
+            pl.bn = bn;
+            pl.splits = s;
+            if (tiles * s * 4 >= sms * 3) break;
+        }
+        const int per = (kb + pl.splits - 1) / pl.splits;
         pl.splits = (kb + per - 1) / per;
-        // a split costs a fold launch over the partials: only worth it when it buys >= min_split x
-        static const int min_split = [] {
-            const char *e = getenv("MTX_TC_MINSPLIT");  // development knob
-            return e ? atoi(e) : 2;
-        }();
-        if (pl.splits < min_split) pl.splits = 1;
     }
+    // development overrides for plan sweeps (tools/gemm_plan_sweep.py), read on every call
+    if (const char *e = getenv("MTX_TC_BN")) {
+        const int v = atoi(e);
+        if (v == 32 || v == 64 || v == 128) pl.bn = v;
+    }
+    if (const char *e = getenv("MTX_TC_SPLITS")) pl.splits = std::max(1, std::min(atoi(e), kb));
     return pl;
 }
 
@@ -655,7 +663,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
         if (e != cudaSuccess) return e;
     }
     if (g.aug)  // bias gradient row: db[n] = sum_k B[k][n]  (the ones row of the augmented A)
-        e = colsum(g.B, K, N, g.ldb, g.C + (int64_t)M * g.ldc, g.partial, g.partial_cap, g.counters + 255, s, h);
+        e = colsum(g.B, K, N, g.ldb, g.C + (int64_t)M * g.ldc, g.partial, g.partial_cap, g.counters + 256, s, h);
     return e;
 }
 

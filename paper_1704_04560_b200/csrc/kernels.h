@@ -52,8 +52,10 @@ struct LaunchHook {
 cudaError_t gemm_simt(const GemmDesc &g, cudaStream_t s, LaunchHook *h);
 
 // out[n] = sum_{k} X[k][n] for X [K][ld] (column sums, e.g. the bias gradient colsum(dZ)):
-// fixed-order per-block sums into partial[z][N]; the last block (ticket, zero on entry and
-// re-armed on exit) folds them in ascending z -- deterministic, one launch.
+// fixed-order per-block sums into partial[z][N]; per 128-column group, the last block to finish
+// (ticket[group], zero on entry and re-armed on exit) folds the group's partials with a fixed
+// summation tree -- deterministic, one launch.  ticket points at COLSUM_MAX_GROUPS counters.
+constexpr int COLSUM_MAX_GROUPS = 64;  // N <= 8192
 cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *partial, int64_t partial_cap,
                    unsigned *ticket, cudaStream_t s, LaunchHook *h);
 

@@ -352,12 +352,12 @@ __global__ void __launch_bounds__(256) colsum_kernel(const float *__restrict__ X
         return make_float4(n < N ? src[0] : 0.f, n + 1 < N ? src[1] : 0.f, n + 2 < N ? src[2] : 0.f,
                            n + 3 < N ? src[3] : 0.f);
     };
-    for (int k = k0 + w; k < k1; k += 32) {
-        float4 v[4];
+    for (int k = k0 + w; k < k1; k += 64) {  // 8 independent row loads in flight per thread
+        float4 v[8];
 #pragma unroll
-        for (int u = 0; u < 4; u++) v[u] = (k + 8 * u < k1) ? load(k + 8 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < 8; u++) v[u] = (k + 8 * u < k1) ? load(k + 8 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < 8; u++) {
             acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
         }
     }
@@ -375,24 +375,66 @@ __global__ void __launch_bounds__(256) colsum_kernel(const float *__restrict__ X
         if (n + 2 < N) dst[2] = s.z;
         if (n + 3 < N) dst[3] = s.w;
     }
-    // the last block to finish folds the per-split partials in ascending split order
+    // the last block to finish for this 128-column group folds the group's per-split partials:
+    // warp w sums splits w, w + 8, ... (loads issued together), then warp 0 adds the 8 warp sums in
+    // order -- a fixed summation tree, so the result is deterministic
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1;
+    if (threadIdx.x == 0) last = atomicAdd(ticket + blockIdx.x, 1u) == gridDim.y - 1;
     __syncthreads();
     if (!last) return;
     __threadfence();
-    for (int c = threadIdx.x; c < N; c += blockDim.x) {
-        float s = 0.f;
-        for (unsigned z = 0; z < gridDim.y; z++) s += __ldcg(partial + (int64_t)z * N + c);
-        out[c] = s;
+    float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (n < N) {
+        const int Z = (int)gridDim.y;
+        for (int z0 = w; z0 < Z; z0 += 64) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int z = z0 + 8 * u;
+                v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (z < Z) {
+                    const float *src = partial + (int64_t)z * N + n;
+                    v[u].x = __ldcg(src);
+                    if (n + 1 < N) v[u].y = __ldcg(src + 1);
+                    if (n + 2 < N) v[u].z = __ldcg(src + 2);
+                    if (n + 3 < N) v[u].w = __ldcg(src + 3);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                f.x += v[u].x; f.y += v[u].y; f.z += v[u].z; f.w += v[u].w;
+            }
+        }
     }
-    if (threadIdx.x == 0) *ticket = 0u;
+    __syncthreads();
+    sh[w][lane] = f;
+    __syncthreads();
+    if (w == 0 && n < N) {
+        float4 s = sh[0][lane];
+#pragma unroll
+        for (int i = 1; i < 8; i++) {
+            s.x += sh[i][lane].x; s.y += sh[i][lane].y; s.z += sh[i][lane].z; s.w += sh[i][lane].w;
+        }
+        out[n] = s.x;
+        if (n + 1 < N) out[n + 1] = s.y;
+        if (n + 2 < N) out[n + 2] = s.z;
+        if (n + 3 < N) out[n + 3] = s.w;
+    }
+    if (threadIdx.x == 0) ticket[blockIdx.x] = 0u;  // re-armed for the next launch
 }
 }  // namespace
 
 cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *partial, int64_t partial_cap,
                    unsigned *ticket, cudaStream_t s, LaunchHook *h) {
+    if (N > 128 * COLSUM_MAX_GROUPS) {  // wider than the ticket array: consecutive launches per column block
+        for (int c0 = 0; c0 < N; c0 += 128 * COLSUM_MAX_GROUPS) {
+            const cudaError_t e = colsum(X + c0, K, std::min(N - c0, 128 * COLSUM_MAX_GROUPS), ld, out + c0, partial,
+                                         partial_cap, ticket, s, h);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
     const int cols = (N + 127) / 128;
     int splits = std::max(1, std::min((K + 63) / 64, (2 * 148 + cols - 1) / cols));
     while (splits > 1 && (int64_t)splits * N > partial_cap) splits--;

@@ -135,6 +135,11 @@ struct mtx_ctx {
     float *loss_part = nullptr;
     unsigned *ticket = nullptr;
     unsigned *counters = nullptr;  // tensor-core split-K tile counters
+    // mtx_debug_gemm engine 2/3: grow-only scratch planes and the operands they were split from
+    float *dbg_planes = nullptr;
+    int64_t dbg_floats = 0;
+    const void *dbg_key[2] = {nullptr, nullptr};
+    int64_t dbg_n[2] = {0, 0};
     // MTX_REDUCE_FUSED: peer mappings of every rank's workspace
     PeerPtrs pp{};
     std::vector<void *> ipc_opened;
@@ -404,7 +409,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     plane(sx, b * c->d0);
     int32_t *sy = (int32_t *)take(4 * b);
     float *loss_part = (float *)take(4 * 1024);
-    unsigned *counters = (unsigned *)take(4 * 256);
+    unsigned *counters = (unsigned *)take(4 * 512);  // [0,254) split-K tiles, 254 narrow, 256.. colsum
     uint8_t *misc = take(512 + 128 * (uint64_t)c->world);
     if (assign) {
         c->params = params; c->vel = vel; c->grads = grads; c->gather = gather;
@@ -1288,23 +1293,29 @@ mtx_status mtx_debug_gemm(mtx_ctx *c, int32_t engine, int32_t M, int32_t N, int3
     g.counters = c->counters;
     cudaStream_t s = pick(c, stream);
     cudaError_t e;
-    std::vector<void *> tmp;  // diagnostic path: temporary operand planes for engine 2
-    struct Free {
-        std::vector<void *> &v;
-        ~Free() {
-            for (void *p : v) cudaFree(p);
-        }
-    } freer{tmp};
-    if (engine == 2) {
+    if (engine == 2 || engine == 3) {
         const int64_t na = ta ? (int64_t)K * lda : (int64_t)M * lda, nb = tb ? (int64_t)N * ldb : (int64_t)K * ldb;
-        float *pl[4];
-        for (int i = 0; i < 4; i++) {
-            CK(cudaMalloc(&pl[i], 4 * (i < 2 ? na : nb)));
-            tmp.push_back(pl[i]);
+        const int64_t na4 = (na + 63) & ~63ll, nb4 = (nb + 63) & ~63ll;
+        if (engine == 3 && (c->dbg_key[0] != A || c->dbg_key[1] != B || c->dbg_n[0] != na || c->dbg_n[1] != nb))
+            return fail(c, MTX_ERR_STATE, "engine 3 needs a preceding engine-2 call on the same operands");
+        if (engine == 2) {
+            if (2 * (na4 + nb4) > c->dbg_floats) {
+                CK(cudaStreamSynchronize(s));
+                if (c->dbg_planes) cudaFree(c->dbg_planes);
+                c->dbg_planes = nullptr;
+                c->dbg_floats = 0;
+                CK(cudaMalloc(&c->dbg_planes, 4 * 2 * (na4 + nb4)));
+                c->dbg_floats = 2 * (na4 + nb4);
+            }
         }
-        CK(split_planes(A, 1, na, na, pl[0], pl[1], s, nullptr));
-        CK(split_planes(B, 1, nb, nb, pl[2], pl[3], s, nullptr));
+        float *pl[4] = {c->dbg_planes, c->dbg_planes + na4, c->dbg_planes + 2 * na4, c->dbg_planes + 2 * na4 + nb4};
+        if (engine == 2) {
+            CK(split_planes(A, 1, na, na, pl[0], pl[1], s, nullptr));
+            CK(split_planes(B, 1, nb, nb, pl[2], pl[3], s, nullptr));
+            c->dbg_key[0] = A; c->dbg_key[1] = B; c->dbg_n[0] = na; c->dbg_n[1] = nb;
+        }
         g.A_hi = pl[0]; g.A_lo = pl[1]; g.B_hi = pl[2]; g.B_lo = pl[3];
+        engine = 2;
     }
     if (engine == 1 || engine == 2) {
         g.tf32x3 = engine == 2;
@@ -1347,6 +1358,7 @@ mtx_status mtx_finalize(mtx_ctx *c) {
     if (c->comm_s) cudaStreamDestroy(c->comm_s);
     if (c->h_loss) cudaFreeHost(c->h_loss);
     if (c->h_flag) cudaFreeHost(c->h_flag);
+    if (c->dbg_planes) cudaFree(c->dbg_planes);
     if (c->tc) tc_destroy(c->tc);
     delete c;
     return MTX_OK;
