@@ -30,6 +30,7 @@ namespace {
 
 constexpr int64_t ALIGN_F = 32;  // 128-byte alignment of every layer block (floats)
 constexpr int64_t LOSS_SLOT = 32;
+constexpr int COUNTERS_PER_LANE = 512;
 
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -134,7 +135,14 @@ struct mtx_ctx {
     unsigned long long *dig = nullptr;
     float *loss_part = nullptr;
     unsigned *ticket = nullptr;
-    unsigned *counters = nullptr;  // tensor-core split-K tile counters
+    unsigned *counters = nullptr;  // split-K / colsum / narrow-wgrad tickets, COUNTERS_PER_LANE per lane
+    // MLP backward: every weight gradient but the first layer's runs on a side stream ("lane") so
+    // it overlaps the dgrad chain; each lane owns a split-K partial region and its tickets
+    static constexpr int LANES = 3;
+    int lanes = 1;
+    cudaStream_t side[LANES - 1] = {nullptr, nullptr};
+    cudaEvent_t ev_lane[LANES] = {nullptr, nullptr, nullptr};
+    std::vector<float *> dzs;  // MLP: dZ_l [b][d_l] for l = 1 .. L-1 (one buffer per layer)
     // mtx_debug_gemm engine 2/3: grow-only scratch planes and the operands they were split from
     float *dbg_planes = nullptr;
     int64_t dbg_floats = 0;
@@ -162,7 +170,6 @@ struct mtx_ctx {
     ncclComm_t comm = nullptr;
     cudaStream_t own = nullptr, comm_s = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    std::vector<cudaEvent_t> ev_bucket;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};  // [0] resident data, [1] staged host data
     cudaGraphExec_t graph_timed[2] = {nullptr, nullptr};  // same, with event nodes around every kernel
     cudaStream_t graph_stream[2] = {nullptr, nullptr};
@@ -335,7 +342,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     float *vel = (float *)take(4 * c->N_pad);
     float *grads = (float *)take(4 * (c->N_pad + LOSS_SLOT));
     float *gather = c->opt.reduce == MTX_REDUCE_ORDERED ? (float *)take(4 * c->world * (c->N_pad + LOSS_SLOT)) : nullptr;
-    std::vector<float *> acts, fcA;
+    std::vector<float *> acts, fcA, dzs;
     std::vector<float *> cR, cP, cDR, cDP;
     std::vector<uint8_t *> cArg;
     int64_t maxd = 1;
@@ -346,7 +353,11 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         for (int l = 1; l < L; l++) {
             acts[l] = (float *)take(4 * b * c->dims[l]);
             if (l < L - 1) plane(acts[l], b * c->dims[l]);  // A_{L-1} feeds only the SIMT head/narrow wgrad
-            maxd = std::max<int64_t>(maxd, c->dims[l]);
+        }
+        dzs.assign(L, nullptr);
+        for (int l = 1; l < L; l++) {  // dZ_l: A operand of dgrad(l), B operand of wgrad(l)
+            dzs[l] = (float *)take(4 * b * c->dims[l]);
+            plane(dzs[l], b * c->dims[l]);
         }
         for (int l = 1; l <= L; l++) {
             int64_t M = c->dims[l - 1] + 1, N = c->dims[l];
@@ -398,22 +409,27 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     int64_t maxN = 1;
     for (const Layer &L : c->layers) maxN = std::max<int64_t>(maxN, L.cols);
     partial = std::max<int64_t>(partial, 9472 + maxN + 32);
-    float *dz0 = (float *)take(4 * b * maxd);
-    plane(dz0, b * maxd);
-    float *dz1 = (float *)take(4 * b * maxd);
-    plane(dz1, b * maxd);
+    float *dz0 = nullptr, *dz1 = nullptr;
+    if (c->kind != MTX_MLP) {  // CNN: ping-pong dZ buffers of the fc stack
+        dz0 = (float *)take(4 * b * maxd);
+        plane(dz0, b * maxd);
+        dz1 = (float *)take(4 * b * maxd);
+        plane(dz1, b * maxd);
+    }
+    const int lanes = c->kind == MTX_MLP ? mtx_ctx::LANES : 1;
     float *dzL = (float *)take(4 * b * c->classes);
     float *loss_rows = (float *)take(4 * b);
-    float *part = partial ? (float *)take(4 * partial) : nullptr;
+    float *part = partial ? (float *)take(4 * partial * lanes) : nullptr;
     float *sx = (float *)take(4 * b * c->d0);
     plane(sx, b * c->d0);
     int32_t *sy = (int32_t *)take(4 * b);
     float *loss_part = (float *)take(4 * 1024);
-    unsigned *counters = (unsigned *)take(4 * 512);  // [0,254) split-K tiles, 254 narrow, 256.. colsum
+    // per lane: [0,254) split-K tiles, 254 narrow wgrad, 256.. colsum groups
+    unsigned *counters = (unsigned *)take(4 * COUNTERS_PER_LANE * lanes);
     uint8_t *misc = take(512 + 128 * (uint64_t)c->world);
     if (assign) {
         c->params = params; c->vel = vel; c->grads = grads; c->gather = gather;
-        c->acts = acts; c->fcA = fcA;
+        c->acts = acts; c->fcA = fcA; c->dzs = dzs; c->lanes = lanes;
         c->convR = cR; c->convP = cP; c->convDR = cDR; c->convDP = cDP; c->convArg = cArg;
         c->dz[0] = dz0; c->dz[1] = dz1; c->dzL = dzL; c->loss_rows = loss_rows;
         c->partial = part; c->partial_floats = partial;
@@ -450,14 +466,63 @@ bool plane_of(const mtx_ctx *c, const float *p, const float **hi, const float **
 // ------------------------------------------------------------------ step schedule
 struct Runner {
     mtx_ctx *c;
-    cudaStream_t s;
+    cudaStream_t s;  // the stream launches go to: the caller's stream, or a side lane's inside on_lane()
     bool staged;
     LaunchHook *h;
+    int lane = 0;            // 0: the caller's stream; 1..LANES-1: c->side[lane - 1]
+    unsigned dirty = 0;      // side lanes with gradient work no consumer has waited on yet
+    unsigned used = 0;       // side lanes forked this step (joined back at the end of the step)
+
+    float *part() const { return c->partial ? c->partial + (int64_t)lane * c->partial_floats : nullptr; }
+    unsigned *ctrs() const { return c->counters + (int64_t)lane * COUNTERS_PER_LANE; }
+
+    // Issue fn() on side lane ln, ordered after everything issued so far on the caller's stream.
+    template <class F>
+    mtx_status on_lane(int ln, F fn) {
+        // no lane, or the per-kernel timing pass (kernels timed in isolation, like ncu's launch list)
+        if (ln <= 0 || ln >= c->lanes || !c->side[ln - 1] || c->hook.enabled) return fn();
+        CK(cudaEventRecord(c->ev_lane[0], s));
+        CK(cudaStreamWaitEvent(c->side[ln - 1], c->ev_lane[0], 0));
+        const cudaStream_t keep = s;
+        s = c->side[ln - 1];
+        lane = ln;
+        const mtx_status st = fn();
+        s = keep;
+        lane = 0;
+        dirty |= 1u << ln;
+        used |= 1u << ln;
+        return st;
+    }
+    // Make `target` wait for all gradient work issued so far: the caller's stream and every side lane
+    // with unwaited work.  (target == the caller's stream: only the side lanes.)
+    mtx_status grads_ready(cudaStream_t target) {
+        for (int ln = 1; ln < c->lanes; ln++)
+            if (dirty & (1u << ln)) {
+                CK(cudaEventRecord(c->ev_lane[ln], c->side[ln - 1]));
+                CK(cudaStreamWaitEvent(target, c->ev_lane[ln], 0));
+            }
+        dirty = 0;
+        if (target != s) {
+            CK(cudaEventRecord(c->ev_lane[0], s));
+            CK(cudaStreamWaitEvent(target, c->ev_lane[0], 0));
+        }
+        return MTX_OK;
+    }
+    // Join every lane forked this step back into the caller's stream (graph capture needs it).
+    mtx_status join_lanes() {
+        for (int ln = 1; ln < c->lanes; ln++)
+            if (used & (1u << ln)) {
+                CK(cudaEventRecord(c->ev_lane[ln], c->side[ln - 1]));
+                CK(cudaStreamWaitEvent(s, c->ev_lane[ln], 0));
+            }
+        used = dirty = 0;
+        return MTX_OK;
+    }
 
     mtx_status gemm(GemmDesc g) {
-        g.partial = c->partial;
+        g.partial = part();
         g.partial_cap = c->partial_floats;
-        g.counters = c->counters;
+        g.counters = ctrs();
         if (g.arow.win) g.a_rows_total = c->n_data + c->B;
         cudaError_t e;
         g.tf32x3 = c->opt.precision == MTX_3XTF32;
@@ -489,7 +554,7 @@ struct Runner {
         const Layer &L = c->layers[li];
         if (L.cols <= 16) {  // classifier-width layers: thread-per-input-feature kernel, bias row included
             cudaError_t e = wgrad_narrow(A, L.rows_w, arow, dZ, (int)c->b, L.rows_w, L.cols, c->grads + L.pad_off,
-                                         c->partial, c->partial_floats, c->counters + 254, s, h);
+                                         part(), c->partial_floats, ctrs() + 254, s, h);
             if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "wgrad_narrow: %s", cudaGetErrorString(e));
             return MTX_OK;
         }
@@ -527,17 +592,19 @@ struct Runner {
         const float *Ain = L == 1 ? xbase() : c->acts[L - 1];
         RowSel ar = L == 1 ? xrow() : RowSel{nullptr, 0};
         const float *dph = nullptr, *dpl = nullptr;
-        if (L > 1) plane_of(c, c->dz[0], &dph, &dpl);
+        if (L > 1) plane_of(c, c->dzs[L - 1], &dph, &dpl);
         cudaError_t e = head_fused((int)b, d[L - 1], d[L], Ain, ar, c->params + LL.pad_off, ybase(), xrow(),
-                                   1.0f / (float)b, c->dzL, L > 1 ? c->dz[0] : nullptr, (float *)dph, (float *)dpl,
+                                   1.0f / (float)b, c->dzL, L > 1 ? c->dzs[L - 1] : nullptr, (float *)dph, (float *)dpl,
                                    c->loss_rows, c->loss_part, c->ticket, c->grads + c->N_pad, s, h);
         if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "head: %s", cudaGetErrorString(e));
-        // backward l = L .. 1.  dgrad(l) reads W_l, so it is issued before wgrad(l) completes the
-        // bucket holding W_l: the bucket's update (comm stream) may then overwrite W_l safely.
-        int cur = 0;
+        // backward l = L .. 1.  The dgrad chain dZ_{L-1} -> ... -> dZ_1 stays on the caller's stream;
+        // wgrad(l) for l >= 2 is forked onto the side lanes (alternating) and overlaps it, wgrad(1)
+        // closes the chain.  dgrad(l) reads W_l, so it is issued before wgrad(l) completes the bucket
+        // holding W_l: the bucket's update (which waits for this stream too) may then overwrite W_l.
         size_t bk = 0;
+        int next_lane = 1;
         for (int l = L; l >= 1; l--) {
-            const float *dZ = (l == L) ? c->dzL : c->dz[cur];
+            const float *dZ = (l == L) ? c->dzL : c->dzs[l];
             if (l < L && l > 1) {
                 // dZ_{l-1} = (dZ_l W_l^T) .* [A_{l-1} > 0]
                 const Layer &Ly = c->layers[l - 1];
@@ -547,15 +614,21 @@ struct Runner {
                 g.A = dZ; g.lda = d[l];
                 g.B = c->params + Ly.pad_off; g.ldb = d[l];
                 g.mask = c->acts[l - 1]; g.ldm = d[l - 1];
-                g.C = c->dz[cur ^ 1]; g.ldc = d[l - 1];
+                g.C = c->dzs[l - 1]; g.ldc = d[l - 1];
                 if ((st = gemm(g))) return st;
             }
             const float *Aprev = l == 1 ? xbase() : c->acts[l - 1];
-            if ((st = wgrad(l - 1, Aprev, l == 1 ? xrow() : RowSel{nullptr, 0}, dZ))) return st;
+            const RowSel arow = l == 1 ? xrow() : RowSel{nullptr, 0};
+            if (l > 1) {
+                st = on_lane(next_lane, [&] { return wgrad(l - 1, Aprev, arow, dZ); });
+                next_lane = next_lane % (c->lanes - 1 > 0 ? c->lanes - 1 : 1) + 1;
+            } else {
+                st = wgrad(l - 1, Aprev, arow, dZ);
+            }
+            if (st) return st;
             if ((st = bucket_ready(l - 1, bk))) return st;
-            if (l < L && l > 1) cur ^= 1;
         }
-        return MTX_OK;
+        return join_lanes();
     }
 
     // After layer block `li`'s wgrad: launch the allreduce + update of every bucket it completes.
@@ -576,9 +649,7 @@ struct Runner {
         if (c->world > 1 && c->opt.reduce == MTX_REDUCE_LAYERWISE) {
             // paper-literal: after the backward, one allreduce per variable in canonical order
             if (!last) return MTX_OK;
-            cudaEvent_t ev = c->ev_bucket[0];
-            CK(cudaEventRecord(ev, s));
-            CK(cudaStreamWaitEvent(c->comm_s, ev, 0));
+            if (mtx_status st = grads_ready(c->comm_s)) return st;
             for (const Layer &L : c->layers) {
                 const int64_t wsz = (int64_t)L.rows_w * L.cols;
                 NK(ncclAllReduce(c->grads + L.pad_off, c->grads + L.pad_off, wsz, ncclFloat, ncclSum, c->comm, c->comm_s));
@@ -595,9 +666,7 @@ struct Runner {
         if (c->world > 1 && c->opt.reduce == MTX_REDUCE_ZERO1) {
             // reduce-scatter -> update of this rank's shard -> all-gather of w (and v)
             if (!last) return MTX_OK;
-            cudaEvent_t ev = c->ev_bucket[0];
-            CK(cudaEventRecord(ev, s));
-            CK(cudaStreamWaitEvent(c->comm_s, ev, 0));
+            if (mtx_status st = grads_ready(c->comm_s)) return st;
             const int64_t shard = c->N_pad / c->world, off = shard * c->rank;
             NK(ncclReduceScatter(c->grads, c->grads + off, shard, ncclFloat, ncclSum, c->comm, c->comm_s));
             NK(ncclAllReduce(c->grads + c->N_pad, c->grads + c->N_pad, 1, ncclFloat, ncclSum, c->comm, c->comm_s));
@@ -614,6 +683,7 @@ struct Runner {
         }
         if (c->fused) {  // one fused collective + update over the whole buffer after the last wgrad
             if (!last) return MTX_OK;
+            if (mtx_status st = grads_ready(s)) return st;
             int64_t *win = staged ? nullptr : c->win;
             cudaError_t e = peer_barrier(c->pp, c->world, c->rank, c->epoch, c->flag, s, h);
             if (e == cudaSuccess)
@@ -626,14 +696,13 @@ struct Runner {
         int64_t upd_hi = std::min<int64_t>(bkt.hi, c->N_pad);
         int64_t *win = (last && !staged) ? c->win : nullptr;
         if (c->world == 1) {
+            if (mtx_status st = grads_ready(s)) return st;
             cudaError_t e = avg_update(c->grads + bkt.lo, c->params + bkt.lo, vel_or_null(bkt.lo), upd_hi - bkt.lo,
                                        invP, c->opt.lr, c->opt.momentum, c->flag, win, c->B, c->n_data, s, h);
             if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "update: %s", cudaGetErrorString(e));
             return MTX_OK;
         }
-        cudaEvent_t ev = c->ev_bucket[&bkt - &c->buckets[0]];
-        CK(cudaEventRecord(ev, s));
-        CK(cudaStreamWaitEvent(c->comm_s, ev, 0));
+        if (mtx_status st = grads_ready(c->comm_s)) return st;
         int64_t cnt = bkt.hi - bkt.lo;
         if (c->opt.reduce == MTX_REDUCE_ORDERED) {
             // allgather every rank's slice, then the ascending-rank left fold (A2 test mode)
@@ -965,8 +1034,13 @@ mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t ui
         delete c;
         return MTX_ERR_CUDA;
     }
-    c->ev_bucket.resize(c->buckets.size());
-    for (auto &e : c->ev_bucket) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    for (int i = 0; i < mtx_ctx::LANES; i++)
+        if (cudaEventCreateWithFlags(&c->ev_lane[i], cudaEventDisableTiming) != cudaSuccess ||
+            (i > 0 && c->kind == MTX_MLP &&
+             cudaStreamCreateWithFlags(&c->side[i - 1], cudaStreamNonBlocking) != cudaSuccess)) {
+            delete c;
+            return MTX_ERR_CUDA;
+        }
     if (world > 1) {
         ncclUniqueId id;
         memcpy(&id, uid, 128);
@@ -1351,7 +1425,10 @@ mtx_status mtx_finalize(mtx_ctx *c) {
         if (g) cudaGraphExecDestroy(g);
     for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
     if (c->comm) ncclCommDestroy(c->comm);
-    for (auto &e : c->ev_bucket) cudaEventDestroy(e);
+    for (auto &e : c->ev_lane)
+        if (e) cudaEventDestroy(e);
+    for (auto &st : c->side)
+        if (st) cudaStreamDestroy(st);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->own) cudaStreamDestroy(c->own);
