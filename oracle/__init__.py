@@ -64,6 +64,10 @@ def lib():
             "orc_batch_slice": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32, i64, i64]),
             "orc_local_grad": (C.c_double, [net, d, f, i32, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
                                             C.c_int32, d]),
+            "orc_local_grad_tf32emu": (C.c_double, [net, d, f, i32, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
+                                                    C.c_int32, d]),
+            "orc_mlp_activations_tf32emu": (None, [net, d, f, i32, C.c_int64, C.c_int, d]),
+            "orc_tf32": (C.c_double, [C.c_double]),
             "orc_batch_grad": (C.c_double, [net, d, f, i32, C.c_int64, d]),
             "orc_mlp_activations": (None, [net, d, f, i32, C.c_int64, C.c_int, d]),
             "orc_fold_f64": (None, [C.c_int32, C.c_int64, d, d]),
@@ -148,15 +152,23 @@ def batch_slice(n: int, B: int, step: int, rank: int, P: int):
     return (int(b[0]), int(b[1])), (int(l[0]), int(l[1]))
 
 
-def local_grad(net: Net, params: np.ndarray, X: np.ndarray, y: np.ndarray, B: int, step: int, rank: int, P: int):
-    """O5-O7 on rank's shard: (grad [N] f64 of the local MEAN loss, local loss SUM)."""
+def local_grad(net: Net, params: np.ndarray, X: np.ndarray, y: np.ndarray, B: int, step: int, rank: int, P: int,
+               tf32emu: bool = False):
+    """O5-O7 on rank's shard: (grad [N] f64 of the local MEAN loss, local loss SUM).
+    tf32emu: the TF32 tier's contractions with A12-truncated operands (MLP only, readings A12/A23)."""
     params = np.ascontiguousarray(params, np.float64)
     X = np.ascontiguousarray(X, np.float32)
     y = np.ascontiguousarray(y, np.int32)
     g = np.zeros(param_count(net), np.float64)
-    loss = lib().orc_local_grad(C.byref(net.c()), _ptr(params, C.c_double), _ptr(X, C.c_float),
-                                _ptr(y, C.c_int32), X.shape[0], B, step, rank, P, _ptr(g, C.c_double))
+    fn = lib().orc_local_grad_tf32emu if tf32emu else lib().orc_local_grad
+    loss = fn(C.byref(net.c()), _ptr(params, C.c_double), _ptr(X, C.c_float), _ptr(y, C.c_int32), X.shape[0], B,
+              step, rank, P, _ptr(g, C.c_double))
     return g, float(loss)
+
+
+def tf32(x: float) -> float:
+    """A12: an fp32 value as tcgen05 kind::tf32 consumes it (low 13 mantissa bits dropped)."""
+    return float(lib().orc_tf32(float(x)))
 
 
 def batch_grad(net: Net, params: np.ndarray, X: np.ndarray, y: np.ndarray, want_grad: bool = True):
@@ -170,12 +182,12 @@ def batch_grad(net: Net, params: np.ndarray, X: np.ndarray, y: np.ndarray, want_
     return g, float(loss)
 
 
-def mlp_activations(net: Net, params, X, y, layer: int) -> np.ndarray:
+def mlp_activations(net: Net, params, X, y, layer: int, tf32emu: bool = False) -> np.ndarray:
     params = np.ascontiguousarray(params, np.float64)
     X = np.ascontiguousarray(X, np.float32)
     y = np.ascontiguousarray(y, np.int32)
     out = np.zeros((X.shape[0], net.dims[layer]), np.float64)
-    lib().orc_mlp_activations(C.byref(net.c()), _ptr(params, C.c_double), _ptr(X, C.c_float), _ptr(y, C.c_int32),
+    (lib().orc_mlp_activations_tf32emu if tf32emu else lib().orc_mlp_activations)(C.byref(net.c()), _ptr(params, C.c_double), _ptr(X, C.c_float), _ptr(y, C.c_int32),
                               X.shape[0], layer, _ptr(out, C.c_double))
     return out
 

@@ -204,6 +204,25 @@ static double softmax_xent_row(const double *z, int C, int y, double inv_b, doub
     return loss;
 }
 
+/* ------------------------------------------------------------------ tf32emu
+ * The TF32 tier's contractions, emulated: tcgen05 kind::tf32 reads each fp32 operand with its low
+ * 13 mantissa bits dropped (reading A12, measured: 1+2^-11+2^-12 -> 1, 1+3*2^-11 -> 1+2^-10).  The
+ * operand is first rounded to fp32, the format it is stored in, then truncated; products and sums
+ * stay exact-ish (double).  Which contractions the TF32 tier issues on tensor cores (reading A23):
+ * the hidden layers' forward (d_l >= 16), dgrad (d_{l-1} >= 16) and weight gradient (d_l > 16),
+ * when both widths are multiples of 4; the last layer (softmax head), narrow weight gradients and
+ * every bias gradient (column sums) are fp32 CUDA-core arithmetic, i.e. exact here. */
+static double tf32_of(double x) {
+    float f = (float)x;
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    u &= 0xFFFFE000u;
+    memcpy(&f, &u, 4);
+    return (double)f;
+}
+
+double orc_tf32(double x) { return tf32_of(x); }
+
 /* ------------------------------------------------------------------ MLP O5-O7
  * Local gradient of the mean loss over this rank's shard (b = B/P rows) at the
  * given parameters, written in canonical order into grad (length N); returns
@@ -217,12 +236,18 @@ static double softmax_xent_row(const double *z, int C, int y, double inv_b, doub
  * out ([b][d_l], post-ReLU for hidden layers, logits for the last). */
 static double mlp_local(const orc_net *m, const double *params, const float *X, const int32_t *y, int64_t n,
                         int64_t B, int64_t step, int32_t rank, int32_t P, int64_t b_override, double *grad,
-                        int acts_layer, double *acts) {
+                        int acts_layer, double *acts, int tf32emu) {
     orc_tensors t;
     enum_tensors(m, &t);
     const int L = m->n_dims - 1;
     const int64_t b = b_override > 0 ? b_override : B / P;
     const int *d = m->dims;
+    /* tf32emu: which contractions of layer l take TF32 operands (A23, see tf32_of) */
+#define AL4(l) (d[(l) - 1] % 4 == 0 && d[(l)] % 4 == 0)
+#define FWD_TC(l) (tf32emu && (l) < L && d[(l)] >= 16 && AL4(l))
+#define DGRAD_TC(l) (tf32emu && (l) < L && d[(l) - 1] >= 16 && AL4(l))
+#define WGRAD_TC(l) (tf32emu && (l) < L && d[(l)] > 16 && AL4(l))
+#define OP(tc, x) ((tc) ? tf32_of(x) : (x))
     double **A = calloc((size_t)L + 1, sizeof(double *));
     for (int l = 0; l <= L; l++) A[l] = calloc((size_t)(b * d[l]), sizeof(double));
     for (int64_t i = 0; i < b; i++) {
@@ -235,11 +260,12 @@ static double mlp_local(const orc_net *m, const double *params, const float *X, 
     for (int l = 1; l <= L; l++) {
         const double *W = params + t.off[2 * (l - 1)];
         const double *bias = params + t.off[2 * (l - 1) + 1];
+        const int tc = FWD_TC(l);
         for (int64_t i = 0; i < b; i++) {
             for (int j = 0; j < d[l]; j++) acc[j] = 0.0;
             for (int k = 0; k < d[l - 1]; k++) {
-                double a = A[l - 1][i * d[l - 1] + k];
-                for (int j = 0; j < d[l]; j++) acc[j] += a * W[(int64_t)k * d[l] + j];
+                double a = OP(tc, A[l - 1][i * d[l - 1] + k]);
+                for (int j = 0; j < d[l]; j++) acc[j] += a * OP(tc, W[(int64_t)k * d[l] + j]);
             }
             for (int j = 0; j < d[l]; j++) {
                 double z = acc[j] + bias[j];
@@ -263,11 +289,12 @@ static double mlp_local(const orc_net *m, const double *params, const float *X, 
             double *dW = grad + t.off[2 * (l - 1)];
             double *db = grad + t.off[2 * (l - 1) + 1];
             const double *W = params + t.off[2 * (l - 1)];
+            const int tcw = WGRAD_TC(l), tcd = DGRAD_TC(l);
             for (int64_t i = 0; i < b; i++) {
                 const double *a = A[l - 1] + i * d[l - 1];
                 const double *dz = dZ + i * d[l];
                 for (int k = 0; k < d[l - 1]; k++)
-                    for (int j = 0; j < d[l]; j++) dW[(int64_t)k * d[l] + j] += a[k] * dz[j];
+                    for (int j = 0; j < d[l]; j++) dW[(int64_t)k * d[l] + j] += OP(tcw, a[k]) * OP(tcw, dz[j]);
                 for (int j = 0; j < d[l]; j++) db[j] += dz[j];
             }
             if (l > 1) {
@@ -275,7 +302,8 @@ static double mlp_local(const orc_net *m, const double *params, const float *X, 
                 for (int64_t i = 0; i < b; i++) {
                     for (int k = 0; k < d[l - 1]; k++) {
                         double s = 0.0;
-                        for (int j = 0; j < d[l]; j++) s += dZ[i * d[l] + j] * W[(int64_t)k * d[l] + j];
+                        for (int j = 0; j < d[l]; j++)
+                            s += OP(tcd, dZ[i * d[l] + j]) * OP(tcd, W[(int64_t)k * d[l] + j]);
                         dprev[i * d[l - 1] + k] = A[l - 1][i * d[l - 1] + k] > 0.0 ? s : 0.0;
                     }
                 }
@@ -289,6 +317,11 @@ static double mlp_local(const orc_net *m, const double *params, const float *X, 
     for (int l = 0; l <= L; l++) free(A[l]);
     free(A);
     return loss_sum;
+#undef AL4
+#undef FWD_TC
+#undef DGRAD_TC
+#undef WGRAD_TC
+#undef OP
 }
 
 /* ------------------------------------------------------------------ CNN O5-O7
@@ -463,21 +496,35 @@ static double cnn_local(const orc_net *m, const double *params, const float *X, 
 /* Local gradient for rank `rank` of P at `step` (O5-O7).  Returns loss sum. */
 double orc_local_grad(const orc_net *m, const double *params, const float *X, const int32_t *y, int64_t n,
                       int64_t B, int64_t step, int32_t rank, int32_t P, double *grad) {
-    if (m->kind == 0) return mlp_local(m, params, X, y, n, B, step, rank, P, 0, grad, 0, NULL);
+    if (m->kind == 0) return mlp_local(m, params, X, y, n, B, step, rank, P, 0, grad, 0, NULL, 0);
     return cnn_local(m, params, X, y, n, B, step, rank, P, 0, grad);
+}
+
+/* O5-O7 of the TF32 tier (tf32emu: SURVEY.md §8(c), readings A12/A23) on rank's shard; MLP only
+ * (returns NaN for the CNN, whose convolutions are CUDA-core fp32). */
+double orc_local_grad_tf32emu(const orc_net *m, const double *params, const float *X, const int32_t *y, int64_t n,
+                              int64_t B, int64_t step, int32_t rank, int32_t P, double *grad) {
+    if (m->kind != 0) return NAN;
+    return mlp_local(m, params, X, y, n, B, step, rank, P, 0, grad, 0, NULL, 1);
+}
+
+/* tf32emu forward activations of layer l for an explicit batch. */
+void orc_mlp_activations_tf32emu(const orc_net *m, const double *params, const float *X, const int32_t *y,
+                                 int64_t b, int layer, double *out) {
+    mlp_local(m, params, X, y, b, b, 0, 0, 1, b, NULL, layer, out, 1);
 }
 
 /* Same on an explicit batch of b rows X[0..b) (no sharding) -- used by FD checks. */
 double orc_batch_grad(const orc_net *m, const double *params, const float *X, const int32_t *y, int64_t b,
                       double *grad) {
-    if (m->kind == 0) return mlp_local(m, params, X, y, b, b, 0, 0, 1, b, grad, 0, NULL);
+    if (m->kind == 0) return mlp_local(m, params, X, y, b, b, 0, 0, 1, b, grad, 0, NULL, 0);
     return cnn_local(m, params, X, y, b, b, 0, 0, 1, b, grad);
 }
 
 /* MLP forward activations of layer l for an explicit batch (S:93 worked value). */
 void orc_mlp_activations(const orc_net *m, const double *params, const float *X, const int32_t *y, int64_t b,
                          int layer, double *out) {
-    mlp_local(m, params, X, y, b, b, 0, 0, 1, b, NULL, layer, out);
+    mlp_local(m, params, X, y, b, b, 0, 0, 1, b, NULL, layer, out, 0);
 }
 
 /* ------------------------------------------------------------------ O9 reduce (A2)

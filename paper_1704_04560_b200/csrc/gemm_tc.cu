@@ -78,7 +78,87 @@ struct TcParams {
     const int64_t *a_win;  // dataset operand: sample-dimension offset read on the device
     int64_t a_base;
     unsigned *counters;    // split-K: one arrival counter per output tile (zero between launches)
+    int cluster;           // 1: the splits of a tile form one thread-block cluster and are folded
+                           // through distributed shared memory (no partial buffer, no fold launch)
 };
+
+// Work unit t -> (k-split z, output tile r).  Cluster mode: the splits of a tile are consecutive
+// CTAs (one cluster, z = rank in the cluster); otherwise splits are outermost.
+__device__ __forceinline__ void unit_of(const TcParams &p, int t, int tiles_mn, int &z, int &r) {
+    if (p.cluster) {
+        z = t % p.splits;
+        r = t / p.splits;
+    } else {
+        z = t / tiles_mn;
+        r = t % tiles_mn;
+    }
+}
+
+// The fused epilogue on 4 consecutive outputs C[m][n..n+3] (coalesced across a warp): bias (+ReLU)
+// or ReLU mask, the fp32 store and, for a 3xTF32 consumer, the hi/lo planes.
+__device__ __forceinline__ void epi_store(const TcParams &p, int m, int n, float4 sv) {
+    const bool vec4 = n + 3 < p.N;
+    float o[4] = {sv.x, sv.y, sv.z, sv.w};
+    if (p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) {
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+            if (n + e < p.N) {
+                o[e] += __ldg(p.bias + n + e);
+                if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e], 0.f);
+            }
+    } else if (p.epi == EPI_MASK) {
+        const float *mk = p.mask + (int64_t)m * p.ldm + n;
+        float mv[4];
+        if (vec4) {
+            const float4 t4 = __ldg((const float4 *)mk);
+            mv[0] = t4.x; mv[1] = t4.y; mv[2] = t4.z; mv[3] = t4.w;
+        } else {
+            for (int e = 0; e < 4; e++) mv[e] = n + e < p.N ? mk[e] : 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+            if (!(mv[e] > 0.f)) o[e] = 0.f;
+    }
+    const int64_t off = (int64_t)m * p.ldc + n;
+    if (vec4) *(float4 *)(p.C + off) = make_float4(o[0], o[1], o[2], o[3]);
+    else for (int e = 0; e < 4 && n + e < p.N; e++) p.C[off + e] = o[e];
+    if (p.C_hi) {  // hi/lo planes for the consuming 3xTF32 GEMM
+        float hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) split_tf32(o[e], hi[e], lo[e]);
+        if (vec4) {
+            *(float4 *)(p.C_hi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+            *(float4 *)(p.C_lo + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+        } else {
+            for (int e = 0; e < 4 && n + e < p.N; e++) {
+                p.C_hi[off + e] = hi[e];
+                p.C_lo[off + e] = lo[e];
+            }
+        }
+    }
+}
+
+// Cluster split-K: the fp32 partial tile [BM][BN] of a CTA lives at the start of its (then idle)
+// stage ring, 16-B chunks XOR-swizzled within each 128-B group so that both the row-per-lane writes
+// and the chunk-per-lane reads are bank-conflict free.
+template <int BN>
+__device__ __forceinline__ uint32_t ktile_off(int row, int j) {
+    return (uint32_t)row * (BN * 4) + (uint32_t)(((j & ~7) | ((j ^ row) & 7)) * 16);
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t local_addr, uint32_t cta) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(cta));
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(remote)
+                 : "memory");
+    return v;
+}
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -205,6 +285,37 @@ __device__ __noinline__ void splitk_fixup(const TcParams &p, int r, int m0) {
     }
 }
 
+// Cluster split-K fold (run by the 256 epilogue threads of each CTA after the first cluster barrier):
+// CTA z of the tile's cluster folds rows [z*BM/S, (z+1)*BM/S) of the S partial tiles, read from
+// every CTA's shared memory (DSMEM) in ascending split order, and stores them with the epilogue.
+// Out of line so its registers do not add to the epilogue's accumulator registers.
+template <int BN>
+__device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base) {
+    int z, r;
+    unit_of(p, blockIdx.x, p.tiles_m * p.tiles_n, z, r);
+    const int m0 = (r / p.tiles_n) * BM, n0 = (r % p.tiles_n) * BN;
+    const int S = p.splits;
+    const int r0 = BM * z / S, r1 = BM * (z + 1) / S;
+    constexpr int CPR = BN / 4;
+    for (int idx = threadIdx.x - 128; idx < (r1 - r0) * CPR; idx += 256) {
+        const int row = r0 + idx / CPR, j = idx % CPR;
+        const int m = m0 + row, n = n0 + 4 * j;
+        if (m >= p.M || n >= p.N) continue;
+        const uint32_t la = base + ktile_off<BN>(row, j);
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            if (u < S) v[u] = ld_dsmem_f4(la, (uint32_t)u);
+        float4 sum = v[0];
+#pragma unroll
+        for (int u = 1; u < 8; u++)
+            if (u < S) {
+                sum.x += v[u].x; sum.y += v[u].y; sum.z += v[u].z; sum.w += v[u].w;
+            }
+        epi_store(p, m, n, sum);
+    }
+}
+
 template <int BN, bool SPLIT>
 __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
     using L = SmemLayout<BN, SPLIT>;
@@ -262,7 +373,8 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
             int stage = 0;
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                const int z = t / tiles_mn, r = t % tiles_mn;
+                int z, r;
+                unit_of(p, t, tiles_mn, z, r);
                 // raster n-fastest: the CTAs sharing an A row-panel run together (A read from DRAM once,
                 // B -- the weights -- stays L2-resident)
                 const int m0 = (r / p.tiles_n) * BM, n0 = (r % p.tiles_n) * BN;
@@ -304,7 +416,8 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
             int buf = 0;
             uint32_t buf_phase = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                const int z = t / tiles_mn;
+                int z, r;
+                unit_of(p, t, tiles_mn, z, r);
                 const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
                 for (int c0 = kb0; c0 < kb1; c0 += L::CHUNK) {
                     const int c1 = min(kb1, c0 + L::CHUNK);
@@ -352,7 +465,8 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
         int buf = 0;
         uint32_t buf_phase = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x) {
-            const int z = t / tiles_mn, r = t % tiles_mn;
+            int z, r;
+            unit_of(p, t, tiles_mn, z, r);
             const int m0 = (r / p.tiles_n) * BM, n0 = (r % p.tiles_n) * BN + h * HALF;
             const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
             float acc[HALF];
@@ -381,6 +495,14 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                 if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
                 if (++buf == NBUF) { buf = 0; buf_phase ^= 1; }
             }
+            if (p.cluster) {  // partial tile -> own smem; folded across the cluster below
+                const int row = 32 * q + lane;
+#pragma unroll
+                for (int j = 0; j < HALF / 4; j++)
+                    *(float4 *)(smem + ktile_off<BN>(row, h * (HALF / 4) + j)) =
+                        make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+                continue;
+            }
             // ---- store: stage each 32-row x CW-column sub-tile in shared memory (lane = row, 16-B
             // chunks XOR-swizzled: conflict-free both ways), then the warp writes whole row segments
             // (CPR lanes per row, RPI rows per instruction) with the fused epilogue applied there.
@@ -404,51 +526,16 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                     const int m = m0 + 32 * q + r;
                     const float4 sv = *(const float4 *)(stg + r * SW + 4 * swz(r, jj));
                     if (m >= p.M || n >= p.N) continue;
-                    const bool vec4 = n + 3 < p.N;
-                    float o[4] = {sv.x, sv.y, sv.z, sv.w};
                     if (p.splits > 1) {  // split-K partial (folded with the epilogue by splitk_reduce)
                         float *dst = p.partial + ((int64_t)z * p.M + m) * p.N + n;
-                        if (vec4) *(float4 *)dst = sv;
-                        else for (int e = 0; e < 4 && n + e < p.N; e++) dst[e] = o[e];
+                        if (n + 3 < p.N) *(float4 *)dst = sv;
+                        else {
+                            const float o[4] = {sv.x, sv.y, sv.z, sv.w};
+                            for (int e = 0; e < 4 && n + e < p.N; e++) dst[e] = o[e];
+                        }
                         continue;
                     }
-                    if (p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) {
-#pragma unroll
-                        for (int e = 0; e < 4; e++)
-                            if (n + e < p.N) {
-                                o[e] += __ldg(p.bias + n + e);
-                                if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e], 0.f);
-                            }
-                    } else if (p.epi == EPI_MASK) {
-                        const float *mk = p.mask + (int64_t)m * p.ldm + n;
-                        float mv[4];
-                        if (vec4) {
-                            const float4 t4 = __ldg((const float4 *)mk);
-                            mv[0] = t4.x; mv[1] = t4.y; mv[2] = t4.z; mv[3] = t4.w;
-                        } else {
-                            for (int e = 0; e < 4; e++) mv[e] = n + e < p.N ? mk[e] : 0.f;
-                        }
-#pragma unroll
-                        for (int e = 0; e < 4; e++)
-                            if (!(mv[e] > 0.f)) o[e] = 0.f;
-                    }
-                    const int64_t off = (int64_t)m * p.ldc + n;
-                    if (vec4) *(float4 *)(p.C + off) = make_float4(o[0], o[1], o[2], o[3]);
-                    else for (int e = 0; e < 4 && n + e < p.N; e++) p.C[off + e] = o[e];
-                    if (p.C_hi) {  // hi/lo planes for the consuming 3xTF32 GEMM
-                        float hi[4], lo[4];
-#pragma unroll
-                        for (int e = 0; e < 4; e++) split_tf32(o[e], hi[e], lo[e]);
-                        if (vec4) {
-                            *(float4 *)(p.C_hi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-                            *(float4 *)(p.C_lo + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
-                        } else {
-                            for (int e = 0; e < 4 && n + e < p.N; e++) {
-                                p.C_hi[off + e] = hi[e];
-                                p.C_lo[off + e] = lo[e];
-                            }
-                        }
-                    }
+                    epi_store(p, m, n, sv);
                 }
                 __syncwarp();
             }
@@ -465,6 +552,14 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                 if (threadIdx.x == 128) p.counters[r] = 0u;  // re-armed for the next launch
             }
         }
+    }
+    if (p.cluster) {
+        // every CTA of the cluster holds its split's partial tile: CTA z folds rows
+        // [z*BM/S, (z+1)*BM/S) over the splits in ascending order (deterministic) and stores them
+        // with the fused epilogue; the second barrier keeps every CTA's smem alive until read
+        cluster_sync_all();
+        if (warp >= 4 && warp < 12) cluster_fold<BN>(p, smem_u32(smem));
+        cluster_sync_all();
     }
     tc_fence_before();
     __syncthreads();
@@ -506,6 +601,10 @@ struct TcGemm {
     // split-K fold inside the kernel by the tile's last CTA (MTX_TC_FIXUP=1).  Off: a one-SM fold of
     // splits x 64 KB is slower than the all-SM fold kernel on every measured shape.
     bool fixup = false;
+    // split-K folded through distributed shared memory (MTX_TC_CLUSTER=0 disables: global partials
+    // + splitk_reduce launch)
+    bool cluster = true;
+    int max_clusters[2][3][9] = {};  // [SPLIT][BN 128/64/32][cluster size]: co-resident clusters (0 = unknown)
 };
 
 bool tc_available() { return true; }
@@ -557,6 +656,7 @@ TcGemm *tc_create(int device) {
     }
     t->encode = (EncodeTiled)fn;
     if (const char *k = getenv("MTX_TC_FIXUP")) t->fixup = atoi(k) != 0;  // development A/B knob
+    if (const char *k = getenv("MTX_TC_CLUSTER")) t->cluster = atoi(k) != 0;
     cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, device);
     int major = 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
@@ -585,7 +685,7 @@ bool tc_supports(TcGemm *t, const GemmDesc &g) {
 }
 
 template <int BN, bool SPLIT>
-static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s) {
+static cudaError_t prepare(TcGemm *t) {
     using L = SmemLayout<BN, SPLIT>;
     const int slot = (SPLIT ? 1 : 0) + 2 * (BN == 128 ? 0 : BN == 64 ? 1 : 2);
     if (!t->attr_set[slot]) {
@@ -594,7 +694,62 @@ static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s
         if (e != cudaSuccess) return e;
         t->attr_set[slot] = true;
     }
-    return launch_pdl(tc_gemm_kernel<BN, SPLIT>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
+    return cudaSuccess;
+}
+
+// How many clusters of `cs` CTAs of this variant can be resident at once (cached).
+template <int BN, bool SPLIT>
+static int co_resident_clusters(TcGemm *t, int cs) {
+    using L = SmemLayout<BN, SPLIT>;
+    int &slot = t->max_clusters[SPLIT ? 1 : 0][BN == 128 ? 0 : BN == 64 ? 1 : 2][cs];
+    if (slot) return slot;
+    if (prepare<BN, SPLIT>(t) != cudaSuccess) return 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs * 148);
+    cfg.blockDim = dim3(L::THREADS);
+    cfg.dynamicSmemBytes = L::TOTAL;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (void *)tc_gemm_kernel<BN, SPLIT>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = -1;  // query failed: never use the cluster path for this variant
+    }
+    slot = n;
+    return n;
+}
+
+template <int BN, bool SPLIT>
+static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s) {
+    using L = SmemLayout<BN, SPLIT>;
+    cudaError_t e = prepare<BN, SPLIT>(t);
+    if (e != cudaSuccess) return e;
+    if (!p.cluster) return launch_pdl(tc_gemm_kernel<BN, SPLIT>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(L::THREADS);
+    cfg.dynamicSmemBytes = L::TOTAL;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = p.splits;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT>, p);
+}
+
+template <int BN>
+static int co_resident(TcGemm *t, bool split, int cs) {
+    return split ? co_resident_clusters<BN, true>(t, cs) : co_resident_clusters<BN, false>(t, cs);
 }
 
 cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h) {
@@ -629,14 +784,29 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.tiles_n = (N + BN - 1) / BN;
     p.kb_total = (K + BK - 1) / BK;
     const int tiles = p.tiles_m * p.tiles_n;
-    int splits = 1;
-    if (g.partial && N % 4 == 0) {  // few output tiles: split K to fill the SMs
-        splits = plan.splits;
+    int splits = plan.splits;
+    // split-K fold through DSMEM when the tile's splits fit one cluster and all clusters are co-resident
+    bool cluster = false;
+    if (splits > 1 && splits <= 8 && t->cluster) {
+        const int per = (p.kb_total + splits - 1) / splits;
+        const int sp = (p.kb_total + per - 1) / per;
+        const int nc = BN == 128 ? co_resident<128>(t, g.tf32x3, sp)
+                     : BN == 64  ? co_resident<64>(t, g.tf32x3, sp)
+                                 : co_resident<32>(t, g.tf32x3, sp);
+        if (sp > 1 && nc >= tiles) {
+            cluster = true;
+            splits = sp;
+        }
+    }
+    if (!cluster) {
+        if (!g.partial || N % 4) splits = 1;
         while (splits > 1 && (int64_t)splits * M * N > g.partial_cap) splits--;
     }
     p.kb_per_split = (p.kb_total + splits - 1) / splits;
     splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+    if (splits == 1) cluster = false;
     p.splits = splits;
+    p.cluster = cluster ? 1 : 0;
     p.epi = g.epi;
     p.bias = g.bias;
     p.mask = g.mask;
@@ -644,13 +814,13 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.C = g.C;
     p.ldc = g.ldc;
     p.partial = g.partial;
-    p.counters = (t->fixup && !g.C_hi) ? g.counters : nullptr;
+    p.counters = (t->fixup && !g.C_hi && !cluster) ? g.counters : nullptr;
     const int total = tiles * splits;
-    const int grid = std::min(total, t->sms);
+    const int grid = cluster ? total : std::min(total, t->sms);
     const char *kind = g.epi == EPI_MASK ? "dgrad" : (g.ta ? "wgrad" : "fwd");
     char name[96];
-    snprintf(name, sizeof name, "gemm_tc%s_%s[M=%d,N=%d,K=%d,splits=%d,bn=%d]", g.tf32x3 ? "3x" : "", kind, M, N, K,
-             splits, BN);
+    snprintf(name, sizeof name, "gemm_tc%s_%s[M=%d,N=%d,K=%d,splits=%d,cluster=%d,bn=%d]", g.tf32x3 ? "3x" : "", kind,
+             M, N, K, splits, cluster ? 1 : 0, BN);
     if (h) h->before(name, s);
     cudaError_t e;
     if (BN == 128) e = g.tf32x3 ? launch<128, true>(t, p, grid, s) : launch<128, false>(t, p, grid, s);
@@ -658,7 +828,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     else e = g.tf32x3 ? launch<32, true>(t, p, grid, s) : launch<32, false>(t, p, grid, s);
     if (h) h->after(name, s);
     if (e != cudaSuccess) return e;
-    if (splits > 1 && !p.counters) {  // no in-kernel fixup: fold with the epilogue in a separate kernel
+    if (splits > 1 && !p.counters && !cluster) {  // fold with the epilogue in a separate kernel
         e = splitk_reduce(g.partial, splits, M, N, g.C, g.ldc, s, h, g.epi, g.bias, g.mask, g.ldm, g.C_hi, g.C_lo);
         if (e != cudaSuccess) return e;
     }

@@ -456,7 +456,7 @@ cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *
 // partial sums are combined with a fixed xor-shuffle tree.  W_L (d x C, <= 64 KB)
 // and b_L are staged in shared memory once per CTA.
 namespace {
-constexpr int HEAD_WARPS = 8;
+constexpr int HEAD_WARPS = 4;  // rows are latency chains: more, smaller CTAs
 
 // NV = float4 groups per lane (d <= 128 * NV): lane owns features 4*lane + 128*t .. +3, loaded as
 // float4 with all of the row's loads in flight before the FMAs.
@@ -476,32 +476,12 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
     __shared__ float swl[HEAD_WARPS];
     __shared__ bool last;
     const int dp = (d + 1 + 3) & ~3;
-    {
-        const int n = (d + 1) * C;
-        for (int e0 = threadIdx.x; e0 < n; e0 += 4 * blockDim.x) {
-            float v[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int e = e0 + u * blockDim.x;
-                v[u] = e < n ? __ldg(Wb + e) : 0.f;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int e = e0 + u * blockDim.x;
-                if (e < n) sWt[(e % C) * dp + e / C] = v[u];
-            }
-        }
-        const int pad = dp - d - 1;  // zero the row padding: it meets zero features in 128-bit reads
-        for (int e = threadIdx.x; e < C * pad; e += blockDim.x) sWt[(e / pad) * dp + d + 1 + e % pad] = 0.f;
-    }
-    __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float *Abase = A + arow.row0() * (int64_t)d;
     const int32_t *lab = labels + lrow.row0();
-    float wloss = 0.f;  // this warp's rows, in row order
-    for (int i = blockIdx.x * HEAD_WARPS + warp; i < rows; i += gridDim.x * HEAD_WARPS) {
+    float av[NV][4];
+    auto load_row = [&](int i) {  // features 4*lane + 128*t .. +3 of row i, all loads in flight
         const float *a = Abase + (int64_t)i * d;
-        float av[NV][4];
 #pragma unroll
         for (int t = 0; t < NV; t++) {
             const int k = 4 * lane + 128 * t;
@@ -513,6 +493,40 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
                 for (int u = 0; u < 4; u++) av[t][u] = (k + u < d) ? __ldg(a + k + u) : 0.f;
             }
         }
+    };
+    const int i_first = blockIdx.x * HEAD_WARPS + warp;
+    if (i_first < rows) load_row(i_first);  // in flight while W_L is staged
+    {
+        const int n = (d + 1) * C;
+        auto put = [&](int e, float v) { sWt[(e % C) * dp + e / C] = v; };
+        int done = 0;
+        if (((uintptr_t)Wb & 15) == 0) {  // 128-bit loads, 8 in flight per thread
+            const int n4 = n / 4;
+            for (int e0 = threadIdx.x; e0 < n4; e0 += 8 * blockDim.x) {
+                float4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int e = e0 + u * blockDim.x;
+                    v[u] = e < n4 ? __ldg((const float4 *)Wb + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int e = e0 + u * blockDim.x;
+                    if (e < n4) {
+                        put(4 * e, v[u].x); put(4 * e + 1, v[u].y); put(4 * e + 2, v[u].z); put(4 * e + 3, v[u].w);
+                    }
+                }
+            }
+            done = 4 * n4;
+        }
+        for (int e = done + threadIdx.x; e < n; e += blockDim.x) put(e, __ldg(Wb + e));
+        const int pad = dp - d - 1;  // zero the row padding: it meets zero features in 128-bit reads
+        for (int e = threadIdx.x; e < C * pad; e += blockDim.x) sWt[(e / pad) * dp + d + 1 + e % pad] = 0.f;
+    }
+    __syncthreads();
+    float wloss = 0.f;  // this warp's rows, in row order
+    for (int i = i_first; i < rows; i += gridDim.x * HEAD_WARPS) {
+        if (i != i_first) load_row(i);
         float z[HEAD_MAXC];
 #pragma unroll
         for (int j = 0; j < HEAD_MAXC; j++) z[j] = 0.f;

@@ -74,3 +74,49 @@ def test_gemm_layouts(rep, engine, layout, shape):
     # fp32 tier (SIMT, 3xTF32): fp32 products/sums; tf32: truncated 10-bit operand mantissas
     tol = 2e-3 if engine == 1 else 1e-5
     assert maxrel(C, ref) <= tol * max(1.0, np.sqrt(K / 1024)), maxrel(C, ref)
+
+
+def _tf32_trunc(x: np.ndarray) -> np.ndarray:
+    """fp32 -> TF32 by truncating the low 13 mantissa bits: how tcgen05 kind::tf32 consumes fp32
+    shared-memory operands (reading A12, measured with tools/tc_probe.cu)."""
+    return (np.ascontiguousarray(x, dtype=np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
+@pytest.mark.skipif(not TC, reason="tcgen05 engine not built")
+@pytest.mark.parametrize("layout", [(0, 0, 1), (0, 1, 3), (1, 0, 0)])
+@pytest.mark.parametrize("shape", [(1024, 1024, 1024), (512, 512, 784), (1024, 640, 256), (8192, 1024, 28)])
+def test_tf32_engine_matches_tf32_emulation(rep, layout, shape):
+    """Engine 1 equals the TF32 contraction itself -- both operands truncated (A12), exact products, fp32
+    accumulation -- far tighter than its 2e-3 gate against the exact product: the only residual is
+    the fp32 accumulation order (TMEM chunks promoted into fp32 registers)."""
+    ta, tb, epi = layout
+    M, N, K = shape
+    rng = np.random.default_rng(M + 5 * N + 11 * K)
+    A = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+    bias = rng.standard_normal(N).astype(np.float32)
+    mask = np.maximum(rng.standard_normal((M, N)), 0).astype(np.float32)
+    d = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    Ad, Bd, bd, md = d(A), d(B), d(bias), d(mask)
+    Cd = torch.full((M, N), np.nan, device="cuda")
+    torch.cuda.synchronize()
+    mtx.mtx_debug_gemm(rep.ctx, 1, M, N, K, ta, tb, epi, Ad.data_ptr(), M if ta else K, Bd.data_ptr(),
+                       K if tb else N, Cd.data_ptr(), N, bd.data_ptr(), md.data_ptr(), N, rep.s)
+    rep.sync()
+    a = _tf32_trunc(A.T if ta else A).astype(np.float64)
+    b = _tf32_trunc(B.T if tb else B).astype(np.float64)
+    ref = a @ b
+    if epi == 1:
+        ref = np.maximum(ref + bias, 0)
+    elif epi == 3:
+        ref = np.where(mask > 0, ref, 0)
+    C = Cd.cpu().numpy()
+    exact = (A.T if ta else A).astype(np.float64) @ (B.T if tb else B).astype(np.float64)
+    if epi == 1:
+        exact = np.maximum(exact + bias, 0)
+    elif epi == 3:
+        exact = np.where(mask > 0, exact, 0)
+    e_emu, e_exact = maxrel(C, ref), maxrel(C, exact)
+    # fp32 accumulation of K products: <= ~K * 2^-24 worst case, ~sqrt(K) * 2^-24 typical
+    assert e_emu <= 2e-6 * max(1.0, np.sqrt(K / 256)), (e_emu, e_exact)
+    assert e_emu < e_exact / 20, (e_emu, e_exact)  # the emulation explains the TF32 error

@@ -11,7 +11,7 @@ import pytest
 
 import mtx_synth as S
 import oracle
-from tests._util import GRAD_TOL, TOL, digest_np, maxrel, per_tensor_maxrel
+from tests._util import GRAD_TOL, TF32EMU_TOL, TOL, digest_np, maxrel, per_tensor_maxrel
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -338,3 +338,28 @@ def test_graph_launch_count_and_determinism():
         finally:
             r.close()
     assert outs[0] == outs[1]  # run-to-run bitwise determinism (no float atomics)
+
+
+# ----------------------------------------------------------------------------- TF32 tier vs tf32emu
+TC = "tcgen05" in mtx.mtx_build_info()
+
+
+@pytest.mark.skipif(not TC, reason="tcgen05 engine not built")
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg4"])
+def test_tf32_step_matches_tf32emu(name):
+    """MTX_TF32 computes exactly the TF32-operand contractions (readings A12/A23):
+    against the oracle's tf32emu mode its per-tensor gradient error is fp32-accumulation-sized, where
+    against the exact (f64) oracle it is the TF32 band GRAD_TOL[MTX_TF32]."""
+    cfg = {"cfg1": small_cfg("cfg1", B=64), "cfg2": small_cfg("cfg2"), "cfg4": small_cfg("cfg4", B=96, n=5000)}[name]
+    X, y = S.higgs_like(1, 5000) if name == "cfg4" else S.mnist_like(1, 4096)
+    net = oracle.Net.from_cfg(cfg)
+    tab = oracle.tensor_table(net)
+    start = oracle.init_params(net, 42)
+    (loss, G, _), = _gpu_run(cfg, X, y, 1, P.MTX_TF32, start=start, start_step=2)
+    g_emu, l_emu = oracle.local_grad(net, start.astype(np.float64), X, y, cfg["B"], 2, 0, 1, tf32emu=True)
+    g_ex, _ = oracle.local_grad(net, start.astype(np.float64), X, y, cfg["B"], 2, 0, 1)
+    e_emu, e_ex = per_tensor_maxrel(G, g_emu, tab), per_tensor_maxrel(G, g_ex, tab)
+    print(name, "vs tf32emu", [f"{e:.2e}" for e in e_emu], "vs f64", [f"{e:.2e}" for e in e_ex])
+    assert max(e_emu) <= TF32EMU_TOL, (e_emu, e_ex)
+    assert max(e_emu) <= max(e_ex) / 50, (e_emu, e_ex)  # the emulation explains the TF32 error
+    assert abs(loss - l_emu / cfg["B"]) <= 1e-5 * abs(l_emu / cfg["B"])

@@ -418,3 +418,72 @@ def test_cnn_dp_equals_sequential():
     seq, _ = oracle.local_grad(net, p, X, y, 16, 1, 0, 1)
     G = oracle.fold(np.stack([oracle.local_grad(net, p, X, y, 16, 1, r, 4)[0] for r in range(4)])) * 0.25
     assert np.abs(G - seq).max() <= 1e-12 * np.abs(seq).max()
+
+
+# ----------------------------------------------------------------------------- tf32emu (readings A12 / A23)
+def test_tf32_truncation_measured_values_and_properties():
+    """A12: the values tools/tc_probe.cu measured on B200 (1+2^-11+2^-12 -> 1, 1+3*2^-11 -> 1+2^-10), and
+    what truncation of the low 13 mantissa bits implies: sign symmetry, |tf32(x)| <= |x| with relative
+    gap < 2^-10, TF32-representable values fixed, fp32 rounding first."""
+    assert oracle.tf32(1 + 2**-11 + 2**-12) == 1.0
+    assert oracle.tf32(1 + 3 * 2**-11) == 1 + 2**-10
+    rng = np.random.default_rng(12)
+    for x in rng.standard_normal(2000) * 10.0 ** rng.integers(-6, 6, 2000):
+        t = oracle.tf32(x)
+        assert oracle.tf32(-x) == -t
+        x32 = float(np.float32(x))
+        assert abs(t) <= abs(x32) and abs(x32 - t) < 2**-10 * abs(x32)
+        assert oracle.tf32(t) == t
+        m = np.frexp(t)[0] * 2**11  # 11 significant bits (1 implicit + 10 stored)
+        assert m == int(m)
+    assert oracle.tf32(1 + 2**-10) == 1 + 2**-10  # exactly representable: unchanged
+    assert oracle.tf32(1 + 2**-30) == 1.0          # rounds to fp32 1.0 first
+
+
+def test_tf32emu_is_exact_when_no_contraction_is_tensor_core_shaped():
+    """Widths < 16 (A23: CUDA-core fp32 contractions) -> tf32emu is the f64 oracle, bitwise."""
+    net = oracle.Net("mlp", [12, 8, 3])
+    X = np.random.default_rng(4).standard_normal((16, 12)).astype(np.float32)
+    y = (np.arange(16) % 3).astype(np.int32)
+    p = oracle.init_params(net, 5).astype(np.float64)
+    g0, l0 = oracle.local_grad(net, p, X, y, 16, 0, 0, 1)
+    g1, l1 = oracle.local_grad(net, p, X, y, 16, 0, 0, 1, tf32emu=True)
+    assert np.array_equal(g0, g1) and l0 == l1
+
+
+def test_tf32emu_is_exact_on_tf32_representable_operands():
+    """[8, 16, 3]: only layer 1's forward is tensor-core shaped (d_1 = 16 >= 16; its weight gradient needs
+    d_1 > 16; the head is fp32).  With X and W_1 holding values of <= 11 significant bits the truncation is
+    the identity, so tf32emu equals the f64 oracle bitwise -- truncation touches operands only."""
+    net = oracle.Net("mlp", [8, 16, 3])
+    rng = np.random.default_rng(6)
+    X = (rng.integers(-64, 64, (32, 8)) / 32.0).astype(np.float32)
+    y = (np.arange(32) % 3).astype(np.int32)
+    p = oracle.init_params(net, 7).astype(np.float64)
+    (o_w1, n_w1), = oracle.tensor_table(net)[:1]
+    p[o_w1:o_w1 + n_w1] = rng.integers(-512, 512, n_w1) / 1024.0
+    g0, l0 = oracle.local_grad(net, p, X, y, 32, 0, 0, 1)
+    g1, l1 = oracle.local_grad(net, p, X, y, 32, 0, 0, 1, tf32emu=True)
+    assert np.array_equal(g0, g1) and l0 == l1
+    p[o_w1] += 2**-13  # one weight no longer TF32-representable: the emulation now differs
+    g0, _ = oracle.local_grad(net, p, X, y, 32, 0, 0, 1)
+    g1, _ = oracle.local_grad(net, p, X, y, 32, 0, 0, 1, tf32emu=True)
+    assert not np.array_equal(g0, g1)
+
+
+def test_tf32emu_forward_truncates_toward_zero_within_bound():
+    """Non-negative inputs and weights: truncating both operands toward zero can only lower each product,
+    by < (2^-9 + 2^-20) of it (two 2^-10 relative gaps), so 0 <= exact - emu <= (2^-9 + 2^-20) * exact
+    for the pre-activations (biases zero) -- and the gap is not zero."""
+    net = oracle.Net("mlp", [32, 64, 3])
+    rng = np.random.default_rng(8)
+    X = rng.random((20, 32)).astype(np.float32)
+    y = (np.arange(20) % 3).astype(np.int32)
+    p = np.abs(oracle.init_params(net, 9).astype(np.float64))
+    (o_b1, n_b1) = oracle.tensor_table(net)[1]
+    p[o_b1:o_b1 + n_b1] = 0.0
+    ex = oracle.mlp_activations(net, p, X, y, 1)
+    em = oracle.mlp_activations(net, p, X, y, 1, tf32emu=True)
+    gap = ex - em
+    assert (gap >= 0).all() and (gap <= (2**-9 + 2**-20) * ex + 1e-300).all()
+    assert gap.max() > 0
