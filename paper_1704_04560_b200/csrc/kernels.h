@@ -121,17 +121,23 @@ struct ConvGeom {
     int hc, wc;       // conv output (valid, stride 1)
     int hp, wp;       // pooled output (2x2 / 2, floor)
 };
-// R = ReLU(conv(X) + b) [rows][hc][wc][co];  P = maxpool(R), argmax index (0..3) per pooled element.
-cudaError_t conv_fwd(const ConvGeom &g, int rows, const float *X, RowSel xrow, const float *Wb, float *R, float *P,
-                     uint8_t *arg, cudaStream_t s, LaunchHook *h);
-// dR = route(dP via arg) .* [R > 0]
-cudaError_t pool_relu_bwd(const ConvGeom &g, int rows, const float *dP, const uint8_t *arg, const float *R, float *dR,
-                          cudaStream_t s, LaunchHook *h);
-// dWb[(k*k*ci)+1][co] = sum over rows/positions of im2col(X)^T dR (+ bias row), deterministic split.
-cudaError_t conv_wgrad(const ConvGeom &g, int rows, const float *X, RowSel xrow, const float *dR, float *dWb,
-                       float *partial, int splits, cudaStream_t s, LaunchHook *h);
-// dX[rows][hi][wi][ci] = full-correlation of dR with W (no mask; the caller's previous layer routes it).
-cudaError_t conv_dgrad(const ConvGeom &g, int rows, const float *dR, const float *Wb, float *dX, cudaStream_t s,
-                       LaunchHook *h);
+// Limits of the conv kernels (checked at mtx_init): ci <= 16, co <= 32, shared-memory staging fits.
+constexpr size_t CONV_SMEM_MAX = 200 * 1024;
+bool conv_supported(const ConvGeom &g);
+size_t conv_fwd_smem(const ConvGeom &g, int spc);
+size_t conv_bwd_smem(const ConvGeom &g);
+// P = maxpool2x2(ReLU(conv(X) + b)) [rows][hp][wp][co] and the argmax (0..3, first maximum) per
+// pooled element; the pre-pool activation is not stored (the backward's mask at the argmax is P > 0).
+cudaError_t conv_fwd(const ConvGeom &g, int rows, const float *X, RowSel xrow, const float *Wb, float *P, uint8_t *arg,
+                     cudaStream_t s, LaunchHook *h);
+// Backward of one conv + ReLU + pool layer from dP (gradient of its pooled output):
+//   dR = route(dP via arg) .* [P > 0]                                   (never materialised)
+//   dWb[(k*k*ci)+1][co] = im2col(X)^T dR (+ bias row)  -- per-CTA partials (<= partial_cap floats),
+//                                                         folded deterministically
+//   dX[rows][hi][wi][ci] = full correlation of dR with W, if dX != nullptr (no mask: the previous
+//                          layer's own backward applies its pool/ReLU routing)
+cudaError_t conv_bwd(const ConvGeom &g, int rows, const float *X, RowSel xrow, const float *dP, const float *P,
+                     const uint8_t *arg, const float *Wb, float *dX, float *dWb, float *partial, int64_t partial_cap,
+                     cudaStream_t s, LaunchHook *h);
 
 }  // namespace mtx

@@ -1,11 +1,20 @@
 // kernels_conv.cu -- LeNet-style convolution layers of the local forward/backward
 // (CNN rows; config 3).  NHWC activations, weights
-// W[kh][kw][ci][co] followed by the bias row (the augmented block of the flat
-// buffer).  Channel counts are small (C_out = 6, 16), so these are SIMT kernels:
-// the fused forward computes conv + bias + ReLU + 2x2 max-pool (+ first-max argmax,
-// reading A6) in one pass; the backward routes the pooled gradient through the
-// argmax and the ReLU mask, and the weight gradient is a deterministic blocked
-// reduction over (sample, position) folded in a fixed order.
+// W[kh][kw][ci][co] followed by the bias row (the augmented block of the flat buffer).
+// Channel counts are small (C_out = 6, 16), so these are CUDA-core kernels built around
+// shared-memory staging of whole images, templated on the output channels padded to CO:
+//
+//   conv_fwd  -- a CTA stages its samples' input images and the weights; one thread per pooled
+//                output computes the 2x2 window's conv outputs for every channel (4 x CO register
+//                accumulators, k*k*ci ascending), adds the bias, applies ReLU and the 2x2 max-pool
+//                with the first maximum winning ties (reading A6).  Only the pooled value and its
+//                argmax are stored: the backward's ReLU mask at the argmax is [P > 0].
+//   conv_bwd  -- a CTA walks its samples: stages the input image, rebuilds dR = dP routed to the
+//                argmax, masked by [P > 0] (max-pool + ReLU backward), straight into shared memory,
+//                then (i) accumulates the weight gradient: each thread owns 4 patch elements x CO
+//                channels over a fixed set of output positions, and (ii) writes the input gradient
+//                dX (full correlation with W) of the sample.  Per-CTA weight-gradient partials are
+//                folded by fold_parts in a fixed order (deterministic).
 #include <stdio.h>
 
 #include <algorithm>
@@ -17,233 +26,335 @@ namespace {
 
 inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 
-// One thread per pooled output (n, ph, pw, co): the 2x2 conv outputs of its window,
-// bias, ReLU, then max with the first maximum in (dh, dw) order winning ties.
-__global__ void __launch_bounds__(256) conv_fwd_kernel(ConvGeom g, int rows, const float *__restrict__ X, RowSel xrow,
-                                                     const float *__restrict__ Wb, float *__restrict__ R,
-                                                     float *__restrict__ P, uint8_t *__restrict__ arg) {
+constexpr int CONV_T = 256;
+constexpr int CONV_CI_MAX = 16;
+
+__device__ __forceinline__ void stage_copy(const float *__restrict__ src, float *__restrict__ dst, int n) {
+    if ((((uintptr_t)src) & 15) == 0 && (n & 3) == 0) {
+#pragma unroll 4
+        for (int i = threadIdx.x; i < n / 4; i += blockDim.x) ((float4 *)dst)[i] = __ldg((const float4 *)src + i);
+    } else {
+#pragma unroll 4
+        for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+}
+
+// sW[e][CO] = W[e][co] for e < rows, zero for co >= g.co (rows of CO floats: 128-bit reads)
+template <int CO>
+__device__ __forceinline__ void stage_weights(const float *__restrict__ Wb, int rows, int co, float *__restrict__ sW) {
+    for (int i = threadIdx.x; i < rows * CO; i += blockDim.x) {
+        const int e = i / CO, j = i % CO;
+        sW[i] = j < co ? __ldg(Wb + (int64_t)e * co + j) : 0.f;
+    }
+}
+
+template <int CO>
+__global__ void __launch_bounds__(CONV_T) conv_fwd_kernel(ConvGeom g, int rows, int spc, const float *__restrict__ X,
+                                                        RowSel xrow, const float *__restrict__ Wb,
+                                                        float *__restrict__ P, uint8_t *__restrict__ arg) {
     pdl_wait();
-    extern __shared__ float sw[];  // (k*k*ci + 1) * co
+    extern __shared__ __align__(16) float sm[];
     const int KK = g.k * g.k * g.ci;
-    for (int e = threadIdx.x; e < (KK + 1) * g.co; e += blockDim.x) sw[e] = Wb[e];
+    const int in_sz = g.hi * g.wi * g.ci;
+    float *sW = sm;                   // (KK + 1) x CO, bias row last
+    float *sX = sm + (KK + 1) * CO;   // spc images
+    stage_weights<CO>(Wb, KK + 1, g.co, sW);
+    const int n0 = blockIdx.x * spc;
+    const int ns = min(spc, rows - n0);
+    stage_copy(X + (xrow.row0() + n0) * (int64_t)in_sz, sX, ns * in_sz);  // consecutive rows: one block
     __syncthreads();
-    const int64_t total = (int64_t)rows * g.hp * g.wp * g.co;
-    const int64_t in_sz = (int64_t)g.hi * g.wi * g.ci;
-    const float *Xb = X + xrow.row0() * in_sz;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int co = (int)(idx % g.co);
-        int64_t t = idx / g.co;
-        const int pw = (int)(t % g.wp);
-        t /= g.wp;
-        const int ph = (int)(t % g.hp);
-        const int64_t n = t / g.hp;
-        const float *x = Xb + n * in_sz;
-        float best = 0.f;
-        int barg = 0;
+    const int Pp = g.hp * g.wp;
+    const int dx = g.ci, dy = g.wi * g.ci;  // window neighbours (0,1) and (1,0)
+    for (int t = threadIdx.x; t < ns * Pp; t += blockDim.x) {
+        const int s = t / Pp, pp = t % Pp;
+        const int ph = pp / g.wp, pw = pp % g.wp;
+        const float *xs = sX + s * in_sz;
+        float acc[4][CO];
 #pragma unroll
-        for (int d = 0; d < 4; d++) {
-            const int oh = 2 * ph + (d >> 1), ow = 2 * pw + (d & 1);
-            float acc = 0.f;
-            for (int kh = 0; kh < g.k; kh++)
-                for (int kw = 0; kw < g.k; kw++) {
-                    const float *xp = x + ((int64_t)(oh + kh) * g.wi + (ow + kw)) * g.ci;
-                    const float *wp = sw + ((kh * g.k + kw) * g.ci) * g.co + co;
-                    for (int ci = 0; ci < g.ci; ci++) acc = __fmaf_rn(xp[ci], wp[ci * g.co], acc);
+        for (int d = 0; d < 4; d++)
+#pragma unroll
+            for (int j = 0; j < CO; j++) acc[d][j] = 0.f;
+        for (int kh = 0; kh < g.k; kh++)
+            for (int kw = 0; kw < g.k; kw++) {
+                const float *x0 = xs + ((2 * ph + kh) * g.wi + (2 * pw + kw)) * g.ci;
+                const float *wr = sW + ((kh * g.k + kw) * g.ci) * CO;
+                for (int c = 0; c < g.ci; c++) {
+                    const float xv[4] = {x0[c], x0[dx + c], x0[dy + c], x0[dy + dx + c]};
+#pragma unroll
+                    for (int j4 = 0; j4 < CO / 4; j4++) {
+                        const float4 w = *(const float4 *)(wr + c * CO + 4 * j4);
+#pragma unroll
+                        for (int d = 0; d < 4; d++) {
+                            acc[d][4 * j4 + 0] = __fmaf_rn(xv[d], w.x, acc[d][4 * j4 + 0]);
+                            acc[d][4 * j4 + 1] = __fmaf_rn(xv[d], w.y, acc[d][4 * j4 + 1]);
+                            acc[d][4 * j4 + 2] = __fmaf_rn(xv[d], w.z, acc[d][4 * j4 + 2]);
+                            acc[d][4 * j4 + 3] = __fmaf_rn(xv[d], w.w, acc[d][4 * j4 + 3]);
+                        }
+                    }
                 }
-            const float z = fmaxf(acc + sw[KK * g.co + co], 0.f);  // bias after the sum, ReLU
-            R[((n * g.hc + oh) * g.wc + ow) * g.co + co] = z;
-            if (d == 0 || z > best) {
-                best = z;
-                barg = d;
             }
+        const int64_t ob = ((int64_t)(n0 + s) * Pp + pp) * g.co;
+#pragma unroll
+        for (int j = 0; j < CO; j++) {
+            if (j >= g.co) break;
+            const float bias = sW[KK * CO + j];
+            float best = 0.f;
+            int barg = 0;
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+                const float z = fmaxf(acc[d][j] + bias, 0.f);  // bias after the sum (A13), ReLU
+                if (d == 0 || z > best) {                       // first maximum wins (A6)
+                    best = z;
+                    barg = d;
+                }
+            }
+            P[ob + j] = best;
+            arg[ob + j] = (uint8_t)barg;
         }
-        P[idx] = best;
-        arg[idx] = (uint8_t)barg;
     }
 }
 
-// dR = dP routed to its argmax, times the ReLU mask [R > 0]; positions outside every
-// pooling window (odd edges) get 0.  One thread per conv output element.
-__global__ void pool_relu_bwd_kernel(ConvGeom g, int rows, const float *__restrict__ dP,
-                                     const uint8_t *__restrict__ arg, const float *__restrict__ R,
-                                     float *__restrict__ dR) {
-    pdl_wait();
-    const int64_t total = (int64_t)rows * g.hc * g.wc * g.co;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int co = (int)(idx % g.co);
-        int64_t t = idx / g.co;
-        const int ow = (int)(t % g.wc);
-        t /= g.wc;
-        const int oh = (int)(t % g.hc);
-        const int64_t n = t / g.hc;
-        const int ph = oh >> 1, pw = ow >> 1;
-        float v = 0.f;
-        if (ph < g.hp && pw < g.wp) {
-            const int64_t pidx = ((n * g.hp + ph) * g.wp + pw) * g.co + co;
-            if (arg[pidx] == (uint8_t)(((oh & 1) << 1) | (ow & 1)) && R[idx] > 0.f) v = dP[pidx];
-        }
-        dR[idx] = v;
-    }
-}
-
-// Weight gradient: dWb[e][co] = sum over (n, oh, ow) of patch(n, oh, ow)[e] * dR(n, oh, ow)[co],
-// e < k*k*ci; row e == k*k*ci is the bias gradient sum dR.  Block z takes a contiguous range of
-// output positions; per 32-position tile it stages the patches and dR rows in shared memory, then
-// each thread accumulates its fixed (e, co) pairs in position order.  Partial per block; the
-// caller folds partials in block order (deterministic).
-constexpr int WG_T = 256, WG_POS = 32;
-__global__ void __launch_bounds__(WG_T) conv_wgrad_kernel(ConvGeom g, int rows, const float *__restrict__ X,
-                                                        RowSel xrow, const float *__restrict__ dR, int64_t pos_per,
+template <int CO>
+__global__ void __launch_bounds__(CONV_T) conv_bwd_kernel(ConvGeom g, int rows, int spc, const float *__restrict__ X,
+                                                        RowSel xrow, const float *__restrict__ dP,
+                                                        const float *__restrict__ P, const uint8_t *__restrict__ arg,
+                                                        const float *__restrict__ Wb, float *__restrict__ dX,
                                                         float *__restrict__ partial) {
     pdl_wait();
-    extern __shared__ float sm[];
-    const int KK = g.k * g.k * g.ci, E = KK + 1;
-    float *sp = sm;                 // [WG_POS][E]
-    float *sd = sm + WG_POS * E;    // [WG_POS][co]
-    const int pairs = E * g.co;
-    constexpr int MAXP = 16;        // pairs per thread (E*co <= 16*256)
-    float acc[MAXP];
+    extern __shared__ __align__(16) float sm[];
+    const int KK = g.k * g.k * g.ci, E = KK + 1, EB = (E + 3) / 4;
+    const int in_sz = g.hi * g.wi * g.ci;
+    const int HWc = g.hc * g.wc, Pp = g.hp * g.wp;
+    float *sD = sm;                           // dR of the current sample [hc*wc][CO]
+    float *sX = sD + HWc * CO;                // its input image
+    float *sW = sX + ((in_sz + 3) & ~3);      // W [KK][CO] (input gradient only)
+    if (dX) stage_weights<CO>(Wb, KK, g.co, sW);
+    const int tid = threadIdx.x;
+    // weight-gradient role: patch-element block eb (4 consecutive e) x position group pg
+    const int PG = blockDim.x / EB;
+    const int eb = tid % EB, pg = tid / EB;
+    const bool wg = pg < PG;
+    int off[4];
+    bool ones[4], valid[4];
 #pragma unroll
-    for (int i = 0; i < MAXP; i++) acc[i] = 0.f;
-    const int64_t npos = (int64_t)rows * g.hc * g.wc;
-    const int64_t p0 = blockIdx.x * pos_per, p1 = min(npos, p0 + pos_per);
-    const int64_t in_sz = (int64_t)g.hi * g.wi * g.ci;
-    const float *Xb = X + xrow.row0() * in_sz;
-    for (int64_t pt = p0; pt < p1; pt += WG_POS) {
-        const int np = (int)(p1 - pt < WG_POS ? p1 - pt : WG_POS);
-        for (int e = threadIdx.x; e < WG_POS * E; e += WG_T) {
-            const int pl = e / E, el = e % E;
-            float v = 0.f;
-            if (pl < np) {
-                const int64_t p = pt + pl;
-                const int ow = (int)(p % g.wc);
-                const int64_t t = p / g.wc;
-                const int oh = (int)(t % g.hc);
-                const int64_t n = t / g.hc;
-                if (el == KK) {
-                    v = 1.f;
-                } else {
-                    const int ci = el % g.ci, kw = (el / g.ci) % g.k, kh = el / (g.ci * g.k);
-                    v = Xb[n * in_sz + ((int64_t)(oh + kh) * g.wi + (ow + kw)) * g.ci + ci];
+    for (int j = 0; j < 4; j++) {
+        const int e = 4 * eb + j;
+        valid[j] = e < E;
+        ones[j] = e == KK;  // the bias row: the patch element is 1
+        const int kc = g.k * g.ci;
+        const int kh = e / kc, r = e % kc, kw = r / g.ci, c = r % g.ci;
+        off[j] = e < KK ? (kh * g.wi + kw) * g.ci + c : 0;
+    }
+    float acc[4][CO];
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+#pragma unroll
+        for (int q = 0; q < CO; q++) acc[j][q] = 0.f;
+    const int n_begin = blockIdx.x * spc, n_end = min(rows, n_begin + spc);
+    const float *Xb = X + xrow.row0() * (int64_t)in_sz;
+    for (int n = n_begin; n < n_end; n++) {
+        stage_copy(Xb + (int64_t)n * in_sz, sX, in_sz);
+        for (int i = tid; i < HWc * CO / 4; i += blockDim.x) ((float4 *)sD)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncthreads();
+        // max-pool + ReLU backward: dR = dP at the argmax when P > 0, zero elsewhere
+        for (int i = tid; i < Pp * g.co; i += blockDim.x) {
+            const int64_t pi = (int64_t)n * Pp * g.co + i;
+            const float pv = __ldg(P + pi);
+            if (pv > 0.f) {
+                const int co = i % g.co, pp = i / g.co, ph = pp / g.wp, pw = pp % g.wp;
+                const int d = __ldg(arg + pi);
+                sD[((2 * ph + (d >> 1)) * g.wc + 2 * pw + (d & 1)) * CO + co] = __ldg(dP + pi);
+            }
+        }
+        __syncthreads();
+        if (wg) {  // dW[e][co] += patch[p][e] * dR[p][co] over this thread's positions p = pg + PG*i
+            int oh = pg / g.wc, ow = pg % g.wc;
+            for (int p = pg; p < HWc; p += PG) {
+                const float *xr = sX + (oh * g.wi + ow) * g.ci;
+                float xv[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) xv[j] = ones[j] ? 1.f : (valid[j] ? xr[off[j]] : 0.f);
+                const float *dr = sD + p * CO;
+#pragma unroll
+                for (int q4 = 0; q4 < CO / 4; q4++) {
+                    const float4 dv = *(const float4 *)(dr + 4 * q4);
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        acc[j][4 * q4 + 0] = __fmaf_rn(xv[j], dv.x, acc[j][4 * q4 + 0]);
+                        acc[j][4 * q4 + 1] = __fmaf_rn(xv[j], dv.y, acc[j][4 * q4 + 1]);
+                        acc[j][4 * q4 + 2] = __fmaf_rn(xv[j], dv.z, acc[j][4 * q4 + 2]);
+                        acc[j][4 * q4 + 3] = __fmaf_rn(xv[j], dv.w, acc[j][4 * q4 + 3]);
+                    }
+                }
+                ow += PG;
+                while (ow >= g.wc) {
+                    ow -= g.wc;
+                    oh++;
                 }
             }
-            sp[e] = v;
         }
-        for (int e = threadIdx.x; e < WG_POS * g.co; e += WG_T) {
-            const int pl = e / g.co;
-            sd[e] = pl < np ? dR[(pt + pl) * g.co + e % g.co] : 0.f;
-        }
-        __syncthreads();
+        if (dX) {  // dX[h][w][c] = sum_{kh,kw,co} dR[h-kh][w-kw][co] W[kh][kw][c][co]  (kh, kw, co ascending)
+            for (int q = tid; q < g.hi * g.wi; q += blockDim.x) {
+                const int h = q / g.wi, w = q % g.wi;
+                float a[CONV_CI_MAX];
 #pragma unroll
-        for (int i = 0; i < MAXP; i++) {
-            const int pr = threadIdx.x + i * WG_T;
-            if (pr < pairs) {
-                const int el = pr / g.co, co = pr % g.co;
-                float tsum = 0.f;  // blocked summation: a 32-term chain per tile, then one add
-                for (int pl = 0; pl < np; pl++) tsum = __fmaf_rn(sp[pl * E + el], sd[pl * g.co + co], tsum);
-                acc[i] = __fadd_rn(acc[i], tsum);
+                for (int c = 0; c < CONV_CI_MAX; c++) a[c] = 0.f;
+                for (int kh = 0; kh < g.k; kh++) {
+                    const int oh = h - kh;
+                    if (oh < 0 || oh >= g.hc) continue;
+                    for (int kw = 0; kw < g.k; kw++) {
+                        const int ow = w - kw;
+                        if (ow < 0 || ow >= g.wc) continue;
+                        const float *dr = sD + (oh * g.wc + ow) * CO;
+                        const float *wr = sW + ((kh * g.k + kw) * g.ci) * CO;
+#pragma unroll
+                        for (int q4 = 0; q4 < CO / 4; q4++) {
+                            const float4 dv = *(const float4 *)(dr + 4 * q4);
+#pragma unroll
+                            for (int c = 0; c < CONV_CI_MAX; c++) {
+                                if (c >= g.ci) break;
+                                const float4 wv = *(const float4 *)(wr + c * CO + 4 * q4);
+                                a[c] = __fmaf_rn(dv.x, wv.x, a[c]);
+                                a[c] = __fmaf_rn(dv.y, wv.y, a[c]);
+                                a[c] = __fmaf_rn(dv.z, wv.z, a[c]);
+                                a[c] = __fmaf_rn(dv.w, wv.w, a[c]);
+                            }
+                        }
+                    }
+                }
+                float *out = dX + ((int64_t)n * g.hi * g.wi + q) * g.ci;
+#pragma unroll
+                for (int c = 0; c < CONV_CI_MAX; c++)
+                    if (c < g.ci) out[c] = a[c];
             }
         }
+        __syncthreads();  // sX / sD are rewritten for the next sample
+    }
+    // the PG position groups of each patch-element block are summed in ascending group order through
+    // shared memory (the staging buffers are idle now), then the CTA's partial is written out
+    float *red = sm;  // [4*EB][CO]
+    for (int r = 0; r < PG; r++) {
+        if (wg && pg == r) {
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+#pragma unroll
+                for (int q = 0; q < CO; q++) {
+                    float *dst = red + (4 * eb + j) * CO + q;
+                    *dst = r == 0 ? acc[j][q] : *dst + acc[j][q];
+                }
+        }
         __syncthreads();
     }
-#pragma unroll
-    for (int i = 0; i < MAXP; i++) {
-        const int pr = threadIdx.x + i * WG_T;
-        if (pr < pairs) partial[(int64_t)blockIdx.x * pairs + pr] = acc[i];
-    }
+    float *pb = partial + (int64_t)blockIdx.x * E * g.co;
+    for (int i = tid; i < E * g.co; i += blockDim.x) pb[i] = red[(i / g.co) * CO + i % g.co];
 }
 
-// Input gradient (full correlation): dX[n][h][w][ci] = sum_{kh,kw,co} dR[n][h-kh][w-kw][co] W[kh][kw][ci][co].
-__global__ void __launch_bounds__(256) conv_dgrad_kernel(ConvGeom g, int rows, const float *__restrict__ dR,
-                                                       const float *__restrict__ Wb, float *__restrict__ dX) {
+// out[j] = sum_p partial[p][j]: one warp per output, lane l sums p = l, l+32, ... ascending, then a
+// fixed xor-shuffle tree -- deterministic.
+__global__ void __launch_bounds__(256) fold_parts_kernel(const float *__restrict__ partial, int parts, int n,
+                                                       float *__restrict__ out) {
     pdl_wait();
-    extern __shared__ float sw[];
-    const int KK = g.k * g.k * g.ci;
-    for (int e = threadIdx.x; e < KK * g.co; e += blockDim.x) sw[e] = Wb[e];
-    __syncthreads();
-    const int64_t total = (int64_t)rows * g.hi * g.wi * g.ci;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int ci = (int)(idx % g.ci);
-        int64_t t = idx / g.ci;
-        const int w = (int)(t % g.wi);
-        t /= g.wi;
-        const int h = (int)(t % g.hi);
-        const int64_t n = t / g.hi;
-        float acc = 0.f;
-        for (int kh = 0; kh < g.k; kh++) {
-            const int oh = h - kh;
-            if (oh < 0 || oh >= g.hc) continue;
-            for (int kw = 0; kw < g.k; kw++) {
-                const int ow = w - kw;
-                if (ow < 0 || ow >= g.wc) continue;
-                const float *d = dR + ((n * g.hc + oh) * g.wc + ow) * g.co;
-                const float *wp = sw + ((kh * g.k + kw) * g.ci + ci) * g.co;
-                for (int co = 0; co < g.co; co++) acc = __fmaf_rn(d[co], wp[co], acc);
-            }
-        }
-        dX[idx] = acc;
-    }
+    const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (j >= n) return;
+    float s = 0.f;
+    for (int p = lane; p < parts; p += 32) s += __ldg(partial + (int64_t)p * n + j);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[j] = s;
+}
+
+inline int co_pad(int co) { return co <= 8 ? 8 : co <= 16 ? 16 : 32; }
+
+cudaError_t set_smem(const void *fn, size_t smem) {
+    if (smem > 48 * 1024) return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaSuccess;
+}
+
+template <int CO>
+cudaError_t launch_fwd(unsigned grid, int threads, size_t smem, cudaStream_t s, const ConvGeom &g, int rows, int spc,
+                       const float *X, RowSel xrow, const float *Wb, float *P, uint8_t *arg) {
+    cudaError_t e = set_smem((const void *)conv_fwd_kernel<CO>, smem);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(conv_fwd_kernel<CO>, dim3(grid), dim3(threads), smem, s, g, rows, spc, X, xrow, Wb, P, arg);
+}
+
+template <int CO>
+cudaError_t launch_bwd(unsigned grid, size_t smem, cudaStream_t s, const ConvGeom &g, int rows, int spc, const float *X,
+                       RowSel xrow, const float *dP, const float *P, const uint8_t *arg, const float *Wb, float *dX,
+                       float *partial) {
+    cudaError_t e = set_smem((const void *)conv_bwd_kernel<CO>, smem);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(conv_bwd_kernel<CO>, dim3(grid), dim3(CONV_T), smem, s, g, rows, spc, X, xrow, dP, P, arg, Wb, dX,
+                      partial);
 }
 
 }  // namespace
 
-cudaError_t conv_fwd(const ConvGeom &g, int rows, const float *X, RowSel xrow, const float *Wb, float *R, float *P,
-                     uint8_t *arg, cudaStream_t s, LaunchHook *h) {
-    const size_t smem = sizeof(float) * (size_t)(g.k * g.k * g.ci + 1) * g.co;
-    const int64_t total = (int64_t)rows * g.hp * g.wp * g.co;
-    unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 148 * 16));
+size_t conv_fwd_smem(const ConvGeom &g, int spc) {
+    return sizeof(float) * ((size_t)(g.k * g.k * g.ci + 1) * co_pad(g.co) + (size_t)spc * g.hi * g.wi * g.ci);
+}
+size_t conv_bwd_smem(const ConvGeom &g) {
+    const size_t in_sz = (size_t)g.hi * g.wi * g.ci;
+    return sizeof(float) * ((size_t)g.hc * g.wc * co_pad(g.co) + ((in_sz + 3) & ~(size_t)3) +
+                            (size_t)g.k * g.k * g.ci * co_pad(g.co));
+}
+bool conv_supported(const ConvGeom &g) {
+    return g.co >= 1 && g.co <= 32 && g.ci >= 1 && g.ci <= CONV_CI_MAX && (g.k * g.k * g.ci + 1 + 3) / 4 <= CONV_T &&
+           conv_fwd_smem(g, 1) <= CONV_SMEM_MAX && conv_bwd_smem(g) <= CONV_SMEM_MAX;
+}
+
+cudaError_t conv_fwd(const ConvGeom &g, int rows, const float *X, RowSel xrow, const float *Wb, float *P, uint8_t *arg,
+                     cudaStream_t s, LaunchHook *h) {
+    if (!conv_supported(g)) return cudaErrorInvalidValue;
+    const int Pp = g.hp * g.wp;
+    // samples per CTA: fill the block with pooled outputs, but keep >= 2 CTAs per SM of work
+    int spc = std::max(1, std::min(CONV_T / Pp, (int)cdiv(rows, 2 * 148)));
+    while (spc > 1 && conv_fwd_smem(g, spc) > CONV_SMEM_MAX) spc--;
+    const int threads = std::min(CONV_T, (int)((spc * Pp + 31) / 32 * 32));
+    const size_t smem = conv_fwd_smem(g, spc);
+    const unsigned grid = cdiv(rows, spc);
     char name[96];
-    snprintf(name, sizeof name, "conv_fwd[rows=%d,hi=%d,ci=%d,k=%d,co=%d]", rows, g.hi, g.ci, g.k, g.co);
+    snprintf(name, sizeof name, "conv_fwd[rows=%d,hi=%d,ci=%d,k=%d,co=%d,spc=%d]", rows, g.hi, g.ci, g.k, g.co, spc);
     if (h) h->before(name, s);
-    launch_pdl(conv_fwd_kernel, dim3(blocks), dim3(256), smem, s, g, rows, X, xrow, Wb, R, P, arg);
+    cudaError_t e;
+    switch (co_pad(g.co)) {
+        case 8: e = launch_fwd<8>(grid, threads, smem, s, g, rows, spc, X, xrow, Wb, P, arg); break;
+        case 16: e = launch_fwd<16>(grid, threads, smem, s, g, rows, spc, X, xrow, Wb, P, arg); break;
+        default: e = launch_fwd<32>(grid, threads, smem, s, g, rows, spc, X, xrow, Wb, P, arg);
+    }
     if (h) h->after(name, s);
-    return cudaGetLastError();
+    return e;
 }
 
-cudaError_t pool_relu_bwd(const ConvGeom &g, int rows, const float *dP, const uint8_t *arg, const float *R, float *dR,
-                          cudaStream_t s, LaunchHook *h) {
-    const int64_t total = (int64_t)rows * g.hc * g.wc * g.co;
-    unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 148 * 16));
-    char name[80];
-    snprintf(name, sizeof name, "pool_relu_bwd[n=%lld]", (long long)total);
-    if (h) h->before(name, s);
-    launch_pdl(pool_relu_bwd_kernel, dim3(blocks), dim3(256), 0, s, g, rows, dP, arg, R, dR);
-    if (h) h->after(name, s);
-    return cudaGetLastError();
-}
-
-cudaError_t conv_wgrad(const ConvGeom &g, int rows, const float *X, RowSel xrow, const float *dR, float *dWb,
-                       float *partial, int splits, cudaStream_t s, LaunchHook *h) {
+cudaError_t conv_bwd(const ConvGeom &g, int rows, const float *X, RowSel xrow, const float *dP, const float *P,
+                     const uint8_t *arg, const float *Wb, float *dX, float *dWb, float *partial, int64_t partial_cap,
+                     cudaStream_t s, LaunchHook *h) {
+    if (!conv_supported(g)) return cudaErrorInvalidValue;
     const int E = g.k * g.k * g.ci + 1;
-    if (E * g.co > 16 * WG_T) return cudaErrorInvalidValue;
-    const int64_t npos = (int64_t)rows * g.hc * g.wc;
-    const int64_t pos_per = (npos + splits - 1) / splits;
-    splits = (int)((npos + pos_per - 1) / pos_per);
-    const size_t smem = sizeof(float) * (size_t)WG_POS * (E + g.co);
-    char name[96];
-    snprintf(name, sizeof name, "conv_wgrad[pos=%lld,E=%d,co=%d,splits=%d]", (long long)npos, E, g.co, splits);
+    int ctas = std::min(rows, 2 * 148);
+    while (ctas > 1 && (int64_t)ctas * E * g.co > partial_cap) ctas--;
+    if ((int64_t)ctas * E * g.co > partial_cap) return cudaErrorInvalidValue;
+    const int spc = (int)cdiv(rows, ctas);
+    ctas = (int)cdiv(rows, spc);
+    const size_t smem = conv_bwd_smem(g);
+    char name[112];
+    snprintf(name, sizeof name, "conv_bwd[rows=%d,hc=%d,E=%d,co=%d,dgrad=%d,ctas=%d]", rows, g.hc, E, g.co, dX ? 1 : 0,
+             ctas);
     if (h) h->before(name, s);
-    launch_pdl(conv_wgrad_kernel, dim3(splits), dim3(WG_T), smem, s, g, rows, X, xrow, dR, pos_per, partial);
+    cudaError_t e;
+    switch (co_pad(g.co)) {
+        case 8: e = launch_bwd<8>(ctas, smem, s, g, rows, spc, X, xrow, dP, P, arg, Wb, dX, partial); break;
+        case 16: e = launch_bwd<16>(ctas, smem, s, g, rows, spc, X, xrow, dP, P, arg, Wb, dX, partial); break;
+        default: e = launch_bwd<32>(ctas, smem, s, g, rows, spc, X, xrow, dP, P, arg, Wb, dX, partial);
+    }
     if (h) h->after(name, s);
-    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return splitk_reduce(partial, splits, E, g.co, dWb, g.co, s, h);
-}
-
-cudaError_t conv_dgrad(const ConvGeom &g, int rows, const float *dR, const float *Wb, float *dX, cudaStream_t s,
-                       LaunchHook *h) {
-    const size_t smem = sizeof(float) * (size_t)g.k * g.k * g.ci * g.co;
-    const int64_t total = (int64_t)rows * g.hi * g.wi * g.ci;
-    unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 148 * 16));
-    char name[80];
-    snprintf(name, sizeof name, "conv_dgrad[n=%lld,k=%d,co=%d]", (long long)total, g.k, g.co);
+    const int nout = E * g.co;
+    snprintf(name, sizeof name, "fold_parts[parts=%d,n=%d]", ctas, nout);
     if (h) h->before(name, s);
-    launch_pdl(conv_dgrad_kernel, dim3(blocks), dim3(256), smem, s, g, rows, dR, Wb, dX);
+    e = launch_pdl(fold_parts_kernel, dim3(cdiv(nout, 8)), dim3(256), 0, s, (const float *)partial, ctas, nout, dWb);
     if (h) h->after(name, s);
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace mtx

@@ -155,7 +155,7 @@ struct mtx_ctx {
     bool fused = false;
     uint64_t *proto = nullptr;  // P x 8 bytes for the model-digest allgather
     // CNN activations
-    std::vector<float *> convR, convP, convDR, convDP;
+    std::vector<float *> convP, convDP;
     std::vector<uint8_t *> convArg;
     std::vector<float *> fcA;  // fc hidden activations
     int64_t partial_floats = 0;
@@ -273,6 +273,9 @@ mtx_status build_layout(mtx_ctx *c) {
             g.hi = h; g.wi = w; g.ci = ch; g.k = c->conv_k[i]; g.co = c->conv_c[i];
             g.hc = h - g.k + 1; g.wc = w - g.k + 1; g.hp = g.hc / 2; g.wp = g.wc / 2;
             if (g.hc < 2 || g.wc < 2) return fail(c, MTX_ERR_INVALID_ARG, "conv layer %zu too small", i);
+            if (!conv_supported(g))
+                return fail(c, MTX_ERR_UNSUPPORTED, "conv layer %zu: needs ci <= 16, co <= 32 and images that fit "
+                            "shared memory", i);
             c->convs.push_back(g);
             add(g.k * g.k * g.ci, g.co, g.k * g.k * g.ci, g.k * g.k * g.co);
             h = g.hp; w = g.wp; ch = g.co;
@@ -343,7 +346,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     float *grads = (float *)take(4 * (c->N_pad + LOSS_SLOT));
     float *gather = c->opt.reduce == MTX_REDUCE_ORDERED ? (float *)take(4 * c->world * (c->N_pad + LOSS_SLOT)) : nullptr;
     std::vector<float *> acts, fcA, dzs;
-    std::vector<float *> cR, cP, cDR, cDP;
+    std::vector<float *> cP, cDP;
     std::vector<uint8_t *> cArg;
     int64_t maxd = 1;
     int64_t partial = 0;
@@ -372,8 +375,6 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         }
     } else {
         for (auto &g : c->convs) {
-            cR.push_back((float *)take(4 * b * g.hc * g.wc * g.co));
-            cDR.push_back((float *)take(4 * b * g.hc * g.wc * g.co));
             cP.push_back((float *)take(4 * b * g.hp * g.wp * g.co));
             cDP.push_back((float *)take(4 * b * g.hp * g.wp * g.co));
             cArg.push_back(take(b * g.hp * g.wp * g.co));
@@ -430,7 +431,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     if (assign) {
         c->params = params; c->vel = vel; c->grads = grads; c->gather = gather;
         c->acts = acts; c->fcA = fcA; c->dzs = dzs; c->lanes = lanes;
-        c->convR = cR; c->convP = cP; c->convDR = cDR; c->convDP = cDP; c->convArg = cArg;
+        c->convP = cP; c->convDP = cDP; c->convArg = cArg;
         c->dz[0] = dz0; c->dz[1] = dz1; c->dzL = dzL; c->loss_rows = loss_rows;
         c->partial = part; c->partial_floats = partial;
         c->stage_x = sx; c->stage_y = sy;
@@ -781,8 +782,8 @@ mtx_status Runner::forward_backward_cnn() {
     for (int ci = 0; ci < NC; ci++) {
         const float *in = ci == 0 ? xbase() : c->convP[ci - 1];
         RowSel row = ci == 0 ? xrow() : RowSel{nullptr, 0};
-        e = conv_fwd(c->convs[ci], (int)b, in, row, c->params + c->layers[ci].pad_off, c->convR[ci], c->convP[ci],
-                     c->convArg[ci], s, h);
+        e = conv_fwd(c->convs[ci], (int)b, in, row, c->params + c->layers[ci].pad_off, c->convP[ci], c->convArg[ci], s,
+                     h);
         if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "conv_fwd: %s", cudaGetErrorString(e));
     }
     const float *flat = c->convP[NC - 1];
@@ -833,22 +834,14 @@ mtx_status Runner::forward_backward_cnn() {
         if (f < NF && f > 1) cur ^= 1;
     }
     for (int ci = NC - 1; ci >= 0; ci--) {
+        // pool + ReLU backward, weight gradient and (ci > 0) input gradient of conv layer ci, one kernel
         const ConvGeom &g = c->convs[ci];
-        e = pool_relu_bwd(g, (int)b, c->convDP[ci], c->convArg[ci], c->convR[ci], c->convDR[ci], s, h);
-        if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "pool_relu_bwd: %s", cudaGetErrorString(e));
-        if (ci > 0) {
-            e = conv_dgrad(g, (int)b, c->convDR[ci], c->params + c->layers[ci].pad_off, c->convDP[ci - 1], s, h);
-            if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "conv_dgrad: %s", cudaGetErrorString(e));
-        }
         const float *in = ci == 0 ? xbase() : c->convP[ci - 1];
         RowSel row = ci == 0 ? xrow() : RowSel{nullptr, 0};
-        const int64_t npos = b * g.hc * g.wc;
-        const int E = g.k * g.k * g.ci + 1;
-        int splits = (int)std::max<int64_t>(1, std::min<int64_t>(296, npos / 256));
-        splits = (int)std::min<int64_t>(splits, c->partial_floats / ((int64_t)E * g.co));
-        e = conv_wgrad(g, (int)b, in, row, c->convDR[ci], c->grads + c->layers[ci].pad_off, c->partial,
-                       std::max(1, splits), s, h);
-        if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "conv_wgrad: %s", cudaGetErrorString(e));
+        e = conv_bwd(g, (int)b, in, row, c->convDP[ci], c->convP[ci], c->convArg[ci], c->params + c->layers[ci].pad_off,
+                     ci > 0 ? c->convDP[ci - 1] : nullptr, c->grads + c->layers[ci].pad_off, c->partial,
+                     c->partial_floats, s, h);
+        if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "conv_bwd: %s", cudaGetErrorString(e));
         if ((st = bucket_ready(ci, bk))) return st;
     }
     return MTX_OK;
