@@ -121,6 +121,8 @@ struct ConvGeom {
     int hc, wc;       // conv output (valid, stride 1)
     int hp, wp;       // pooled output (2x2 / 2, floor)
 };
+// Bytes per sample of the pooled-argmax array (16-B multiple: bulk-copyable per sample).
+__host__ __device__ inline int conv_arg_pitch(const ConvGeom &g) { return (g.hp * g.wp * g.co + 15) & ~15; }
 // Limits of the conv kernels (checked at mtx_init): ci <= 16, co <= 32, shared-memory staging fits.
 constexpr size_t CONV_SMEM_MAX = 200 * 1024;
 bool conv_supported(const ConvGeom &g);

@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(CONV_T) conv_fwd_kernel(ConvGeom g, int rows, 
                 }
             }
         const int64_t ob = ((int64_t)(n0 + s) * Pp + pp) * g.co;
+        uint8_t *ab = arg + (int64_t)(n0 + s) * conv_arg_pitch(g) + pp * g.co;
 #pragma unroll
         for (int j = 0; j < CO; j++) {
             if (j >= g.co) break;
@@ -109,10 +110,48 @@ __global__ void __launch_bounds__(CONV_T) conv_fwd_kernel(ConvGeom g, int rows, 
                 }
             }
             P[ob + j] = best;
-            arg[ob + j] = (uint8_t)barg;
+            ab[j] = (uint8_t)barg;
         }
     }
 }
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint32_t bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done)
+                     : "r"(bar), "r"(parity)
+                     : "memory");
+    } while (!done);
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on the mbarrier in bytes
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+// dR row p of the backward's shared tile: CO floats as CO/4 16-B chunks, XOR-swizzled by the row so
+// that neighbouring rows (one per lane in the input-gradient loop) fall on different banks.
+template <int CO>
+__device__ __forceinline__ int dr_off(int p, int chunk) {
+    constexpr int NCH = CO / 4, R = 32 / CO;  // chunks per row, rows per 128-B line
+    return p * CO + 4 * (chunk ^ ((p / R) % NCH));
+}
+
+// Per-sample inputs of the backward, double-buffered in shared memory.
+struct BwdBuf {
+    float *x, *p, *dp;
+    uint8_t *a;
+};
 
 template <int CO>
 __global__ void __launch_bounds__(CONV_T) conv_bwd_kernel(ConvGeom g, int rows, int spc, const float *__restrict__ X,
@@ -125,9 +164,19 @@ __global__ void __launch_bounds__(CONV_T) conv_bwd_kernel(ConvGeom g, int rows, 
     const int KK = g.k * g.k * g.ci, E = KK + 1, EB = (E + 3) / 4;
     const int in_sz = g.hi * g.wi * g.ci;
     const int HWc = g.hc * g.wc, Pp = g.hp * g.wp;
+    const int ppc = Pp * g.co, apitch = conv_arg_pitch(g);
+    const int in_pad = (in_sz + 3) & ~3, ppc_pad = (ppc + 3) & ~3;
     float *sD = sm;                           // dR of the current sample [hc*wc][CO]
-    float *sX = sD + HWc * CO;                // its input image
-    float *sW = sX + ((in_sz + 3) & ~3);      // W [KK][CO] (input gradient only)
+    float *sW = sD + HWc * CO;                // W [KK][CO] (input gradient only)
+    float *red = sW + (dX ? KK * CO : 0);     // [4*EB][CO] CTA reduction of the weight gradient
+    float *bufs = red + 4 * EB * CO;
+    const int bstride = in_pad + 2 * ppc_pad + apitch / 4;
+    auto buf = [&](int b) {
+        float *base = bufs + b * bstride;
+        return BwdBuf{base, base + in_pad, base + in_pad + ppc_pad, (uint8_t *)(base + in_pad + 2 * ppc_pad)};
+    };
+    uint64_t *bars = (uint64_t *)(bufs + 2 * bstride);
+    const uint32_t bar0 = smem_addr(bars);
     if (dX) stage_weights<CO>(Wb, KK, g.co, sW);
     const int tid = threadIdx.x;
     // weight-gradient role: patch-element block eb (4 consecutive e) x position group pg
@@ -138,7 +187,7 @@ __global__ void __launch_bounds__(CONV_T) conv_bwd_kernel(ConvGeom g, int rows, 
     bool ones[4], valid[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-        const int e = 4 * eb + j;
+        const int e = eb + EB * j;  // lanes of a warp read consecutive patch elements: no bank conflicts
         valid[j] = e < E;
         ones[j] = e == KK;  // the bias row: the patch element is 1
         const int kc = g.k * g.ci;
@@ -152,21 +201,53 @@ __global__ void __launch_bounds__(CONV_T) conv_bwd_kernel(ConvGeom g, int rows, 
         for (int q = 0; q < CO; q++) acc[j][q] = 0.f;
     const int n_begin = blockIdx.x * spc, n_end = min(rows, n_begin + spc);
     const float *Xb = X + xrow.row0() * (int64_t)in_sz;
+    // bulk path: every per-sample block is a 16-B multiple at a 16-B aligned address
+    const bool bulk = (in_sz % 4 == 0) && (ppc % 4 == 0) && ((((uintptr_t)Xb) | ((uintptr_t)P) | ((uintptr_t)dP) |
+                                                              ((uintptr_t)arg)) & 15) == 0;
+    auto issue = [&](int n, int b) {  // one thread: the four copies of sample n into buffer b
+        const uint32_t bar = bar0 + 8 * b;
+        const BwdBuf B = buf(b);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // buffer's previous reads done (barrier)
+        bar_expect(bar, (uint32_t)(4 * in_sz + 8 * ppc + apitch));
+        bulk_g2s(B.x, Xb + (int64_t)n * in_sz, 4 * in_sz, bar);
+        bulk_g2s(B.p, P + (int64_t)n * ppc, 4 * ppc, bar);
+        bulk_g2s(B.dp, dP + (int64_t)n * ppc, 4 * ppc, bar);
+        bulk_g2s(B.a, arg + (int64_t)n * apitch, apitch, bar);
+    };
+    if (bulk && tid == 0) {
+        bar_init(bar0);
+        bar_init(bar0 + 8);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (bulk && tid == 0 && n_begin < n_end) issue(n_begin, 0);
     for (int n = n_begin; n < n_end; n++) {
-        stage_copy(Xb + (int64_t)n * in_sz, sX, in_sz);
+        const int it = n - n_begin, b = it & 1;
+        const BwdBuf B = buf(b);
+        if (bulk) {
+            if (tid == 0 && n + 1 < n_end) issue(n + 1, b ^ 1);  // prefetch: overlaps this sample's compute
+        } else {
+            for (int i = tid; i < in_sz; i += blockDim.x) B.x[i] = __ldg(Xb + (int64_t)n * in_sz + i);
+            for (int i = tid; i < ppc; i += blockDim.x) {
+                B.p[i] = __ldg(P + (int64_t)n * ppc + i);
+                B.dp[i] = __ldg(dP + (int64_t)n * ppc + i);
+                B.a[i] = __ldg(arg + (int64_t)n * apitch + i);
+            }
+        }
         for (int i = tid; i < HWc * CO / 4; i += blockDim.x) ((float4 *)sD)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (bulk) bar_wait(bar0 + 8 * b, (it >> 1) & 1);
         __syncthreads();
         // max-pool + ReLU backward: dR = dP at the argmax when P > 0, zero elsewhere
-        for (int i = tid; i < Pp * g.co; i += blockDim.x) {
-            const int64_t pi = (int64_t)n * Pp * g.co + i;
-            const float pv = __ldg(P + pi);
-            if (pv > 0.f) {
+        for (int i = tid; i < ppc; i += blockDim.x) {
+            if (B.p[i] > 0.f) {
                 const int co = i % g.co, pp = i / g.co, ph = pp / g.wp, pw = pp % g.wp;
-                const int d = __ldg(arg + pi);
-                sD[((2 * ph + (d >> 1)) * g.wc + 2 * pw + (d & 1)) * CO + co] = __ldg(dP + pi);
+                const int d = B.a[i];
+                const int p = (2 * ph + (d >> 1)) * g.wc + 2 * pw + (d & 1);
+                sD[dr_off<CO>(p, co >> 2) + (co & 3)] = B.dp[i];
             }
         }
         __syncthreads();
+        const float *sX = B.x;
         if (wg) {  // dW[e][co] += patch[p][e] * dR[p][co] over this thread's positions p = pg + PG*i
             int oh = pg / g.wc, ow = pg % g.wc;
             for (int p = pg; p < HWc; p += PG) {
@@ -174,10 +255,10 @@ __global__ void __launch_bounds__(CONV_T) conv_bwd_kernel(ConvGeom g, int rows, 
                 float xv[4];
 #pragma unroll
                 for (int j = 0; j < 4; j++) xv[j] = ones[j] ? 1.f : (valid[j] ? xr[off[j]] : 0.f);
-                const float *dr = sD + p * CO;
+                const float *dr = sD;
 #pragma unroll
                 for (int q4 = 0; q4 < CO / 4; q4++) {
-                    const float4 dv = *(const float4 *)(dr + 4 * q4);
+                    const float4 dv = *(const float4 *)(dr + dr_off<CO>(p, q4));
 #pragma unroll
                     for (int j = 0; j < 4; j++) {
                         acc[j][4 * q4 + 0] = __fmaf_rn(xv[j], dv.x, acc[j][4 * q4 + 0]);
@@ -205,11 +286,11 @@ __global__ void __launch_bounds__(CONV_T) conv_bwd_kernel(ConvGeom g, int rows, 
                     for (int kw = 0; kw < g.k; kw++) {
                         const int ow = w - kw;
                         if (ow < 0 || ow >= g.wc) continue;
-                        const float *dr = sD + (oh * g.wc + ow) * CO;
+                        const int p = oh * g.wc + ow;
                         const float *wr = sW + ((kh * g.k + kw) * g.ci) * CO;
 #pragma unroll
                         for (int q4 = 0; q4 < CO / 4; q4++) {
-                            const float4 dv = *(const float4 *)(dr + 4 * q4);
+                            const float4 dv = *(const float4 *)(sD + dr_off<CO>(p, q4));
 #pragma unroll
                             for (int c = 0; c < CONV_CI_MAX; c++) {
                                 if (c >= g.ci) break;
@@ -231,15 +312,14 @@ __global__ void __launch_bounds__(CONV_T) conv_bwd_kernel(ConvGeom g, int rows, 
         __syncthreads();  // sX / sD are rewritten for the next sample
     }
     // the PG position groups of each patch-element block are summed in ascending group order through
-    // shared memory (the staging buffers are idle now), then the CTA's partial is written out
-    float *red = sm;  // [4*EB][CO]
+    // shared memory, then the CTA's partial is written out
     for (int r = 0; r < PG; r++) {
         if (wg && pg == r) {
 #pragma unroll
             for (int j = 0; j < 4; j++)
 #pragma unroll
                 for (int q = 0; q < CO; q++) {
-                    float *dst = red + (4 * eb + j) * CO + q;
+                    float *dst = red + (eb + EB * j) * CO + q;
                     *dst = r == 0 ? acc[j][q] : *dst + acc[j][q];
                 }
         }
@@ -294,9 +374,12 @@ size_t conv_fwd_smem(const ConvGeom &g, int spc) {
     return sizeof(float) * ((size_t)(g.k * g.k * g.ci + 1) * co_pad(g.co) + (size_t)spc * g.hi * g.wi * g.ci);
 }
 size_t conv_bwd_smem(const ConvGeom &g) {
-    const size_t in_sz = (size_t)g.hi * g.wi * g.ci;
-    return sizeof(float) * ((size_t)g.hc * g.wc * co_pad(g.co) + ((in_sz + 3) & ~(size_t)3) +
-                            (size_t)g.k * g.k * g.ci * co_pad(g.co));
+    const size_t in_pad = ((size_t)g.hi * g.wi * g.ci + 3) & ~(size_t)3;
+    const size_t ppc_pad = ((size_t)g.hp * g.wp * g.co + 3) & ~(size_t)3;
+    const size_t KK = (size_t)g.k * g.k * g.ci, EB = (KK + 1 + 3) / 4, CO = co_pad(g.co);
+    return sizeof(float) * ((size_t)g.hc * g.wc * CO + KK * CO + 4 * EB * CO +
+                            2 * (in_pad + 2 * ppc_pad + conv_arg_pitch(g) / 4)) +
+           16;  // two mbarriers
 }
 bool conv_supported(const ConvGeom &g) {
     return g.co >= 1 && g.co <= 32 && g.ci >= 1 && g.ci <= CONV_CI_MAX && (g.k * g.k * g.ci + 1 + 3) / 4 <= CONV_T &&

@@ -377,7 +377,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         for (auto &g : c->convs) {
             cP.push_back((float *)take(4 * b * g.hp * g.wp * g.co));
             cDP.push_back((float *)take(4 * b * g.hp * g.wp * g.co));
-            cArg.push_back(take(b * g.hp * g.wp * g.co));
+            cArg.push_back(take(b * conv_arg_pitch(g)));
             int64_t kk = (int64_t)g.k * g.k * g.ci + 1;
             partial = std::max<int64_t>(partial, 296 * kk * g.co);  // conv_wgrad block partials
         }
