@@ -168,14 +168,21 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
         peak, unit = 148 * FP32_FMA_PER_SM_CLK * 2 * clk * 1e6 / 1e12, "TFLOP/s"
     # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
     # (profiles/ncu_traffic.json, written by tools/ncu_summary.py), averaged over its captured launches
-    ncu_kernel = {"gemm_tc3x": "tc_gemm_kernel<128, 1>", "gemm_tc": "tc_gemm_kernel<128, 0>",
+    # the tensor-core GEMM's template is <N tile, 3xTF32>: take the N tile of the group's longest launch
+    longest = max((kv for kv in timing.items() if kv[0].split("[")[0] == top_name), key=lambda kv: kv[1][0])[0]
+    bn = re.search(r"bn=(\d+)", longest)
+    bn = bn.group(1) if bn else "128"
+    ncu_kernel = {"gemm_tc3x": f"tc_gemm_kernel<{bn}, 1>", "gemm_tc": f"tc_gemm_kernel<{bn}, 0>",
                   "avg_update": "avg_update_kernel<1>", "head_softmax_xent": "head_kernel",
-                  "colsum": "colsum_kernel", "splitk_reduce": "splitk_reduce_kernel"}
+                  "colsum": "colsum_kernel", "splitk_reduce": "splitk_reduce_kernel", "conv_bwd": "conv_bwd_kernel",
+                  "conv_fwd": "conv_fwd_kernel"}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     key = next((v for k, v in ncu_kernel.items() if top_name.startswith(k)), None)
     if os.path.exists(tp) and key:
-        traffic = json.load(open(tp)).get(f"{config}:{key}")
+        tj = json.load(open(tp))
+        traffic = next((v for k, v in tj.items() if k == f"{config}:{key}" or k.startswith(f"{config}:{key}<")
+                        or k.startswith(f"{config}:{key}(")), None)
     return {"kernel": top_name, "bound": top["bound"], "achieved": round(achieved, 3), "peak": round(peak, 1),
             "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic,
             "work_per_launch": per_launch_work, "launch_us": round(per_launch_s * 1e6, 3),
