@@ -78,6 +78,7 @@ struct TcParams {
     const int64_t *a_win;  // dataset operand: sample-dimension offset read on the device
     int64_t a_base;
     unsigned *counters;    // split-K: one arrival counter per output tile (zero between launches)
+    int dbg;               // development only (MTX_TC_DBG): 1 skip epilogue stores, 2 skip TMA loads
     int cluster;           // 1: the splits of a tile form one thread-block cluster and are folded
                            // through distributed shared memory (no partial buffer, no fold launch)
 };
@@ -181,6 +182,37 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "r"(bar), "r"(parity)
             : "memory");
     } while (!done);
+}
+// Warp-converged issue: the whole warp runs the producer / MMA loops (warp-uniform values stay in
+// uniform registers) and elect.sync picks the one lane that issues each asynchronous operation.
+__device__ __forceinline__ void mbar_expect_tx_elect(uint32_t bar, uint32_t bytes) {
+    asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n @e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(bar),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_elect(uint32_t bar) {
+    asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n @e mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_elect(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1) {
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n}\n" ::"r"(
+            dst),
+        "l"((uint64_t)map), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void umma_tf32_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+        " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(bar)
+        : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1) {
     asm volatile(
@@ -367,8 +399,8 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
     const int total = tiles_mn * p.splits;
 
     if (warp == 0) {
-        // ================= TMA producer
-        if (lane == 0) {
+        // ================= TMA producer (the whole warp runs the loop; one elected lane issues)
+        {
             const int64_t row0 = p.a_win ? (*p.a_win + p.a_base) : 0;
             int stage = 0;
             uint32_t phase = 0;
@@ -383,23 +415,29 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                     mbar_wait(empty0 + 8 * stage, phase ^ 1);
                     const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::A_BYTES;
                     const uint32_t fb = full0 + 8 * stage;
-                    mbar_expect_tx(fb, L::STAGE_BYTES);
+                    if (p.dbg & 2) {  // development: MMA-only timing
+                        mbar_arrive_elect(fb);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
+                    mbar_expect_tx_elect(fb, L::STAGE_BYTES);
                     const int k0 = kb * BK;
 #pragma unroll
                     for (int plane = 0; plane < (SPLIT ? 2 : 1); plane++) {  // hi into the raw region, lo after it
                         const CUtensorMap *ma = plane ? &p.ta_lo : &p.ta, *mb = plane ? &p.tb_lo : &p.tb;
                         const uint32_t pa = sa + plane * L::RAW_BYTES, pb = sb + plane * L::RAW_BYTES;
                         if (!p.a_mn) {
-                            tma_load_2d(pa, ma, fb, k0, (int)(row0 + m0));
+                            tma_load_2d_elect(pa, ma, fb, k0, (int)(row0 + m0));
                         } else {
 #pragma unroll
-                            for (int j = 0; j < BM / 32; j++) tma_load_2d(pa + j * 4096, ma, fb, m0 + 32 * j, (int)(row0 + k0));
+                            for (int j = 0; j < BM / 32; j++)
+                                tma_load_2d_elect(pa + j * 4096, ma, fb, m0 + 32 * j, (int)(row0 + k0));
                         }
                         if (!p.b_mn) {
-                            tma_load_2d(pb, mb, fb, k0, n0);
+                            tma_load_2d_elect(pb, mb, fb, k0, n0);
                         } else {
 #pragma unroll
-                            for (int j = 0; j < BN / 32; j++) tma_load_2d(pb + j * 4096, mb, fb, n0 + 32 * j, k0);
+                            for (int j = 0; j < BN / 32; j++) tma_load_2d_elect(pb + j * 4096, mb, fb, n0 + 32 * j, k0);
                         }
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -407,10 +445,16 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
             }
         }
     } else if (warp == 1) {
-        // ================= MMA issuer (single thread).  Each tile's k-range is cut into chunks of
-        // CHUNK k-blocks; chunk i accumulates into TMEM buffer (i & 1) and is handed to the epilogue.
-        if (lane == 0) {
+        // ================= MMA issuer (whole warp, one elected lane issues).  Each tile's k-range is cut
+        // into chunks of CHUNK k-blocks; chunk i accumulates into TMEM buffer (i % NBUF) and is handed to
+        // the epilogue.  Descriptors: built once per k-block, advanced by a constant per 8-element k-step
+        // (K-major: 32 B inside the 128-B swizzled row; MN-major: two 4-row K groups = 1024 B).
+        {
             const uint32_t idesc = instr_desc(BM, BN, p.a_mn, p.b_mn);
+            const uint64_t a_hi = p.a_mn ? smem_desc(0, BK * 128, 512, 1) : smem_desc(0, 16, 1024, 2);
+            const uint64_t b_hi = p.b_mn ? smem_desc(0, BK * 128, 512, 1) : smem_desc(0, 16, 1024, 2);
+            const uint32_t a_step = p.a_mn ? (1024 >> 4) : (32 >> 4), b_step = p.b_mn ? (1024 >> 4) : (32 >> 4);
+            constexpr uint64_t LO = L::RAW_BYTES >> 4;  // hi plane -> lo plane of the same operand tile
             int stage = 0;
             uint32_t phase = 0;
             int buf = 0;
@@ -428,30 +472,24 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                         mbar_wait(full0 + 8 * stage, phase);
                         tc_fence_after();
                         const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::A_BYTES;
+                        const uint64_t ad0 = a_hi | ((sa >> 4) & 0x3FFF), bd0 = b_hi | ((sb >> 4) & 0x3FFF);
 #pragma unroll
                         for (int kk = 0; kk < BK / 8; kk++) {
-                            // K-major: advance 8 elements = 32 B inside the 128-B swizzled row;
-                            // MN-major: advance two 4-row K groups = 1024 B.
-                            const uint64_t ad = p.a_mn ? smem_desc(sa + kk * 1024, BK * 128, 512, 1)
-                                                       : smem_desc(sa + kk * 32, 16, 1024, 2);
-                            const uint64_t bd = p.b_mn ? smem_desc(sb + kk * 1024, BK * 128, 512, 1)
-                                                       : smem_desc(sb + kk * 32, 16, 1024, 2);
+                            const uint64_t ad = ad0 + kk * a_step, bd = bd0 + kk * b_step;
                             const uint32_t acc0 = (kb > c0 || kk > 0) ? 1u : 0u;
                             if (SPLIT) {
                                 // 3xTF32: hi.lo + lo.hi + hi.hi (hi = rne_tf32(x), lo = rne_tf32(x - hi))
-                                const uint64_t ads = ad + (uint64_t)(L::RAW_BYTES >> 4),
-                                               bds = bd + (uint64_t)(L::RAW_BYTES >> 4);
-                                umma_tf32(d_tmem, ad, bds, idesc, acc0);
-                                umma_tf32(d_tmem, ads, bd, idesc, 1u);
-                                umma_tf32(d_tmem, ad, bd, idesc, 1u);
+                                umma_tf32_elect(d_tmem, ad, bd + LO, idesc, acc0);
+                                umma_tf32_elect(d_tmem, ad + LO, bd, idesc, 1u);
+                                umma_tf32_elect(d_tmem, ad, bd, idesc, 1u);
                             } else {
-                                umma_tf32(d_tmem, ad, bd, idesc, acc0);
+                                umma_tf32_elect(d_tmem, ad, bd, idesc, acc0);
                             }
                         }
-                        umma_commit(empty0 + 8 * stage);  // frees the smem slot when these MMAs retire
+                        umma_commit_elect(empty0 + 8 * stage);  // frees the smem slot when these MMAs retire
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
-                    umma_commit(tfull0 + 8 * buf);  // chunk partial ready for promotion
+                    umma_commit_elect(tfull0 + 8 * buf);  // chunk partial ready for promotion
                     if (++buf == NBUF) { buf = 0; buf_phase ^= 1; }
                 }
             }
@@ -525,7 +563,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                     const int r = it * RPI + rl;
                     const int m = m0 + 32 * q + r;
                     const float4 sv = *(const float4 *)(stg + r * SW + 4 * swz(r, jj));
-                    if (m >= p.M || n >= p.N) continue;
+                    if (m >= p.M || n >= p.N || (p.dbg & 1)) continue;
                     if (p.splits > 1) {  // split-K partial (folded with the epilogue by splitk_reduce)
                         float *dst = p.partial + ((int64_t)z * p.M + m) * p.N + n;
                         if (n + 3 < p.N) *(float4 *)dst = sv;
@@ -807,6 +845,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     if (splits == 1) cluster = false;
     p.splits = splits;
     p.cluster = cluster ? 1 : 0;
+    if (const char *k = getenv("MTX_TC_DBG")) p.dbg = atoi(k);  // development timing knob
     p.epi = g.epi;
     p.bias = g.bias;
     p.mask = g.mask;
