@@ -34,16 +34,23 @@ constexpr int BM = 128, BK = 32;
 
 // Shared-memory plan per variant.  SPLIT (3xTF32) stages two planes of each operand tile: hi =
 // rne_tf32(x) and lo = rne_tf32(x - hi), written once by the tensor's producer.
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, bool PAIR = false>
 struct SmemLayout {
     // warps 0 TMA, 1 MMA, 2 TMEM alloc, 3 spare, 4-11 epilogue
     static constexpr int THREADS = 384;
     // k-blocks accumulated in TMEM before the epilogue warps promote the partial into fp32
     // registers (the tensor core's internal accumulation truncates)
-    static constexpr int CHUNK = SPLIT ? 4 : 8;
+#ifndef MTX_CHUNK3
+#define MTX_CHUNK3 4
+#endif
+    static constexpr int CHUNK = SPLIT ? MTX_CHUNK3 : 8;
     static constexpr uint32_t A_BYTES = BM * BK * 4;
-    static constexpr uint32_t B_BYTES = BN * BK * 4;
+    // PAIR (cta_group::2): the CTA pair computes a 256 x BN tile; each CTA holds its 128 rows of A and
+    // half of B's BN columns (the MMA reads both halves; measured by tools/tc_pair_probe.cu)
+    static constexpr uint32_t B_BYTES = (PAIR ? BN / 2 : BN) * BK * 4;
+    // stage: [A][B] (hi planes) followed, for 3xTF32, by [A_lo][B_lo] at RAW_BYTES
     static constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;
+    static constexpr uint32_t B_OFF = A_BYTES;
     static constexpr uint32_t STAGE_BYTES = RAW_BYTES * (SPLIT ? 2 : 1);
     // epilogue staging: one 32 x 32 fp32 sub-tile per epilogue warp (coalesced stores)
     static constexpr uint32_t EPI_BYTES = 8 * 32 * 32 * 4;
@@ -55,8 +62,9 @@ struct SmemLayout {
     static constexpr uint32_t BAR_OFF = EPI_OFF + EPI_BYTES;
     static constexpr uint32_t TOTAL = BAR_OFF + 256 + 1024;  // barriers + tmem slot + 1024-B alignment slack
     // TMEM accumulator ring: the MMA warp runs up to NBUF chunks ahead of the epilogue
-    static constexpr int NBUF = 512 / BN > 4 ? 4 : 512 / BN;
-    static constexpr uint32_t TMEM_COLS = NBUF * BN;
+    static constexpr int ACC_COLS = BN;
+    static constexpr int NBUF = 512 / ACC_COLS > 4 ? 4 : 512 / ACC_COLS;
+    static constexpr uint32_t TMEM_COLS = NBUF * ACC_COLS;
 };
 
 struct TcParams {
@@ -208,11 +216,46 @@ __device__ __forceinline__ void umma_tf32_elect(uint32_t d_tmem, uint64_t adesc,
         " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+
 __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
     asm volatile(
         "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
         " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(bar)
         : "memory");
+}
+// CTA pair (cta_group::2) variants: TMA into this CTA's smem completing on the leader's mbarrier (a
+// shared::cluster address), the pair MMA, and commits multicast to both CTAs' mbarriers.
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair_elect(uint32_t dst, const CUtensorMap *map, uint32_t bar_cluster, int c0,
+                                                       int c1) {
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n}\n" ::"r"(
+            dst),
+        "l"((uint64_t)map), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void umma_tf32_pair_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                     uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+        " @e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_pair_elect(uint32_t bar) {
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+            bar),
+        "h"((uint16_t)3)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1) {
     asm volatile(
@@ -348,9 +391,9 @@ __device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base) {
     }
 }
 
-template <int BN, bool SPLIT>
-__global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
-    using L = SmemLayout<BN, SPLIT>;
+template <int BN, bool SPLIT, bool PAIR>
+__global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
+    using L = SmemLayout<BN, SPLIT, PAIR>;
     constexpr int STAGES = L::STAGES;
     extern __shared__ uint8_t smem_raw[];
     // SWIZZLE_128B atoms need 1024-B aligned stage buffers
@@ -364,6 +407,9 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
     uint32_t *tmem_slot = (uint32_t *)(smem + L::BAR_OFF + 224);
     volatile int *fix_flag = (volatile int *)(smem + L::BAR_OFF + 232);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t rank = 0;  // PAIR: rank in the CTA pair; rank 0 (the leader) issues the MMAs
+    if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const bool leader = rank == 0;
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&p.ta) : "memory");
@@ -378,25 +424,41 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
         }
         for (int a = 0; a < NBUF; a++) {
             mbar_init(tfull0 + 8 * a, 1);
-            mbar_init(tempty0 + 8 * a, 8);
+            mbar_init(tempty0 + 8 * a, PAIR ? 16 : 8);  // the epilogue warps (of both CTAs of a pair)
         }
 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(L::TMEM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(L::TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(L::TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();  // the peer's barriers exist before any TMA / arrive targets them
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_wait();  // prologue above overlaps the previous kernel's tail (programmatic launch)
 
     const int tiles_mn = p.tiles_m * p.tiles_n;
     const int total = tiles_mn * p.splits;
+    // work units: one per CTA, or one per CTA pair (both CTAs of a pair walk the same units).  Written
+    // inline in each loop (from blockIdx / gridDim) so the loop counters stay in uniform registers.
+#define MTX_UNITS(t) for (int t = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x; t < total; \
+                          t += PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x)
+    constexpr int TILE_M = PAIR ? 2 * BM : BM;      // output rows per work unit
+    constexpr int B_COLS = PAIR ? BN / 2 : BN;      // B columns this CTA loads
+    const int m_off = PAIR ? BM * (int)rank : 0;    // this CTA's rows within the unit
+    const int nb_off = PAIR ? B_COLS * (int)rank : 0;
 
     if (warp == 0) {
         // ================= TMA producer (the whole warp runs the loop; one elected lane issues)
@@ -404,53 +466,58 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
             const int64_t row0 = p.a_win ? (*p.a_win + p.a_base) : 0;
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            MTX_UNITS(t) {
                 int z, r;
                 unit_of(p, t, tiles_mn, z, r);
                 // raster n-fastest: the CTAs sharing an A row-panel run together (A read from DRAM once,
                 // B -- the weights -- stays L2-resident)
-                const int m0 = (r / p.tiles_n) * BM, n0 = (r % p.tiles_n) * BN;
+                const int m0 = (r / p.tiles_n) * TILE_M + m_off, n0 = (r % p.tiles_n) * BN + nb_off;
                 const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
                 for (int kb = kb0; kb < kb1; kb++) {
                     mbar_wait(empty0 + 8 * stage, phase ^ 1);
-                    const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::A_BYTES;
+                    const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::B_OFF;
                     const uint32_t fb = full0 + 8 * stage;
+                    // PAIR: both CTAs' loads complete on the leader's full barrier, armed by the leader alone
+                    const uint32_t fbc = PAIR ? mapa_u32(fb, 0) : fb;
                     if (p.dbg & 2) {  // development: MMA-only timing
-                        mbar_arrive_elect(fb);
+                        if (leader) mbar_arrive_elect(fb);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                         continue;
                     }
-                    mbar_expect_tx_elect(fb, L::STAGE_BYTES);
+                    if (leader) mbar_expect_tx_elect(fb, PAIR ? 2 * L::STAGE_BYTES : L::STAGE_BYTES);
                     const int k0 = kb * BK;
 #pragma unroll
                     for (int plane = 0; plane < (SPLIT ? 2 : 1); plane++) {  // hi into the raw region, lo after it
                         const CUtensorMap *ma = plane ? &p.ta_lo : &p.ta, *mb = plane ? &p.tb_lo : &p.tb;
                         const uint32_t pa = sa + plane * L::RAW_BYTES, pb = sb + plane * L::RAW_BYTES;
+                        auto load = [&](uint32_t dst, const CUtensorMap *map, int c0, int c1) {
+                            if (PAIR) tma_load_2d_pair_elect(dst, map, fbc, c0, c1);
+                            else tma_load_2d_elect(dst, map, fb, c0, c1);
+                        };
                         if (!p.a_mn) {
-                            tma_load_2d_elect(pa, ma, fb, k0, (int)(row0 + m0));
+                            load(pa, ma, k0, (int)(row0 + m0));
                         } else {
 #pragma unroll
-                            for (int j = 0; j < BM / 32; j++)
-                                tma_load_2d_elect(pa + j * 4096, ma, fb, m0 + 32 * j, (int)(row0 + k0));
+                            for (int j = 0; j < BM / 32; j++) load(pa + j * 4096, ma, m0 + 32 * j, (int)(row0 + k0));
                         }
                         if (!p.b_mn) {
-                            tma_load_2d_elect(pb, mb, fb, k0, n0);
+                            load(pb, mb, k0, n0);
                         } else {
 #pragma unroll
-                            for (int j = 0; j < BN / 32; j++) tma_load_2d_elect(pb + j * 4096, mb, fb, n0 + 32 * j, k0);
+                            for (int j = 0; j < B_COLS / 32; j++) load(pb + j * 4096, mb, n0 + 32 * j, k0);
                         }
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
-    } else if (warp == 1) {
-        // ================= MMA issuer (whole warp, one elected lane issues).  Each tile's k-range is cut
+    } else if (warp == 1 && leader) {
+        // ================= MMA issuer (whole warp, one elected lane issues; PAIR: the leader CTA's only).  Each tile's k-range is cut
         // into chunks of CHUNK k-blocks; chunk i accumulates into TMEM buffer (i % NBUF) and is handed to
         // the epilogue.  Descriptors: built once per k-block, advanced by a constant per 8-element k-step
         // (K-major: 32 B inside the 128-B swizzled row; MN-major: two 4-row K groups = 1024 B).
         {
-            const uint32_t idesc = instr_desc(BM, BN, p.a_mn, p.b_mn);
+            const uint32_t idesc = instr_desc(TILE_M, BN, p.a_mn, p.b_mn);
             const uint64_t a_hi = p.a_mn ? smem_desc(0, BK * 128, 512, 1) : smem_desc(0, 16, 1024, 2);
             const uint64_t b_hi = p.b_mn ? smem_desc(0, BK * 128, 512, 1) : smem_desc(0, 16, 1024, 2);
             const uint32_t a_step = p.a_mn ? (1024 >> 4) : (32 >> 4), b_step = p.b_mn ? (1024 >> 4) : (32 >> 4);
@@ -459,7 +526,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
             uint32_t phase = 0;
             int buf = 0;
             uint32_t buf_phase = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            MTX_UNITS(t) {
                 int z, r;
                 unit_of(p, t, tiles_mn, z, r);
                 const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
@@ -467,29 +534,37 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                     const int c1 = min(kb1, c0 + L::CHUNK);
                     mbar_wait(tempty0 + 8 * buf, buf_phase ^ 1);
                     tc_fence_after();
-                    const uint32_t d_tmem = tmem_base + buf * BN;
+                    const uint32_t d_tmem = tmem_base + buf * L::ACC_COLS;
                     for (int kb = c0; kb < c1; kb++) {
                         mbar_wait(full0 + 8 * stage, phase);
                         tc_fence_after();
-                        const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::A_BYTES;
+                        const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::B_OFF;
                         const uint64_t ad0 = a_hi | ((sa >> 4) & 0x3FFF), bd0 = b_hi | ((sb >> 4) & 0x3FFF);
 #pragma unroll
                         for (int kk = 0; kk < BK / 8; kk++) {
                             const uint64_t ad = ad0 + kk * a_step, bd = bd0 + kk * b_step;
                             const uint32_t acc0 = (kb > c0 || kk > 0) ? 1u : 0u;
+                            auto mma = [&](uint64_t x, uint64_t y, uint32_t acc) {
+                                if (PAIR) umma_tf32_pair_elect(d_tmem, x, y, idesc, acc);
+                                else umma_tf32_elect(d_tmem, x, y, idesc, acc);
+                            };
                             if (SPLIT) {
                                 // 3xTF32: hi.lo + lo.hi + hi.hi (hi = rne_tf32(x), lo = rne_tf32(x - hi))
-                                umma_tf32_elect(d_tmem, ad, bd + LO, idesc, acc0);
-                                umma_tf32_elect(d_tmem, ad + LO, bd, idesc, 1u);
-                                umma_tf32_elect(d_tmem, ad, bd, idesc, 1u);
+                                mma(ad, bd + LO, acc0);
+                                mma(ad + LO, bd, 1u);
+                                mma(ad, bd, 1u);
                             } else {
-                                umma_tf32_elect(d_tmem, ad, bd, idesc, acc0);
+                                mma(ad, bd, acc0);
                             }
                         }
-                        umma_commit_elect(empty0 + 8 * stage);  // frees the smem slot when these MMAs retire
+                        // frees the smem slot (of both CTAs of a pair) when these MMAs retire
+                        if (PAIR) umma_commit_pair_elect(empty0 + 8 * stage);
+                        else umma_commit_elect(empty0 + 8 * stage);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
-                    umma_commit_elect(tfull0 + 8 * buf);  // chunk partial ready for promotion
+                    // chunk partial ready for promotion (in both CTAs' TMEM for a pair)
+                    if (PAIR) umma_commit_pair_elect(tfull0 + 8 * buf);
+                    else umma_commit_elect(tfull0 + 8 * buf);
                     if (++buf == NBUF) { buf = 0; buf_phase ^= 1; }
                 }
             }
@@ -502,10 +577,10 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
         const int q = warp & 3, h = (warp - 4) >> 2;
         int buf = 0;
         uint32_t buf_phase = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        MTX_UNITS(t) {
             int z, r;
             unit_of(p, t, tiles_mn, z, r);
-            const int m0 = (r / p.tiles_n) * BM, n0 = (r % p.tiles_n) * BN + h * HALF;
+            const int m0 = (r / p.tiles_n) * TILE_M + m_off, n0 = (r % p.tiles_n) * BN + h * HALF;
             const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
             float acc[HALF];
             bool first = true;
@@ -516,7 +591,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
 #pragma unroll
                 for (int c = 0; c < HALF / CW; c++) {
                     uint32_t v[CW];
-                    const uint32_t taddr = tmem_base + buf * BN + ((uint32_t)(32 * q) << 16) + h * HALF + CW * c;
+                    const uint32_t taddr = tmem_base + buf * L::ACC_COLS + ((uint32_t)(32 * q) << 16) + h * HALF + CW * c;
                     if constexpr (CW == 32) {
                         TMEM_LD32(taddr, v);
                     } else {
@@ -530,7 +605,10 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
                 first = false;
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(tempty0 + 8 * buf);
+                if (lane == 0) {  // accumulator buffer drained (PAIR: on the leader, which issues into it)
+                    if (PAIR) mbar_arrive_cluster(mapa_u32(tempty0 + 8 * buf, 0));
+                    else mbar_arrive(tempty0 + 8 * buf);
+                }
                 if (++buf == NBUF) { buf = 0; buf_phase ^= 1; }
             }
             if (p.cluster) {  // partial tile -> own smem; folded across the cluster below
@@ -591,6 +669,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
             }
         }
     }
+#undef MTX_UNITS
     if (p.cluster) {
         // every CTA of the cluster holds its split's partial tile: CTA z folds rows
         // [z*BM/S, (z+1)*BM/S) over the splits in ascending order (deterministic) and stores them
@@ -601,10 +680,15 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT>::THREADS, 1) tc_gemm_ker
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();  // both CTAs done with the pair's TMEM and barriers
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(L::TMEM_COLS)
-                     : "memory");
+        if (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(L::TMEM_COLS)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(L::TMEM_COLS)
+                         : "memory");
     }
 }
 
@@ -635,7 +719,7 @@ bool make_map(EncodeTiled enc, CUtensorMap *m, const float *ptr, int64_t rows, i
 struct TcGemm {
     EncodeTiled encode = nullptr;
     int sms = 148;
-    bool attr_set[8] = {};
+    bool attr_set[16] = {};
     // split-K fold inside the kernel by the tile's last CTA (MTX_TC_FIXUP=1).  Off: a one-SM fold of
     // splits x 64 KB is slower than the all-SM fold kernel on every measured shape.
     bool fixup = false;
@@ -643,6 +727,8 @@ struct TcGemm {
     // + splitk_reduce launch)
     bool cluster = true;
     int max_clusters[2][3][9] = {};  // [SPLIT][BN 128/64/32][cluster size]: co-resident clusters (0 = unknown)
+    // CTA-pair (cta_group::2) 256 x 128 tiles for large GEMMs (MTX_TC_PAIR=0 disables)
+    bool pair = true;
 };
 
 bool tc_available() { return true; }
@@ -695,6 +781,7 @@ TcGemm *tc_create(int device) {
     t->encode = (EncodeTiled)fn;
     if (const char *k = getenv("MTX_TC_FIXUP")) t->fixup = atoi(k) != 0;  // development A/B knob
     if (const char *k = getenv("MTX_TC_CLUSTER")) t->cluster = atoi(k) != 0;
+    if (const char *k = getenv("MTX_TC_PAIR")) t->pair = atoi(k) != 0;
     cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, device);
     int major = 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
@@ -722,13 +809,13 @@ bool tc_supports(TcGemm *t, const GemmDesc &g) {
     return true;
 }
 
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, bool PAIR = false>
 static cudaError_t prepare(TcGemm *t) {
-    using L = SmemLayout<BN, SPLIT>;
-    const int slot = (SPLIT ? 1 : 0) + 2 * (BN == 128 ? 0 : BN == 64 ? 1 : 2);
+    using L = SmemLayout<BN, SPLIT, PAIR>;
+    const int slot = (SPLIT ? 1 : 0) + 2 * (BN == 128 ? 0 : BN == 64 ? 1 : 2) + (PAIR ? 8 : 0);
     if (!t->attr_set[slot]) {
-        cudaError_t e =
-            cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT, PAIR>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
         if (e != cudaSuccess) return e;
         t->attr_set[slot] = true;
     }
@@ -754,7 +841,7 @@ static int co_resident_clusters(TcGemm *t, int cs) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, (void *)tc_gemm_kernel<BN, SPLIT>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, (void *)tc_gemm_kernel<BN, SPLIT, false>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         n = -1;  // query failed: never use the cluster path for this variant
     }
@@ -762,12 +849,13 @@ static int co_resident_clusters(TcGemm *t, int cs) {
     return n;
 }
 
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, bool PAIR = false>
 static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s) {
-    using L = SmemLayout<BN, SPLIT>;
-    cudaError_t e = prepare<BN, SPLIT>(t);
+    using L = SmemLayout<BN, SPLIT, PAIR>;
+    cudaError_t e = prepare<BN, SPLIT, PAIR>(t);
     if (e != cudaSuccess) return e;
-    if (!p.cluster) return launch_pdl(tc_gemm_kernel<BN, SPLIT>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
+    if (!p.cluster && !PAIR)
+        return launch_pdl(tc_gemm_kernel<BN, SPLIT, PAIR>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(L::THREADS);
@@ -775,14 +863,14 @@ static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s
     cfg.stream = s;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = p.splits;
+    at[0].val.clusterDim.x = PAIR ? 2 : p.splits;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT>, p);
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT, PAIR>, p);
 }
 
 template <int BN>
@@ -795,6 +883,11 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     const int N = g.N, K = g.K;
     const TcPlan plan = tc_plan(t->sms, M, N, K);
     const int BN = plan.bn;
+    // CTA pairs for large unsplit GEMMs: a 256 x 128 tile per pair halves B's per-SM operand traffic.
+    // Not for dgrad: its masked epilogue is the heavier one and the pair couples both SMs' epilogues
+    // through the shared accumulator barrier (measured slower).
+    const bool pair = t->pair && g.epi != EPI_MASK && BN == 128 && plan.splits == 1 && N % 64 == 0 && M > BM &&
+                      (int64_t)((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * 2 >= t->sms / 2;
     TcParams p{};
     p.M = M; p.N = N; p.K = K;
     p.a_mn = g.ta ? 1 : 0;
@@ -808,7 +901,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
                      : make_map(t->encode, m, ptr, g.arow.win ? a_rows_total : K, M, g.lda, BK, true);
     };
     auto map_b = [&](CUtensorMap *m, const float *ptr) {
-        return g.tb ? make_map(t->encode, m, ptr, N, K, g.ldb, BN, false)   // [N][K], K-major
+        return g.tb ? make_map(t->encode, m, ptr, N, K, g.ldb, pair ? BN / 2 : BN, false)   // [N][K], K-major
                     : make_map(t->encode, m, ptr, K, N, g.ldb, BK, true);   // [K][N], MN-major
     };
     if (g.tf32x3) ok = map_a(&p.ta, g.A_hi) && map_a(&p.ta_lo, g.A_lo) && map_b(&p.tb, g.B_hi) && map_b(&p.tb_lo, g.B_lo);
@@ -818,14 +911,14 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.C_lo = g.C_lo;
     p.a_win = g.arow.win;
     p.a_base = g.arow.base;
-    p.tiles_m = (M + BM - 1) / BM;
+    p.tiles_m = pair ? (M + 2 * BM - 1) / (2 * BM) : (M + BM - 1) / BM;
     p.tiles_n = (N + BN - 1) / BN;
     p.kb_total = (K + BK - 1) / BK;
     const int tiles = p.tiles_m * p.tiles_n;
     int splits = plan.splits;
     // split-K fold through DSMEM when the tile's splits fit one cluster and all clusters are co-resident
     bool cluster = false;
-    if (splits > 1 && splits <= 8 && t->cluster) {
+    if (splits > 1 && splits <= 8 && t->cluster && !pair) {
         const int per = (p.kb_total + splits - 1) / splits;
         const int sp = (p.kb_total + per - 1) / per;
         const int nc = BN == 128 ? co_resident<128>(t, g.tf32x3, sp)
@@ -855,14 +948,15 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.partial = g.partial;
     p.counters = (t->fixup && !g.C_hi && !cluster) ? g.counters : nullptr;
     const int total = tiles * splits;
-    const int grid = cluster ? total : std::min(total, t->sms);
+    const int grid = cluster ? total : pair ? 2 * std::min(total, t->sms / 2) : std::min(total, t->sms);
     const char *kind = g.epi == EPI_MASK ? "dgrad" : (g.ta ? "wgrad" : "fwd");
     char name[96];
-    snprintf(name, sizeof name, "gemm_tc%s_%s[M=%d,N=%d,K=%d,splits=%d,cluster=%d,bn=%d]", g.tf32x3 ? "3x" : "", kind,
-             M, N, K, splits, cluster ? 1 : 0, BN);
+    snprintf(name, sizeof name, "gemm_tc%s_%s[M=%d,N=%d,K=%d,splits=%d,cluster=%d,pair=%d,bn=%d]", g.tf32x3 ? "3x" : "",
+             kind, M, N, K, splits, cluster ? 1 : 0, pair ? 1 : 0, BN);
     if (h) h->before(name, s);
     cudaError_t e;
-    if (BN == 128) e = g.tf32x3 ? launch<128, true>(t, p, grid, s) : launch<128, false>(t, p, grid, s);
+    if (pair) e = g.tf32x3 ? launch<128, true, true>(t, p, grid, s) : launch<128, false, true>(t, p, grid, s);
+    else if (BN == 128) e = g.tf32x3 ? launch<128, true>(t, p, grid, s) : launch<128, false>(t, p, grid, s);
     else if (BN == 64) e = g.tf32x3 ? launch<64, true>(t, p, grid, s) : launch<64, false>(t, p, grid, s);
     else e = g.tf32x3 ? launch<32, true>(t, p, grid, s) : launch<32, false>(t, p, grid, s);
     if (h) h->after(name, s);
