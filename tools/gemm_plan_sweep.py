@@ -16,6 +16,9 @@ SHAPES = {  # (M, N, K, ta, tb, epi)
     "cfg2_wgrad2": (512, 512, 512, 1, 0, 0),
     "cfg4_fwd": (8192, 1024, 1024, 0, 0, 1), "cfg4_dgrad": (8192, 1024, 1024, 0, 1, 3),
     "cfg4_wgrad": (1024, 1024, 8192, 1, 0, 0), "cfg4_fwd1": (8192, 1024, 28, 0, 0, 1),
+    # fixed-cost probes: one tile / one k-block, and one tile with a deep K
+    "tiny_1tile_1kb": (128, 64, 32, 0, 0, 0), "tiny_1tile_8kb": (128, 64, 256, 0, 0, 0),
+    "tiny_148tiles_1kb": (128 * 37, 256, 32, 0, 0, 0),
 }
 only = sys.argv[1:] or list(SHAPES)
 
@@ -60,7 +63,7 @@ for name in only:
         os.environ.pop("MTX_TC_BN", None); os.environ.pop("MTX_TC_SPLITS", None)
         res = {"shape": name, "prec": tag, "default_us": round(timed(run), 2)}
         kb = (K + 31) // 32
-        for bn in (128, 64, 32):
+        for bn in ((128, 64, 32) if not name.startswith("tiny") else ()):
             for sp in (1, 2, 3, 4, 6, 8, 12, 16):
                 if sp > kb:
                     continue

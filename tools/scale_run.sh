@@ -5,7 +5,7 @@ timeout 900 python -m pytest tests/test_multigpu.py -m gpu -q > gpurun_out/pytes
 for N in 2 4; do
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2950$N tools/cfg5_sweep.py > gpurun_out/cfg5_P$N.log 2>&1; tail -12 gpurun_out/cfg5_P$N.log
 done
-for cfg in cfg2 cfg4; do
+for cfg in cfg2 cfg3 cfg4; do
   for N in 1 2 4; do
     if [ $N = 1 ]; then
       timeout 300 python bench.py --config $cfg --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/scale_${cfg}_N$N.json 2> gpurun_out/scale_${cfg}_N$N.err

@@ -15,12 +15,13 @@ L = [f"# Gradient-reduction modes, ablation ({rnd})", "",
      "`nccl` = flat buffer, reverse-layer 1 MiB buckets, ncclAllReduce per bucket overlapped with the backward, then K6;",
      "`fused` = the averaging operator fused with its collective over NVLink peer memory (one kernel + 2 flag barriers);",
      "`layerwise` = the paper's design (P:304-306): one ncclAllReduce per variable in canonical order after the backward;",
-     "`zero1` = ncclReduceScatter, update of the 1/P shard, ncclAllGather of w, v (and G).", "",
+     "`zero1` = ncclReduceScatter, update of the 1/P shard, ncclAllGather of w, v (and G);",
+     "`ordered` = test mode: allgather of every rank's buckets + an ascending-rank left fold (the oracle's order).", "",
      "| config | P | mode | µs/step | samples/s | vs fused |", "|---|---:|---|---:|---:|---:|"]
 for cfg in ("cfg2", "cfg4"):
     for n in (2, 4):
         base = rows.get((cfg, n, "fused"))
-        for mode in ("nccl", "fused", "layerwise", "zero1"):
+        for mode in ("nccl", "fused", "layerwise", "zero1", "ordered"):
             d = rows.get((cfg, n, mode))
             if not d:
                 continue
