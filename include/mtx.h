@@ -207,6 +207,19 @@ mtx_status mtx_train_step(mtx_ctx *ctx, int64_t step, float *host_loss, void *st
 mtx_status mtx_train_step_host(mtx_ctx *ctx, const float *X_host, const int32_t *y_host, float *host_loss,
                                void *stream);
 
+/* Pipelined variant of mtx_train_step_host -- the data-reader pattern of a training loop.  Enqueues,
+ * without synchronising: the host->device copy of this step's b rows and labels (pinned X_host /
+ * y_host, read asynchronously: keep them unchanged until the next mtx_sync) on the library's copy
+ * stream into one of two device landing buffers -- so it overlaps the previous step's compute --,
+ * the step itself on `stream`, and the device->host copy of the step's loss sum into a pinned
+ * library ring.  Same results as mtx_train_step_host on the same rows. */
+mtx_status mtx_train_step_host_async(mtx_ctx *ctx, const float *X_host, const int32_t *y_host, void *stream);
+
+/* Waits for everything enqueued on `stream` and the copy stream; writes the global loss of the most
+ * recent pipelined step to *host_loss (nullable) and reports deferred errors (MTX_ERR_NUMERIC for a
+ * non-finite averaged gradient, MTX_ERR_NCCL for a peer-barrier timeout). */
+mtx_status mtx_sync(mtx_ctx *ctx, float *host_loss, void *stream);
+
 /* The averaging + update operator on caller buffers (config 5 sweep; no model
  * needed beyond the context's communicator): grad[count] <- allreduce-sum over
  * ranks; if apply_update: gbar = grad * fl(1/P), velocity <- fma(mu, velocity,

@@ -85,6 +85,14 @@ class Replica:
     def step_host(self, X_rows: np.ndarray, y_rows: np.ndarray) -> float:
         return mtx.mtx_train_step_host(self.ctx, X_rows.ctypes.data, y_rows.ctypes.data, self.s)
 
+    def step_host_async(self, X_rows: np.ndarray, y_rows: np.ndarray) -> None:
+        """Pipelined host-input step (rows must stay valid and unchanged until sync_host())."""
+        mtx.mtx_train_step_host_async(self.ctx, X_rows.ctypes.data, y_rows.ctypes.data, self.s)
+
+    def sync_host(self) -> float:
+        """Waits for the pipelined steps; returns the last step's global loss."""
+        return mtx.mtx_sync(self.ctx, self.s)
+
     def sync(self):
         self.stream.synchronize()
 

@@ -166,6 +166,15 @@ struct mtx_ctx {
     // host pinned slots
     float *h_loss = nullptr;
     int *h_flag = nullptr;
+    // pipelined host-input steps (mtx_train_step_host_async): double-buffered device landing areas
+    // filled on copy_s while the previous step computes, a pinned ring of per-step loss sums
+    float *land_x[2] = {nullptr, nullptr};
+    int32_t *land_y[2] = {nullptr, nullptr};
+    cudaStream_t copy_s = nullptr;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+    int land_next = 0;
+    int64_t async_steps = 0;
+    float *h_loss_ring = nullptr;  // 64 slots
     // runtime
     ncclComm_t comm = nullptr;
     cudaStream_t own = nullptr, comm_s = nullptr;
@@ -424,6 +433,8 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     float *sx = (float *)take(4 * b * c->d0);
     plane(sx, b * c->d0);
     int32_t *sy = (int32_t *)take(4 * b);
+    float *lx0 = (float *)take(4 * b * c->d0), *lx1 = (float *)take(4 * b * c->d0);
+    int32_t *ly0 = (int32_t *)take(4 * b), *ly1 = (int32_t *)take(4 * b);
     float *loss_part = (float *)take(4 * 1024);
     // per lane: [0,254) split-K tiles, 254 narrow wgrad, 256.. colsum groups
     unsigned *counters = (unsigned *)take(4 * COUNTERS_PER_LANE * lanes);
@@ -435,6 +446,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         c->dz[0] = dz0; c->dz[1] = dz1; c->dzL = dzL; c->loss_rows = loss_rows;
         c->partial = part; c->partial_floats = partial;
         c->stage_x = sx; c->stage_y = sy;
+        c->land_x[0] = lx0; c->land_x[1] = lx1; c->land_y[0] = ly0; c->land_y[1] = ly1;
         c->planes = planes;
         for (auto &pr : planes) {
             if (pr.base == params) { c->params_hi = pr.hi; c->params_lo = pr.lo; }
@@ -1023,7 +1035,13 @@ mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t ui
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaHostAlloc(&c->h_loss, 64, cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&c->h_flag, 64, cudaHostAllocDefault) != cudaSuccess) {
+        cudaHostAlloc(&c->h_flag, 64, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&c->h_loss_ring, 64 * sizeof(float), cudaHostAllocDefault) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->copy_s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_copied[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_copied[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_free[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_free[1], cudaEventDisableTiming) != cudaSuccess) {
         delete c;
         return MTX_ERR_CUDA;
     }
@@ -1214,6 +1232,49 @@ mtx_status mtx_train_step_host(mtx_ctx *c, const float *X_host, const int32_t *y
     CK(cudaMemcpyAsync(c->stage_y, y_host, (size_t)c->b * 4, cudaMemcpyHostToDevice, s));
     if ((st = run_step(c, s, true))) return st;
     return sync_loss(c, s, host_loss);
+}
+
+mtx_status mtx_train_step_host_async(mtx_ctx *c, const float *X_host, const int32_t *y_host, void *stream) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (c->state != mtx_ctx::S_READY && c->state != mtx_ctx::S_BCAST)
+        return fail(c, MTX_ERR_STATE, "train_step_host_async needs bcast_params");
+    if (!X_host || !y_host) return fail(c, MTX_ERR_INVALID_ARG, "null host buffer");
+    cudaStream_t s = pick(c, stream);
+    if (c->n_data == 0) c->n_data = c->B;  // window advance is unused on the staged path
+    const int k = c->land_next;
+    c->land_next ^= 1;
+    const size_t xb = (size_t)c->b * c->d0 * 4, yb = (size_t)c->b * 4;
+    // copy stream: landing buffer k is free once the step that consumed it has copied it out
+    CK(cudaStreamWaitEvent(c->copy_s, c->ev_free[k], 0));
+    CK(cudaMemcpyAsync(c->land_x[k], X_host, xb, cudaMemcpyHostToDevice, c->copy_s));
+    CK(cudaMemcpyAsync(c->land_y[k], y_host, yb, cudaMemcpyHostToDevice, c->copy_s));
+    CK(cudaEventRecord(c->ev_copied[k], c->copy_s));
+    // compute stream: move the rows into the step's staging buffer, release the landing buffer, step
+    CK(cudaStreamWaitEvent(s, c->ev_copied[k], 0));
+    CK(cudaMemcpyAsync(c->stage_x, c->land_x[k], xb, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->stage_y, c->land_y[k], yb, cudaMemcpyDeviceToDevice, s));
+    CK(cudaEventRecord(c->ev_free[k], s));
+    if ((st = run_step(c, s, true))) return st;
+    // the step's result to host memory, every step (read by mtx_sync)
+    CK(cudaMemcpyAsync(c->h_loss_ring + (c->async_steps & 63), c->grads + c->N_pad + (c->fused ? 1 : 0), sizeof(float),
+                       cudaMemcpyDeviceToHost, s));
+    c->async_steps++;
+    return MTX_OK;
+}
+
+mtx_status mtx_sync(mtx_ctx *c, float *host_loss, void *stream) {
+    mtx_status st = live(c);
+    if (st) return st;
+    cudaStream_t s = pick(c, stream);
+    CK(cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(c->copy_s));
+    if (c->async_steps > 0) c->last_loss = (float)((double)c->h_loss_ring[(c->async_steps - 1) & 63] / (double)c->B);
+    if (host_loss) *host_loss = c->last_loss;
+    if (c->h_flag[0] & 2) return fail(c, MTX_ERR_NCCL, "peer barrier timeout (a rank did not reach the step)");
+    if (c->h_flag[0]) return fail(c, MTX_ERR_NUMERIC, "non-finite averaged gradient");
+    return MTX_OK;
 }
 
 mtx_status mtx_allreduce_avg(mtx_ctx *c, float *grad, float *param, float *velocity, uint64_t count, float lr,
@@ -1427,6 +1488,12 @@ mtx_status mtx_finalize(mtx_ctx *c) {
     if (c->own) cudaStreamDestroy(c->own);
     if (c->comm_s) cudaStreamDestroy(c->comm_s);
     if (c->h_loss) cudaFreeHost(c->h_loss);
+    if (c->h_loss_ring) cudaFreeHost(c->h_loss_ring);
+    for (int i = 0; i < 2; i++) {
+        if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
+        if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
+    }
+    if (c->copy_s) cudaStreamDestroy(c->copy_s);
     if (c->h_flag) cudaFreeHost(c->h_flag);
     if (c->dbg_planes) cudaFree(c->dbg_planes);
     if (c->tc) tc_destroy(c->tc);

@@ -62,6 +62,8 @@ def _load():
         "mtx_batch_slice": [C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32, i64, i64],
         "mtx_train_step": [vp, C.c_int64, f, vp],
         "mtx_train_step_host": [vp, vp, vp, f, vp],
+        "mtx_train_step_host_async": [vp, vp, vp, vp],
+        "mtx_sync": [vp, f, vp],
         "mtx_allreduce_avg": [vp, vp, vp, vp, C.c_uint64, C.c_float, C.c_float, C.c_int32, vp],
         "mtx_get_buffer": [vp, C.c_int32, f, C.c_uint64],
         "mtx_set_buffer": [vp, C.c_int32, f, C.c_uint64],
@@ -170,6 +172,17 @@ def mtx_train_step_host(ctx, X_ptr: int, y_ptr: int, stream: int | None = None) 
     loss = C.c_float()
     _check(_lib.mtx_train_step_host(ctx, C.c_void_p(X_ptr), C.c_void_p(y_ptr), C.byref(loss), C.c_void_p(stream)),
            ctx, "mtx_train_step_host")
+    return loss.value
+
+
+def mtx_train_step_host_async(ctx, X_ptr: int, y_ptr: int, stream: int | None = None) -> None:
+    _check(_lib.mtx_train_step_host_async(ctx, C.c_void_p(X_ptr), C.c_void_p(y_ptr), C.c_void_p(stream)), ctx,
+           "mtx_train_step_host_async")
+
+
+def mtx_sync(ctx, stream: int | None = None) -> float:
+    loss = C.c_float()
+    _check(_lib.mtx_sync(ctx, C.byref(loss), C.c_void_p(stream)), ctx, "mtx_sync")
     return loss.value
 
 

@@ -283,6 +283,34 @@ def test_host_staged_step_matches_resident():
         r2.close()
 
 
+@pytest.mark.parametrize("precision", [p for p in PRECISIONS if p != P.MTX_TF32])
+def test_pipelined_host_steps_match_synchronous(precision):
+    """mtx_train_step_host_async (double-buffered landing, copy of step t+1 overlapping step t) gives the
+    bit-identical trajectory of mtx_train_step_host on the same rows, and mtx_sync reports its last loss."""
+    import torch
+    cfg = small_cfg("cfg2")
+    X, y = S.mnist_like(1, 4096)
+    r1, r2 = make(cfg, precision=precision), make(cfg, precision=precision)
+    try:
+        for r in (r1, r2):
+            r.bcast()
+        rows = []
+        for t in range(5):
+            (b0, b1), (n0, n1) = mtx.mtx_batch_slice(4096, 512, t, 0, 1)
+            idx = np.r_[b0:b0 + n0, b1:b1 + n1]
+            rows.append((torch.from_numpy(np.ascontiguousarray(X[idx])).pin_memory(),
+                         torch.from_numpy(np.ascontiguousarray(y[idx])).pin_memory()))
+        losses = [r1.step_host(Xr.numpy(), yr.numpy()) for Xr, yr in rows]
+        for Xr, yr in rows:
+            r2.step_host_async(Xr.numpy(), yr.numpy())
+        last = r2.sync_host()
+        assert last == losses[-1]
+        assert np.array_equal(r1.get().view(np.uint32), r2.get().view(np.uint32))
+    finally:
+        r1.close()
+        r2.close()
+
+
 def test_state_machine_and_errors():
     cfg = small_cfg("cfg1", B=64)
     r = make(cfg)
