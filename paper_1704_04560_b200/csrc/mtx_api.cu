@@ -920,6 +920,23 @@ mtx_status sync_loss(mtx_ctx *c, cudaStream_t s, float *host_loss) {
     return MTX_OK;
 }
 
+// MTX_REDUCE_FUSED keeps velocity and the reduced gradient sharded: rank q's copy is authoritative
+// only on its owned slice S_q (p2p_fused.cu).  Pull every peer's slices into the local buffers so a
+// diagnostic read sees the full state.  Call after a synchronisation: the step's second peer barrier
+// guarantees every owner finished writing.
+mtx_status assemble_shards(mtx_ctx *c) {
+    if (!c->fused || c->world <= 1) return MTX_OK;
+    const int64_t n4 = c->N_pad / 4;
+    for (int q = 0; q < c->world; q++) {
+        if (q == c->rank) continue;
+        const int64_t lo = 4 * (n4 * q / c->world), hi = 4 * (n4 * (q + 1) / c->world);
+        CK(cudaMemcpyAsync(c->vel + lo, c->pp.v[q] + lo, 4 * (hi - lo), cudaMemcpyDeviceToDevice, c->own));
+        CK(cudaMemcpyAsync(c->grads + lo, c->pp.G[q] + lo, 4 * (hi - lo), cudaMemcpyDeviceToDevice, c->own));
+    }
+    CK(cudaStreamSynchronize(c->own));
+    return MTX_OK;
+}
+
 mtx_status check_flag(mtx_ctx *c, cudaStream_t s) {
     if (!c->flag) return MTX_OK;
     CK(cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1320,6 +1337,7 @@ mtx_status mtx_get_buffer(mtx_ctx *c, int32_t which, float *host_out, uint64_t c
                : which == MTX_BUF_GRADS ? c->grads : nullptr;
     if (!src) return fail(c, MTX_ERR_INVALID_ARG, "buffer id %d", which);
     CK(cudaDeviceSynchronize());
+    if (which != MTX_BUF_PARAMS && (st = assemble_shards(c))) return st;
     for (const Layer &L : c->layers)
         CK(cudaMemcpy(host_out + L.log_off, src + L.pad_off, 4 * L.size(), cudaMemcpyDeviceToHost));
     return check_flag(c, c->own);
@@ -1357,6 +1375,7 @@ mtx_status mtx_param_digest(mtx_ctx *c, uint64_t *out) {
     if (st) return st;
     if (c->state == mtx_ctx::S_INIT || !out) return fail(c, MTX_ERR_STATE, "no workspace");
     CK(cudaDeviceSynchronize());
+    if ((st = assemble_shards(c))) return st;
     CK(cudaMemsetAsync(c->dig, 0, 8, c->own));
     for (const Layer &L : c->layers) {
         CK(digest(c->params + L.pad_off, L.size(), (uint64_t)L.log_off, c->dig, c->own));

@@ -7,7 +7,8 @@
 //   fused_avg_update -- rank r owns slice S_r of the flat buffer: it loads g_0..g_{P-1} on S_r
 //                     (local + NVLink loads), folds them in ascending rank order (the oracle's
 //                     left fold, reading A2), ḡ = G·fl(1/P), v = fma(mu,v,ḡ), w = fma(-lr,v,w),
-//                     and stores w, v, G to its own buffers and to every peer (NVLink stores)
+//                     stores w to its own buffer and to every peer (NVLink stores) and keeps v and
+//                     G on S_r locally (the owner is the only reader of its optimizer-state shard)
 //   peer_barrier   -- "my slice is published"; afterwards every replica holds identical w, v, G
 // Each element is computed by exactly one rank, so replicas are bit-identical, and the sum is
 // bit-exact with MTX_REDUCE_ORDERED and with the oracle's f32 fold of the same g_r.
@@ -95,12 +96,13 @@ __global__ void __launch_bounds__(256) fused_avg_update_kernel(PeerPtrs pp, int 
             }
         }
 #pragma unroll
-        for (int q = 0; q < 8; q++)
-            if (q < P) {  // publish the owner's results to every replica (local store for q == rank)
-                __stcg((float4 *)pp.w[q] + i, w);
-                if (HAS_V) __stcg((float4 *)pp.v[q] + i, v);
-                __stcg((float4 *)pp.G[q] + i, G);
-            }
+        for (int q = 0; q < 8; q++)  // the updated weights go to every replica (local store for q == rank)
+            if (q < P) __stcg((float4 *)pp.w[q] + i, w);
+        // velocity and the reduced gradient stay with their owner (sharded optimizer state, ZeRO-1
+        // style): only the owner reads them in the next step; mtx_get_buffer / mtx_param_digest
+        // assemble the full buffers from the peers' mapped workspaces on demand
+        if (HAS_V) __stcg((float4 *)pp.v[rank] + i, v);
+        __stcg((float4 *)pp.G[rank] + i, G);
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
