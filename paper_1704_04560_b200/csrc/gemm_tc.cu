@@ -40,10 +40,7 @@ struct SmemLayout {
     static constexpr int THREADS = 384;
     // k-blocks accumulated in TMEM before the epilogue warps promote the partial into fp32
     // registers (the tensor core's internal accumulation truncates)
-#ifndef MTX_CHUNK3
-#define MTX_CHUNK3 4
-#endif
-    static constexpr int CHUNK = SPLIT ? MTX_CHUNK3 : 8;
+    static constexpr int CHUNK = SPLIT ? 4 : 8;
     static constexpr uint32_t A_BYTES = BM * BK * 4;
     // PAIR (cta_group::2): the CTA pair computes a 256 x BN tile; each CTA holds its 128 rows of A and
     // half of B's BN columns (the MMA reads both halves; measured by tools/tc_pair_probe.cu)
