@@ -962,7 +962,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
         e = splitk_reduce(g.partial, splits, M, N, g.C, g.ldc, s, h, g.epi, g.bias, g.mask, g.ldm, g.C_hi, g.C_lo);
         if (e != cudaSuccess) return e;
     }
-    if (g.aug)  // bias gradient row: db[n] = sum_k B[k][n]  (the ones row of the augmented A)
+    if (g.aug && !g.colsum_external)  // bias gradient row: db[n] = sum_k B[k][n]  (the ones row of augmented A)
         e = colsum(g.B, K, N, g.ldb, g.C + (int64_t)M * g.ldc, g.partial, g.partial_cap, g.counters + 256, s, h);
     return e;
 }

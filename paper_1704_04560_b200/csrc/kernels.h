@@ -19,6 +19,7 @@ enum Epi : int { EPI_STORE = 0, EPI_BIAS_RELU = 1, EPI_BIAS = 2, EPI_MASK = 3 };
 struct GemmDesc {
     int M = 0, N = 0, K = 0;
     bool ta = false, tb = false, aug = false;
+    bool colsum_external = false;  // aug on the tensor-core engine: the caller launches the bias column sum
     int epi = EPI_STORE;
     const float *A = nullptr;
     int64_t lda = 0;

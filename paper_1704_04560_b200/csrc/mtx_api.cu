@@ -138,10 +138,11 @@ struct mtx_ctx {
     unsigned *counters = nullptr;  // split-K / colsum / narrow-wgrad tickets, COUNTERS_PER_LANE per lane
     // MLP backward: every weight gradient but the first layer's runs on a side stream ("lane") so
     // it overlaps the dgrad chain; each lane owns a split-K partial region and its tickets
-    static constexpr int LANES = 3;
+    // lanes 1-2: weight gradients, lane 3: bias column sums (they run beside their wgrad GEMM)
+    static constexpr int LANES = 4, COLSUM_LANE = 3;
     int lanes = 1;
-    cudaStream_t side[LANES - 1] = {nullptr, nullptr};
-    cudaEvent_t ev_lane[LANES] = {nullptr, nullptr, nullptr};
+    cudaStream_t side[LANES - 1] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev_lane[LANES] = {nullptr, nullptr, nullptr, nullptr};
     std::vector<float *> dzs;  // MLP: dZ_l [b][d_l] for l = 1 .. L-1 (one buffer per layer)
     // mtx_debug_gemm engine 2/3: grow-only scratch planes and the operands they were split from
     float *dbg_planes = nullptr;
@@ -497,11 +498,12 @@ struct Runner {
         CK(cudaEventRecord(c->ev_lane[0], s));
         CK(cudaStreamWaitEvent(c->side[ln - 1], c->ev_lane[0], 0));
         const cudaStream_t keep = s;
+        const int keep_lane = lane;
         s = c->side[ln - 1];
         lane = ln;
         const mtx_status st = fn();
         s = keep;
-        lane = 0;
+        lane = keep_lane;
         dirty |= 1u << ln;
         used |= 1u << ln;
         return st;
@@ -546,6 +548,19 @@ struct Runner {
             if (plane_of(c, g.C, &ch, &cl)) { g.C_hi = (float *)ch; g.C_lo = (float *)cl; }
         }
         if (c->opt.precision != MTX_FP32 && c->tc && tc_supports(c->tc, g)) {
+            if (g.aug && c->lanes > mtx_ctx::COLSUM_LANE && !c->hook.enabled) {
+                // the bias row (column sums of B = dZ) runs on its own lane beside the GEMM
+                const GemmDesc gc = g;
+                mtx_status cs = on_lane(mtx_ctx::COLSUM_LANE, [&] {
+                    const int Mw = gc.M - 1;
+                    const cudaError_t ec = colsum(gc.B, gc.K, gc.N, gc.ldb, gc.C + (int64_t)Mw * gc.ldc, part(),
+                                                  c->partial_floats, ctrs() + 256, s, h);
+                    if (ec != cudaSuccess) return fail(c, MTX_ERR_CUDA, "colsum: %s", cudaGetErrorString(ec));
+                    return MTX_OK;
+                });
+                if (cs) return cs;
+                g.colsum_external = true;
+            }
             e = tc_gemm(c->tc, g, s, h);
         } else {
             e = gemm_simt(g, s, h);
@@ -634,7 +649,7 @@ struct Runner {
             const RowSel arow = l == 1 ? xrow() : RowSel{nullptr, 0};
             if (l > 1) {
                 st = on_lane(next_lane, [&] { return wgrad(l - 1, Aprev, arow, dZ); });
-                next_lane = next_lane % (c->lanes - 1 > 0 ? c->lanes - 1 : 1) + 1;
+                next_lane = next_lane == 1 ? 2 : 1;  // the two weight-gradient lanes
             } else {
                 st = wgrad(l - 1, Aprev, arow, dZ);
             }
