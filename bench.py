@@ -119,7 +119,7 @@ def kernel_work(name: str):
     if kind.startswith("conv_") or kind == "pool_relu_bwd":
         return None
     if kind == "avg_update":
-        return "byte", (20 if a["v"] else 12) * a["n"], "hbm"
+        return "byte", ((20 if a["v"] else 12) + (8 if a.get("planes") else 0)) * a["n"], "hbm"
     if kind == "head_softmax_xent":  # read A rows, write dZ_{L-1} (and dZ_L, loss)
         return "byte", 4 * a["rows"] * (a["d"] * (1 + a["dgrad"]) + a["C"] + 1), "hbm"
     if kind == "splitk_reduce":

@@ -95,9 +95,11 @@ cudaError_t reduce_sum(const float *v, int n, float *out, cudaStream_t s, Launch
 // K6: gbar = G * invP; v = fma(mu, v, gbar); w = fma(-lr, v, w) over n floats
 // (n % 4 == 0, 16-byte aligned).  v == nullptr: mu must be 0 and w = fma(-lr, gbar, w).
 // flag |= 1 on a non-finite gbar.  If win != nullptr, thread 0 advances the
-// window start: *win = (*win + B) mod n_data.
+// window start: *win = (*win + B) mod n_data.  whi / wlo (nullable): also write the 3xTF32 hi/lo
+// planes of the updated w (rne_tf32 split, as split_planes).
 cudaError_t avg_update(float *G, float *w, float *v, int64_t n, float invP, float lr, float mu, int *flag,
-                       int64_t *win, int64_t B, int64_t n_data, cudaStream_t s, LaunchHook *h);
+                       int64_t *win, int64_t B, int64_t n_data, cudaStream_t s, LaunchHook *h, float *whi = nullptr,
+                       float *wlo = nullptr);
 
 // Ordered reduce (test mode): G[e] = ((g_0[e] + g_1[e]) + ...) + g_{P-1}[e], g_r at gathered + r*stride.
 cudaError_t ordered_fold(const float *gathered, int P, int64_t stride, int64_t n, float *G, cudaStream_t s,

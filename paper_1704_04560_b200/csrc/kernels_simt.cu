@@ -737,7 +737,8 @@ template <bool HAS_V>
 __global__ void __launch_bounds__(UPD_T) avg_update_kernel(const float4 *__restrict__ G, float4 *__restrict__ w,
                                                          float4 *__restrict__ v, int64_t n4, float invP, float lr,
                                                          float mu, int *flag, int64_t *win, int64_t B,
-                                                         int64_t n_data, int tail) {
+                                                         int64_t n_data, int tail, float4 *__restrict__ whi,
+                                                         float4 *__restrict__ wlo) {
     pdl_wait();
     bool bad = false;
     const int64_t stride = (int64_t)gridDim.x * UPD_T * UPD_U;
@@ -770,6 +771,13 @@ __global__ void __launch_bounds__(UPD_T) avg_update_kernel(const float4 *__restr
             }
             __stcs(w + i, wv[u]);
             if (HAS_V) __stcs(v + i, vv[u]);
+            if (whi) {  // 3xTF32: the next step's hi/lo planes of the updated weights
+                float hi[4], lo[4];
+#pragma unroll
+                for (int c = 0; c < 4; c++) split_tf32(pw[c], hi[c], lo[c]);
+                whi[i] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                wlo[i] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+            }
         }
     }
     if (blockIdx.x == 0 && threadIdx.x < tail) {  // the n % 4 scalar tail
@@ -783,6 +791,7 @@ __global__ void __launch_bounds__(UPD_T) avg_update_kernel(const float4 *__restr
         } else {
             ws[i] = __fmaf_rn(-lr, gb, ws[i]);
         }
+        if (whi) split_tf32(ws[i], ((float *)whi)[i], ((float *)wlo)[i]);
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0 && flag) atomicOr(flag, 1);
     if (win && blockIdx.x == 0 && threadIdx.x == 0) *win = (*win + B) % n_data;
@@ -790,20 +799,21 @@ __global__ void __launch_bounds__(UPD_T) avg_update_kernel(const float4 *__restr
 }  // namespace
 
 cudaError_t avg_update(float *G, float *w, float *v, int64_t n, float invP, float lr, float mu, int *flag,
-                       int64_t *win, int64_t B, int64_t n_data, cudaStream_t s, LaunchHook *h) {
+                       int64_t *win, int64_t B, int64_t n_data, cudaStream_t s, LaunchHook *h, float *whi,
+                       float *wlo) {
     int64_t n4 = n / 4;
     int tail = (int)(n - 4 * n4);
     int64_t need = (n4 + UPD_T * UPD_U - 1) / (UPD_T * UPD_U);
     unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, 148 * 8));
     char name[64];
-    snprintf(name, sizeof name, "avg_update[n=%lld,v=%d]", (long long)n, v ? 1 : 0);
+    snprintf(name, sizeof name, "avg_update[n=%lld,v=%d,planes=%d]", (long long)n, v ? 1 : 0, whi ? 1 : 0);
     if (h) h->before(name, s);
     if (v)
         launch_pdl(avg_update_kernel<true>, dim3(blocks), dim3(UPD_T), 0, s, (const float4 *)G, (float4 *)w, (float4 *)v,
-                   n4, invP, lr, mu, flag, win, B, n_data, tail);
+                   n4, invP, lr, mu, flag, win, B, n_data, tail, (float4 *)whi, (float4 *)wlo);
     else
         launch_pdl(avg_update_kernel<false>, dim3(blocks), dim3(UPD_T), 0, s, (const float4 *)G, (float4 *)w,
-                   (float4 *)nullptr, n4, invP, lr, mu, flag, win, B, n_data, tail);
+                   (float4 *)nullptr, n4, invP, lr, mu, flag, win, B, n_data, tail, (float4 *)whi, (float4 *)wlo);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }

@@ -725,8 +725,10 @@ struct Runner {
         int64_t *win = (last && !staged) ? c->win : nullptr;
         if (c->world == 1) {
             if (mtx_status st = grads_ready(s)) return st;
+            // 3xTF32: the update also writes the next step's weight planes (no split at step start)
+            float *whi = c->params_hi ? c->params_hi + bkt.lo : nullptr, *wlo = c->params_lo ? c->params_lo + bkt.lo : nullptr;
             cudaError_t e = avg_update(c->grads + bkt.lo, c->params + bkt.lo, vel_or_null(bkt.lo), upd_hi - bkt.lo,
-                                       invP, c->opt.lr, c->opt.momentum, c->flag, win, c->B, c->n_data, s, h);
+                                       invP, c->opt.lr, c->opt.momentum, c->flag, win, c->B, c->n_data, s, h, whi, wlo);
             if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "update: %s", cudaGetErrorString(e));
             return MTX_OK;
         }
@@ -776,7 +778,8 @@ struct Runner {
             CK(cudaStreamWaitEvent(c->comm_s, c->ev_fork, 0));
         }
         if (c->params_hi) {  // 3xTF32: planes of this step's parameters (and of a staged batch)
-            CK(split_planes(c->params, 1, c->N_pad, c->N_pad, c->params_hi, c->params_lo, s, h));
+            // P = 1: the previous update (or the last external parameter change) already wrote them
+            if (c->world > 1) CK(split_planes(c->params, 1, c->N_pad, c->N_pad, c->params_hi, c->params_lo, s, h));
             if (staged && c->stage_hi && c->d0 % 4 == 0)
                 CK(split_planes(c->stage_x, c->b, c->d0, c->d0, c->stage_hi, c->stage_lo, s, h));
         }
@@ -949,6 +952,14 @@ mtx_status assemble_shards(mtx_ctx *c) {
         CK(cudaMemcpyAsync(c->grads + lo, c->pp.G[q] + lo, 4 * (hi - lo), cudaMemcpyDeviceToDevice, c->own));
     }
     CK(cudaStreamSynchronize(c->own));
+    return MTX_OK;
+}
+
+// 3xTF32: hi/lo planes of the parameters after a change outside the step (init, broadcast,
+// mtx_set_buffer); at P = 1 the step itself relies on them being current.
+mtx_status refresh_param_planes(mtx_ctx *c, cudaStream_t s) {
+    if (!c->params_hi) return MTX_OK;
+    CK(split_planes(c->params, 1, c->N_pad, c->N_pad, c->params_hi, c->params_lo, s, nullptr));
     return MTX_OK;
 }
 
@@ -1147,6 +1158,7 @@ mtx_status mtx_bind_workspace(mtx_ctx *c, void *dev_ptr, uint64_t bytes) {
             if (all[r] != mine) return fail(c, MTX_ERR_PROTOCOL, "rank %d model digest differs from rank %d", r, c->rank);
     }
     if (c->world > 1 && c->opt.reduce == MTX_REDUCE_FUSED && (st = map_peers(c))) return st;
+    if ((st = refresh_param_planes(c, c->own))) return st;
     CK(cudaStreamSynchronize(c->own));
     c->state = mtx_ctx::S_BOUND;
     return MTX_OK;
@@ -1160,6 +1172,7 @@ mtx_status mtx_bcast_params(mtx_ctx *c, int32_t root, void *stream) {
     cudaStream_t s = pick(c, stream);
     if (c->world > 1) NK(ncclBroadcast(c->params, c->params, c->N_pad, ncclFloat, root, c->comm, s));
     CK(cudaMemsetAsync(c->vel, 0, 4 * c->N_pad, s));
+    if ((st = refresh_param_planes(c, s))) return st;
     if (c->state == mtx_ctx::S_BOUND) c->state = mtx_ctx::S_BCAST;
     return MTX_OK;
 }
@@ -1370,6 +1383,10 @@ mtx_status mtx_set_buffer(mtx_ctx *c, int32_t which, const float *host_in, uint6
     CK(cudaDeviceSynchronize());
     for (const Layer &L : c->layers)
         CK(cudaMemcpy(dst + L.pad_off, host_in + L.log_off, 4 * L.size(), cudaMemcpyHostToDevice));
+    if (which == MTX_BUF_PARAMS) {
+        if ((st = refresh_param_planes(c, c->own))) return st;
+        CK(cudaStreamSynchronize(c->own));
+    }
     return MTX_OK;
 }
 
