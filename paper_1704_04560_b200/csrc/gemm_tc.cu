@@ -100,9 +100,19 @@ __device__ __forceinline__ void unit_of(const TcParams &p, int t, int tiles_mn, 
     }
 }
 
+// ReLU-mask values mask[m][n..n+3] (dgrad epilogue): loaded ahead of the stores they gate, so a
+// warp's mask loads are in flight together instead of one HBM round trip per store.
+__device__ __forceinline__ float4 load_mask(const TcParams &p, int m, int n) {
+    const float *mk = p.mask + (int64_t)m * p.ldm + n;
+    if (n + 3 < p.N) return __ldg((const float4 *)mk);
+    float mv[4];
+    for (int e = 0; e < 4; e++) mv[e] = n + e < p.N ? mk[e] : 0.f;
+    return make_float4(mv[0], mv[1], mv[2], mv[3]);
+}
+
 // The fused epilogue on 4 consecutive outputs C[m][n..n+3] (coalesced across a warp): bias (+ReLU)
-// or ReLU mask, the fp32 store and, for a 3xTF32 consumer, the hi/lo planes.
-__device__ __forceinline__ void epi_store(const TcParams &p, int m, int n, float4 sv) {
+// or ReLU mask (mkv, from load_mask), the fp32 store and, for a 3xTF32 consumer, the hi/lo planes.
+__device__ __forceinline__ void epi_store(const TcParams &p, int m, int n, float4 sv, float4 mkv) {
     const bool vec4 = n + 3 < p.N;
     float o[4] = {sv.x, sv.y, sv.z, sv.w};
     if (p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) {
@@ -113,14 +123,7 @@ __device__ __forceinline__ void epi_store(const TcParams &p, int m, int n, float
                 if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e], 0.f);
             }
     } else if (p.epi == EPI_MASK) {
-        const float *mk = p.mask + (int64_t)m * p.ldm + n;
-        float mv[4];
-        if (vec4) {
-            const float4 t4 = __ldg((const float4 *)mk);
-            mv[0] = t4.x; mv[1] = t4.y; mv[2] = t4.z; mv[3] = t4.w;
-        } else {
-            for (int e = 0; e < 4; e++) mv[e] = n + e < p.N ? mk[e] : 0.f;
-        }
+        const float mv[4] = {mkv.x, mkv.y, mkv.z, mkv.w};
 #pragma unroll
         for (int e = 0; e < 4; e++)
             if (!(mv[e] > 0.f)) o[e] = 0.f;
@@ -384,7 +387,7 @@ __device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base) {
             if (u < S) {
                 sum.x += v[u].x; sum.y += v[u].y; sum.z += v[u].z; sum.w += v[u].w;
             }
-        epi_store(p, m, n, sum);
+        epi_store(p, m, n, sum, p.epi == EPI_MASK ? load_mask(p, m, n) : make_float4(0.f, 0.f, 0.f, 0.f));
     }
 }
 
@@ -633,22 +636,36 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                                     acc[SW * c + 4 * j + 3]);
                 __syncwarp();
                 const int n = n0 + SW * c + 4 * jj;
-#pragma unroll 4
-                for (int it = 0; it < 32 / RPI; it++) {
-                    const int r = it * RPI + rl;
-                    const int m = m0 + 32 * q + r;
-                    const float4 sv = *(const float4 *)(stg + r * SW + 4 * swz(r, jj));
-                    if (m >= p.M || n >= p.N || (p.dbg & 1)) continue;
-                    if (p.splits > 1) {  // split-K partial (folded with the epilogue by splitk_reduce)
-                        float *dst = p.partial + ((int64_t)z * p.M + m) * p.N + n;
-                        if (n + 3 < p.N) *(float4 *)dst = sv;
-                        else {
-                            const float o[4] = {sv.x, sv.y, sv.z, sv.w};
-                            for (int e = 0; e < 4 && n + e < p.N; e++) dst[e] = o[e];
-                        }
-                        continue;
+                constexpr int ITS = 32 / RPI;  // row groups of the sub-tile
+#pragma unroll
+                for (int it0 = 0; it0 < ITS; it0 += 4) {
+                    float4 mk[4];  // dgrad: the 4 groups' mask values, loads in flight together
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int m = m0 + 32 * q + (it0 + u) * RPI + rl;
+                        mk[u] = (p.epi == EPI_MASK && p.splits == 1 && it0 + u < ITS && m < p.M && n < p.N)
+                                    ? load_mask(p, m, n)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
-                    epi_store(p, m, n, sv);
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int it = it0 + u;
+                        if (it >= ITS) break;
+                        const int r = it * RPI + rl;
+                        const int m = m0 + 32 * q + r;
+                        const float4 sv = *(const float4 *)(stg + r * SW + 4 * swz(r, jj));
+                        if (m >= p.M || n >= p.N || (p.dbg & 1)) continue;
+                        if (p.splits > 1) {  // split-K partial (folded with the epilogue by splitk_reduce)
+                            float *dst = p.partial + ((int64_t)z * p.M + m) * p.N + n;
+                            if (n + 3 < p.N) *(float4 *)dst = sv;
+                            else {
+                                const float o[4] = {sv.x, sv.y, sv.z, sv.w};
+                                for (int e = 0; e < 4 && n + e < p.N; e++) dst[e] = o[e];
+                            }
+                            continue;
+                        }
+                        epi_store(p, m, n, sv, mk[u]);
+                    }
                 }
                 __syncwarp();
             }
