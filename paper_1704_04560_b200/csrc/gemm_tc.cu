@@ -112,21 +112,23 @@ __device__ __forceinline__ float4 load_mask(const TcParams &p, int m, int n) {
 
 // The fused epilogue on 4 consecutive outputs C[m][n..n+3] (coalesced across a warp): bias (+ReLU)
 // or ReLU mask (mkv, from load_mask), the fp32 store and, for a 3xTF32 consumer, the hi/lo planes.
+// MASK: compile-time dgrad variant (EPI_MASK); otherwise bias (+ReLU) or a plain store.
+template <bool MASK>
 __device__ __forceinline__ void epi_store(const TcParams &p, int m, int n, float4 sv, float4 mkv) {
     const bool vec4 = n + 3 < p.N;
     float o[4] = {sv.x, sv.y, sv.z, sv.w};
-    if (p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) {
+    if constexpr (MASK) {
+        const float mv[4] = {mkv.x, mkv.y, mkv.z, mkv.w};
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+            if (!(mv[e] > 0.f)) o[e] = 0.f;
+    } else if (p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) {
 #pragma unroll
         for (int e = 0; e < 4; e++)
             if (n + e < p.N) {
                 o[e] += __ldg(p.bias + n + e);
                 if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e], 0.f);
             }
-    } else if (p.epi == EPI_MASK) {
-        const float mv[4] = {mkv.x, mkv.y, mkv.z, mkv.w};
-#pragma unroll
-        for (int e = 0; e < 4; e++)
-            if (!(mv[e] > 0.f)) o[e] = 0.f;
     }
     const int64_t off = (int64_t)m * p.ldc + n;
     if (vec4) *(float4 *)(p.C + off) = make_float4(o[0], o[1], o[2], o[3]);
@@ -364,7 +366,7 @@ __device__ __noinline__ void splitk_fixup(const TcParams &p, int r, int m0) {
 // CTA z of the tile's cluster folds rows [z*BM/S, (z+1)*BM/S) of the S partial tiles, read from
 // every CTA's shared memory (DSMEM) in ascending split order, and stores them with the epilogue.
 // Out of line so its registers do not add to the epilogue's accumulator registers.
-template <int BN>
+template <int BN, bool MASK>
 __device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base) {
     int z, r;
     unit_of(p, blockIdx.x, p.tiles_m * p.tiles_n, z, r);
@@ -387,11 +389,11 @@ __device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base) {
             if (u < S) {
                 sum.x += v[u].x; sum.y += v[u].y; sum.z += v[u].z; sum.w += v[u].w;
             }
-        epi_store(p, m, n, sum, p.epi == EPI_MASK ? load_mask(p, m, n) : make_float4(0.f, 0.f, 0.f, 0.f));
+        epi_store<MASK>(p, m, n, sum, MASK ? load_mask(p, m, n) : make_float4(0.f, 0.f, 0.f, 0.f));
     }
 }
 
-template <int BN, bool SPLIT, bool PAIR>
+template <int BN, bool SPLIT, bool PAIR, bool MASK>
 __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
     using L = SmemLayout<BN, SPLIT, PAIR>;
     constexpr int STAGES = L::STAGES;
@@ -637,18 +639,19 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                 __syncwarp();
                 const int n = n0 + SW * c + 4 * jj;
                 constexpr int ITS = 32 / RPI;  // row groups of the sub-tile
+                constexpr int G4 = MASK ? 4 : 1;  // dgrad: 4 groups' mask loads in flight together
 #pragma unroll
-                for (int it0 = 0; it0 < ITS; it0 += 4) {
-                    float4 mk[4];  // dgrad: the 4 groups' mask values, loads in flight together
+                for (int it0 = 0; it0 < ITS; it0 += G4) {
+                    float4 mk[G4];
 #pragma unroll
-                    for (int u = 0; u < 4; u++) {
+                    for (int u = 0; u < G4; u++) {
                         const int m = m0 + 32 * q + (it0 + u) * RPI + rl;
-                        mk[u] = (p.epi == EPI_MASK && p.splits == 1 && it0 + u < ITS && m < p.M && n < p.N)
+                        mk[u] = (MASK && p.splits == 1 && it0 + u < ITS && m < p.M && n < p.N)
                                     ? load_mask(p, m, n)
                                     : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; u++) {
+                    for (int u = 0; u < G4; u++) {
                         const int it = it0 + u;
                         if (it >= ITS) break;
                         const int r = it * RPI + rl;
@@ -664,7 +667,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                             }
                             continue;
                         }
-                        epi_store(p, m, n, sv, mk[u]);
+                        epi_store<MASK>(p, m, n, sv, mk[u]);
                     }
                 }
                 __syncwarp();
@@ -689,7 +692,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
         // [z*BM/S, (z+1)*BM/S) over the splits in ascending order (deterministic) and stores them
         // with the fused epilogue; the second barrier keeps every CTA's smem alive until read
         cluster_sync_all();
-        if (warp >= 4 && warp < 12) cluster_fold<BN>(p, smem_u32(smem));
+        if (warp >= 4 && warp < 12) cluster_fold<BN, MASK>(p, smem_u32(smem));
         cluster_sync_all();
     }
     tc_fence_before();
@@ -733,7 +736,7 @@ bool make_map(EncodeTiled enc, CUtensorMap *m, const float *ptr, int64_t rows, i
 struct TcGemm {
     EncodeTiled encode = nullptr;
     int sms = 148;
-    bool attr_set[16] = {};
+    bool attr_set[32] = {};
     // split-K fold inside the kernel by the tile's last CTA (MTX_TC_FIXUP=1).  Off: a one-SM fold of
     // splits x 64 KB is slower than the all-SM fold kernel on every measured shape.
     bool fixup = false;
@@ -823,12 +826,12 @@ bool tc_supports(TcGemm *t, const GemmDesc &g) {
     return true;
 }
 
-template <int BN, bool SPLIT, bool PAIR = false>
+template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false>
 static cudaError_t prepare(TcGemm *t) {
     using L = SmemLayout<BN, SPLIT, PAIR>;
-    const int slot = (SPLIT ? 1 : 0) + 2 * (BN == 128 ? 0 : BN == 64 ? 1 : 2) + (PAIR ? 8 : 0);
+    const int slot = (SPLIT ? 1 : 0) + 2 * (BN == 128 ? 0 : BN == 64 ? 1 : 2) + (PAIR ? 8 : 0) + (MASK ? 16 : 0);
     if (!t->attr_set[slot]) {
-        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT, PAIR>,
+        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT, PAIR, MASK>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
         if (e != cudaSuccess) return e;
         t->attr_set[slot] = true;
@@ -855,7 +858,7 @@ static int co_resident_clusters(TcGemm *t, int cs) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, (void *)tc_gemm_kernel<BN, SPLIT, false>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, (void *)tc_gemm_kernel<BN, SPLIT, false, false>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         n = -1;  // query failed: never use the cluster path for this variant
     }
@@ -863,13 +866,13 @@ static int co_resident_clusters(TcGemm *t, int cs) {
     return n;
 }
 
-template <int BN, bool SPLIT, bool PAIR = false>
+template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false>
 static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s) {
     using L = SmemLayout<BN, SPLIT, PAIR>;
-    cudaError_t e = prepare<BN, SPLIT, PAIR>(t);
+    cudaError_t e = prepare<BN, SPLIT, PAIR, MASK>(t);
     if (e != cudaSuccess) return e;
     if (!p.cluster && !PAIR)
-        return launch_pdl(tc_gemm_kernel<BN, SPLIT, PAIR>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
+        return launch_pdl(tc_gemm_kernel<BN, SPLIT, PAIR, MASK>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(L::THREADS);
@@ -884,7 +887,7 @@ static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s
     at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT, PAIR>, p);
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT, PAIR, MASK>, p);
 }
 
 template <int BN>
@@ -969,8 +972,13 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
              kind, M, N, K, splits, cluster ? 1 : 0, pair ? 1 : 0, BN);
     if (h) h->before(name, s);
     cudaError_t e;
+    const bool mask = g.epi == EPI_MASK;  // dgrad: the masked-epilogue instantiation (never paired)
     if (pair) e = g.tf32x3 ? launch<128, true, true>(t, p, grid, s) : launch<128, false, true>(t, p, grid, s);
-    else if (BN == 128) e = g.tf32x3 ? launch<128, true>(t, p, grid, s) : launch<128, false>(t, p, grid, s);
+    else if (mask) {
+        if (BN == 128) e = g.tf32x3 ? launch<128, true, false, true>(t, p, grid, s) : launch<128, false, false, true>(t, p, grid, s);
+        else if (BN == 64) e = g.tf32x3 ? launch<64, true, false, true>(t, p, grid, s) : launch<64, false, false, true>(t, p, grid, s);
+        else e = g.tf32x3 ? launch<32, true, false, true>(t, p, grid, s) : launch<32, false, false, true>(t, p, grid, s);
+    } else if (BN == 128) e = g.tf32x3 ? launch<128, true>(t, p, grid, s) : launch<128, false>(t, p, grid, s);
     else if (BN == 64) e = g.tf32x3 ? launch<64, true>(t, p, grid, s) : launch<64, false>(t, p, grid, s);
     else e = g.tf32x3 ? launch<32, true>(t, p, grid, s) : launch<32, false>(t, p, grid, s);
     if (h) h->after(name, s);
