@@ -74,6 +74,9 @@ cudaError_t split_planes(const float *x, int64_t rows, int64_t cols, int64_t ld,
 // Narrow weight gradient (N <= 16, e.g. the classifier layer): dWb[k][j] = sum_i A[i][k] dZ[i][j]
 // for k < K_in, plus (aug) the bias row dWb[K_in][j] = sum_i dZ[i][j].  Thread per k, rows split
 // over blocks, blocked fp32 sums, ascending fold.  A's row offset: arow (dataset operand).
+// out[j] = sum_{p ascending per lane, fixed shuffle tree} partial[p][j], j < n: deterministic fold of
+// per-block partials (one warp per output).
+cudaError_t fold_partials(const float *partial, int parts, int n, float *out, cudaStream_t s, LaunchHook *h);
 cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *dZ, int rows, int K_in, int N,
                          float *dWb, float *partial, int64_t partial_cap, unsigned *ticket, cudaStream_t s,
                          LaunchHook *h);

@@ -14,7 +14,7 @@
 //                then (i) accumulates the weight gradient: each thread owns 4 patch elements x CO
 //                channels over a fixed set of output positions, and (ii) writes the input gradient
 //                dX (full correlation with W) of the sample.  Per-CTA weight-gradient partials are
-//                folded by fold_parts in a fixed order (deterministic).
+//                folded by fold_partials in a fixed order (deterministic).
 #include <stdio.h>
 
 #include <algorithm>
@@ -329,20 +329,6 @@ __global__ void __launch_bounds__(CONV_T) conv_bwd_kernel(ConvGeom g, int rows, 
     for (int i = tid; i < E * g.co; i += blockDim.x) pb[i] = red[(i / g.co) * CO + i % g.co];
 }
 
-// out[j] = sum_p partial[p][j]: one warp per output, lane l sums p = l, l+32, ... ascending, then a
-// fixed xor-shuffle tree -- deterministic.
-__global__ void __launch_bounds__(256) fold_parts_kernel(const float *__restrict__ partial, int parts, int n,
-                                                       float *__restrict__ out) {
-    pdl_wait();
-    const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (j >= n) return;
-    float s = 0.f;
-    for (int p = lane; p < parts; p += 32) s += __ldg(partial + (int64_t)p * n + j);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[j] = s;
-}
-
 inline int co_pad(int co) { return co <= 8 ? 8 : co <= 16 ? 16 : 32; }
 
 cudaError_t set_smem(const void *fn, size_t smem) {
@@ -432,12 +418,7 @@ cudaError_t conv_bwd(const ConvGeom &g, int rows, const float *X, RowSel xrow, c
     }
     if (h) h->after(name, s);
     if (e != cudaSuccess) return e;
-    const int nout = E * g.co;
-    snprintf(name, sizeof name, "fold_parts[parts=%d,n=%d]", ctas, nout);
-    if (h) h->before(name, s);
-    e = launch_pdl(fold_parts_kernel, dim3(cdiv(nout, 8)), dim3(256), 0, s, (const float *)partial, ctas, nout, dWb);
-    if (h) h->after(name, s);
-    return e;
+    return fold_partials(partial, ctas, E * g.co, dWb, s, h);
 }
 
 }  // namespace mtx

@@ -264,29 +264,30 @@ cudaError_t split_planes(const float *x, int64_t rows, int64_t cols, int64_t ld,
 // ------------------------------------------------------------------ narrow weight gradient (N <= 16)
 namespace {
 constexpr int NW_T = 128, NW_ROWS = 32, NW_MAXN = 16;
+// NJ: output columns rounded up to 2/4/8/16 (the HIGGS head has 2: no 16-wide padding work)
+template <int NJ>
 __global__ void __launch_bounds__(NW_T) wgrad_narrow_kernel(const float *__restrict__ A, int64_t lda, RowSel arow,
                                                           const float *__restrict__ dZ, int rows, int K_in, int N,
-                                                          int rows_per, float *__restrict__ partial, unsigned *ticket,
-                                                          float *__restrict__ dWb) {
+                                                          int rows_per, float *__restrict__ partial) {
     pdl_wait();
-    __shared__ float sdz[NW_ROWS][NW_MAXN];
+    __shared__ float sdz[NW_ROWS][NJ];
     const int k = blockIdx.x * NW_T + threadIdx.x;
     const int r0 = blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
     const float *Ab = A + arow.row0() * lda;
-    float acc[NW_MAXN];
+    float acc[NJ];
 #pragma unroll
-    for (int j = 0; j < NW_MAXN; j++) acc[j] = 0.f;
+    for (int j = 0; j < NJ; j++) acc[j] = 0.f;
     for (int i0 = r0; i0 < r1; i0 += NW_ROWS) {
         const int nr = min(NW_ROWS, r1 - i0);
-        for (int e = threadIdx.x; e < NW_ROWS * NW_MAXN; e += NW_T) {
-            const int i = e / NW_MAXN, j = e % NW_MAXN;
+        for (int e = threadIdx.x; e < NW_ROWS * NJ; e += NW_T) {
+            const int i = e / NJ, j = e % NJ;
             sdz[i][j] = (i < nr && j < N) ? dZ[(int64_t)(i0 + i) * N + j] : 0.f;
         }
         __syncthreads();
         if (k <= K_in) {
-            float t[NW_MAXN];
+            float t[NJ];
 #pragma unroll
-            for (int j = 0; j < NW_MAXN; j++) t[j] = 0.f;
+            for (int j = 0; j < NJ; j++) t[j] = 0.f;
             for (int ib = 0; ib < nr; ib += 8) {
                 float a8[8];
 #pragma unroll
@@ -295,24 +296,48 @@ __global__ void __launch_bounds__(NW_T) wgrad_narrow_kernel(const float *__restr
 #pragma unroll
                 for (int u = 0; u < 8; u++)
 #pragma unroll
-                    for (int j = 0; j < NW_MAXN; j++) t[j] = __fmaf_rn(a8[u], sdz[ib + u][j], t[j]);
+                    for (int j = 0; j < NJ; j++) t[j] = __fmaf_rn(a8[u], sdz[ib + u][j], t[j]);
             }
 #pragma unroll
-            for (int j = 0; j < NW_MAXN; j++) acc[j] = __fadd_rn(acc[j], t[j]);  // blocked summation
+            for (int j = 0; j < NJ; j++) acc[j] = __fadd_rn(acc[j], t[j]);  // blocked summation
         }
         __syncthreads();
     }
     if (k <= K_in) {
 #pragma unroll
-        for (int j = 0; j < NW_MAXN; j++)
+        for (int j = 0; j < NJ; j++)
             if (j < N) partial[((int64_t)blockIdx.y * (K_in + 1) + k) * N + j] = acc[j];
     }
 }
+
+// out[j] = sum_p partial[p][j]: one warp per output, lane l sums p = l, l+32, ... ascending, then a
+// fixed xor-shuffle tree -- deterministic.
+__global__ void __launch_bounds__(256) fold_partials_kernel(const float *__restrict__ partial, int parts, int n,
+                                                          float *__restrict__ out) {
+    pdl_wait();
+    const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (j >= n) return;
+    float s = 0.f;
+    for (int p = lane; p < parts; p += 32) s += __ldg(partial + (int64_t)p * n + j);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[j] = s;
+}
 }  // namespace
+
+cudaError_t fold_partials(const float *partial, int parts, int n, float *out, cudaStream_t s, LaunchHook *h) {
+    char name[64];
+    snprintf(name, sizeof name, "fold_partials[parts=%d,n=%d]", parts, n);
+    if (h) h->before(name, s);
+    const cudaError_t e = launch_pdl(fold_partials_kernel, dim3(cdiv(n, 8)), dim3(256), 0, s, partial, parts, n, out);
+    if (h) h->after(name, s);
+    return e;
+}
 
 cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *dZ, int rows, int K_in, int N,
                          float *dWb, float *partial, int64_t partial_cap, unsigned *ticket, cudaStream_t s,
                          LaunchHook *h) {
+    (void)ticket;
     if (N > NW_MAXN) return cudaErrorInvalidValue;
     const int kb = (K_in + 1 + NW_T - 1) / NW_T;
     int splits = std::max(1, std::min((4 * 148 + kb - 1) / kb, (rows + 31) / 32));
@@ -322,12 +347,15 @@ cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *
     char name[80];
     snprintf(name, sizeof name, "wgrad_narrow[M=%d,N=%d,K=%d,splits=%d]", K_in + 1, N, rows, splits);
     if (h) h->before(name, s);
-    launch_pdl(wgrad_narrow_kernel, dim3(kb, splits), dim3(NW_T), 0, s, A, lda, arow, dZ, rows, K_in, N, rows_per,
-               partial, ticket, dWb);
+    cudaError_t e;
+    const dim3 grid(kb, splits);
+    if (N <= 2) e = launch_pdl(wgrad_narrow_kernel<2>, grid, dim3(NW_T), 0, s, A, lda, arow, dZ, rows, K_in, N, rows_per, partial);
+    else if (N <= 4) e = launch_pdl(wgrad_narrow_kernel<4>, grid, dim3(NW_T), 0, s, A, lda, arow, dZ, rows, K_in, N, rows_per, partial);
+    else if (N <= 8) e = launch_pdl(wgrad_narrow_kernel<8>, grid, dim3(NW_T), 0, s, A, lda, arow, dZ, rows, K_in, N, rows_per, partial);
+    else e = launch_pdl(wgrad_narrow_kernel<16>, grid, dim3(NW_T), 0, s, A, lda, arow, dZ, rows, K_in, N, rows_per, partial);
     if (h) h->after(name, s);
-    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return splitk_reduce(partial, splits, K_in + 1, N, dWb, N, s, h);  // all-SM ascending fold
+    return fold_partials(partial, splits, (K_in + 1) * N, dWb, s, h);  // deterministic warp-per-output fold
 }
 
 // ------------------------------------------------------------------ column sums (bias gradients)
