@@ -82,7 +82,6 @@ struct TcParams {
     float *partial;
     const int64_t *a_win;  // dataset operand: sample-dimension offset read on the device
     int64_t a_base;
-    unsigned *counters;    // split-K: one arrival counter per output tile (zero between launches)
     int dbg;               // development only (MTX_TC_DBG): 1 skip epilogue stores, 2 skip TMA loads
     int cluster;           // 1: the splits of a tile form one thread-block cluster and are folded
                            // through distributed shared memory (no partial buffer, no fold launch)
@@ -318,54 +317,6 @@ __host__ __device__ constexpr uint32_t instr_desc(int M, int N, int a_mn, int b_
            ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// Split-K fixup run by the last CTA of a tile (MTX_TC_FIXUP=1): fold all splits in ascending order,
-// coalesced -- the 256 epilogue threads sweep the 128 x BN tile row by row, one float4 each.
-// Kept out of line so its registers do not add to the epilogue's accumulator registers.
-template <int BN>
-__device__ __noinline__ void splitk_fixup(const TcParams &p, int r, int m0) {
-    {   // last CTA of the tile: fold all splits in ascending order, coalesced -- the 256
-        // epilogue threads sweep the 128 x BN tile row by row, one float4 each
-        const int et = threadIdx.x - 128;
-        const int mt0 = m0, nt0 = (r % p.tiles_n) * BN;
-        for (int idx = et; idx < BM * (BN / 4); idx += 256) {
-            const int mm = mt0 + idx / (BN / 4), nn = nt0 + 4 * (idx % (BN / 4));
-            if (mm >= p.M || nn >= p.N) continue;
-            const bool vec4 = nn + 3 < p.N;
-            float o[4] = {0.f, 0.f, 0.f, 0.f};
-            for (int z0 = 0; z0 < p.splits; z0 += 4) {
-                float4 v[4];
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    if (z0 + u >= p.splits) break;
-                    const float *src = p.partial + ((int64_t)(z0 + u) * p.M + mm) * p.N + nn;
-                    if (vec4) v[u] = __ldcg((const float4 *)src);
-                    else v[u] = make_float4(__ldcg(src), nn + 1 < p.N ? __ldcg(src + 1) : 0.f,
-                                            nn + 2 < p.N ? __ldcg(src + 2) : 0.f, 0.f);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    if (z0 + u >= p.splits) break;
-                    o[0] += v[u].x; o[1] += v[u].y; o[2] += v[u].z; o[3] += v[u].w;
-                }
-            }
-#pragma unroll
-            for (int e = 0; e < 4; e++) {
-                if (nn + e >= p.N) break;
-                if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e] + p.bias[nn + e], 0.f);
-                else if (p.epi == EPI_BIAS) o[e] += p.bias[nn + e];
-                else if (p.epi == EPI_MASK && !(p.mask[(int64_t)mm * p.ldm + nn + e] > 0.f)) o[e] = 0.f;
-            }
-            float *dst = p.C + (int64_t)mm * p.ldc + nn;
-            if (vec4) *(float4 *)dst = make_float4(o[0], o[1], o[2], o[3]);
-            else for (int e = 0; e < 4 && nn + e < p.N; e++) dst[e] = o[e];
-        }
-    }
-}
-
-// Cluster split-K fold (run by the 256 epilogue threads of each CTA after the first cluster barrier):
-// CTA z of the tile's cluster folds rows [z*BM/S, (z+1)*BM/S) of the S partial tiles, read from
-// every CTA's shared memory (DSMEM) in ascending split order, and stores them with the epilogue.
-// Out of line so its registers do not add to the epilogue's accumulator registers.
 template <int BN, bool MASK>
 __device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base) {
     int z, r;
@@ -407,7 +358,6 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * STAGES, tfull0 = empty0 + 8 * STAGES,
                    tempty0 = tfull0 + 8 * NBUF;
     uint32_t *tmem_slot = (uint32_t *)(smem + L::BAR_OFF + 224);
-    volatile int *fix_flag = (volatile int *)(smem + L::BAR_OFF + 232);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t rank = 0;  // PAIR: rank in the CTA pair; rank 0 (the leader) issues the MMAs
     if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
@@ -672,18 +622,6 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                 }
                 __syncwarp();
             }
-            if (p.splits > 1 && p.counters) {
-                // in-kernel fixup (MTX_TC_FIXUP=1): the last CTA to arrive for the tile folds all
-                // partials in ascending split order and applies the epilogue (deterministic)
-                __threadfence();
-                asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps
-                if (threadIdx.x == 128) *fix_flag = atomicAdd(p.counters + r, 1u) == (unsigned)(p.splits - 1);
-                asm volatile("bar.sync 1, 256;" ::: "memory");
-                if (!*fix_flag) continue;
-                __threadfence();
-                splitk_fixup<BN>(p, r, m0);
-                if (threadIdx.x == 128) p.counters[r] = 0u;  // re-armed for the next launch
-            }
         }
     }
 #undef MTX_UNITS
@@ -737,9 +675,6 @@ struct TcGemm {
     EncodeTiled encode = nullptr;
     int sms = 148;
     bool attr_set[32] = {};
-    // split-K fold inside the kernel by the tile's last CTA (MTX_TC_FIXUP=1).  Off: a one-SM fold of
-    // splits x 64 KB is slower than the all-SM fold kernel on every measured shape.
-    bool fixup = false;
     // split-K folded through distributed shared memory (MTX_TC_CLUSTER=0 disables: global partials
     // + splitk_reduce launch)
     bool cluster = true;
@@ -796,7 +731,6 @@ TcGemm *tc_create(int device) {
         return nullptr;
     }
     t->encode = (EncodeTiled)fn;
-    if (const char *k = getenv("MTX_TC_FIXUP")) t->fixup = atoi(k) != 0;  // development A/B knob
     if (const char *k = getenv("MTX_TC_CLUSTER")) t->cluster = atoi(k) != 0;
     if (const char *k = getenv("MTX_TC_PAIR")) t->pair = atoi(k) != 0;
     cudaDeviceGetAttribute(&t->sms, cudaDevAttrMultiProcessorCount, device);
@@ -963,7 +897,6 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.C = g.C;
     p.ldc = g.ldc;
     p.partial = g.partial;
-    p.counters = (t->fixup && !g.C_hi && !cluster) ? g.counters : nullptr;
     const int total = tiles * splits;
     const int grid = cluster ? total : pair ? 2 * std::min(total, t->sms / 2) : std::min(total, t->sms);
     const char *kind = g.epi == EPI_MASK ? "dgrad" : (g.ta ? "wgrad" : "fwd");
@@ -983,7 +916,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     else e = g.tf32x3 ? launch<32, true>(t, p, grid, s) : launch<32, false>(t, p, grid, s);
     if (h) h->after(name, s);
     if (e != cudaSuccess) return e;
-    if (splits > 1 && !p.counters && !cluster) {  // fold with the epilogue in a separate kernel
+    if (splits > 1 && !cluster) {  // fold with the epilogue in a separate kernel
         e = splitk_reduce(g.partial, splits, M, N, g.C, g.ldc, s, h, g.epi, g.bias, g.mask, g.ldm, g.C_hi, g.C_lo);
         if (e != cudaSuccess) return e;
     }
