@@ -288,13 +288,16 @@ __global__ void __launch_bounds__(NW_T) wgrad_narrow_kernel(const float *__restr
             float t[NJ];
 #pragma unroll
             for (int j = 0; j < NJ; j++) t[j] = 0.f;
-            for (int ib = 0; ib < nr; ib += 8) {
-                float a8[8];
+            // rows in flight per thread: the whole staged chunk for narrow outputs (few accumulators),
+            // 8 otherwise -- the loads, not the FMAs, bound this kernel
+            constexpr int RB = NJ <= 4 ? NW_ROWS : 8;
+            for (int ib = 0; ib < nr; ib += RB) {
+                float a8[RB];
 #pragma unroll
-                for (int u = 0; u < 8; u++)  // k == K_in: the bias row (a = 1)
+                for (int u = 0; u < RB; u++)  // k == K_in: the bias row (a = 1)
                     a8[u] = (ib + u < nr) ? (k < K_in ? __ldg(Ab + (int64_t)(i0 + ib + u) * lda + k) : 1.f) : 0.f;
 #pragma unroll
-                for (int u = 0; u < 8; u++)
+                for (int u = 0; u < RB; u++)
 #pragma unroll
                     for (int j = 0; j < NJ; j++) t[j] = __fmaf_rn(a8[u], sdz[ib + u][j], t[j]);
             }
