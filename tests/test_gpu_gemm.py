@@ -31,6 +31,7 @@ SHAPES = [  # (M, N, K) incl. the step's shapes: cfg4 fwd/dgrad/wgrad, cfg2, K =
     (1024, 1024, 1024), (512, 512, 784), (8192, 1024, 28), (28, 1024, 2048), (300, 200, 100), (128, 64, 96),
     (1000, 384, 520), (1024, 640, 256), (64, 784, 512),  # tcgen05 N-tile 64 / 32 plans
     (4096, 1024, 256), (4000, 512, 200),  # CTA-pair (cta_group::2) 256 x 128 tiles, ragged M / K
+    (8192, 1024, 256), (8100, 640, 300),  # stream-K remainder (last round split into K-halves), ragged
 ]
 
 
@@ -86,7 +87,7 @@ def _tf32_trunc(x: np.ndarray) -> np.ndarray:
 @pytest.mark.skipif(not TC, reason="tcgen05 engine not built")
 @pytest.mark.parametrize("layout", [(0, 0, 1), (0, 1, 3), (1, 0, 0)])
 @pytest.mark.parametrize("shape", [(1024, 1024, 1024), (512, 512, 784), (1024, 640, 256), (8192, 1024, 28),
-                                   (4000, 512, 200)])
+                                   (4000, 512, 200), (8100, 640, 300)])
 def test_tf32_engine_matches_tf32_emulation(rep, layout, shape):
     """Engine 1 equals the TF32 contraction itself -- both operands truncated (A12), exact products, fp32
     accumulation -- far tighter than its 2e-3 gate against the exact product: the only residual is
