@@ -172,7 +172,9 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
     longest = max((kv for kv in timing.items() if kv[0].split("[")[0] == top_name), key=lambda kv: kv[1][0])[0]
     bn = re.search(r"bn=(\d+)", longest)
     bn = bn.group(1) if bn else "128"
-    ncu_kernel = {"gemm_tc3x": f"tc_gemm_kernel<{bn}, 1>", "gemm_tc": f"tc_gemm_kernel<{bn}, 0>",
+    pr = re.search(r"pair=(\d)", longest)
+    tpl = f"{bn}, {{}}, {pr.group(1) if pr else 0}, {1 if '_dgrad' in longest else 0}"  # <BN, 3x, PAIR, MASK>
+    ncu_kernel = {"gemm_tc3x": f"tc_gemm_kernel<{tpl.format(1)}>", "gemm_tc": f"tc_gemm_kernel<{tpl.format(0)}>",
                   "avg_update": "avg_update_kernel<1>", "head_softmax_xent": "head_kernel",
                   "colsum": "colsum_kernel", "splitk_reduce": "splitk_reduce_kernel", "conv_bwd": "conv_bwd_kernel",
                   "conv_fwd": "conv_fwd_kernel"}
