@@ -260,6 +260,27 @@ def test_full_size_cfg4_replicated_rows(precision):
     assert abs(loss - lsum / 64) <= 1e-5 * abs(lsum / 64)
 
 
+@pytest.mark.parametrize("precision", [p for p in PRECISIONS if p != P.MTX_TF32])
+def test_full_size_cfg3_replicated_rows(precision):
+    """Full cfg3 launch configuration (LeNet, B = 1024, the conv kernels' bench grid) on a dataset of
+    64 copies of 16 CIFAR-shaped images: the mean gradient over 1024 rows equals the oracle's over the
+    16 distinct images, and one momentum step lands on the oracle's weights."""
+    cfg = small_cfg("cfg3", n=1024)
+    X16, y16 = S.cifar_like(1, 16)
+    X = np.tile(X16, (64, 1, 1, 1))
+    y = np.tile(y16, 64)
+    net = oracle.Net.from_cfg(cfg)
+    start = oracle.init_params(net, 42)
+    (loss, G, w1), = _gpu_run(cfg, X, y, 1, precision, start=start)
+    g_ref, lsum = oracle.local_grad(net, start.astype(np.float64), X16, y16, 16, 0, 0, 1)
+    tab = oracle.tensor_table(net)
+    assert max(per_tensor_maxrel(G, g_ref, tab)) <= 1e-5
+    assert abs(loss - lsum / 16) <= 1e-5 * abs(lsum / 16)
+    w_ref = start.astype(np.float64).copy()
+    oracle.avg_update(g_ref, w_ref, np.zeros_like(w_ref), 1, cfg["lr"], cfg["mu"])
+    assert max(per_tensor_maxrel(w1, w_ref, tab)) <= 1e-5
+
+
 # ----------------------------------------------------------------------------- host-input path, state machine
 def test_host_staged_step_matches_resident():
     cfg = small_cfg("cfg2")
