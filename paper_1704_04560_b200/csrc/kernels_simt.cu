@@ -487,11 +487,12 @@ cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *
 // partial sums are combined with a fixed xor-shuffle tree.  W_L (d x C, <= 64 KB)
 // and b_L are staged in shared memory once per CTA.
 namespace {
-constexpr int HEAD_WARPS = 4;  // rows are latency chains: more, smaller CTAs
 
 // NV = float4 groups per lane (d <= 128 * NV): lane owns features 4*lane + 128*t .. +3, loaded as
 // float4 with all of the row's loads in flight before the FMAs.
-template <int NV, bool VEC, int HEAD_MAXC>
+// HEAD_WARPS: warps (rows in flight) per CTA -- 8 for small batches (cfg2: 64 CTAs), 2 for large ones
+// (cfg4: more CTAs share the weight staging); measured, DESIGN.md §9
+template <int NV, bool VEC, int HEAD_MAXC, int HEAD_WARPS>
 __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, int C, const float *__restrict__ A,
                                                              RowSel arow, const float *__restrict__ Wb,
                                                              const int32_t *__restrict__ labels, RowSel lrow,
@@ -678,16 +679,16 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
     }
 }
 
-template <int NV, bool VEC, int CM>
+template <int NV, bool VEC, int CM, int W>
 cudaError_t launch_head(unsigned blocks, size_t smem, cudaStream_t s, int rows, int d, int C, const float *A, RowSel arow,
                         const float *Wb, const int32_t *labels, RowSel lrow, float inv_b, float *dZL, float *dprev,
                         float *dp_hi, float *dp_lo, float *loss_rows, float *loss_part, unsigned *ticket,
                         float *loss_out) {
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(head_kernel<NV, VEC, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(head_kernel<NV, VEC, CM, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    return launch_pdl(head_kernel<NV, VEC, CM>, dim3(blocks), dim3(HEAD_WARPS * 32), smem, s, rows, d, C, A, arow, Wb,
+    return launch_pdl(head_kernel<NV, VEC, CM, W>, dim3(blocks), dim3(W * 32), smem, s, rows, d, C, A, arow, Wb,
                       labels, lrow, inv_b, dZL, dprev, dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out);
 }
 }  // namespace
@@ -699,18 +700,25 @@ cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, cons
     if (C > 16 || C < 1 || d > 1024) return cudaErrorInvalidValue;
     const size_t smem = sizeof(float) * (size_t)((d + 1 + 3) & ~3) * C;
     // enough rows per block that the block count stays <= 1024 (loss partial slots)
-    const unsigned blocks = std::min<unsigned>(cdiv(rows, HEAD_WARPS), 1024u);
+    const bool big = rows > 2048;
+    const unsigned blocks = std::min<unsigned>(cdiv(rows, big ? 2 : 8), 1024u);
     const bool vec = (d % 4 == 0) && ((uintptr_t)A % 16 == 0) && (dprev == nullptr || (uintptr_t)dprev % 16 == 0) &&
                      (dp_hi == nullptr || ((uintptr_t)dp_hi % 16 == 0 && (uintptr_t)dp_lo % 16 == 0));
     char name[80];
     snprintf(name, sizeof name, "head_softmax_xent[rows=%d,d=%d,C=%d,dgrad=%d]", rows, d, C, dprev ? 1 : 0);
     if (h) h->before(name, s);
     cudaError_t e;
-#define HEAD_CASE3(NVv, CMv)                                                                                   \
-    e = vec ? launch_head<NVv, true, CMv>(blocks, smem, s, rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL, dprev, \
-                                          dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out)                \
-            : launch_head<NVv, false, CMv>(blocks, smem, s, rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL,     \
-                                           dprev, dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out)
+#define HEAD_CASE4(NVv, CMv, Wv)                                                                               \
+    e = vec ? launch_head<NVv, true, CMv, Wv>(blocks, smem, s, rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL,   \
+                                              dprev, dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out)     \
+            : launch_head<NVv, false, CMv, Wv>(blocks, smem, s, rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL,  \
+                                               dprev, dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out)
+#define HEAD_CASE3(NVv, CMv)          \
+    if (big) {                        \
+        HEAD_CASE4(NVv, CMv, 2);      \
+    } else {                          \
+        HEAD_CASE4(NVv, CMv, 8);      \
+    }
 #define HEAD_CASE(NVv)             \
     if (C <= 2) {                  \
         HEAD_CASE3(NVv, 2);        \
@@ -725,6 +733,7 @@ cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, cons
     else { HEAD_CASE(8); }
 #undef HEAD_CASE
 #undef HEAD_CASE3
+#undef HEAD_CASE4
     if (h) h->after(name, s);
     return e;
 }
