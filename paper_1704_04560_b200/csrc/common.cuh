@@ -40,6 +40,28 @@ MTX_DEVI void split_tf32(float x, float &hi, float &lo) {
     lo = __uint_as_float(rne_tf32_bits(__float_as_uint(x - hi)));
 }
 
+// Shared-memory mbarriers (completion tracking of TMA / bulk copies and tcgen05 commits).
+MTX_DEVI uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+MTX_DEVI void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+MTX_DEVI void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+MTX_DEVI void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+MTX_DEVI void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
 // Programmatic dependent launch.  Every kernel of the step starts with pdl_wait()
 // (griddepcontrol.wait: returns once the preceding grid has completed and its memory is
 // visible; a no-op when the launch was not programmatic) and is launched with

@@ -115,26 +115,10 @@ __global__ void __launch_bounds__(CONV_T) conv_fwd_kernel(ConvGeom g, int rows, 
     }
 }
 
-__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void bar_init(uint32_t bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void bar_expect(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t done = 0;
-    do {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-                     : "=r"(done)
-                     : "r"(bar), "r"(parity)
-                     : "memory");
-    } while (!done);
-}
 // 1-D bulk copy global -> shared (TMA engine), completion counted on the mbarrier in bytes
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_addr(dst)),
+                     smem_u32(dst)),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
@@ -176,7 +160,7 @@ __global__ void __launch_bounds__(CONV_T) conv_bwd_kernel(ConvGeom g, int rows, 
         return BwdBuf{base, base + in_pad, base + in_pad + ppc_pad, (uint8_t *)(base + in_pad + 2 * ppc_pad)};
     };
     uint64_t *bars = (uint64_t *)(bufs + 2 * bstride);
-    const uint32_t bar0 = smem_addr(bars);
+    const uint32_t bar0 = smem_u32(bars);
     if (dX) stage_weights<CO>(Wb, KK, g.co, sW);
     const int tid = threadIdx.x;
     // weight-gradient role: patch-element block eb (4 consecutive e) x position group pg
@@ -208,15 +192,15 @@ __global__ void __launch_bounds__(CONV_T) conv_bwd_kernel(ConvGeom g, int rows, 
         const uint32_t bar = bar0 + 8 * b;
         const BwdBuf B = buf(b);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // buffer's previous reads done (barrier)
-        bar_expect(bar, (uint32_t)(4 * in_sz + 8 * ppc + apitch));
+        mbar_expect_tx(bar, (uint32_t)(4 * in_sz + 8 * ppc + apitch));
         bulk_g2s(B.x, Xb + (int64_t)n * in_sz, 4 * in_sz, bar);
         bulk_g2s(B.p, P + (int64_t)n * ppc, 4 * ppc, bar);
         bulk_g2s(B.dp, dP + (int64_t)n * ppc, 4 * ppc, bar);
         bulk_g2s(B.a, arg + (int64_t)n * apitch, apitch, bar);
     };
     if (bulk && tid == 0) {
-        bar_init(bar0);
-        bar_init(bar0 + 8);
+        mbar_init(bar0, 1);
+        mbar_init(bar0 + 8, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -235,7 +219,7 @@ __global__ void __launch_bounds__(CONV_T) conv_bwd_kernel(ConvGeom g, int rows, 
             }
         }
         for (int i = tid; i < HWc * CO / 4; i += blockDim.x) ((float4 *)sD)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (bulk) bar_wait(bar0 + 8 * b, (it >> 1) & 1);
+        if (bulk) mbar_wait(bar0 + 8 * b, (it >> 1) & 1);
         __syncthreads();
         // max-pool + ReLU backward: dR = dP at the argmax when P > 0, zero elsewhere
         for (int i = tid; i < ppc; i += blockDim.x) {
