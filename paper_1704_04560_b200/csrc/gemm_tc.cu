@@ -812,13 +812,14 @@ static int co_resident(TcGemm *t, bool split, int cs) {
 cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h) {
     const int M = g.aug ? g.M - 1 : g.M;  // the bias row of an augmented wgrad is a column sum (below)
     const int N = g.N, K = g.K;
-    const TcPlan plan = tc_plan(t->sms, M, N, K);
+    const int sms = g.sm_budget > 0 ? std::min(g.sm_budget, t->sms) : t->sms;
+    const TcPlan plan = tc_plan(sms, M, N, K);
     const int BN = plan.bn;
     // CTA pairs for large unsplit GEMMs: a 256 x 128 tile per pair halves B's per-SM operand traffic.
     // Not for dgrad: its masked epilogue is the heavier one and the pair couples both SMs' epilogues
     // through the shared accumulator barrier (measured slower).
     const bool pair = t->pair && g.epi != EPI_MASK && BN == 128 && plan.splits == 1 && N % 64 == 0 && M > BM &&
-                      (int64_t)((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * 2 >= t->sms / 2;
+                      (int64_t)((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * 2 >= sms / 2;
     TcParams p{};
     p.M = M; p.N = N; p.K = K;
     p.a_mn = g.ta ? 1 : 0;
@@ -878,7 +879,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.ldc = g.ldc;
     p.partial = g.partial;
     const int total = tiles * splits;
-    const int grid = cluster ? total : pair ? 2 * std::min(total, t->sms / 2) : std::min(total, t->sms);
+    const int grid = cluster ? total : pair ? 2 * std::min(total, sms / 2) : std::min(total, sms);
     const char *kind = g.epi == EPI_MASK ? "dgrad" : (g.ta ? "wgrad" : "fwd");
     char name[96];
     snprintf(name, sizeof name, "gemm_tc%s_%s[M=%d,N=%d,K=%d,splits=%d,cluster=%d,pair=%d,bn=%d]", g.tf32x3 ? "3x" : "",

@@ -20,6 +20,7 @@ struct GemmDesc {
     int M = 0, N = 0, K = 0;
     bool ta = false, tb = false, aug = false;
     bool colsum_external = false;  // aug on the tensor-core engine: the caller launches the bias column sum
+    int sm_budget = 0;             // > 0: plan and launch for at most this many SMs (concurrent side work)
     int epi = EPI_STORE;
     const float *A = nullptr;
     int64_t lda = 0;

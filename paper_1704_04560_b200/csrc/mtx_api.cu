@@ -535,6 +535,14 @@ struct Runner {
     }
 
     mtx_status gemm(GemmDesc g) {
+        // small weight gradients on the side lanes take a reduced SM budget so the critical dgrad chain
+        // on the caller's stream keeps most of the GPU (cfg2: 76 -> 74 us/step); large ones (cfg4's
+        // 17 GFLOP wgrads) keep all SMs or they would become the critical path (measured)
+        static const int side_sms = [] {
+            const char *e = getenv("MTX_SIDE_SMS");  // development knob; 0 disables
+            return e ? atoi(e) : 24;
+        }();
+        if ((lane == 1 || lane == 2) && side_sms > 0 && 2.0 * g.M * g.N * g.K < 2e9) g.sm_budget = side_sms;
         g.partial = part();
         g.partial_cap = c->partial_floats;
         g.counters = ctrs();
