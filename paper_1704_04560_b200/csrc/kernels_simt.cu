@@ -493,7 +493,7 @@ namespace {
 // HEAD_WARPS: warps (rows in flight) per CTA -- 8 for small batches (cfg2: 64 CTAs), 2 for large ones
 // (cfg4: more CTAs share the weight staging); measured, DESIGN.md §9
 template <int NV, bool VEC, int HEAD_MAXC, int HEAD_WARPS>
-__global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, int C, const float *__restrict__ A,
+__global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, int C_arg, const float *__restrict__ A,
                                                              RowSel arow, const float *__restrict__ Wb,
                                                              const int32_t *__restrict__ labels, RowSel lrow,
                                                              float inv_b, float *__restrict__ dZL,
@@ -502,6 +502,10 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
                                                              float *__restrict__ loss_part, unsigned *ticket,
                                                              float *__restrict__ loss_out) {
     pdl_wait();
+    // HEAD_MAXC 2 and 10 are exact class counts (HIGGS, MNIST/CIFAR-10): the class loops compile
+    // without predicates; the other instances take C at run time
+    constexpr bool EXACT = HEAD_MAXC == 2 || HEAD_MAXC == 10;
+    const int C = EXACT ? HEAD_MAXC : C_arg;
     // W_L staged TRANSPOSED: sWt[j][k], row pitch dp = round_up(d + 1, 4) (k == d: bias), so a lane
     // reads the weights of its 4 consecutive features as one conflict-free 128-bit load
     extern __shared__ __align__(16) float sWt[];
@@ -528,32 +532,25 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
     };
     const int i_first = blockIdx.x * HEAD_WARPS + warp;
     if (i_first < rows) load_row(i_first);  // in flight while W_L is staged
-    {
-        const int n = (d + 1) * C;
-        auto put = [&](int e, float v) { sWt[(e % C) * dp + e / C] = v; };
-        int done = 0;
-        if (((uintptr_t)Wb & 15) == 0) {  // 128-bit loads, 8 in flight per thread
-            const int n4 = n / 4;
-            for (int e0 = threadIdx.x; e0 < n4; e0 += 8 * blockDim.x) {
-                float4 v[8];
+    // row k of W_L (C weights; k == d is the bias row) -> column k of sWt, k in [d+1, dp) zeroed:
+    // two rows per thread in flight, consecutive k across the warp (conflict-free stores), no
+    // index division (it cost ~700 instructions per warp when it was e -> (e % C, e / C))
+    for (int k0 = threadIdx.x; k0 < dp; k0 += 2 * HEAD_WARPS * 32) {
+        float v[2][HEAD_MAXC];
 #pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const int e = e0 + u * blockDim.x;
-                    v[u] = e < n4 ? __ldg((const float4 *)Wb + e) : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
+        for (int r = 0; r < 2; r++) {
+            const int k = k0 + r * HEAD_WARPS * 32;
 #pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const int e = e0 + u * blockDim.x;
-                    if (e < n4) {
-                        put(4 * e, v[u].x); put(4 * e + 1, v[u].y); put(4 * e + 2, v[u].z); put(4 * e + 3, v[u].w);
-                    }
-                }
-            }
-            done = 4 * n4;
+            for (int j = 0; j < HEAD_MAXC; j++) v[r][j] = (j < C && k <= d) ? __ldg(Wb + (int64_t)k * C + j) : 0.f;
         }
-        for (int e = done + threadIdx.x; e < n; e += blockDim.x) put(e, __ldg(Wb + e));
-        const int pad = dp - d - 1;  // zero the row padding: it meets zero features in 128-bit reads
-        for (int e = threadIdx.x; e < C * pad; e += blockDim.x) sWt[(e / pad) * dp + d + 1 + e % pad] = 0.f;
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+            const int k = k0 + r * HEAD_WARPS * 32;
+            if (k < dp) {
+#pragma unroll
+                for (int j = 0; j < HEAD_MAXC; j++) if (j < C) sWt[j * dp + k] = v[r][j];
+            }
+        }
     }
     __syncthreads();
     float wloss = 0.f;  // this warp's rows, in row order
@@ -720,8 +717,10 @@ cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, cons
         HEAD_CASE4(NVv, CMv, 8);      \
     }
 #define HEAD_CASE(NVv)             \
-    if (C <= 2) {                  \
+    if (C == 2) {                  \
         HEAD_CASE3(NVv, 2);        \
+    } else if (C == 10) {          \
+        HEAD_CASE3(NVv, 10);       \
     } else if (C <= 4) {           \
         HEAD_CASE3(NVv, 4);        \
     } else {                       \
