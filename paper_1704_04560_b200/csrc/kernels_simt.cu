@@ -5,6 +5,7 @@
 // (P:182-184), update.  Design notes: DESIGN.md §Kernels.
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -533,18 +534,19 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
     const int i_first = blockIdx.x * HEAD_WARPS + warp;
     if (i_first < rows) load_row(i_first);  // in flight while W_L is staged
     // row k of W_L (C weights; k == d is the bias row) -> column k of sWt, k in [d+1, dp) zeroed:
-    // two rows per thread in flight, consecutive k across the warp (conflict-free stores), no
+    // R rows per thread in flight, consecutive k across the warp (conflict-free stores), no
     // index division (it cost ~700 instructions per warp when it was e -> (e % C, e / C))
-    for (int k0 = threadIdx.x; k0 < dp; k0 += 2 * HEAD_WARPS * 32) {
-        float v[2][HEAD_MAXC];
+    constexpr int R = HEAD_WARPS >= 8 ? 3 : 4;  // rows per thread in flight: d <= 767 in one pass at 8 warps
+    for (int k0 = threadIdx.x; k0 < dp; k0 += R * HEAD_WARPS * 32) {
+        float v[R][HEAD_MAXC];
 #pragma unroll
-        for (int r = 0; r < 2; r++) {
+        for (int r = 0; r < R; r++) {
             const int k = k0 + r * HEAD_WARPS * 32;
 #pragma unroll
             for (int j = 0; j < HEAD_MAXC; j++) v[r][j] = (j < C && k <= d) ? __ldg(Wb + (int64_t)k * C + j) : 0.f;
         }
 #pragma unroll
-        for (int r = 0; r < 2; r++) {
+        for (int r = 0; r < R; r++) {
             const int k = k0 + r * HEAD_WARPS * 32;
             if (k < dp) {
 #pragma unroll
@@ -697,8 +699,9 @@ cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, cons
     if (C > 16 || C < 1 || d > 1024) return cudaErrorInvalidValue;
     const size_t smem = sizeof(float) * (size_t)((d + 1 + 3) & ~3) * C;
     // enough rows per block that the block count stays <= 1024 (loss partial slots)
-    const bool big = rows > 2048;
-    const unsigned blocks = std::min<unsigned>(cdiv(rows, big ? 2 : 8), 1024u);
+    int hw = rows > 2048 ? 2 : 8;
+    if (const char *e = getenv("MTX_HEAD_WARPS")) hw = atoi(e) == 4 ? 4 : atoi(e) == 2 ? 2 : 8;  // development knob
+    const unsigned blocks = std::min<unsigned>(cdiv(rows, hw), 1024u);
     const bool vec = (d % 4 == 0) && ((uintptr_t)A % 16 == 0) && (dprev == nullptr || (uintptr_t)dprev % 16 == 0) &&
                      (dp_hi == nullptr || ((uintptr_t)dp_hi % 16 == 0 && (uintptr_t)dp_lo % 16 == 0));
     char name[80];
@@ -711,8 +714,10 @@ cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, cons
             : launch_head<NVv, false, CMv, Wv>(blocks, smem, s, rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL,  \
                                                dprev, dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out)
 #define HEAD_CASE3(NVv, CMv)          \
-    if (big) {                        \
+    if (hw == 2) {                    \
         HEAD_CASE4(NVv, CMv, 2);      \
+    } else if (hw == 4) {             \
+        HEAD_CASE4(NVv, CMv, 4);      \
     } else {                          \
         HEAD_CASE4(NVv, CMv, 8);      \
     }
