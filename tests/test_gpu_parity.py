@@ -221,6 +221,19 @@ def test_ragged_mlp_one_step(precision):
     _check_step(cfg, X, y, precision, 4, start)
 
 
+@pytest.mark.parametrize("C,d,B", [(10, 71, 75), (2, 71, 75), (10, 64, 2100), (2, 33, 2100), (1, 40, 75),
+                                   (5, 130, 75), (16, 129, 75)])
+def test_head_class_counts(C, d, B):
+    """The fused head's instances: exact C = 2 / 10 (HIGGS, MNIST/CIFAR), generic C <= 4 / <= 16,
+    vector and scalar (d % 4 != 0) row loads, and the > 2048-row launch shape; B is ragged."""
+    cfg = dict(kind="mlp", dims=[24, d, C], data="mnist", n=B + 50, B=B, lr=0.05, mu=0.9)
+    rng = np.random.default_rng(C * 1000 + d)
+    X = rng.standard_normal((B + 50, 24)).astype(np.float32)
+    y = rng.integers(0, C, B + 50).astype(np.int32)
+    start = oracle.init_params(oracle.Net.from_cfg(cfg), 42)
+    _check_step(cfg, X, y, P.MTX_3XTF32, 1, start)
+
+
 @pytest.mark.parametrize("precision", [p for p in PRECISIONS if p != P.MTX_TF32])
 def test_cnn_lenet_one_step(precision):
     """configs[2] model (LeNet on CIFAR-shaped NHWC 32x32x3) at a batch the oracle finishes in seconds;
