@@ -116,6 +116,11 @@ def kernel_work(name: str):
         return "byte", 4 * a["K"] * a["N"], "hbm"
     if kind == "wgrad_narrow":  # streams A [K x (M-1)] once; dZ is tiny
         return "byte", 4 * a["K"] * (a["M"] - 1 + a["N"]), "hbm"
+    if kind == "conv_fwd":  # direct convolution, valid, stride 1: 2 * b * ho^2 * co * ci * k^2 (CUDA-core FMA)
+        ho = a["hi"] - a["k"] + 1
+        return "flop", 2 * a["rows"] * ho * ho * a["co"] * a["ci"] * a["k"] * a["k"], "alu"
+    if kind == "conv_bwd":  # wgrad (+ dgrad): E - 1 = ci * k^2 products per conv output and channel, each
+        return "flop", 2 * a["rows"] * a["hc"] * a["hc"] * a["co"] * (a["E"] - 1) * (1 + a["dgrad"]), "alu"
     if kind.startswith("conv_") or kind == "pool_relu_bwd":
         return None
     if kind == "avg_update":

@@ -172,6 +172,12 @@ struct mtx_ctx {
     float *land_x[2] = {nullptr, nullptr};
     int32_t *land_y[2] = {nullptr, nullptr};
     cudaStream_t copy_s = nullptr;
+    // one pinned H2D stream moves ~17 GB/s at 1.6 MB (measured, tools/h2d_probe.py); the input rows
+    // are split over up to COPY_LANES streams (default 4) so several copy engines share the PCIe link
+    static constexpr int COPY_LANES = 8;
+    cudaStream_t copy_x[COPY_LANES - 1] = {};
+    cudaEvent_t ev_cfork = nullptr, ev_cjoin[COPY_LANES - 1] = {};
+    int copy_lanes = 4;  // measured 1/2/4/6/8
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
     int land_next = 0;
     int64_t async_steps = 0;
@@ -180,8 +186,9 @@ struct mtx_ctx {
     ncclComm_t comm = nullptr;
     cudaStream_t own = nullptr, comm_s = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    cudaGraphExec_t graph[2] = {nullptr, nullptr};  // [0] resident data, [1] staged host data
-    cudaGraphExec_t graph_timed[2] = {nullptr, nullptr};  // same, with event nodes around every kernel
+    // [0] resident data, [1] host data staged in stage_x, [2 + k] host data read from landing area k
+    cudaGraphExec_t graph[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaGraphExec_t graph_timed[4] = {nullptr, nullptr, nullptr, nullptr};  // same, with event nodes around every kernel
     cudaStream_t graph_stream[2] = {nullptr, nullptr};
     int launches_per_step = 0;
     int64_t next_step = 0;
@@ -434,7 +441,10 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     float *sx = (float *)take(4 * b * c->d0);
     plane(sx, b * c->d0);
     int32_t *sy = (int32_t *)take(4 * b);
-    float *lx0 = (float *)take(4 * b * c->d0), *lx1 = (float *)take(4 * b * c->d0);
+    float *lx0 = (float *)take(4 * b * c->d0);
+    plane(lx0, b * c->d0);
+    float *lx1 = (float *)take(4 * b * c->d0);
+    plane(lx1, b * c->d0);
     int32_t *ly0 = (int32_t *)take(4 * b), *ly1 = (int32_t *)take(4 * b);
     float *loss_part = (float *)take(4 * 1024);
     // per lane: [0,254) split-K tiles, 254 narrow wgrad, 256.. colsum groups
@@ -483,6 +493,8 @@ struct Runner {
     cudaStream_t s;  // the stream launches go to: the caller's stream, or a side lane's inside on_lane()
     bool staged;
     LaunchHook *h;
+    const float *sx = nullptr;    // staged input rows (stage_x or a landing area) when staged
+    const int32_t *sy = nullptr;
     int lane = 0;            // 0: the caller's stream; 1..LANES-1: c->side[lane - 1]
     unsigned dirty = 0;      // side lanes with gradient work no consumer has waited on yet
     unsigned used = 0;       // side lanes forked this step (joined back at the end of the step)
@@ -582,8 +594,8 @@ struct Runner {
     }
 
     RowSel xrow() const { return staged ? RowSel{nullptr, 0} : RowSel{c->win, (int64_t)c->rank * c->b}; }
-    const float *xbase() const { return staged ? c->stage_x : c->X; }
-    const int32_t *ybase() const { return staged ? c->stage_y : c->Y; }
+    const float *xbase() const { return staged ? sx : c->X; }
+    const int32_t *ybase() const { return staged ? sy : c->Y; }
 
     // Wgrad of layer block `li` (augmented: writes dW and db) from A [b][rows_w] and dZ [b][cols].
     mtx_status wgrad(int li, const float *A, RowSel arow, const float *dZ) {
@@ -788,8 +800,9 @@ struct Runner {
         if (c->params_hi) {  // 3xTF32: planes of this step's parameters (and of a staged batch)
             // P = 1: the previous update (or the last external parameter change) already wrote them
             if (c->world > 1) CK(split_planes(c->params, 1, c->N_pad, c->N_pad, c->params_hi, c->params_lo, s, h));
-            if (staged && c->stage_hi && c->d0 % 4 == 0)
-                CK(split_planes(c->stage_x, c->b, c->d0, c->d0, c->stage_hi, c->stage_lo, s, h));
+            const float *xh = nullptr, *xl = nullptr;
+            if (staged && c->d0 % 4 == 0 && plane_of(c, sx, &xh, &xl))
+                CK(split_planes(sx, c->b, c->d0, c->d0, (float *)xh, (float *)xl, s, h));
         }
         mtx_status st = c->kind == MTX_MLP ? forward_backward_mlp() : forward_backward_cnn();
         if (st) return st;
@@ -887,13 +900,15 @@ mtx_status Runner::forward_backward_cnn() {
 
 namespace {
 
-mtx_status capture(mtx_ctx *c, cudaStream_t s, bool staged, bool timed, cudaGraphExec_t *out) {
+mtx_status capture(mtx_ctx *c, cudaStream_t s, bool staged, int land, bool timed, cudaGraphExec_t *out) {
     c->hook.counting = true;
     c->hook.count = 0;
     c->hook.enabled = timed;
     if (timed) c->hook.begin_capture();
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
     Runner r{c, s, staged, &c->hook};
+    r.sx = land < 0 ? c->stage_x : c->land_x[land];
+    r.sy = land < 0 ? c->stage_y : c->land_y[land];
     if (timed) {  // calibration pairs: the event-node overhead of an empty launch (not counted as a step kernel)
         c->hook.counting = false;
         for (int i = 0; i < 3; i++) empty_launch(s, &c->hook);
@@ -920,12 +935,12 @@ mtx_status capture(mtx_ctx *c, cudaStream_t s, bool staged, bool timed, cudaGrap
 // second captured graph whose every kernel is bracketed by event-record nodes
 // (cudaEventRecordExternal), so each pair measures device time inside the replayed graph;
 // the step then synchronises and the pairs are accumulated.
-mtx_status run_step(mtx_ctx *c, cudaStream_t s, bool staged) {
-    const int gi = staged ? 1 : 0;
+mtx_status run_step(mtx_ctx *c, cudaStream_t s, bool staged, int land = -1) {
+    const int gi = !staged ? 0 : land < 0 ? 1 : 2 + land;
     const bool timed = c->timing;
     cudaGraphExec_t *slot = timed ? &c->graph_timed[gi] : &c->graph[gi];
     mtx_status st;
-    if (!*slot && (st = capture(c, s, staged, timed, slot))) return st;
+    if (!*slot && (st = capture(c, s, staged, land, timed, slot))) return st;
     CK(cudaGraphLaunch(*slot, s));
     if (timed) {
         CK(cudaStreamSynchronize(s));
@@ -1092,10 +1107,19 @@ mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t ui
         cudaEventCreateWithFlags(&c->ev_copied[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_copied[1], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_free[0], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_free[1], cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&c->ev_free[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_cfork, cudaEventDisableTiming) != cudaSuccess) {
         delete c;
         return MTX_ERR_CUDA;
     }
+    for (int i = 0; i < mtx_ctx::COPY_LANES - 1; i++)
+        if (cudaStreamCreateWithFlags(&c->copy_x[i], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_cjoin[i], cudaEventDisableTiming) != cudaSuccess) {
+            delete c;
+            return MTX_ERR_CUDA;
+        }
+    if (const char *e = getenv("MTX_COPY_LANES"))  // development knob (1 .. COPY_LANES)
+        c->copy_lanes = std::max(1, std::min(atoi(e), mtx_ctx::COPY_LANES));
     for (int i = 0; i < mtx_ctx::LANES; i++)
         if (cudaEventCreateWithFlags(&c->ev_lane[i], cudaEventDisableTiming) != cudaSuccess ||
             (i > 0 && c->kind == MTX_MLP &&
@@ -1297,18 +1321,31 @@ mtx_status mtx_train_step_host_async(mtx_ctx *c, const float *X_host, const int3
     if (c->n_data == 0) c->n_data = c->B;  // window advance is unused on the staged path
     const int k = c->land_next;
     c->land_next ^= 1;
-    const size_t xb = (size_t)c->b * c->d0 * 4, yb = (size_t)c->b * 4;
+    const size_t yb = (size_t)c->b * 4;
     // copy stream: landing buffer k is free once the step that consumed it has copied it out
     CK(cudaStreamWaitEvent(c->copy_s, c->ev_free[k], 0));
-    CK(cudaMemcpyAsync(c->land_x[k], X_host, xb, cudaMemcpyHostToDevice, c->copy_s));
+    // row chunks of X over the copy lanes (lane 0 = copy_s, which also carries y and joins the rest)
+    const int nl = (int)std::min<int64_t>(c->copy_lanes, std::max<int64_t>(1, c->b));
+    const int64_t rows_per = (c->b + nl - 1) / nl, row_bytes = (int64_t)c->d0 * 4;
+    if (nl > 1) CK(cudaEventRecord(c->ev_cfork, c->copy_s));
+    for (int i = 0; i < nl; i++) {
+        const int64_t r0 = i * rows_per, r1 = std::min<int64_t>(c->b, r0 + rows_per);
+        if (r1 <= r0) continue;
+        cudaStream_t cs = i == 0 ? c->copy_s : c->copy_x[i - 1];
+        if (i > 0) CK(cudaStreamWaitEvent(cs, c->ev_cfork, 0));
+        CK(cudaMemcpyAsync((char *)c->land_x[k] + r0 * row_bytes, (const char *)X_host + r0 * row_bytes,
+                           (size_t)((r1 - r0) * row_bytes), cudaMemcpyHostToDevice, cs));
+        if (i > 0) CK(cudaEventRecord(c->ev_cjoin[i - 1], cs));
+    }
     CK(cudaMemcpyAsync(c->land_y[k], y_host, yb, cudaMemcpyHostToDevice, c->copy_s));
+    for (int i = 1; i < nl; i++)
+        if ((int64_t)i * rows_per < c->b) CK(cudaStreamWaitEvent(c->copy_s, c->ev_cjoin[i - 1], 0));
     CK(cudaEventRecord(c->ev_copied[k], c->copy_s));
-    // compute stream: move the rows into the step's staging buffer, release the landing buffer, step
+    // compute stream: the step's graph for landing area k reads the rows in place; the area is
+    // free for the copy two steps later once this step has run
     CK(cudaStreamWaitEvent(s, c->ev_copied[k], 0));
-    CK(cudaMemcpyAsync(c->stage_x, c->land_x[k], xb, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(c->stage_y, c->land_y[k], yb, cudaMemcpyDeviceToDevice, s));
+    if ((st = run_step(c, s, true, k))) return st;
     CK(cudaEventRecord(c->ev_free[k], s));
-    if ((st = run_step(c, s, true))) return st;
     // the step's result to host memory, every step (read by mtx_sync)
     CK(cudaMemcpyAsync(c->h_loss_ring + (c->async_steps & 63), c->grads + c->N_pad + (c->fused ? 1 : 0), sizeof(float),
                        cudaMemcpyDeviceToHost, s));
@@ -1553,6 +1590,11 @@ mtx_status mtx_finalize(mtx_ctx *c) {
         if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
     }
     if (c->copy_s) cudaStreamDestroy(c->copy_s);
+    for (int i = 0; i < mtx_ctx::COPY_LANES - 1; i++) {
+        if (c->copy_x[i]) cudaStreamDestroy(c->copy_x[i]);
+        if (c->ev_cjoin[i]) cudaEventDestroy(c->ev_cjoin[i]);
+    }
+    if (c->ev_cfork) cudaEventDestroy(c->ev_cfork);
     if (c->h_flag) cudaFreeHost(c->h_flag);
     if (c->dbg_planes) cudaFree(c->dbg_planes);
     if (c->tc) tc_destroy(c->tc);
