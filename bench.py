@@ -259,7 +259,7 @@ def main():
             return
         X, y = S.dataset(cfg, n=min(cfg["n"], 100_000))
         cb = cpu_oracle(cfg, max(2.0, min(args.cpu_budget, 10.0)), X, y)
-        line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": "samples/s", "n_gpus": 0,
+        line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": "samples/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(cfg["B"] / cb["value"] * 1e3, 3),
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": {"workload": f"{args.config}: {desc(cfg)}", "global_batch": cfg["B"]},
