@@ -1296,6 +1296,28 @@ mtx_status mtx_train_step(mtx_ctx *c, int64_t step, float *host_loss, void *stre
     return MTX_OK;
 }
 
+// Host rows -> device: X split in row chunks over the copy lanes (lane 0 = `s0`, which also carries
+// y and joins the others), so several copy engines share the PCIe link.
+static mtx_status upload_rows(mtx_ctx *c, float *dx, const float *X_host, int32_t *dy, const int32_t *y_host,
+                       cudaStream_t s0) {
+    const int nl = (int)std::min<int64_t>(c->copy_lanes, std::max<int64_t>(1, c->b));
+    const int64_t rows_per = (c->b + nl - 1) / nl, row_bytes = (int64_t)c->d0 * 4;
+    if (nl > 1) CK(cudaEventRecord(c->ev_cfork, s0));
+    for (int i = 0; i < nl; i++) {
+        const int64_t r0 = i * rows_per, r1 = std::min<int64_t>(c->b, r0 + rows_per);
+        if (r1 <= r0) continue;
+        cudaStream_t cs = i == 0 ? s0 : c->copy_x[i - 1];
+        if (i > 0) CK(cudaStreamWaitEvent(cs, c->ev_cfork, 0));
+        CK(cudaMemcpyAsync((char *)dx + r0 * row_bytes, (const char *)X_host + r0 * row_bytes,
+                           (size_t)((r1 - r0) * row_bytes), cudaMemcpyHostToDevice, cs));
+        if (i > 0) CK(cudaEventRecord(c->ev_cjoin[i - 1], cs));
+    }
+    CK(cudaMemcpyAsync(dy, y_host, (size_t)c->b * 4, cudaMemcpyHostToDevice, s0));
+    for (int i = 1; i < nl; i++)
+        if ((int64_t)i * rows_per < c->b) CK(cudaStreamWaitEvent(s0, c->ev_cjoin[i - 1], 0));
+    return MTX_OK;
+}
+
 mtx_status mtx_train_step_host(mtx_ctx *c, const float *X_host, const int32_t *y_host, float *host_loss,
                                void *stream) {
     mtx_status st = live(c);
@@ -1305,8 +1327,7 @@ mtx_status mtx_train_step_host(mtx_ctx *c, const float *X_host, const int32_t *y
     if (!X_host || !y_host || !host_loss) return fail(c, MTX_ERR_INVALID_ARG, "null host buffer");
     cudaStream_t s = pick(c, stream);
     if (c->n_data == 0) c->n_data = c->B;  // window advance is unused on the staged path
-    CK(cudaMemcpyAsync(c->stage_x, X_host, (size_t)c->b * c->d0 * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(c->stage_y, y_host, (size_t)c->b * 4, cudaMemcpyHostToDevice, s));
+    if ((st = upload_rows(c, c->stage_x, X_host, c->stage_y, y_host, s))) return st;
     if ((st = run_step(c, s, true))) return st;
     return sync_loss(c, s, host_loss);
 }
@@ -1321,25 +1342,9 @@ mtx_status mtx_train_step_host_async(mtx_ctx *c, const float *X_host, const int3
     if (c->n_data == 0) c->n_data = c->B;  // window advance is unused on the staged path
     const int k = c->land_next;
     c->land_next ^= 1;
-    const size_t yb = (size_t)c->b * 4;
     // copy stream: landing buffer k is free once the step that consumed it has copied it out
     CK(cudaStreamWaitEvent(c->copy_s, c->ev_free[k], 0));
-    // row chunks of X over the copy lanes (lane 0 = copy_s, which also carries y and joins the rest)
-    const int nl = (int)std::min<int64_t>(c->copy_lanes, std::max<int64_t>(1, c->b));
-    const int64_t rows_per = (c->b + nl - 1) / nl, row_bytes = (int64_t)c->d0 * 4;
-    if (nl > 1) CK(cudaEventRecord(c->ev_cfork, c->copy_s));
-    for (int i = 0; i < nl; i++) {
-        const int64_t r0 = i * rows_per, r1 = std::min<int64_t>(c->b, r0 + rows_per);
-        if (r1 <= r0) continue;
-        cudaStream_t cs = i == 0 ? c->copy_s : c->copy_x[i - 1];
-        if (i > 0) CK(cudaStreamWaitEvent(cs, c->ev_cfork, 0));
-        CK(cudaMemcpyAsync((char *)c->land_x[k] + r0 * row_bytes, (const char *)X_host + r0 * row_bytes,
-                           (size_t)((r1 - r0) * row_bytes), cudaMemcpyHostToDevice, cs));
-        if (i > 0) CK(cudaEventRecord(c->ev_cjoin[i - 1], cs));
-    }
-    CK(cudaMemcpyAsync(c->land_y[k], y_host, yb, cudaMemcpyHostToDevice, c->copy_s));
-    for (int i = 1; i < nl; i++)
-        if ((int64_t)i * rows_per < c->b) CK(cudaStreamWaitEvent(c->copy_s, c->ev_cjoin[i - 1], 0));
+    if ((st = upload_rows(c, c->land_x[k], X_host, c->land_y[k], y_host, c->copy_s))) return st;
     CK(cudaEventRecord(c->ev_copied[k], c->copy_s));
     // compute stream: the step's graph for landing area k reads the rows in place; the area is
     // free for the copy two steps later once this step has run
