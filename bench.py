@@ -268,9 +268,11 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
-    # stdout must carry exactly one JSON line: keep NCCL's version banner off it
+    # stdout must carry exactly one JSON line: NCCL logs to stdout (its version banner prints at
+    # every level from VERSION up, WARN included), so its log goes to stderr
     if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
         os.environ["NCCL_DEBUG"] = "WARN"
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import torch
     import torch.distributed as dist
 

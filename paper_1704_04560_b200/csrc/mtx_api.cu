@@ -181,7 +181,7 @@ struct mtx_ctx {
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
     int land_next = 0;
     int64_t async_steps = 0;
-    float *h_loss_ring = nullptr;  // 64 slots
+    float *h_loss_ring = nullptr;  // [0]: the last pipelined step's loss sum (written by its graph)
     // runtime
     ncclComm_t comm = nullptr;
     cudaStream_t own = nullptr, comm_s = nullptr;
@@ -915,6 +915,13 @@ mtx_status capture(mtx_ctx *c, cudaStream_t s, bool staged, int land, bool timed
         c->hook.counting = true;
     }
     mtx_status st = r.step();
+    // the pipelined host path's per-step result: the loss sum lands in pinned host memory from
+    // inside the graph (a memcpy node), so the step costs no separate read-back call
+    if (!st && land >= 0) {
+        cudaError_t em = cudaMemcpyAsync(c->h_loss_ring, c->grads + c->N_pad + (c->fused ? 1 : 0), sizeof(float),
+                                         cudaMemcpyDeviceToHost, s);
+        if (em != cudaSuccess) st = fail(c, MTX_ERR_CUDA, "loss read-back node: %s", cudaGetErrorString(em));
+    }
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(s, &g);
     c->hook.counting = false;
@@ -1351,9 +1358,7 @@ mtx_status mtx_train_step_host_async(mtx_ctx *c, const float *X_host, const int3
     CK(cudaStreamWaitEvent(s, c->ev_copied[k], 0));
     if ((st = run_step(c, s, true, k))) return st;
     CK(cudaEventRecord(c->ev_free[k], s));
-    // the step's result to host memory, every step (read by mtx_sync)
-    CK(cudaMemcpyAsync(c->h_loss_ring + (c->async_steps & 63), c->grads + c->N_pad + (c->fused ? 1 : 0), sizeof(float),
-                       cudaMemcpyDeviceToHost, s));
+    // the step's loss reaches h_loss_ring[0] from inside the graph (capture())
     c->async_steps++;
     return MTX_OK;
 }
@@ -1365,7 +1370,7 @@ mtx_status mtx_sync(mtx_ctx *c, float *host_loss, void *stream) {
     CK(cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     CK(cudaStreamSynchronize(c->copy_s));
-    if (c->async_steps > 0) c->last_loss = (float)((double)c->h_loss_ring[(c->async_steps - 1) & 63] / (double)c->B);
+    if (c->async_steps > 0) c->last_loss = (float)((double)c->h_loss_ring[0] / (double)c->B);
     if (host_loss) *host_loss = c->last_loss;
     if (c->h_flag[0] & 2) return fail(c, MTX_ERR_NCCL, "peer barrier timeout (a rank did not reach the step)");
     if (c->h_flag[0]) return fail(c, MTX_ERR_NUMERIC, "non-finite averaged gradient");
