@@ -1,0 +1,60 @@
+"""bench.py host logic on CPU: the roofline's work model per launch name, and the reference arm's
+JSON line (the oracle timed on host cores)."""
+import importlib.util
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench():
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+@pytest.mark.parametrize("name,want", [
+    # 2 M N K flops; 3xTF32 is the same algorithmic work against a third of the tensor peak
+    ("gemm_tc3x_fwd[M=512,N=512,K=784,splits=4,cluster=1,pair=0,bn=64]", ("flop", 2 * 512 * 512 * 784, "tensor3x")),
+    ("gemm_tc_wgrad[M=784,N=512,K=512,splits=4,cluster=1,pair=0,bn=128]", ("flop", 2 * 784 * 512 * 512, "tensor")),
+    ("gemm_simt_fwd[M=64,N=128,K=784,splits=1]", ("flop", 2 * 64 * 128 * 784, "alu")),
+    # HBM kernels: bytes they must move
+    ("avg_update[n=1000,v=1,planes=1]", ("byte", 28 * 1000, "hbm")),
+    ("avg_update[n=1000,v=0,planes=0]", ("byte", 12 * 1000, "hbm")),
+    ("colsum[K=512,N=512,splits=8]", ("byte", 4 * 512 * 512, "hbm")),
+    ("head_softmax_xent[rows=512,d=512,C=10,dgrad=1]", ("byte", 4 * 512 * (2 * 512 + 11), "hbm")),
+    # LeNet: conv1 32x32x3 -> 28x28x6 (k = 5); conv2 backward 10x10x16 outputs, 6*25 inputs each
+    ("conv_fwd[rows=1024,hi=32,ci=3,k=5,co=6,spc=1]", ("flop", 2 * 1024 * 28 * 28 * 6 * 3 * 25, "alu")),
+    ("conv_bwd[rows=1024,hc=10,E=151,co=16,dgrad=1,ctas=256]", ("flop", 2 * 2 * 1024 * 100 * 16 * 150, "alu")),
+    ("conv_bwd[rows=1024,hc=28,E=76,co=6,dgrad=0,ctas=256]", ("flop", 2 * 1024 * 784 * 6 * 75, "alu")),
+])
+def test_kernel_work_model(name, want):
+    assert _bench().kernel_work(name) == want
+
+
+def test_kernel_work_unknown_names():
+    b = _bench()
+    assert b.kernel_work("empty_kernel") is None
+    assert b.kernel_work("pool_relu_bwd[rows=4,c=6]") is None
+
+
+def test_reference_arm_prints_one_json_line():
+    """`--impl reference` times the oracle on host cores and prints the contract's line, alone on stdout."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--steps", "2", "--warmup", "3", "--cpu-budget", "2"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env={**os.environ, "RANK": "0", "WORLD_SIZE": "1"})
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["steps"] == 2 and d["warmup"] == 3
+    assert d["unit"] == "samples/s" and d["higher_is_better"] is True and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert d["config"]["workload"].startswith("cfg2")
