@@ -60,3 +60,19 @@ def test_batch_slice_matches_oracle():
         mtx.mtx_batch_slice(100, 6, 0, 0, 4)
     with pytest.raises(mtx.MtxError):
         mtx.mtx_batch_slice(4, 8, 0, 0, 1)
+
+
+def test_build_entry_does_not_need_the_library(tmp_path):
+    """__graft_entry__.build() runs in a fresh checkout, before libmtx.so exists: loading the
+    builder must not import the package (whose import loads the library)."""
+    code = (
+        "import sys, __graft_entry__ as g, importlib.util, os\n"
+        "spec = importlib.util.spec_from_file_location('_b', os.path.join(g.ROOT, 'paper_1704_04560_b200', 'build.py'))\n"
+        "b = importlib.util.module_from_spec(spec); spec.loader.exec_module(b)\n"
+        "assert callable(b.build)\n"
+        "assert 'paper_1704_04560_b200' not in sys.modules, 'builder imported the package'\n"
+        "import inspect\n"
+        "src = inspect.getsource(g.build)\n"
+        "assert src.index('b.build()') < src.index('import paper_1704_04560_b200'), 'package imported before build'\n"
+        "assert 'from paper_1704_04560_b200' not in src\n")
+    subprocess.run(["python", "-c", code], cwd=ROOT, check=True)
