@@ -125,6 +125,10 @@ def kernel_work(name: str):
         return None
     if kind == "avg_update":
         return "byte", ((20 if a["v"] else 12) + (8 if a.get("planes") else 0)) * a["n"], "hbm"
+    if kind == "fused_avg_update":  # per owned element (n/P of them): P gradient reads (P-1 over NVLink),
+        # w (+ v) read, w stored to all P replicas, v and G stored locally
+        P, v = a["P"], a["v"]
+        return "byte", (8 * P + 8 + 8 * v) * (a["n"] // P), "hbm"
     if kind == "head_softmax_xent":  # read A rows, write dZ_{L-1} (and dZ_L, loss)
         return "byte", 4 * a["rows"] * (a["d"] * (1 + a["dgrad"]) + a["C"] + 1), "hbm"
     if kind == "splitk_reduce":
@@ -154,7 +158,9 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
             g["work"] += w[1] * cnt
             g["unit"], g["bound"] = w[0], w[2]
     total = sum(g["ms"] for g in groups.values())
-    top_name, top = max(groups.items(), key=lambda kv: kv[1]["ms"])
+    # kernels without algorithmic work (peer_barrier: a cross-GPU wait) are not roofline candidates
+    worked = {k: g for k, g in groups.items() if g["bound"]} or groups
+    top_name, top = max(worked.items(), key=lambda kv: kv[1]["ms"])
     per_launch_s = top["ms"] / 1e3 / top["cnt"]
     per_launch_work = top["work"] / top["cnt"]
     if top["bound"] == "hbm":
@@ -180,7 +186,7 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
     pr = re.search(r"pair=(\d)", longest)
     tpl = f"{bn}, {{}}, {pr.group(1) if pr else 0}, {1 if '_dgrad' in longest else 0}"  # <BN, 3x, PAIR, MASK>
     ncu_kernel = {"gemm_tc3x": f"tc_gemm_kernel<{tpl.format(1)}>", "gemm_tc": f"tc_gemm_kernel<{tpl.format(0)}>",
-                  "avg_update": "avg_update_kernel<1>", "head_softmax_xent": "head_kernel",
+                  "avg_update": "avg_update_kernel<1>", "fused_avg_update": "fused_avg_update_kernel", "head_softmax_xent": "head_kernel",
                   "colsum": "colsum_kernel", "splitk_reduce": "splitk_reduce_kernel", "conv_bwd": "conv_bwd_kernel",
                   "conv_fwd": "conv_fwd_kernel"}
     traffic = None
