@@ -314,6 +314,10 @@ def main():
     clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
+    # head start: the stream spins (outside every event pair) while the host enqueues all K steps,
+    # so host issue jitter on one rank cannot show up as peer wait inside another rank's step
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(int(min(0.2 * args.steps + 2.0, 100.0) * 2.0e6))
     for k in range(args.steps):
         with torch.cuda.stream(s):
             flush.fill_(k & 0xFF)  # evict L2 (126 MB) before every timed step; outside the events
