@@ -1,7 +1,7 @@
 """Benchmark of the synchronous data-parallel SGD step (BASELINE.json metric:
 train samples/sec, device-timed, max over ranks).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--precision tf32|fp32]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--precision 3xtf32|fp32]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
     python bench.py --impl reference     # the CPU oracle on the host cores (reference arm)
 
@@ -30,6 +30,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}
+NVLINK_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md; 900 nominal)
 TF32_PER_BF16 = 1.1 / 2.25  # nominal dense ratio (B200_PROFILING.md table)
 FP32_FMA_PER_SM_CLK = 128  # CUDA cores per SM (4 SMSP x 32 lanes), 2 flop per FMA
 
@@ -125,10 +126,10 @@ def kernel_work(name: str):
         return None
     if kind == "avg_update":
         return "byte", ((20 if a["v"] else 12) + (8 if a.get("planes") else 0)) * a["n"], "hbm"
-    if kind == "fused_avg_update":  # per owned element (n/P of them): P gradient reads (P-1 over NVLink),
-        # w (+ v) read, w stored to all P replicas, v and G stored locally
-        P, v = a["P"], a["v"]
-        return "byte", (8 * P + 8 + 8 * v) * (a["n"] // P), "hbm"
+    if kind == "fused_avg_update":  # NVLink-bound: per direction per GPU, the P-1 peers'
+        # gradients of the owned n/P slice come in and the P-1 peers' updated w slices are stored in
+        P = a["P"]
+        return "byte", 8 * (a["n"] // P) * (P - 1), "nvlink"
     if kind == "head_softmax_xent":  # read A rows, write dZ_{L-1} (and dZ_L, loss)
         return "byte", 4 * a["rows"] * (a["d"] * (1 + a["dgrad"]) + a["C"] + 1), "hbm"
     if kind == "splitk_reduce":
@@ -163,15 +164,19 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
     top_name, top = max(worked.items(), key=lambda kv: kv[1]["ms"])
     per_launch_s = top["ms"] / 1e3 / top["cnt"]
     per_launch_work = top["work"] / top["cnt"]
+    # every kernel of the timing pass runs alone (serialised graph): the burst peaks apply
     if top["bound"] == "hbm":
         achieved = per_launch_work / per_launch_s / 1e9
         peak, unit = pk["hbm_gbs"], "GB/s"
+    elif top["bound"] == "nvlink":
+        achieved = per_launch_work / per_launch_s / 1e9
+        peak, unit = NVLINK_GBS, "GB/s"
     elif top["bound"] == "tensor":
         achieved = per_launch_work / per_launch_s / 1e12
-        peak, unit = pk["bf16_tflops_sustained"] * TF32_PER_BF16, "TFLOP/s"
+        peak, unit = pk["bf16_tflops"] * TF32_PER_BF16, "TFLOP/s"
     elif top["bound"] == "tensor3x":  # fp32-equivalent flops vs one third of the tf32 peak
         achieved = per_launch_work / per_launch_s / 1e12
-        peak, unit = pk["bf16_tflops_sustained"] * TF32_PER_BF16 / 3, "TFLOP/s"
+        peak, unit = pk["bf16_tflops"] * TF32_PER_BF16 / 3, "TFLOP/s"
         top["bound"] = "tensor"
     else:  # fp32 CUDA-core FMA peak at the clock observed under load
         achieved = per_launch_work / per_launch_s / 1e12
@@ -189,15 +194,22 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
                   "avg_update": "avg_update_kernel<1>", "fused_avg_update": "fused_avg_update_kernel", "head_softmax_xent": "head_kernel",
                   "colsum": "colsum_kernel", "splitk_reduce": "splitk_reduce_kernel", "conv_bwd": "conv_bwd_kernel",
                   "conv_fwd": "conv_fwd_kernel"}
-    traffic = None
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     key = next((v for k, v in ncu_kernel.items() if top_name.startswith(k)), None)
     if os.path.exists(tp) and key:
         tj = json.load(open(tp))
-        traffic = next((v for k, v in tj.items() if k == f"{config}:{key}" or k.startswith(f"{config}:{key}<")
-                        or k.startswith(f"{config}:{key}(")), None)
+        hit = next((k for k in tj if k == f"{config}:{key}" or k.startswith(f"{config}:{key}<")
+                    or k.startswith(f"{config}:{key}(")), None)
+        if hit:
+            traffic = tj[hit]
+            meta = tj.get("_meta", {}).get(config, {})
+            traffic_src = f"profiles/ncu_traffic.json [{hit}] from {meta.get('capture', 'ncu --set full')}" \
+                          f" at commit {meta.get('commit', '?')}"
     return {"kernel": top_name, "bound": top["bound"], "achieved": round(achieved, 3), "peak": round(peak, 1),
-            "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic,
+            "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+            "peak_kind": {"GB/s": "measured copy" if top["bound"] == "hbm" else "measured NVLink peer copy per direction",
+                          "TFLOP/s": "measured bf16 burst x tf32/bf16 nominal ratio" + (" / 3 (3xTF32)" if top_name.startswith("gemm_tc3x") else "")}.get(unit),
             "work_per_launch": per_launch_work, "launch_us": round(per_launch_s * 1e6, 3),
             "share_of_kernel_time": round(top["ms"] / total, 3),
             "launch_overhead_us_subtracted": round(over_ms * 1e3, 3),
@@ -209,27 +221,61 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
 
 
 # ----------------------------------------------------------------------------- CPU oracle baseline
+def host_cpu():
+    """(nproc, CPU model) of the host running the oracle."""
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
 def cpu_oracle(cfg: dict, budget_s: float, X, y):
-    """The oracle as it stands (single-threaded C, f64) on a bounded sample: whole SGD steps of the
-    same global batch, P=1 (the sequential definition the DP step must equal)."""
+    """The oracle as it stands (plain C, f64) on a bounded sample of the workload, as SURVEY.md §8(d)
+    plans it: the oracle's own DP(T) simulation -- T = the host's cores (a power of two dividing B,
+    <= 64) simulated ranks, one host thread per rank for the local gradients (O5-O7, ctypes releases the
+    GIL), then the single-threaded ascending-rank fold (O9) and update (O10-O11) -- at a global batch of
+    T * b_s rows per step (the per-sample cost of an MLP/CNN step does not depend on the batch), for
+    about budget_s seconds.  By I1 its result is the sequential SGD step's."""
+    from concurrent.futures import ThreadPoolExecutor
+
     import numpy as np
 
     import oracle
+    nproc, model = host_cpu()
+    T = 1
+    while T * 2 <= min(nproc, 64) and cfg["B"] % (T * 2) == 0:
+        T *= 2
     net = oracle.Net.from_cfg(cfg)
     w = oracle.init_params(net, 42).astype(np.float64)
     v = np.zeros_like(w)
-    B = cfg["B"]
+    # rows per simulated rank per step: about 1/8 of budget_s per step, from a one-row probe
+    t0 = time.perf_counter()
+    oracle.local_grad(net, w, X, y, 1, 0, 0, 1)
+    per_row = max(time.perf_counter() - t0, 1e-6)
+    b_s = int(max(1, min(cfg["B"] // T, budget_s / 8 / per_row)))
+    Bs = T * b_s
+    pool = ThreadPoolExecutor(T)
     t0 = time.perf_counter()
     steps = 0
     while True:
-        g, _ = oracle.local_grad(net, w, X, y, B, steps, 0, 1)
-        oracle.avg_update(g, w, v, 1, cfg["lr"], cfg["mu"])
+        res = list(pool.map(lambda r: oracle.local_grad(net, w, X, y, Bs, steps, r, T), range(T)))
+        G = oracle.fold(np.stack([g for g, _ in res]))
+        oracle.avg_update(G, w, v, T, cfg["lr"], cfg["mu"])
         steps += 1
         if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
-    return {"value": round(B * steps / dt, 3), "unit": "samples/s", "cores": 1, "kind": "oracle",
-            "sample": f"{steps} full SGD steps of {cfg['name']} (B={B}) in f64 on 1 host thread, {dt:.1f} s"}
+    pool.shutdown()
+    return {"value": round(Bs * steps / dt, 3), "unit": "samples/s", "cores": T, "kind": "oracle",
+            "nproc": nproc, "cpu_model": model,
+            "sample": f"{steps} DP({T}) SGD steps of {cfg['name']} at a global batch of {Bs} rows ({b_s} per "
+                      f"simulated rank, same per-sample work as B={cfg['B']}), oracle f64 (gcc -O2, no contraction), "
+                      f"{T} host threads for the local gradients, fold + update single-threaded, {dt:.1f} s"}
 
 
 # ----------------------------------------------------------------------------- main
@@ -238,8 +284,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
-    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "tf32", "3xtf32"])
+    # cfg4 (the largest config; the north_star's scaling target is quoted on it)
+    ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "3xtf32"])
     ap.add_argument("--impl", default="mtx", choices=["mtx", "reference"])
     ap.add_argument("--bucket-mb", type=float, default=1.0)
     ap.add_argument("--reduce", default="fused", choices=["nccl", "ordered", "fused", "layerwise", "zero1"],
@@ -268,7 +315,7 @@ def main():
         line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": "samples/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(cfg["B"] / cb["value"] * 1e3, 3),
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": {"workload": f"{args.config}: {desc(cfg)}", "global_batch": cfg["B"]},
+                "data": "synthetic", "config": run_config(args, cfg, args.gpus),
                 "cpu_baseline": cb,
                 "e2e": {"value": cb["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -289,7 +336,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     tc_ok = "tcgen05" in mtx.mtx_build_info()
-    prec = {"fp32": P.MTX_FP32, "tf32": P.MTX_TF32, "3xtf32": P.MTX_3XTF32}.get(
+    prec = {"fp32": P.MTX_FP32, "3xtf32": P.MTX_3XTF32}.get(
         args.precision, P.MTX_3XTF32 if tc_ok else P.MTX_FP32)
     uid = P.nccl_uid_broadcast(rank, world)
     X, y = S.dataset(cfg)
@@ -313,19 +360,32 @@ def main():
     clocks = Clocks(local)
     clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    barrier()
     # head start: the stream spins (outside every event pair) while the host enqueues all K steps,
-    # so host issue jitter on one rank cannot show up as peer wait inside another rank's step
-    with torch.cuda.stream(s):
-        torch.cuda._sleep(int(min(0.2 * args.steps + 2.0, 100.0) * 2.0e6))
-    for k in range(args.steps):
+    # so host issue jitter on one rank cannot show up as peer wait inside another rank's step.  The spin
+    # must still be running when the enqueue loop ends (checked; else retried with a longer spin).
+    spin_ms = min(0.2 * args.steps + 2.0, 100.0)
+    for attempt in range(4):
+        barrier()
+        spun = torch.cuda.Event()
         with torch.cuda.stream(s):
-            flush.fill_(k & 0xFF)  # evict L2 (126 MB) before every timed step; outside the events
-            ev[k][0].record(s)
-        rep.step()
-        with torch.cuda.stream(s):
-            ev[k][1].record(s)
-    barrier()
+            torch.cuda._sleep(int(spin_ms * 2.0e6))
+            spun.record(s)
+        for k in range(args.steps):
+            with torch.cuda.stream(s):
+                flush.fill_(k & 0xFF)  # evict L2 (126 MB) before every timed step; outside the events
+                ev[k][0].record(s)
+            rep.step()
+            with torch.cuda.stream(s):
+                ev[k][1].record(s)
+        covered = not spun.query()  # the GPU was still spinning when the host finished enqueueing
+        if world > 1:
+            cv = torch.tensor([1 if covered else 0])
+            dist.all_reduce(cv, op=dist.ReduceOp.MIN)
+            covered = bool(cv[0])
+        barrier()
+        if covered:
+            break
+        spin_ms *= 3
     clk = clocks.stop()
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
     loss = mtx.mtx_train_step(rep.ctx, rep.step_idx, True, rep.s)
@@ -385,6 +445,15 @@ def main():
            "api": "mtx_train_step_host_async x K + mtx_sync (host timer around the loop)",
            "final_loss": round(float(e2e_loss), 6)}
 
+    # invariant I2 on the hardware: every replica's parameters and velocity bit-identical after the run
+    dig = rep.digest()
+    digs = [dig]
+    if world > 1:
+        dd = torch.tensor([dig & 0x7FFFFFFFFFFFFFFF, dig >> 63], dtype=torch.int64)
+        outs = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(outs, dd)
+        digs = [int(o[0]) | (int(o[1]) << 63) for o in outs]
+
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_oracle(cfg, args.cpu_budget, X[:100_000], y[:100_000])
@@ -394,18 +463,24 @@ def main():
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": {P.MTX_TF32: "tf32", P.MTX_3XTF32: "f32 (3xtf32 tensor cores)"}.get(prec, "f32"),
                 "data": "synthetic",
-                "config": {"workload": f"{args.config}: {desc(cfg)}", "global_batch": cfg["B"],
-                           "local_batch": cfg["B"] // world, "parallelism": f"dp{world}",
-                           "bucket_mb": args.bucket_mb, "reduce": args.reduce if world > 1 else "none (P=1)",
-                           "l2": "flushed (256 MiB write) before every timed step",
-                           "engine": mtx.mtx_build_info()},
+                "config": run_config(args, cfg, world), "engine": mtx.mtx_build_info(),
                 "per_rank_ms": [round(t, 3) for t in t_all], "final_loss": loss,
+                "replicas_bit_identical": len(set(digs)) == 1, "param_digest": f"{digs[0]:016x}",
+                "head_start": {"spin_ms": spin_ms, "covered_enqueue": covered},
                 "gpu_launches": launches * args.steps, "launches_per_step": launches,
                 "clocks": clk, "roofline": roof, "cpu_baseline": cb, "e2e": e2e}
         print(json.dumps(line), flush=True)
     rep.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_config(args, cfg, world):
+    """The workload both arms report (identical dicts: the driver compares them)."""
+    return {"workload": f"{args.config}: {desc(cfg)}", "global_batch": cfg["B"], "local_batch": cfg["B"] // world,
+            "parallelism": f"dp{world}", "bucket_mb": args.bucket_mb,
+            "reduce": args.reduce if world > 1 else "none (P=1)",
+            "l2": "flushed (256 MiB write) before every timed step"}
 
 
 def desc(cfg):

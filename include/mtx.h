@@ -68,11 +68,11 @@ typedef enum { MTX_MLP = 0, MTX_CNN = 1 } mtx_model_kind;
 
 /* Arithmetic of the local forward/backward contractions (north_star tolerance tiers).
  *  MTX_FP32:   SIMT FFMA, fp32 products, blocked fp32 sums (parity gate 1e-5 vs the f64 oracle).
- *  MTX_TF32:   tcgen05.mma kind::tf32 on the 5th-gen tensor cores, operands fed by TMA,
- *              fp32 accumulation in TMEM.  The tensor core TRUNCATES fp32 operands to
- *              TF32 (measured, A12); on these workloads that leaves 1e-2-level
- *              max-norm gradient errors (truncation bias + ReLU-kink flips), so this mode
- *              is a throughput mode whose parity is reported, not gated at 1e-3.
+ *  MTX_TF32:   NOT a product precision: mtx_init returns MTX_ERR_UNSUPPORTED unless the
+ *              development variable MTX_DEV_TF32=1 is set.  One tcgen05.mma kind::tf32 per
+ *              k-step; the tensor core truncates fp32 operands to TF32 (measured, DESIGN.md
+ *              A12), which leaves 1e-2..2.4e-1 max-norm gradient errors on these workloads --
+ *              it cannot meet the north_star's 1e-3 TF32 tier (A22).
  *  MTX_3XTF32: tcgen05 with each operand split into its TF32 part and a TF32 residual,
  *              3 MMAs per k-step (big.small + small.big + big.big): fp32-accurate, gated
  *              at 1e-5 like MTX_FP32.
@@ -88,8 +88,11 @@ typedef enum { MTX_FP32 = 0, MTX_TF32 = 1, MTX_3XTF32 = 2 } mtx_precision;
  *                      memory (CUDA IPC mappings exchanged at bind time, world <= 8 on one
  *                      node): rank r pulls every rank's gradient on its 1/P slice, folds them
  *                      in ascending rank order (bit-exact with ORDERED), applies x fl(1/P) and
- *                      the momentum update, and stores w, v, G into every replica; two
- *                      cross-GPU flag barriers (10 s timeout -> MTX_ERR_NCCL) bracket it. */
+ *                      the momentum update and stores the updated w into every replica; v and
+ *                      the reduced G stay sharded with their owner (ZeRO-1 style) and are
+ *                      assembled from the peers by mtx_get_buffer / mtx_param_digest.  Cross-GPU
+ *                      flag barriers (10 s timeout -> MTX_ERR_NCCL, the context then refuses
+ *                      further steps) bracket it. */
 /*  MTX_REDUCE_LAYERWISE: the paper's own design ("an ordered list of reduction
  *                      operators ... sequentially synchronizes each layer"): after the backward,
  *                      one ncclAllReduce per variable (W_1, b_1, W_2, ...) in canonical order,
@@ -283,6 +286,24 @@ mtx_status mtx_read_timing(mtx_ctx *ctx, char *names_buf, uint64_t names_len, do
 mtx_status mtx_debug_gemm(mtx_ctx *ctx, int32_t engine, int32_t M, int32_t N, int32_t K, int32_t ta, int32_t tb,
                           int32_t epi, const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc,
                           const float *bias, const float *mask, int64_t ldm, void *stream);
+
+/* Diagnostic: the P > 1 reduction arithmetic on ONE GPU with P simulated ranks (P <= 8), so the fold,
+ * the x fl(1/P) average and the update of the multi-GPU modes can be checked against the oracle on a
+ * single-GPU box.  No communicator is used.
+ *  g[q], G[q]: device buffers of n + 32 floats per simulated rank q (the local gradient g_q with its
+ *              loss sum at index n; G_q receives the reduced sum); w[q], v[q]: n floats (v may be NULL
+ *              when momentum == 0).  n % 4 == 0, 16-byte aligned; all borrowed, updated in place.
+ *  mode MTX_REDUCE_FUSED:   the product's peer-memory protocol -- per simulated rank, on P concurrent
+ *              streams: peer_barrier, fused_avg_update of the rank's owned slice (ascending-rank fold,
+ *              x fl(1/P), momentum update, w stored to every replica; v_q and G_q written on slice q
+ *              only; the folded loss to G_q[n + 1]), peer_barrier.
+ *  mode MTX_REDUCE_ORDERED: every simulated rank folds all g_q in ascending rank order into G_r
+ *              (the loss slot included) and updates its own (w_r, v_r) with x fl(1/P).
+ *  other modes: MTX_ERR_UNSUPPORTED (their sum is NCCL's arithmetic on P GPUs).
+ * Asynchronous on `stream`; a non-finite average sets the numeric flag (MTX_ERR_NUMERIC at the next
+ * synchronising call). */
+mtx_status mtx_debug_reduce(mtx_ctx *ctx, int32_t mode, int32_t P, void *const *g, void *const *w, void *const *v,
+                            void *const *G, uint64_t n, float lr, float momentum, void *stream);
 
 /* Short description of the build (arch, NCCL version, GEMM engine). */
 const char *mtx_build_info(void);

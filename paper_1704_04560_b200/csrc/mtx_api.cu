@@ -118,6 +118,10 @@ struct mtx_ctx {
     uint8_t *ws = nullptr;
     uint64_t ws_bytes = 0;
     float *params = nullptr, *vel = nullptr, *grads = nullptr, *gather = nullptr;
+    float *gred = nullptr;  // MTX_REDUCE_FUSED: reduced sum G (+ loss slot), sharded by owner
+    // the buffer holding the reduced gradient sum G and the loss slot after a step
+    float *gsum() const { return gred ? gred : grads; }
+    int64_t loss_at() const { return N_pad + (gred ? 1 : 0); }
     std::vector<float *> acts;  // MLP: acts[l] = A_l [b][d_l], l = 1..L-1
     // 3xTF32: hi/lo planes of the buffers tensor-core GEMMs consume (registered ranges)
     struct PlaneRange {
@@ -149,6 +153,10 @@ struct mtx_ctx {
     int64_t dbg_floats = 0;
     const void *dbg_key[2] = {nullptr, nullptr};
     int64_t dbg_n[2] = {0, 0};
+    // mtx_debug_reduce: per-simulated-rank flag arrays + epochs, streams, fork/join events
+    uint64_t *dbg_sync = nullptr;
+    cudaStream_t dbg_streams[MAX_PEERS] = {};
+    cudaEvent_t dbg_ev = nullptr, dbg_ev_join[MAX_PEERS] = {};
     // MTX_REDUCE_FUSED: peer mappings of every rank's workspace
     PeerPtrs pp{};
     std::vector<void *> ipc_opened;
@@ -362,6 +370,9 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     float *vel = (float *)take(4 * c->N_pad);
     float *grads = (float *)take(4 * (c->N_pad + LOSS_SLOT));
     float *gather = c->opt.reduce == MTX_REDUCE_ORDERED ? (float *)take(4 * c->world * (c->N_pad + LOSS_SLOT)) : nullptr;
+    // FUSED: the reduced sum G lives in its own buffer, never written by the backward, so a peer can read
+    // this rank's G slice (mtx_get_buffer) while this rank already computes the next step's local g
+    float *gred = (c->world > 1 && c->opt.reduce == MTX_REDUCE_FUSED) ? (float *)take(4 * (c->N_pad + LOSS_SLOT)) : nullptr;
     std::vector<float *> acts, fcA, dzs;
     std::vector<float *> cP, cDP;
     std::vector<uint8_t *> cArg;
@@ -451,7 +462,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     unsigned *counters = (unsigned *)take(4 * COUNTERS_PER_LANE * lanes);
     uint8_t *misc = take(512 + 128 * (uint64_t)c->world);
     if (assign) {
-        c->params = params; c->vel = vel; c->grads = grads; c->gather = gather;
+        c->params = params; c->vel = vel; c->grads = grads; c->gather = gather; c->gred = gred;
         c->acts = acts; c->fcA = fcA; c->dzs = dzs; c->lanes = lanes;
         c->convP = cP; c->convDP = cDP; c->convArg = cArg;
         c->dz[0] = dz0; c->dz[1] = dz1; c->dzL = dzL; c->loss_rows = loss_rows;
@@ -505,8 +516,17 @@ struct Runner {
     // Issue fn() on side lane ln, ordered after everything issued so far on the caller's stream.
     template <class F>
     mtx_status on_lane(int ln, F fn) {
-        // no lane, or the per-kernel timing pass (kernels timed in isolation, like ncu's launch list)
-        if (ln <= 0 || ln >= c->lanes || !c->side[ln - 1] || c->hook.enabled) return fn();
+        if (ln <= 0 || ln >= c->lanes || !c->side[ln - 1]) return fn();
+        if (c->hook.enabled) {
+            // per-kernel timing pass: serialised on the caller's stream (every kernel timed alone, like
+            // ncu's launch list) but with the lane's launch plan -- its SM budget and scratch -- so each
+            // kernel is the one the timed graph runs
+            const int keep_lane = lane;
+            lane = ln;
+            const mtx_status st = fn();
+            lane = keep_lane;
+            return st;
+        }
         CK(cudaEventRecord(c->ev_lane[0], s));
         CK(cudaStreamWaitEvent(c->side[ln - 1], c->ev_lane[0], 0));
         const cudaStream_t keep = s;
@@ -918,7 +938,7 @@ mtx_status capture(mtx_ctx *c, cudaStream_t s, bool staged, int land, bool timed
     // the pipelined host path's per-step result: the loss sum lands in pinned host memory from
     // inside the graph (a memcpy node), so the step costs no separate read-back call
     if (!st && land >= 0) {
-        cudaError_t em = cudaMemcpyAsync(c->h_loss_ring, c->grads + c->N_pad + (c->fused ? 1 : 0), sizeof(float),
+        cudaError_t em = cudaMemcpyAsync(c->h_loss_ring, c->gsum() + c->loss_at(), sizeof(float),
                                          cudaMemcpyDeviceToHost, s);
         if (em != cudaSuccess) st = fail(c, MTX_ERR_CUDA, "loss read-back node: %s", cudaGetErrorString(em));
     }
@@ -956,11 +976,42 @@ mtx_status run_step(mtx_ctx *c, cudaStream_t s, bool staged, int land = -1) {
     return MTX_OK;
 }
 
+// Asynchronous NCCL failure (a peer died, a network/NVLink error): the paper's system is not fault
+// tolerant, so the whole world aborts -- abort the communicator and poison the context.
+mtx_status poll_nccl(mtx_ctx *c) {
+    if (!c->comm) return MTX_OK;
+    ncclResult_t ar = ncclSuccess;
+    ncclResult_t r = ncclCommGetAsyncError(c->comm, &ar);
+    if (r != ncclSuccess) ar = r;
+    if (ar != ncclSuccess && ar != ncclInProgress) {
+        ncclCommAbort(c->comm);
+        c->comm = nullptr;
+        return fail(c, MTX_ERR_NCCL, "asynchronous NCCL error: %s", ncclGetErrorString(ar));
+    }
+    return MTX_OK;
+}
+
+// Synchronise stream s while polling NCCL for asynchronous errors (a hung collective never returns
+// from cudaStreamSynchronize; polling lets a failed peer abort this rank instead).
+mtx_status sync_polling(mtx_ctx *c, cudaStream_t s) {
+    if (!c->comm) {
+        CK(cudaStreamSynchronize(s));
+        return MTX_OK;
+    }
+    for (;;) {
+        cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) CK(q);
+        if (mtx_status st = poll_nccl(c)) return st;
+    }
+    return poll_nccl(c);
+}
+
 // D2H of the loss slot and numeric flag, synchronise, then report.
 mtx_status sync_loss(mtx_ctx *c, cudaStream_t s, float *host_loss) {
-    CK(cudaMemcpyAsync(c->h_loss, c->grads + c->N_pad + (c->fused ? 1 : 0), sizeof(float), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->h_loss, c->gsum() + c->loss_at(), sizeof(float), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    if (mtx_status st = sync_polling(c, s)) return st;
     c->last_loss = (float)((double)c->h_loss[0] / (double)c->B);
     if (host_loss) *host_loss = c->last_loss;
     if (c->h_flag[0] & 2) return fail(c, MTX_ERR_NCCL, "peer barrier timeout (a rank did not reach the step)");
@@ -969,9 +1020,11 @@ mtx_status sync_loss(mtx_ctx *c, cudaStream_t s, float *host_loss) {
 }
 
 // MTX_REDUCE_FUSED keeps velocity and the reduced gradient sharded: rank q's copy is authoritative
-// only on its owned slice S_q (p2p_fused.cu).  Pull every peer's slices into the local buffers so a
-// diagnostic read sees the full state.  Call after a synchronisation: the step's second peer barrier
-// guarantees every owner finished writing.
+// only on its owned slice S_q (p2p_fused.cu).  Pull every peer's slices into the local buffers' other
+// slices (never read by the kernels) so a diagnostic read sees the full state.  Call after a
+// synchronisation: the step's second peer barrier guarantees every owner finished writing, and an owner
+// cannot overwrite its slice before this rank reaches the next step's first barrier (v and G are written
+// only by the fused kernel, which runs after that barrier).
 mtx_status assemble_shards(mtx_ctx *c) {
     if (!c->fused || c->world <= 1) return MTX_OK;
     const int64_t n4 = c->N_pad / 4;
@@ -979,7 +1032,7 @@ mtx_status assemble_shards(mtx_ctx *c) {
         if (q == c->rank) continue;
         const int64_t lo = 4 * (n4 * q / c->world), hi = 4 * (n4 * (q + 1) / c->world);
         CK(cudaMemcpyAsync(c->vel + lo, c->pp.v[q] + lo, 4 * (hi - lo), cudaMemcpyDeviceToDevice, c->own));
-        CK(cudaMemcpyAsync(c->grads + lo, c->pp.G[q] + lo, 4 * (hi - lo), cudaMemcpyDeviceToDevice, c->own));
+        CK(cudaMemcpyAsync(c->gred + lo, c->pp.G[q] + lo, 4 * (hi - lo), cudaMemcpyDeviceToDevice, c->own));
     }
     CK(cudaStreamSynchronize(c->own));
     return MTX_OK;
@@ -996,7 +1049,7 @@ mtx_status refresh_param_planes(mtx_ctx *c, cudaStream_t s) {
 mtx_status check_flag(mtx_ctx *c, cudaStream_t s) {
     if (!c->flag) return MTX_OK;
     CK(cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    if (mtx_status st = sync_polling(c, s)) return st;
     if (c->h_flag[0] & 2) return fail(c, MTX_ERR_NCCL, "peer barrier timeout (a rank did not reach the step)");
     if (c->h_flag[0]) return fail(c, MTX_ERR_NUMERIC, "non-finite averaged gradient");
     return MTX_OK;
@@ -1043,7 +1096,8 @@ mtx_status map_peers(mtx_ctx *c) {
             c->ipc_opened.push_back(p);
             ws_r = (uint8_t *)p + all[r].off;
         }
-        c->pp.g[r] = c->pp.G[r] = (float *)(ws_r + rel(c->grads));
+        c->pp.g[r] = (float *)(ws_r + rel(c->grads));
+        c->pp.G[r] = (float *)(ws_r + rel(c->gred));
         c->pp.w[r] = (float *)(ws_r + rel(c->params));
         c->pp.v[r] = (float *)(ws_r + rel(c->vel));
         c->pp.flags[r] = (uint64_t *)(ws_r + rel(c->flags));
@@ -1072,6 +1126,12 @@ mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t ui
     if (model->global_batch <= 0 || model->global_batch % world) return MTX_ERR_INVALID_ARG;
     if (opt->precision != MTX_FP32 && opt->precision != MTX_TF32 && opt->precision != MTX_3XTF32)
         return MTX_ERR_INVALID_ARG;
+    // 1xTF32 cannot meet the north_star's 1e-3 on these workloads (A22): it is not a product
+    // precision, only a development mode behind MTX_DEV_TF32=1 (kernel experiments, never the tests or bench)
+    if (opt->precision == MTX_TF32) {
+        const char *dev = getenv("MTX_DEV_TF32");
+        if (!dev || atoi(dev) != 1) return MTX_ERR_UNSUPPORTED;
+    }
     if (opt->reduce < MTX_REDUCE_NCCL || opt->reduce > MTX_REDUCE_ZERO1) return MTX_ERR_INVALID_ARG;
     if (opt->reduce == MTX_REDUCE_FUSED && world > MAX_PEERS) return MTX_ERR_UNSUPPORTED;
     mtx_ctx *c = new mtx_ctx();
@@ -1102,6 +1162,16 @@ mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t ui
     mtx_status st = build_layout(c);
     if (st) { delete c; return st; }
     if (c->classes > 16) { delete c; return MTX_ERR_UNSUPPORTED; }
+    {  // the fused head (last layer GEMV + loss + dlogits) stages W_L in shared memory: d_{L-1} <= 1024
+        const int d_head = c->kind == MTX_MLP ? c->dims[c->dims.size() - 2]
+                                              : (c->fc.size() > 1 ? c->fc[c->fc.size() - 2] : -1);
+        int d_flat = 0;
+        if (c->kind != MTX_MLP && !c->convs.empty()) d_flat = c->convs.back().hp * c->convs.back().wp * c->convs.back().co;
+        if ((d_head > 1024) || (c->kind != MTX_MLP && c->fc.size() == 1 && d_flat > 1024)) {
+            delete c;
+            return MTX_ERR_UNSUPPORTED;
+        }
+    }
     if (cudaSetDevice(device) != cudaSuccess) { delete c; return MTX_ERR_CUDA; }
     if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->comm_s, cudaStreamNonBlocking) != cudaSuccess ||
@@ -1368,7 +1438,7 @@ mtx_status mtx_sync(mtx_ctx *c, float *host_loss, void *stream) {
     if (st) return st;
     cudaStream_t s = pick(c, stream);
     CK(cudaMemcpyAsync(c->h_flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    if ((st = sync_polling(c, s))) return st;
     CK(cudaStreamSynchronize(c->copy_s));
     if (c->async_steps > 0) c->last_loss = (float)((double)c->h_loss_ring[0] / (double)c->B);
     if (host_loss) *host_loss = c->last_loss;
@@ -1417,7 +1487,7 @@ mtx_status mtx_get_buffer(mtx_ctx *c, int32_t which, float *host_out, uint64_t c
     if (count != (uint64_t)c->N) return fail(c, MTX_ERR_SHAPE, "count %llu != N %lld", (unsigned long long)count,
                                              (long long)c->N);
     float *src = which == MTX_BUF_PARAMS ? c->params : which == MTX_BUF_VELOCITY ? c->vel
-               : which == MTX_BUF_GRADS ? c->grads : nullptr;
+               : which == MTX_BUF_GRADS ? c->gsum() : nullptr;
     if (!src) return fail(c, MTX_ERR_INVALID_ARG, "buffer id %d", which);
     CK(cudaDeviceSynchronize());
     if (which != MTX_BUF_PARAMS && (st = assemble_shards(c))) return st;
@@ -1564,6 +1634,85 @@ mtx_status mtx_debug_gemm(mtx_ctx *c, int32_t engine, int32_t M, int32_t N, int3
     return MTX_OK;
 }
 
+// Simulated P-rank reduction on ONE GPU (diagnostic; the driver's round-end box has one GPU): the P > 1
+// arithmetic of the reduce modes run on P sets of buffers on this device, so the fold, x fl(1/P) and the
+// update are checked bit-exact against the oracle for any P <= 8 ("P > 1 on one GPU").
+mtx_status mtx_debug_reduce(mtx_ctx *c, int32_t mode, int32_t P, void *const *g, void *const *w, void *const *v,
+                            void *const *G, uint64_t n, float lr, float momentum, void *stream) {
+    mtx_status st = live(c);
+    if (st) return st;
+    if (c->state == mtx_ctx::S_INIT) return fail(c, MTX_ERR_STATE, "bind the workspace first");
+    if (P < 1 || P > MAX_PEERS || !g || !w || !G || n == 0 || n % 4) return fail(c, MTX_ERR_INVALID_ARG, "debug_reduce args");
+    const bool has_v = momentum != 0.f;
+    for (int q = 0; q < P; q++) {
+        if (!g[q] || !w[q] || !G[q] || (has_v && (!v || !v[q])))
+            return fail(c, MTX_ERR_INVALID_ARG, "null buffer of simulated rank %d", q);
+        if (((uintptr_t)g[q] | (uintptr_t)w[q] | (uintptr_t)G[q] | (has_v ? (uintptr_t)v[q] : 0)) & 15)
+            return fail(c, MTX_ERR_INVALID_ARG, "buffers must be 16-byte aligned");
+    }
+    cudaStream_t s = pick(c, stream);
+    const int64_t stride = (int64_t)n + LOSS_SLOT;
+    if (mode == MTX_REDUCE_ORDERED) {
+        // every rank gathers all g_q (P x [n + loss slot]) and folds them in ascending rank order, then
+        // updates its own replica: G_r = ((g_0 + g_1) + ...) + g_{P-1};  avg_update(G_r, w_r, v_r, 1/P)
+        const int64_t need = (int64_t)P * stride;
+        if (need > c->dbg_floats) {
+            CK(cudaStreamSynchronize(s));
+            if (c->dbg_planes) cudaFree(c->dbg_planes);
+            c->dbg_planes = nullptr;
+            c->dbg_floats = 0;
+            CK(cudaMalloc(&c->dbg_planes, 4 * need));
+            c->dbg_floats = need;
+        }
+        c->dbg_key[0] = c->dbg_key[1] = nullptr;  // the scratch no longer holds engine-2 planes
+        for (int q = 0; q < P; q++)
+            CK(cudaMemcpyAsync(c->dbg_planes + q * stride, g[q], 4 * stride, cudaMemcpyDeviceToDevice, s));
+        for (int r = 0; r < P; r++) {
+            CK(ordered_fold(c->dbg_planes, P, stride, stride, (float *)G[r], s, nullptr));
+            CK(avg_update((float *)G[r], (float *)w[r], has_v ? (float *)v[r] : nullptr, (int64_t)n, 1.0f / (float)P,
+                          lr, momentum, c->flag, nullptr, 0, 1, s, nullptr));
+        }
+        return MTX_OK;
+    }
+    if (mode != MTX_REDUCE_FUSED) return fail(c, MTX_ERR_UNSUPPORTED, "mode %d is NCCL arithmetic (needs P GPUs)", mode);
+    // FUSED: the product protocol with P simulated ranks on P concurrent streams of this GPU -- per rank
+    // peer_barrier -> fused_avg_update (owned slice: rank-ordered fold, x fl(1/P), update, w to every
+    // replica) -> peer_barrier, with PeerPtrs pointing at the P local buffer sets and per-rank flag arrays
+    PeerPtrs pp{};
+    if (!c->dbg_sync) {
+        CK(cudaMalloc(&c->dbg_sync, 8 * (MAX_PEERS * MAX_PEERS + MAX_PEERS)));
+        CK(cudaMemset(c->dbg_sync, 0, 8 * (MAX_PEERS * MAX_PEERS + MAX_PEERS)));
+        for (int q = 0; q < MAX_PEERS; q++) {
+            CK(cudaStreamCreateWithFlags(&c->dbg_streams[q], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c->dbg_ev_join[q], cudaEventDisableTiming));
+        }
+        CK(cudaEventCreateWithFlags(&c->dbg_ev, cudaEventDisableTiming));
+    }
+    for (int q = 0; q < P; q++) {
+        pp.g[q] = (float *)g[q];
+        pp.G[q] = (float *)G[q];
+        pp.w[q] = (float *)w[q];
+        pp.v[q] = has_v ? (float *)v[q] : nullptr;
+        pp.flags[q] = c->dbg_sync + MAX_PEERS * q;
+    }
+    // fresh epochs for every call (each call is a new "world")
+    CK(cudaMemsetAsync(c->dbg_sync, 0, 8 * (MAX_PEERS * MAX_PEERS + MAX_PEERS), s));
+    CK(cudaEventRecord(c->dbg_ev, s));
+    for (int r = 0; r < P; r++) {
+        cudaStream_t sr = c->dbg_streams[r];
+        uint64_t *epoch = c->dbg_sync + MAX_PEERS * MAX_PEERS + r;
+        CK(cudaStreamWaitEvent(sr, c->dbg_ev, 0));
+        CK(peer_barrier(pp, P, r, epoch, c->flag, sr, nullptr));
+        CK(fused_avg_update(pp, P, r, (int64_t)n, lr, momentum, has_v, c->flag, nullptr, 0, 1, sr, nullptr));
+        CK(peer_barrier(pp, P, r, epoch, c->flag, sr, nullptr));
+    }
+    for (int r = 0; r < P; r++) {
+        CK(cudaEventRecord(c->dbg_ev_join[r], c->dbg_streams[r]));
+        CK(cudaStreamWaitEvent(s, c->dbg_ev_join[r], 0));
+    }
+    return MTX_OK;
+}
+
 const char *mtx_build_info(void) {
     static char buf[256];
     int v = 0;
@@ -1607,6 +1756,12 @@ mtx_status mtx_finalize(mtx_ctx *c) {
     if (c->ev_cfork) cudaEventDestroy(c->ev_cfork);
     if (c->h_flag) cudaFreeHost(c->h_flag);
     if (c->dbg_planes) cudaFree(c->dbg_planes);
+    if (c->dbg_sync) cudaFree(c->dbg_sync);
+    for (int q = 0; q < MAX_PEERS; q++) {
+        if (c->dbg_streams[q]) cudaStreamDestroy(c->dbg_streams[q]);
+        if (c->dbg_ev_join[q]) cudaEventDestroy(c->dbg_ev_join[q]);
+    }
+    if (c->dbg_ev) cudaEventDestroy(c->dbg_ev);
     if (c->tc) tc_destroy(c->tc);
     delete c;
     return MTX_OK;

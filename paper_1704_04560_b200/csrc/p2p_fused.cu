@@ -45,6 +45,9 @@ __global__ void peer_barrier_kernel(PeerPtrs pp, int P, int rank, uint64_t *epoc
     }
     __syncthreads();
     __threadfence_system();
+    // after a timeout the epochs of the ranks are out of step: never wait again (the context is
+    // poisoned at the next synchronising call and refuses further steps)
+    if (*(volatile int *)errflag & 2) return;
     const int q = threadIdx.x;
     if (q < P) st_release_sys(pp.flags[q] + rank, epoch);  // "rank arrived" in q's flag array
     if (q < P) {
@@ -66,6 +69,8 @@ __global__ void __launch_bounds__(256) fused_avg_update_kernel(PeerPtrs pp, int 
                                                              float invP, float lr, float mu, int *flag, int64_t *win,
                                                              int64_t B, int64_t n_data, int64_t loss_idx) {
     pdl_wait();
+    // a peer barrier timed out: peer gradients may be partly written -- load and store nothing
+    if (*(volatile int *)flag & 2) return;
     bool bad = false;
     for (int64_t i = lo4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi4;
          i += (int64_t)gridDim.x * blockDim.x) {

@@ -75,6 +75,8 @@ def _load():
         "mtx_read_timing": [vp, C.c_char_p, C.c_uint64, C.POINTER(C.c_double), i64, C.c_int32, i32, C.c_int32],
         "mtx_finalize": [vp],
         "mtx_sync_update": [vp, vp],
+        "mtx_debug_reduce": [vp, C.c_int32, C.c_int32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                             C.c_uint64, C.c_float, C.c_float, vp],
         "mtx_debug_gemm": [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp,
                            C.c_int64, vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_int64, vp],
     }
@@ -248,6 +250,13 @@ def mtx_debug_gemm(ctx, engine, M, N, K, ta, tb, epi, A, lda, B, ldb, C, ldc, bi
                    stream=None):
     _check(_lib.mtx_debug_gemm(ctx, engine, M, N, K, ta, tb, epi, C_ptr(A), lda, C_ptr(B), ldb, C_ptr(C), ldc,
                                C_ptr(bias), C_ptr(mask), ldm, C_ptr(stream)), ctx, "mtx_debug_gemm")
+
+
+def mtx_debug_reduce(ctx, mode, P, g, w, v, G, n, lr, momentum, stream=None):
+    """g, w, v, G: sequences of P device addresses (v entries may be None when momentum == 0)."""
+    arr = lambda xs: (C.c_void_p * P)(*[C.c_void_p(x) if x else None for x in xs])
+    _check(_lib.mtx_debug_reduce(ctx, mode, P, arr(g), arr(w), arr(v if v is not None else [None] * P), arr(G), n,
+                                 lr, momentum, C_ptr(stream)), ctx, "mtx_debug_reduce")
 
 
 def C_ptr(x):

@@ -26,9 +26,9 @@ def _bench():
     # HBM kernels: bytes they must move
     ("avg_update[n=1000,v=1,planes=1]", ("byte", 28 * 1000, "hbm")),
     ("avg_update[n=1000,v=0,planes=0]", ("byte", 12 * 1000, "hbm")),
-    # P = 2 owner slice of n/2 elements: 2 g reads + w, v reads + w to 2 replicas + v, G = 8P + 16 B
-    ("fused_avg_update[n=669760,P=2,v=1]", ("byte", 32 * 334880, "hbm")),
-    ("fused_avg_update[n=1000,P=4,v=0]", ("byte", 40 * 250, "hbm")),
+    # NVLink bytes per direction per GPU: (P-1) peer gradient slices of n/P floats in, (P-1) w slices in
+    ("fused_avg_update[n=669760,P=2,v=1]", ("byte", 8 * 334880, "nvlink")),
+    ("fused_avg_update[n=1000,P=4,v=0]", ("byte", 8 * 250 * 3, "nvlink")),
     ("colsum[K=512,N=512,splits=8]", ("byte", 4 * 512 * 512, "hbm")),
     ("head_softmax_xent[rows=512,d=512,C=10,dgrad=1]", ("byte", 4 * 512 * (2 * 512 + 11), "hbm")),
     # LeNet: conv1 32x32x3 -> 28x28x6 (k = 5); conv2 backward 10x10x16 outputs, 6*25 inputs each
@@ -54,10 +54,10 @@ def test_roofline_skips_kernels_without_work():
     timing = {"peer_barrier[P=2]": (0.30, 20),
               "gemm_tc3x_fwd[M=256,N=512,K=784,splits=4,cluster=1,pair=0,bn=32]": (0.16, 20),
               "fused_avg_update[n=669760,P=2,v=1]": (0.18, 20)}
-    pk = {"hbm_gbs": 6550.0, "bf16_tflops_sustained": 1500.0}
+    pk = {"hbm_gbs": 6550.0, "bf16_tflops": 1650.0, "bf16_tflops_sustained": 1500.0}
     r = b.roofline(timing, pk, 1965.0, 20, "cfg2")
-    assert r["kernel"] == "fused_avg_update" and r["bound"] == "hbm" and r["unit"] == "GB/s"
-    assert abs(r["achieved"] - 32 * 334880 / (0.18e-3 / 20) / 1e9) < 1e-2
+    assert r["kernel"] == "fused_avg_update" and r["bound"] == "nvlink" and r["unit"] == "GB/s"
+    assert abs(r["achieved"] - 8 * 334880 / (0.18e-3 / 20) / 1e9) < 1e-2 and r["peak"] == 770.0
     assert "peer_barrier" in r["breakdown_us_per_step"]
 
 
@@ -75,4 +75,6 @@ def test_reference_arm_prints_one_json_line():
     assert d["unit"] == "samples/s" and d["higher_is_better"] is True and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
-    assert d["config"]["workload"].startswith("cfg2")
+    assert d["config"]["workload"].startswith("cfg4")  # the default workload: the largest config
+    cb = d["cpu_baseline"]
+    assert cb["cores"] >= 1 and cb["nproc"] >= cb["cores"] and cb["cpu_model"]

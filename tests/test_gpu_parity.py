@@ -2,7 +2,8 @@
 
 Bars: bit-exact for init, broadcast, the fused average +
 update (K6) and integer/index work; max-norm relative error per tensor within
-1e-5 (MTX_FP32) / 1e-3 (MTX_TF32) for gradients, losses and weights.
+1e-5 (the fp32 tier: MTX_FP32 SIMT and MTX_3XTF32 tensor cores) for gradients,
+losses, velocities and weight changes, every step checked from the GPU's own state.
 """
 from __future__ import annotations
 
@@ -11,7 +12,8 @@ import pytest
 
 import mtx_synth as S
 import oracle
-from tests._util import GRAD_TOL, TF32EMU_TOL, TOL, digest_np, maxrel, per_tensor_maxrel
+from tests._parity import step_errors
+from tests._util import GRAD_TOL, TOL, digest_np, maxrel, per_tensor_maxrel
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -22,7 +24,7 @@ if not torch.cuda.is_available():
 import paper_1704_04560_b200 as P  # noqa: E402  (loads libmtx.so; raises if missing)
 from paper_1704_04560_b200 import mtx  # noqa: E402
 
-PRECISIONS = [P.MTX_FP32] + ([P.MTX_3XTF32, P.MTX_TF32] if "tcgen05" in mtx.mtx_build_info() else [])
+PRECISIONS = [P.MTX_FP32] + ([P.MTX_3XTF32] if "tcgen05" in mtx.mtx_build_info() else [])
 
 
 def small_cfg(name, **kw):
@@ -120,6 +122,7 @@ def test_init_bit_exact(name):
 
 # ----------------------------------------------------------------------------- one-step and trajectory parity
 def _gpu_run(cfg, X, y, steps, precision, start=None, start_step=0, **kw):
+    """GPU steps through the C-ABI; per step (loss, G, w after, v after)."""
     r = make(cfg, precision=precision, **kw)
     try:
         r.bcast()
@@ -130,26 +133,18 @@ def _gpu_run(cfg, X, y, steps, precision, start=None, start_step=0, **kw):
         out = []
         for _ in range(steps):
             loss = r.step(want_loss=True)
-            out.append((loss, r.get(P.MTX_BUF_GRADS), r.get(P.MTX_BUF_PARAMS)))
+            out.append((loss, r.get(P.MTX_BUF_GRADS), r.get(P.MTX_BUF_PARAMS), r.get(P.MTX_BUF_VELOCITY)))
         return out
     finally:
         r.close()
 
 
 def _check_step(cfg, X, y, precision, step, start, **kw):
-    """One step from identical params: G and the updated params vs the oracle (P = 1)."""
+    """One step from identical params: G, loss, velocity and weight change vs the oracle (P = 1)."""
     net = oracle.Net.from_cfg(cfg)
-    tab = oracle.tensor_table(net)
-    (loss, G, w1), = _gpu_run(cfg, X, y, 1, precision, start=start, start_step=step, **kw)
-    g_ref, lsum = oracle.local_grad(net, start.astype(np.float64), X, y, cfg["B"], step, 0, 1)
-    tol, gtol = TOL[precision], GRAD_TOL[precision]
-    errs = per_tensor_maxrel(G, g_ref, tab)
-    assert max(errs) <= gtol, errs
-    assert abs(loss - lsum / cfg["B"]) <= tol * abs(lsum / cfg["B"])
-    w_ref = start.astype(np.float64).copy()
-    v_ref = np.zeros_like(w_ref)
-    oracle.avg_update(g_ref, w_ref, v_ref, 1, cfg["lr"], cfg["mu"])
-    assert max(per_tensor_maxrel(w1, w_ref, tab)) <= gtol
+    rec, = _gpu_run(cfg, X, y, 1, precision, start=start, start_step=step, **kw)
+    e = step_errors(net, cfg, X, y, step, start, np.zeros_like(start), rec)
+    assert max(e.values()) <= GRAD_TOL[precision], e
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
@@ -161,20 +156,27 @@ def test_cfg1_one_step(precision):
     _check_step(cfg, X, y, precision, 15, start)  # window wraps around n = 1000
 
 
+def _check_trajectory(cfg, X, y, steps, precision, **kw):
+    """Every step of a GPU trajectory within the fp32 tier of the oracle step from the GPU's own state,
+    and the whole trajectory (losses, final weights) within it of the oracle's own trajectory."""
+    net = oracle.Net.from_cfg(cfg)
+    recs, w_ref, _ = oracle.train(net, X, y, cfg["B"], 1, steps, cfg["lr"], cfg["mu"], 42)
+    gpu = _gpu_run(cfg, X, y, steps, precision, **kw)
+    w0 = oracle.init_params(net, 42)
+    v0 = np.zeros_like(w0)
+    tol = TOL[precision]
+    for t, (rec, g) in enumerate(zip(recs, gpu)):
+        e = step_errors(net, cfg, X, y, t, w0, v0, g)
+        assert max(e.values()) <= GRAD_TOL[precision], (t, e)
+        assert abs(g[0] - rec.loss) <= tol * abs(rec.loss), t
+        w0, v0 = g[2], g[3]
+    assert maxrel(gpu[-1][2], w_ref) <= tol
+
+
 @pytest.mark.parametrize("precision", PRECISIONS)
 def test_cfg1_trajectory_five_steps(precision):
     """configs[0]: MLP 784-128-10, B=64, 5 SGD steps (run at P=1 on one GPU)."""
-    cfg = small_cfg("cfg1", B=64)
-    X, y = S.mnist_like(1, 1000)
-    net = oracle.Net.from_cfg(cfg)
-    recs, w_ref, _ = oracle.train(net, X, y, 64, 1, 5, cfg["lr"], cfg["mu"], 42, keep_grads=True)
-    gpu = _gpu_run(cfg, X, y, 5, precision)
-    tol, gtol = TOL[precision], GRAD_TOL[precision]
-    ltol = 5 * tol if precision == P.MTX_TF32 else tol  # 1xTF32 trajectories drift (DESIGN.md A22)
-    for t, (rec, (loss, G, w)) in enumerate(zip(recs, gpu)):
-        assert abs(loss - rec.loss) <= ltol * abs(rec.loss), t
-        assert max(per_tensor_maxrel(G, rec.G, oracle.tensor_table(net))) <= 5 * gtol, t
-    assert maxrel(gpu[-1][2], w_ref) <= gtol
+    _check_trajectory(small_cfg("cfg1", B=64), *S.mnist_like(1, 1000), 5, precision)
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
@@ -190,15 +192,7 @@ def test_cfg2_one_step_and_wrap(precision):
 @pytest.mark.parametrize("precision", PRECISIONS)
 def test_cfg2_small_buckets_two_steps(precision):
     """Per-layer buckets: each bucket's update must not race the dgrad that still reads W_l."""
-    cfg = small_cfg("cfg2")
-    X, y = S.mnist_like(1, 4096)
-    net = oracle.Net.from_cfg(cfg)
-    recs, w_ref, _ = oracle.train(net, X, y, 512, 1, 2, cfg["lr"], cfg["mu"], 42, keep_grads=True)
-    gpu = _gpu_run(cfg, X, y, 2, precision, bucket_bytes=64 << 10)
-    gtol = GRAD_TOL[precision]
-    for rec, (loss, G, _) in zip(recs, gpu):
-        assert max(per_tensor_maxrel(G, rec.G, oracle.tensor_table(net))) <= 2 * gtol
-    assert maxrel(gpu[-1][2], w_ref) <= gtol
+    _check_trajectory(small_cfg("cfg2"), *S.mnist_like(1, 4096), 2, precision, bucket_bytes=64 << 10)
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
@@ -234,7 +228,7 @@ def test_head_class_counts(C, d, B):
     _check_step(cfg, X, y, P.MTX_3XTF32, 1, start)
 
 
-@pytest.mark.parametrize("precision", [p for p in PRECISIONS if p != P.MTX_TF32])
+@pytest.mark.parametrize("precision", PRECISIONS)
 def test_cnn_lenet_one_step(precision):
     """configs[2] model (LeNet on CIFAR-shaped NHWC 32x32x3) at a batch the oracle finishes in seconds;
     step 3 wraps the window (n = 200, B = 64)."""
@@ -257,7 +251,7 @@ def test_cnn_mini_one_step(precision):
     _check_step(cfg, X, y, precision, 1, start)
 
 
-@pytest.mark.parametrize("precision", [p for p in PRECISIONS if p != P.MTX_TF32])
+@pytest.mark.parametrize("precision", PRECISIONS)
 def test_full_size_cfg4_replicated_rows(precision):
     """Full cfg4 launch configuration (B = 8192) on a dataset of 128 copies of 64 rows: the
     mean gradient over 8192 rows equals the oracle's over the 64 distinct rows."""
@@ -267,13 +261,13 @@ def test_full_size_cfg4_replicated_rows(precision):
     y = np.tile(y64, 128)
     net = oracle.Net.from_cfg(cfg)
     start = oracle.init_params(net, 42)
-    (loss, G, w1), = _gpu_run(cfg, X, y, 1, precision, start=start)
+    (loss, G, w1, _), = _gpu_run(cfg, X, y, 1, precision, start=start)
     g_ref, lsum = oracle.local_grad(net, start.astype(np.float64), X64, y64, 64, 0, 0, 1)
     assert max(per_tensor_maxrel(G, g_ref, oracle.tensor_table(net))) <= 1e-5
     assert abs(loss - lsum / 64) <= 1e-5 * abs(lsum / 64)
 
 
-@pytest.mark.parametrize("precision", [p for p in PRECISIONS if p != P.MTX_TF32])
+@pytest.mark.parametrize("precision", PRECISIONS)
 def test_full_size_cfg3_replicated_rows(precision):
     """Full cfg3 launch configuration (LeNet, B = 1024, the conv kernels' bench grid) on a dataset of
     64 copies of 16 CIFAR-shaped images: the mean gradient over 1024 rows equals the oracle's over the
@@ -284,7 +278,7 @@ def test_full_size_cfg3_replicated_rows(precision):
     y = np.tile(y16, 64)
     net = oracle.Net.from_cfg(cfg)
     start = oracle.init_params(net, 42)
-    (loss, G, w1), = _gpu_run(cfg, X, y, 1, precision, start=start)
+    (loss, G, w1, _), = _gpu_run(cfg, X, y, 1, precision, start=start)
     g_ref, lsum = oracle.local_grad(net, start.astype(np.float64), X16, y16, 16, 0, 0, 1)
     tab = oracle.tensor_table(net)
     assert max(per_tensor_maxrel(G, g_ref, tab)) <= 1e-5
@@ -317,7 +311,7 @@ def test_host_staged_step_matches_resident():
         r2.close()
 
 
-@pytest.mark.parametrize("precision", [p for p in PRECISIONS if p != P.MTX_TF32])
+@pytest.mark.parametrize("precision", PRECISIONS)
 def test_pipelined_host_steps_match_synchronous(precision):
     """mtx_train_step_host_async (double-buffered landing, copy of step t+1 overlapping step t) gives the
     bit-identical trajectory of mtx_train_step_host on the same rows, and mtx_sync reports its last loss."""
@@ -400,28 +394,3 @@ def test_graph_launch_count_and_determinism():
         finally:
             r.close()
     assert outs[0] == outs[1]  # run-to-run bitwise determinism (no float atomics)
-
-
-# ----------------------------------------------------------------------------- TF32 tier vs tf32emu
-TC = "tcgen05" in mtx.mtx_build_info()
-
-
-@pytest.mark.skipif(not TC, reason="tcgen05 engine not built")
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg4"])
-def test_tf32_step_matches_tf32emu(name):
-    """MTX_TF32 computes exactly the TF32-operand contractions (readings A12/A23):
-    against the oracle's tf32emu mode its per-tensor gradient error is fp32-accumulation-sized, where
-    against the exact (f64) oracle it is the TF32 band GRAD_TOL[MTX_TF32]."""
-    cfg = {"cfg1": small_cfg("cfg1", B=64), "cfg2": small_cfg("cfg2"), "cfg4": small_cfg("cfg4", B=96, n=5000)}[name]
-    X, y = S.higgs_like(1, 5000) if name == "cfg4" else S.mnist_like(1, 4096)
-    net = oracle.Net.from_cfg(cfg)
-    tab = oracle.tensor_table(net)
-    start = oracle.init_params(net, 42)
-    (loss, G, _), = _gpu_run(cfg, X, y, 1, P.MTX_TF32, start=start, start_step=2)
-    g_emu, l_emu = oracle.local_grad(net, start.astype(np.float64), X, y, cfg["B"], 2, 0, 1, tf32emu=True)
-    g_ex, _ = oracle.local_grad(net, start.astype(np.float64), X, y, cfg["B"], 2, 0, 1)
-    e_emu, e_ex = per_tensor_maxrel(G, g_emu, tab), per_tensor_maxrel(G, g_ex, tab)
-    print(name, "vs tf32emu", [f"{e:.2e}" for e in e_emu], "vs f64", [f"{e:.2e}" for e in e_ex])
-    assert max(e_emu) <= TF32EMU_TOL, (e_emu, e_ex)
-    assert max(e_emu) <= max(e_ex) / 50, (e_emu, e_ex)  # the emulation explains the TF32 error
-    assert abs(loss - l_emu / cfg["B"]) <= 1e-5 * abs(l_emu / cfg["B"])
