@@ -1266,7 +1266,10 @@ mtx_status mtx_bind_workspace(mtx_ctx *c, void *dev_ptr, uint64_t bytes) {
         for (int r = 0; r < c->world; r++)
             if (all[r] != mine) return fail(c, MTX_ERR_PROTOCOL, "rank %d model digest differs from rank %d", r, c->rank);
     }
-    if (c->world > 1 && c->opt.reduce == MTX_REDUCE_FUSED && (st = map_peers(c))) return st;
+    if (c->world > 1 && c->opt.reduce == MTX_REDUCE_FUSED) {
+        if ((st = map_peers(c))) return st;
+        CK(p2p_preload());
+    }
     if ((st = refresh_param_planes(c, c->own))) return st;
     CK(cudaStreamSynchronize(c->own));
     c->state = mtx_ctx::S_BOUND;
@@ -1680,8 +1683,7 @@ mtx_status mtx_debug_reduce(mtx_ctx *c, int32_t mode, int32_t P, void *const *g,
     // replica) -> peer_barrier, with PeerPtrs pointing at the P local buffer sets and per-rank flag arrays
     PeerPtrs pp{};
     if (!c->dbg_sync) {
-        CK(cudaMalloc(&c->dbg_sync, 8 * (MAX_PEERS * MAX_PEERS + MAX_PEERS)));
-        CK(cudaMemset(c->dbg_sync, 0, 8 * (MAX_PEERS * MAX_PEERS + MAX_PEERS)));
+        CK(cudaMalloc(&c->dbg_sync, 8 * (MAX_PEERS * MAX_PEERS + MAX_PEERS)));  // zeroed on `s` below
         for (int q = 0; q < MAX_PEERS; q++) {
             CK(cudaStreamCreateWithFlags(&c->dbg_streams[q], cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&c->dbg_ev_join[q], cudaEventDisableTiming));
@@ -1698,14 +1700,19 @@ mtx_status mtx_debug_reduce(mtx_ctx *c, int32_t mode, int32_t P, void *const *g,
     // fresh epochs for every call (each call is a new "world")
     CK(cudaMemsetAsync(c->dbg_sync, 0, 8 * (MAX_PEERS * MAX_PEERS + MAX_PEERS), s));
     CK(cudaEventRecord(c->dbg_ev, s));
-    for (int r = 0; r < P; r++) {
-        cudaStream_t sr = c->dbg_streams[r];
-        uint64_t *epoch = c->dbg_sync + MAX_PEERS * MAX_PEERS + r;
-        CK(cudaStreamWaitEvent(sr, c->dbg_ev, 0));
-        CK(peer_barrier(pp, P, r, epoch, c->flag, sr, nullptr));
-        CK(fused_avg_update(pp, P, r, (int64_t)n, lr, momentum, has_v, c->flag, nullptr, 0, 1, sr, nullptr));
-        CK(peer_barrier(pp, P, r, epoch, c->flag, sr, nullptr));
-    }
+    CK(p2p_preload());
+    // issue phase by phase over the ranks, so every rank's barrier is enqueued before anything waits on it
+    for (int phase = 0; phase < 3; phase++)
+        for (int r = 0; r < P; r++) {
+            cudaStream_t sr = c->dbg_streams[r];
+            uint64_t *epoch = c->dbg_sync + MAX_PEERS * MAX_PEERS + r;
+            if (phase == 0) CK(cudaStreamWaitEvent(sr, c->dbg_ev, 0));
+            if (phase == 1)
+                CK(fused_avg_update(pp, P, r, (int64_t)n, lr, momentum, has_v, c->flag, nullptr, 0, 1, sr, nullptr,
+                                    false));
+            else
+                CK(peer_barrier(pp, P, r, epoch, c->flag, sr, nullptr, false));
+        }
     for (int r = 0; r < P; r++) {
         CK(cudaEventRecord(c->dbg_ev_join[r], c->dbg_streams[r]));
         CK(cudaStreamWaitEvent(s, c->dbg_ev_join[r], 0));

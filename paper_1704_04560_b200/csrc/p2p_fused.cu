@@ -121,18 +121,30 @@ __global__ void __launch_bounds__(256) fused_avg_update_kernel(PeerPtrs pp, int 
 
 }  // namespace
 
+cudaError_t p2p_preload() {
+    // CUDA 12 loads kernels lazily at their first launch, and loading waits for the device: a first launch
+    // issued while a peer barrier spins on this GPU (mtx_debug_reduce's simulated ranks) would deadlock
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, (const void *)peer_barrier_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_avg_update_kernel<true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_avg_update_kernel<false>);
+    return e;
+}
+
 cudaError_t peer_barrier(const PeerPtrs &pp, int P, int rank, uint64_t *epoch_ctr, int *errflag, cudaStream_t s,
-                         LaunchHook *h) {
+                         LaunchHook *h, bool pdl) {
     char name[32];
     snprintf(name, sizeof name, "peer_barrier[P=%d]", P);
     if (h) h->before(name, s);
-    launch_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, s, pp, P, rank, epoch_ctr, errflag, 10000000000ull);
+    if (pdl) launch_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, s, pp, P, rank, epoch_ctr, errflag, 10000000000ull);
+    else peer_barrier_kernel<<<1, 32, 0, s>>>(pp, P, rank, epoch_ctr, errflag, 10000000000ull);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }
 
 cudaError_t fused_avg_update(const PeerPtrs &pp, int P, int rank, int64_t n_pad, float lr, float mu, bool has_v,
-                             int *flag, int64_t *win, int64_t B, int64_t n_data, cudaStream_t s, LaunchHook *h) {
+                             int *flag, int64_t *win, int64_t B, int64_t n_data, cudaStream_t s, LaunchHook *h,
+                             bool pdl) {
     if (P > 8 || n_pad % 4) return cudaErrorInvalidValue;
     const int64_t n4 = n_pad / 4;
     const int64_t lo4 = n4 * rank / P, hi4 = n4 * (rank + 1) / P;
@@ -142,12 +154,11 @@ cudaError_t fused_avg_update(const PeerPtrs &pp, int P, int rank, int64_t n_pad,
     snprintf(name, sizeof name, "fused_avg_update[n=%lld,P=%d,v=%d]", (long long)n_pad, P, has_v ? 1 : 0);
     if (h) h->before(name, s);
     const float invP = 1.0f / (float)P;
-    if (has_v)
-        launch_pdl(fused_avg_update_kernel<true>, dim3(blocks), dim3(256), 0, s, pp, P, rank, lo4, hi4, invP, lr, mu,
-                   flag, win, B, n_data, n_pad);
+    auto kern = has_v ? fused_avg_update_kernel<true> : fused_avg_update_kernel<false>;
+    if (pdl)
+        launch_pdl(kern, dim3(blocks), dim3(256), 0, s, pp, P, rank, lo4, hi4, invP, lr, mu, flag, win, B, n_data, n_pad);
     else
-        launch_pdl(fused_avg_update_kernel<false>, dim3(blocks), dim3(256), 0, s, pp, P, rank, lo4, hi4, invP, lr, mu,
-                   flag, win, B, n_data, n_pad);
+        kern<<<blocks, 256, 0, s>>>(pp, P, rank, lo4, hi4, invP, lr, mu, flag, win, B, n_data, n_pad);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }

@@ -23,5 +23,5 @@ def step_errors(net, cfg, X, y, t, w0, v0, rec, P_=1):
     half_ulp = np.spacing(np.abs(w1)).astype(np.float64) / 2
     e_dw = [float(np.maximum(np.abs(dw[o:o + n] - dw_ref[o:o + n]) - half_ulp[o:o + n], 0).max(initial=0)
                   / max(np.abs(dw_ref[o:o + n]).max(initial=0), 1e-30)) for o, n in tab]
-    return {"G": max(per_tensor_maxrel(G, G_ref, tab)), "loss": abs(loss - lref) / abs(lref),
+    return {"G": max(per_tensor_maxrel(G, G_ref, tab)), "loss": abs(loss - lref) / max(abs(lref), 1e-30),
             "v": max(per_tensor_maxrel(v1, v_ref, tab)) if cfg["mu"] else 0.0, "dw": max(e_dw)}
