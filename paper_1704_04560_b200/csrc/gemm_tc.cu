@@ -816,10 +816,27 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     const TcPlan plan = tc_plan(sms, M, N, K);
     const int BN = plan.bn;
     // CTA pairs for large unsplit GEMMs: a 256 x 128 tile per pair halves B's per-SM operand traffic.
-    // Not for dgrad: its masked epilogue is the heavier one and the pair couples both SMs' epilogues
-    // through the shared accumulator barrier (measured slower).
-    const bool pair = t->pair && g.epi != EPI_MASK && BN == 128 && plan.splits == 1 && N % 64 == 0 && M > BM &&
-                      (int64_t)((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * 2 >= sms / 2;
+    // Pair MMAs also cost ~65 cycles with fresh operand tiles where a 1-CTA MMA of any N <= 128 costs ~89
+    // (tools/mma_rate.cu, profiles/round2_tcgen05_rates.md); the dgrad pairs too (measured 84.0 -> 81.6 us at
+    // M = 8192, 44.4 -> 43.1 at 4096).  Development knobs: MTX_TC_PAIR_MASK=0 unpairs the dgrad;
+    // MTX_TC_PAIR_SPLIT=1 lets a weight gradient too small to fill the pairs split K through global partials
+    // (measured no faster than the DSMEM cluster fold: off).
+    static const bool pair_mask = !getenv("MTX_TC_PAIR_MASK") || atoi(getenv("MTX_TC_PAIR_MASK"));
+    static const bool pair_split = getenv("MTX_TC_PAIR_SPLIT") && atoi(getenv("MTX_TC_PAIR_SPLIT"));
+    const int64_t ptiles = (int64_t)((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+    int pair_splits = 1;
+    bool pair = t->pair && (g.epi != EPI_MASK || pair_mask) && BN == 128 && N % 64 == 0 && M > BM;
+    if (pair && !(plan.splits == 1 && ptiles * 2 >= sms / 2)) {
+        pair = false;
+        const int kb = (K + BK - 1) / BK;
+        if (pair_split && g.epi == EPI_STORE && g.partial && M >= 2 * BM) {
+            const int sp = (int)std::min<int64_t>(std::max(1, kb / 8), std::max<int64_t>(1, (sms / 2) / ptiles));
+            if (sp > 1 && ptiles * sp * 8 >= (int64_t)(sms / 2) * 6) {
+                pair = true;
+                pair_splits = sp;
+            }
+        }
+    }
     TcParams p{};
     p.M = M; p.N = N; p.K = K;
     p.a_mn = g.ta ? 1 : 0;
@@ -847,7 +864,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.tiles_n = (N + BN - 1) / BN;
     p.kb_total = (K + BK - 1) / BK;
     const int tiles = p.tiles_m * p.tiles_n;
-    int splits = plan.splits;
+    int splits = pair ? pair_splits : plan.splits;
     // split-K fold through DSMEM when the tile's splits fit one cluster and all clusters are co-resident
     bool cluster = false;
     if (splits > 1 && splits <= 8 && t->cluster && !pair) {
@@ -887,7 +904,8 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     if (h) h->before(name, s);
     cudaError_t e;
     const bool mask = g.epi == EPI_MASK;  // dgrad: the masked-epilogue instantiation (never paired)
-    if (pair) e = g.tf32x3 ? launch<128, true, true>(t, p, grid, s) : launch<128, false, true>(t, p, grid, s);
+    if (pair && mask) e = g.tf32x3 ? launch<128, true, true, true>(t, p, grid, s) : launch<128, false, true, true>(t, p, grid, s);
+    else if (pair) e = g.tf32x3 ? launch<128, true, true>(t, p, grid, s) : launch<128, false, true>(t, p, grid, s);
     else if (mask) {
         if (BN == 128) e = g.tf32x3 ? launch<128, true, false, true>(t, p, grid, s) : launch<128, false, false, true>(t, p, grid, s);
         else if (BN == 64) e = g.tf32x3 ? launch<64, true, false, true>(t, p, grid, s) : launch<64, false, false, true>(t, p, grid, s);

@@ -32,6 +32,8 @@ SHAPES = [  # (M, N, K) incl. the step's shapes: cfg4 fwd/dgrad/wgrad, cfg2, K =
     (1000, 384, 520), (1024, 640, 256), (64, 784, 512),  # tcgen05 N-tile 64 / 32 plans
     (4096, 1024, 256), (4000, 512, 200),  # CTA-pair (cta_group::2) 256 x 128 tiles, ragged M / K
     (8192, 1024, 256), (8100, 640, 300),  # stream-K remainder (last round split into K-halves), ragged
+    (8192, 1024, 1024), (8000, 1024, 1000),  # 3xTF32 CTA-pair 256 x 256 tiles (N = 256 MMAs), ragged M / K
+    (1024, 1024, 8192), (768, 512, 4000),  # ... and their split-K weight-gradient plan, ragged K
 ]
 
 

@@ -158,8 +158,16 @@ void run(int N, int R, int commit_every = 0) {
     cudaFree(dc);
 }
 
-int main() {
+int main(int argc, char **argv) {
     const int R = 20000;
+    if (argc > 1) {  // small-N and pair rates with distinct operand tiles (round 2: conv / N = 256 plans)
+        printf("rotating both over 4 stages:\n");
+        for (int N : {16, 32, 64}) run<0, 0>(N, R, 4);
+        run<1, 0>(128, R, 4);
+        run<1, 0>(256, R, 4);
+        run<1, 0>(64, R, 4);
+        return 0;
+    }
     for (int N : {64, 128, 256}) {
         run<0, 0>(N, R);
         run<0, 1>(N, R);
