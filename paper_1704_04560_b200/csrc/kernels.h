@@ -149,4 +149,13 @@ cudaError_t conv_bwd(const ConvGeom &g, int rows, const float *X, RowSel xrow, c
                      const uint8_t *arg, const float *Wb, float *dX, float *dWb, float *partial, int64_t partial_cap,
                      cudaStream_t s, LaunchHook *h);
 
+// Tensor-core (tcgen05, 3xTF32) convolutions, conv_tc.cu: the forward conv + bias + ReLU + pool (same outputs
+// as conv_fwd, plus optional hi/lo planes of P for the consuming fc GEMM) and the input gradient dX of a conv
+// layer from its pooled gradient (routing through the argmax, mask [P > 0]) -- conv_bwd's dX part.
+bool conv_tc_supported(const ConvGeom &g, bool dgrad);
+cudaError_t conv_fwd_tc(const ConvGeom &g, int rows, const float *X, RowSel xrow, const float *Wb, float *P, uint8_t *arg,
+                        float *P_hi, float *P_lo, cudaStream_t s, LaunchHook *h);
+cudaError_t conv_dgrad_tc(const ConvGeom &g, int rows, const float *dP, const float *P, const uint8_t *arg, const float *Wb,
+                          float *dX, cudaStream_t s, LaunchHook *h);
+
 }  // namespace mtx

@@ -850,20 +850,30 @@ mtx_status Runner::forward_backward_cnn() {
     for (int f : c->fc) fd.push_back(f);
     mtx_status st;
     cudaError_t e;
+    // 3xTF32: the convolutions run on the tensor cores (conv_tc.cu), the last one writing the hi/lo planes of
+    // its pooled output for fc1; FP32: CUDA-core kernels (kernels_conv.cu)
+    const bool tc = c->opt.precision == MTX_3XTF32;
+    const float *flat = c->convP[NC - 1];
+    const float *fh = nullptr, *fl = nullptr;
+    const bool flat_planes = plane_of(c, flat, &fh, &fl) && fd[0] % 4 == 0;
+    bool planes_done = false;
     for (int ci = 0; ci < NC; ci++) {
         const float *in = ci == 0 ? xbase() : c->convP[ci - 1];
         RowSel row = ci == 0 ? xrow() : RowSel{nullptr, 0};
-        e = conv_fwd(c->convs[ci], (int)b, in, row, c->params + c->layers[ci].pad_off, c->convP[ci], c->convArg[ci], s,
-                     h);
+        const float *Wb = c->params + c->layers[ci].pad_off;
+        if (tc && conv_tc_supported(c->convs[ci], false)) {
+            const bool last = ci == NC - 1 && flat_planes;
+            e = conv_fwd_tc(c->convs[ci], (int)b, in, row, Wb, c->convP[ci], c->convArg[ci], last ? (float *)fh : nullptr,
+                            last ? (float *)fl : nullptr, s, h);
+            planes_done |= last;
+        } else {
+            e = conv_fwd(c->convs[ci], (int)b, in, row, Wb, c->convP[ci], c->convArg[ci], s, h);
+        }
         if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "conv_fwd: %s", cudaGetErrorString(e));
     }
-    const float *flat = c->convP[NC - 1];
-    {
-        const float *fh = nullptr, *fl = nullptr;
-        if (plane_of(c, flat, &fh, &fl) && fd[0] % 4 == 0) {
-            e = split_planes(flat, b, fd[0], fd[0], (float *)fh, (float *)fl, s, h);
-            if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "split_planes: %s", cudaGetErrorString(e));
-        }
+    if (flat_planes && !planes_done) {
+        e = split_planes(flat, b, fd[0], fd[0], (float *)fh, (float *)fl, s, h);
+        if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "split_planes: %s", cudaGetErrorString(e));
     }
     auto fc_in = [&](int f) -> const float * { return f == 1 ? flat : c->fcA[f - 1]; };
     for (int f = 1; f < NF; f++) {
@@ -909,8 +919,14 @@ mtx_status Runner::forward_backward_cnn() {
         const ConvGeom &g = c->convs[ci];
         const float *in = ci == 0 ? xbase() : c->convP[ci - 1];
         RowSel row = ci == 0 ? xrow() : RowSel{nullptr, 0};
-        e = conv_bwd(g, (int)b, in, row, c->convDP[ci], c->convP[ci], c->convArg[ci], c->params + c->layers[ci].pad_off,
-                     ci > 0 ? c->convDP[ci - 1] : nullptr, c->grads + c->layers[ci].pad_off, c->partial,
+        const float *Wb = c->params + c->layers[ci].pad_off;
+        const bool dgrad_tc = tc && ci > 0 && conv_tc_supported(g, true);
+        if (dgrad_tc) {  // the input gradient on the tensor cores; the weight gradient below on the CUDA cores
+            e = conv_dgrad_tc(g, (int)b, c->convDP[ci], c->convP[ci], c->convArg[ci], Wb, c->convDP[ci - 1], s, h);
+            if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "conv_dgrad_tc: %s", cudaGetErrorString(e));
+        }
+        e = conv_bwd(g, (int)b, in, row, c->convDP[ci], c->convP[ci], c->convArg[ci], Wb,
+                     (ci > 0 && !dgrad_tc) ? c->convDP[ci - 1] : nullptr, c->grads + c->layers[ci].pad_off, c->partial,
                      c->partial_floats, s, h);
         if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "conv_bwd: %s", cudaGetErrorString(e));
         if ((st = bucket_ready(ci, bk))) return st;
