@@ -161,6 +161,7 @@ struct mtx_ctx {
     PeerPtrs pp{};
     std::vector<void *> ipc_opened;
     uint64_t *epoch = nullptr, *flags = nullptr;
+    uint64_t *bflags = nullptr, *stepctr = nullptr;  // per-bucket ready epochs [MAX_BUCKETS][MAX_PEERS]; step counter
     bool fused = false;
     uint64_t *proto = nullptr;  // P x 8 bytes for the model-digest allgather
     // CNN activations
@@ -461,6 +462,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     // per lane: [0,254) split-K tiles, 254 narrow wgrad, 256.. colsum groups
     unsigned *counters = (unsigned *)take(4 * COUNTERS_PER_LANE * lanes);
     uint8_t *misc = take(512 + 128 * (uint64_t)c->world);
+    uint64_t *bflags = (uint64_t *)take(8 * MAX_BUCKETS * MAX_PEERS);
     if (assign) {
         c->params = params; c->vel = vel; c->grads = grads; c->gather = gather; c->gred = gred;
         c->acts = acts; c->fcA = fcA; c->dzs = dzs; c->lanes = lanes;
@@ -482,6 +484,8 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         c->dig = (unsigned long long *)(misc + 32);
         c->epoch = (uint64_t *)(misc + 64);
         c->flags = (uint64_t *)(misc + 128);  // MAX_PEERS epochs
+        c->stepctr = (uint64_t *)(misc + 192);
+        c->bflags = bflags;
         c->proto = (uint64_t *)(misc + 512);  // world x 128 B: model digests / IPC handle records
     }
     return off + 256;
@@ -499,6 +503,23 @@ bool plane_of(const mtx_ctx *c, const float *p, const float **hi, const float **
 }
 
 // ------------------------------------------------------------------ step schedule
+// MTX_REDUCE_FUSED at P > 1, ablation knob MTX_FUSED_OVERLAP=1: the fused reduction runs per bucket on the
+// comm stream while the backward continues, on MTX_COMM_SMS SMs (default 16) that the backward's GEMMs are
+// planned to leave free (a persistent GEMM CTA fills its SM; without a reserve the reduction would queue
+// behind it), the backward then being one chain on the caller's stream.  Measured slower than one fused
+// launch after the backward, so off by default.
+bool fused_overlap() {
+    static const bool v = getenv("MTX_FUSED_OVERLAP") && atoi(getenv("MTX_FUSED_OVERLAP"));
+    return v;
+}
+int comm_sms() {
+    static const int v = [] {
+        const char *e = getenv("MTX_COMM_SMS");
+        return e ? std::max(1, std::min(atoi(e), 64)) : 16;
+    }();
+    return v;
+}
+
 struct Runner {
     mtx_ctx *c;
     cudaStream_t s;  // the stream launches go to: the caller's stream, or a side lane's inside on_lane()
@@ -516,7 +537,9 @@ struct Runner {
     // Issue fn() on side lane ln, ordered after everything issued so far on the caller's stream.
     template <class F>
     mtx_status on_lane(int ln, F fn) {
-        if (ln <= 0 || ln >= c->lanes || !c->side[ln - 1]) return fn();
+        // MTX_REDUCE_FUSED at P > 1: the backward is one chain on the caller's stream, every GEMM planned for the
+        // SMs the per-bucket reduction kernels leave free (concurrent side-lane GEMMs would take those SMs too)
+        if (ln <= 0 || ln >= c->lanes || !c->side[ln - 1] || (c->fused && c->world > 1 && fused_overlap())) return fn();
         if (c->hook.enabled) {
             // per-kernel timing pass: serialised on the caller's stream (every kernel timed alone, like
             // ncu's launch list) but with the lane's launch plan -- its SM budget and scratch -- so each
@@ -567,6 +590,10 @@ struct Runner {
     }
 
     mtx_status gemm(GemmDesc g) {
+        if (c->fused && c->world > 1 && fused_overlap() && (g.epi == EPI_MASK || g.ta)) {  // backward GEMM at P > 1
+            const int avail = 148 - comm_sms();
+            g.sm_budget = g.sm_budget > 0 ? std::min(g.sm_budget, avail) : avail;
+        }
         // small weight gradients on the side lanes take a reduced SM budget so the critical dgrad chain
         // on the caller's stream keeps most of the GPU (cfg2: 76 -> 74 us/step); large ones (cfg4's
         // 17 GFLOP wgrads) keep all SMs or they would become the critical path (measured)
@@ -588,7 +615,7 @@ struct Runner {
             if (plane_of(c, g.C, &ch, &cl)) { g.C_hi = (float *)ch; g.C_lo = (float *)cl; }
         }
         if (c->opt.precision != MTX_FP32 && c->tc && tc_supports(c->tc, g)) {
-            if (g.aug && c->lanes > mtx_ctx::COLSUM_LANE && !c->hook.enabled) {
+            if (g.aug && c->lanes > mtx_ctx::COLSUM_LANE && !c->hook.enabled && !(c->fused && c->world > 1 && fused_overlap())) {
                 // the bias row (column sums of B = dZ) runs on its own lane beside the GEMM
                 const GemmDesc gc = g;
                 mtx_status cs = on_lane(mtx_ctx::COLSUM_LANE, [&] {
@@ -702,7 +729,7 @@ struct Runner {
     // After layer block `li`'s wgrad: launch the allreduce + update of every bucket it completes.
     mtx_status bucket_ready(int li, size_t &bk) {
         while (bk < c->buckets.size() && c->buckets[bk].last_layer == li) {
-            mtx_status st = reduce_update(c->buckets[bk], bk + 1 == c->buckets.size());
+            mtx_status st = reduce_update(c->buckets[bk], (int)bk, bk + 1 == c->buckets.size());
             if (st) return st;
             bk++;
         }
@@ -712,7 +739,7 @@ struct Runner {
     // mu == 0: plain SGD, the velocity buffer is not maintained (12 B/elem instead of 20).
     float *vel_or_null(int64_t off) const { return c->opt.momentum != 0.f ? c->vel + off : nullptr; }
 
-    mtx_status reduce_update(const Bucket &bkt, bool last) {
+    mtx_status reduce_update(const Bucket &bkt, int bi, bool last) {
         const float invP = 1.0f / (float)c->world;
         if (c->world > 1 && c->opt.reduce == MTX_REDUCE_LAYERWISE) {
             // paper-literal: after the backward, one allreduce per variable in canonical order
@@ -749,15 +776,25 @@ struct Runner {
             NK(ncclGroupEnd());
             return MTX_OK;
         }
-        if (c->fused) {  // one fused collective + update over the whole buffer after the last wgrad
-            if (!last) return MTX_OK;
-            if (mtx_status st = grads_ready(s)) return st;
-            int64_t *win = staged ? nullptr : c->win;
-            cudaError_t e = peer_barrier(c->pp, c->world, c->rank, c->epoch, c->flag, s, h);
-            if (e == cudaSuccess)
-                e = fused_avg_update(c->pp, c->world, c->rank, c->N_pad, c->opt.lr, c->opt.momentum,
-                                     c->opt.momentum != 0.f, c->flag, win, c->B, c->n_data, s, h);
-            if (e == cudaSuccess) e = peer_barrier(c->pp, c->world, c->rank, c->epoch, c->flag, s, h);
+        if (c->fused) {
+            // The averaging operator fused with its collective.  The kernel publishes "gradients ready" to
+            // every peer, waits for theirs, folds + updates this rank's share of its range and stores w into
+            // every replica; a barrier after the last one makes every replica's w complete before the next
+            // step reads it.  Default: one launch over the whole buffer after the backward, on all SMs.
+            // fused_overlap(): per bucket on the comm stream, overlapping the rest of the backward on SMs the
+            // backward GEMMs leave free -- measured slower, kept as an ablation.
+            const bool ov = fused_overlap();
+            if (!ov && !last) return MTX_OK;
+            const cudaStream_t cs = ov ? c->comm_s : s;
+            if (mtx_status st = grads_ready(cs)) return st;
+            int64_t *win = (last && !staged) ? c->win : nullptr;
+            const int64_t lo = ov ? bkt.lo : 0, hi = ov ? std::min<int64_t>(bkt.hi, c->N_pad) : c->N_pad;
+            const bool has_loss = ov ? bkt.hi > c->N_pad : true;
+            cudaError_t e = fused_bucket_update(c->pp, c->world, c->rank, ov ? bi : 0, c->stepctr, lo, hi, c->opt.lr,
+                                                c->opt.momentum, c->opt.momentum != 0.f, c->flag, win, c->B, c->n_data,
+                                                has_loss ? c->N_pad : -1, ov ? comm_sms() : 148, cs, h);
+            if (e == cudaSuccess && last)
+                e = peer_barrier_step(c->pp, c->world, c->rank, c->epoch, c->flag, c->stepctr, cs, h);
             if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "fused update: %s", cudaGetErrorString(e));
             return MTX_OK;
         }
@@ -802,7 +839,7 @@ struct Runner {
             CK(cudaStreamWaitEvent(c->comm_s, c->ev_fork, 0));
         }
         for (size_t i = 0; i < c->buckets.size(); i++) {
-            mtx_status st = reduce_update(c->buckets[i], i + 1 == c->buckets.size());
+            mtx_status st = reduce_update(c->buckets[i], (int)i, i + 1 == c->buckets.size());
             if (st) return st;
         }
         if (c->world > 1) {
@@ -1043,13 +1080,21 @@ mtx_status sync_loss(mtx_ctx *c, cudaStream_t s, float *host_loss) {
 // only by the fused kernel, which runs after that barrier).
 mtx_status assemble_shards(mtx_ctx *c) {
     if (!c->fused || c->world <= 1) return MTX_OK;
-    const int64_t n4 = c->N_pad / 4;
-    for (int q = 0; q < c->world; q++) {
-        if (q == c->rank) continue;
-        const int64_t lo = 4 * (n4 * q / c->world), hi = 4 * (n4 * (q + 1) / c->world);
-        CK(cudaMemcpyAsync(c->vel + lo, c->pp.v[q] + lo, 4 * (hi - lo), cudaMemcpyDeviceToDevice, c->own));
-        CK(cudaMemcpyAsync(c->gred + lo, c->pp.G[q] + lo, 4 * (hi - lo), cudaMemcpyDeviceToDevice, c->own));
-    }
+    // the fused kernels share out every bucket (overlap ablation) or the whole buffer to the ranks (bucket_share)
+    std::vector<std::pair<int64_t, int64_t>> ranges;
+    if (fused_overlap())
+        for (const Bucket &bk : c->buckets) ranges.push_back({bk.lo, std::min<int64_t>(bk.hi, c->N_pad)});
+    else
+        ranges.push_back({0, c->N_pad});
+    for (const auto &rg : ranges)
+        for (int q = 0; q < c->world; q++) {
+            if (q == c->rank) continue;
+            int64_t lo, hi;
+            bucket_share(rg.first, rg.second, c->world, q, lo, hi);
+            if (hi <= lo) continue;
+            CK(cudaMemcpyAsync(c->vel + lo, c->pp.v[q] + lo, 4 * (hi - lo), cudaMemcpyDeviceToDevice, c->own));
+            CK(cudaMemcpyAsync(c->gred + lo, c->pp.G[q] + lo, 4 * (hi - lo), cudaMemcpyDeviceToDevice, c->own));
+        }
     CK(cudaStreamSynchronize(c->own));
     return MTX_OK;
 }
@@ -1117,6 +1162,7 @@ mtx_status map_peers(mtx_ctx *c) {
         c->pp.w[r] = (float *)(ws_r + rel(c->params));
         c->pp.v[r] = (float *)(ws_r + rel(c->vel));
         c->pp.flags[r] = (uint64_t *)(ws_r + rel(c->flags));
+        c->pp.bflags[r] = (uint64_t *)(ws_r + rel(c->bflags));
     }
     c->fused = true;
     return MTX_OK;
@@ -1177,6 +1223,7 @@ mtx_status mtx_init(mtx_ctx **out, int32_t rank, int32_t world, const uint8_t ui
     }
     mtx_status st = build_layout(c);
     if (st) { delete c; return st; }
+    if (c->buckets.size() > (size_t)MAX_BUCKETS) { delete c; return MTX_ERR_UNSUPPORTED; }
     if (c->classes > 16) { delete c; return MTX_ERR_UNSUPPORTED; }
     {  // the fused head (last layer GEMV + loss + dlogits) stages W_L in shared memory: d_{L-1} <= 1024
         const int d_head = c->kind == MTX_MLP ? c->dims[c->dims.size() - 2]

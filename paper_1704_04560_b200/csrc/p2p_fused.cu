@@ -36,7 +36,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 
 __global__ void peer_barrier_kernel(PeerPtrs pp, int P, int rank, uint64_t *epoch_ctr, int *errflag,
-                                    uint64_t timeout_ns) {
+                                    uint64_t timeout_ns, uint64_t *stepctr) {
     pdl_wait();
     __shared__ uint64_t epoch;
     if (threadIdx.x == 0) {
@@ -62,6 +62,98 @@ __global__ void peer_barrier_kernel(PeerPtrs pp, int P, int rank, uint64_t *epoc
     }
     __syncthreads();
     __threadfence_system();
+    if (stepctr && threadIdx.x == 0) *stepctr += 1;  // every bucket flag of the next step uses the next epoch
+}
+
+// Wait (thread 0) until every rank's flag for `slot` in this rank's flag array reaches epoch; timeout -> error bit
+__device__ __forceinline__ bool wait_flags(const uint64_t *mine, int P, uint64_t epoch, int *errflag) {
+    const uint64_t t0 = globaltimer();
+    for (int q = 0; q < P; q++)
+        while (ld_acquire_sys(mine + q) < epoch) {
+            if (*(volatile int *)errflag & 2) return false;
+            if (globaltimer() - t0 > 10000000000ull) {
+                atomicOr(errflag, 2);
+                return false;
+            }
+        }
+    return true;
+}
+
+template <bool HAS_V>
+__global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, int rank, int bucket,
+                                                         const uint64_t *stepctr, int64_t lo4, int64_t hi4, float invP,
+                                                         float lr, float mu, int *flag, int64_t *win, int64_t B,
+                                                         int64_t n_data, int64_t loss_idx) {
+    pdl_wait();
+    __shared__ int go;
+    const uint64_t epoch = *(volatile const uint64_t *)stepctr + 1;
+    if (threadIdx.x == 0) {
+        go = 0;
+        if (!(*(volatile int *)flag & 2)) {
+            if (blockIdx.x == 0) {  // publish "my bucket is ready" in every peer's flag array
+                __threadfence_system();
+                for (int q = 0; q < P; q++) st_release_sys(pp.bflags[q] + bucket * MAX_PEERS + rank, epoch);
+            }
+            go = wait_flags(pp.bflags[rank] + bucket * MAX_PEERS, P, epoch, flag) ? 1 : 0;
+        }
+    }
+    __syncthreads();
+    if (!go) return;  // a peer timed out: load and store nothing (the context is poisoned at the next sync)
+    bool bad = false;
+    // two float4 per peer per thread in flight (2P loads), ascending-rank fold, update, w to every replica
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = lo4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < hi4; i0 += 2 * stride) {
+        const int64_t i1 = i0 + stride;
+        const bool two = i1 < hi4;
+        float4 g0[MAX_PEERS], g1[MAX_PEERS];
+#pragma unroll
+        for (int q = 0; q < MAX_PEERS; q++)
+            if (q < P) {
+                g0[q] = __ldcv((const float4 *)pp.g[q] + i0);
+                if (two) g1[q] = __ldcv((const float4 *)pp.g[q] + i1);
+            }
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            if (u == 1 && !two) break;
+            const int64_t i = u ? i1 : i0;
+            float4 G = u ? g1[0] : g0[0];
+#pragma unroll
+            for (int q = 1; q < MAX_PEERS; q++)
+                if (q < P) {
+                    const float4 x = u ? g1[q] : g0[q];
+                    G.x = __fadd_rn(G.x, x.x); G.y = __fadd_rn(G.y, x.y);
+                    G.z = __fadd_rn(G.z, x.z); G.w = __fadd_rn(G.w, x.w);
+                }
+            float4 w = ((const float4 *)pp.w[rank])[i], v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (HAS_V) v = ((const float4 *)pp.v[rank])[i];
+            float gb[4] = {G.x * invP, G.y * invP, G.z * invP, G.w * invP};
+            float *pw = &w.x, *pv = &v.x;
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                bad |= !isfinite(gb[c]);
+                if (HAS_V) {
+                    pv[c] = __fmaf_rn(mu, pv[c], gb[c]);
+                    pw[c] = __fmaf_rn(-lr, pv[c], pw[c]);
+                } else {
+                    pw[c] = __fmaf_rn(-lr, gb[c], pw[c]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < MAX_PEERS; q++)
+                if (q < P) __stcg((float4 *)pp.w[q] + i, w);
+            if (HAS_V) __stcg((float4 *)pp.v[rank] + i, v);
+            __stcg((float4 *)pp.G[rank] + i, G);
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (loss_idx >= 0) {  // every rank folds all ranks' local loss sums itself (same order, same bits)
+            float L = __ldcv(pp.g[0] + loss_idx);
+            for (int q = 1; q < P; q++) L = __fadd_rn(L, __ldcv(pp.g[q] + loss_idx));
+            pp.G[rank][loss_idx + 1] = L;
+        }
+        if (win) *win = (*win + B) % n_data;
+    }
 }
 
 template <bool HAS_V>
@@ -126,6 +218,8 @@ cudaError_t p2p_preload() {
     // issued while a peer barrier spins on this GPU (mtx_debug_reduce's simulated ranks) would deadlock
     cudaFuncAttributes a;
     cudaError_t e = cudaFuncGetAttributes(&a, (const void *)peer_barrier_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<false>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_avg_update_kernel<true>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_avg_update_kernel<false>);
     return e;
@@ -136,8 +230,37 @@ cudaError_t peer_barrier(const PeerPtrs &pp, int P, int rank, uint64_t *epoch_ct
     char name[32];
     snprintf(name, sizeof name, "peer_barrier[P=%d]", P);
     if (h) h->before(name, s);
-    if (pdl) launch_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, s, pp, P, rank, epoch_ctr, errflag, 10000000000ull);
-    else peer_barrier_kernel<<<1, 32, 0, s>>>(pp, P, rank, epoch_ctr, errflag, 10000000000ull);
+    if (pdl)
+        launch_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, s, pp, P, rank, epoch_ctr, errflag, 10000000000ull,
+                   (uint64_t *)nullptr);
+    else peer_barrier_kernel<<<1, 32, 0, s>>>(pp, P, rank, epoch_ctr, errflag, 10000000000ull, nullptr);
+    if (h) h->after(name, s);
+    return cudaGetLastError();
+}
+
+cudaError_t peer_barrier_step(const PeerPtrs &pp, int P, int rank, uint64_t *epoch_ctr, int *errflag, uint64_t *stepctr,
+                              cudaStream_t s, LaunchHook *h) {
+    char name[32];
+    snprintf(name, sizeof name, "peer_barrier[P=%d]", P);
+    if (h) h->before(name, s);
+    launch_pdl(peer_barrier_kernel, dim3(1), dim3(32), 0, s, pp, P, rank, epoch_ctr, errflag, 10000000000ull, stepctr);
+    if (h) h->after(name, s);
+    return cudaGetLastError();
+}
+
+cudaError_t fused_bucket_update(const PeerPtrs &pp, int P, int rank, int bucket, const uint64_t *stepctr, int64_t lo,
+                                int64_t hi, float lr, float mu, bool has_v, int *flag, int64_t *win, int64_t B,
+                                int64_t n_data, int64_t loss_idx, int ctas, cudaStream_t s, LaunchHook *h) {
+    if (P > MAX_PEERS || bucket >= MAX_BUCKETS || lo % 4 || hi % 4) return cudaErrorInvalidValue;
+    int64_t a, b;
+    bucket_share(lo, hi, P, rank, a, b);
+    char name[96];
+    snprintf(name, sizeof name, "fused_avg_update[n=%lld,P=%d,v=%d]", (long long)(hi - lo), P, has_v ? 1 : 0);
+    if (h) h->before(name, s);
+    const float invP = 1.0f / (float)P;
+    auto kern = has_v ? fused_bucket_kernel<true> : fused_bucket_kernel<false>;
+    launch_pdl(kern, dim3(std::max(1, ctas)), dim3(512), 0, s, pp, P, rank, bucket, stepctr, a / 4, b / 4, invP, lr, mu,
+               flag, win, B, n_data, loss_idx);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }

@@ -18,7 +18,10 @@ struct PeerPtrs {
     float *v[MAX_PEERS];
     float *G[MAX_PEERS];
     uint64_t *flags[MAX_PEERS];  // per-rank arrival epochs, indexed by source rank
+    uint64_t *bflags[MAX_PEERS]; // per-rank "bucket ready" epochs, [bucket][source rank] (MAX_BUCKETS x MAX_PEERS)
 };
+
+constexpr int MAX_BUCKETS = 64;
 
 // Loads the kernels of this file (CUDA lazy loading would otherwise load them at their first launch).
 cudaError_t p2p_preload();
@@ -28,6 +31,25 @@ cudaError_t p2p_preload();
 // the next kernel's CTAs park on the SMs that another simulated rank's barrier still needs).
 cudaError_t peer_barrier(const PeerPtrs &pp, int P, int rank, uint64_t *epoch_ctr, int *errflag, cudaStream_t s,
                          LaunchHook *h, bool pdl = true);
+
+// One gradient bucket [lo, hi) of the flat buffer, overlapping the rest of the backward:
+// the kernel publishes "bucket b ready at epoch *stepctr + 1" to every peer, waits for every peer's flag of
+// bucket b, then folds the P gradients of this rank's share of the bucket in ascending rank order, applies
+// x fl(1/P) and the momentum update and stores w into every replica (v and G stay with the owner).
+// loss_idx >= 0: this bucket carries the loss slot (folded into slot loss_idx + 1); win != nullptr: the
+// window start advances (the step's last bucket).  `ctas` CTAs (the SMs the backward GEMMs leave free).
+cudaError_t fused_bucket_update(const PeerPtrs &pp, int P, int rank, int bucket, const uint64_t *stepctr, int64_t lo,
+                                int64_t hi, float lr, float mu, bool has_v, int *flag, int64_t *win, int64_t B,
+                                int64_t n_data, int64_t loss_idx, int ctas, cudaStream_t s, LaunchHook *h);
+// The rank's share of bucket [lo, hi) (float indices, multiples of 4): [lo + 4*(n4*r/P), lo + 4*(n4*(r+1)/P)).
+inline void bucket_share(int64_t lo, int64_t hi, int P, int r, int64_t &a, int64_t &b) {
+    const int64_t n4 = (hi - lo) / 4;
+    a = lo + 4 * (n4 * r / P);
+    b = lo + 4 * (n4 * (r + 1) / P);
+}
+// Final barrier of a step: as peer_barrier, then (stepctr != nullptr) advances the step counter.
+cudaError_t peer_barrier_step(const PeerPtrs &pp, int P, int rank, uint64_t *epoch_ctr, int *errflag, uint64_t *stepctr,
+                              cudaStream_t s, LaunchHook *h);
 
 // Rank-ordered reduce of the owned slice + fused average/momentum update, results published to
 // every replica; loss slot n_pad folded by every rank into slot n_pad + 1.
