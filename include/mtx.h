@@ -90,9 +90,10 @@ typedef enum { MTX_FP32 = 0, MTX_TF32 = 1, MTX_3XTF32 = 2 } mtx_precision;
  *                      in ascending rank order (bit-exact with ORDERED), applies x fl(1/P) and
  *                      the momentum update and stores the updated w into every replica; v and
  *                      the reduced G stay sharded with their owner (ZeRO-1 style) and are
- *                      assembled from the peers by mtx_get_buffer / mtx_param_digest.  Cross-GPU
- *                      flag barriers (10 s timeout -> MTX_ERR_NCCL, the context then refuses
- *                      further steps) bracket it. */
+ *                      assembled from the peers by mtx_get_buffer / mtx_param_digest.  The kernel
+ *                      waits for every peer's "gradients ready" flag and a closing cross-GPU barrier
+ *                      follows it (10 s timeout -> MTX_ERR_NCCL; after a timeout the kernels load
+ *                      and store nothing and the context refuses further steps). */
 /*  MTX_REDUCE_LAYERWISE: the paper's own design ("an ordered list of reduction
  *                      operators ... sequentially synchronizes each layer"): after the backward,
  *                      one ncclAllReduce per variable (W_1, b_1, W_2, ...) in canonical order,

@@ -76,3 +76,16 @@ def test_build_entry_does_not_need_the_library(tmp_path):
         "assert src.index('b.build()') < src.index('import paper_1704_04560_b200'), 'package imported before build'\n"
         "assert 'from paper_1704_04560_b200' not in src\n")
     subprocess.run(["python", "-c", code], cwd=ROOT, check=True)
+
+
+def test_tf32_is_not_a_product_precision():
+    """Reading A22: mtx_init refuses MTX_TF32 (1xTF32 cannot meet the north_star's 1e-3) unless the development
+    variable is set; the check precedes any CUDA call, so it runs on a CPU host."""
+    import mtx_synth as S
+    from paper_1704_04560_b200 import mtx
+    if os.environ.get("MTX_DEV_TF32"):
+        pytest.skip("development override set")
+    cfg = S.CONFIGS["cfg1"]
+    with pytest.raises(mtx.MtxError) as e:
+        mtx.mtx_init(0, 1, None, 0, mtx.model_desc(cfg, 64), mtx.optim_desc(0.1, 0.0, mtx.MTX_TF32, 0, 0, 42))
+    assert e.value.status == 9  # MTX_ERR_UNSUPPORTED

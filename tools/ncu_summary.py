@@ -104,6 +104,12 @@ if os.path.exists(rep):
 open(out_md, "w").write("\n".join(lines) + "\n")
 tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 old = json.load(open(tp)) if os.path.exists(tp) else {}
+for k in [k for k in old if k.startswith(f"{config}:")]:  # a new capture of this config replaces the old one
+    del old[k]
 old.update(traffic)
+if traffic:  # provenance of this config's capture, read back by bench.py (traffic_source)
+    head = subprocess.run(["git", "-C", ROOT, "rev-parse", "--short", "HEAD"], capture_output=True, text=True).stdout.strip()
+    old.setdefault("_meta", {})[config] = {"capture": f"gpurun_out/prof_{tag}.ncu-rep (ncu --set full, summary "
+                                                      f"profiles/{rnd}_{tag}.md)", "commit": head}
 json.dump(old, open(tp, "w"), indent=1, sort_keys=True)
 print(out_md)
