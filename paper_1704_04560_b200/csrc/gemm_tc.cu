@@ -227,12 +227,12 @@ __device__ __forceinline__ void umma_tf32_pair_elect(uint32_t d_tmem, uint64_t a
         " @e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
-__device__ __forceinline__ void umma_commit_pair_elect(uint32_t bar) {
+__device__ __forceinline__ void umma_commit_pair_elect(uint32_t bar, uint16_t mask) {
     asm volatile(
         "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
         " @e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
             bar),
-        "h"((uint16_t)3)
+        "h"(mask)
         : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
@@ -297,11 +297,17 @@ __host__ __device__ constexpr uint32_t instr_desc(int M, int N, int a_mn, int b_
            ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int BN, bool MASK>
+// PAIR: the cluster holds the S pairs of a tile's splits (cluster rank = 2 * split + rank in the pair); the CTAs
+// holding the same 128-row half (rank in the pair pr) fold that half: CTA (z, pr) rows [z*BM/S, (z+1)*BM/S) of
+// it, reading cluster ranks 2u + pr.
+template <int BN, bool MASK, bool PAIR>
 __device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base) {
     int z, r;
-    unit_of(p, blockIdx.x, p.tiles_m * p.tiles_n, z, r);
-    const int m0 = (r / p.tiles_n) * BM, n0 = (r % p.tiles_n) * BN;
+    uint32_t crank = 0;
+    if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    const int pr = PAIR ? (int)(crank & 1) : 0;
+    unit_of(p, PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x, p.tiles_m * p.tiles_n, z, r);
+    const int m0 = (r / p.tiles_n) * (PAIR ? 2 * BM : BM) + BM * pr, n0 = (r % p.tiles_n) * BN;
     const int S = p.splits;
     const int r0 = BM * z / S, r1 = BM * (z + 1) / S;
     constexpr int CPR = BN / 4;
@@ -313,7 +319,7 @@ __device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base) {
         float4 v[8];
 #pragma unroll
         for (int u = 0; u < 8; u++)
-            if (u < S) v[u] = ld_dsmem_f4(la, (uint32_t)u);
+            if (u < S) v[u] = ld_dsmem_f4(la, PAIR ? (uint32_t)(2 * u + pr) : (uint32_t)u);
         float4 sum = v[0];
 #pragma unroll
         for (int u = 1; u < 8; u++)
@@ -339,9 +345,12 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                    tempty0 = tfull0 + 8 * NBUF;
     uint32_t *tmem_slot = (uint32_t *)(smem + L::BAR_OFF + 224);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t rank = 0;  // PAIR: rank in the CTA pair; rank 0 (the leader) issues the MMAs
-    if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    uint32_t crank = 0;  // PAIR: cluster rank; pairs are cluster ranks (2j, 2j + 1) -- a cluster holds one pair,
+                         // or the S pairs of a tile's K splits (p.cluster)
+    if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    const uint32_t rank = crank & 1, lead_rank = crank & ~1u;  // rank in the pair; cluster rank of its leader
     const bool leader = rank == 0;
+    const uint16_t pair_mask = (uint16_t)(3u << lead_rank);  // commit multicast to both CTAs of this pair
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&p.ta) : "memory");
@@ -410,7 +419,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                     const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::B_OFF;
                     const uint32_t fb = full0 + 8 * stage;
                     // PAIR: both CTAs' loads complete on the leader's full barrier, armed by the leader alone
-                    const uint32_t fbc = PAIR ? mapa_u32(fb, 0) : fb;
+                    const uint32_t fbc = PAIR ? mapa_u32(fb, lead_rank) : fb;
                     if (p.dbg & 2) {  // development: MMA-only timing
                         if (leader) mbar_arrive_elect(fb);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -490,12 +499,12 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                             }
                         }
                         // frees the smem slot (of both CTAs of a pair) when these MMAs retire
-                        if (PAIR) umma_commit_pair_elect(empty0 + 8 * stage);
+                        if (PAIR) umma_commit_pair_elect(empty0 + 8 * stage, pair_mask);
                         else umma_commit_elect(empty0 + 8 * stage);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                     // chunk partial ready for promotion (in both CTAs' TMEM for a pair)
-                    if (PAIR) umma_commit_pair_elect(tfull0 + 8 * buf);
+                    if (PAIR) umma_commit_pair_elect(tfull0 + 8 * buf, pair_mask);
                     else umma_commit_elect(tfull0 + 8 * buf);
                     if (++buf == NBUF) { buf = 0; buf_phase ^= 1; }
                 }
@@ -538,7 +547,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {  // accumulator buffer drained (PAIR: on the leader, which issues into it)
-                    if (PAIR) mbar_arrive_cluster(mapa_u32(tempty0 + 8 * buf, 0));
+                    if (PAIR) mbar_arrive_cluster(mapa_u32(tempty0 + 8 * buf, lead_rank));
                     else mbar_arrive(tempty0 + 8 * buf);
                 }
                 if (++buf == NBUF) { buf = 0; buf_phase ^= 1; }
@@ -610,7 +619,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
         // [z*BM/S, (z+1)*BM/S) over the splits in ascending order (deterministic) and stores them
         // with the fused epilogue; the second barrier keeps every CTA's smem alive until read
         cluster_sync_all();
-        if (warp >= 4 && warp < 12) cluster_fold<BN, MASK>(p, smem_u32(smem));
+        if (warp >= 4 && warp < 12) cluster_fold<BN, MASK, PAIR>(p, smem_u32(smem));
         cluster_sync_all();
     }
     tc_fence_before();
@@ -659,6 +668,7 @@ struct TcGemm {
     // + splitk_reduce launch)
     bool cluster = true;
     int max_clusters[2][3][9] = {};  // [SPLIT][BN 128/64/32][cluster size]: co-resident clusters (0 = unknown)
+    int max_pair_clusters[2][9] = {};  // [SPLIT][cluster size] for the 128-wide pair variant
     // CTA-pair (cta_group::2) 256 x 128 tiles for large GEMMs (MTX_TC_PAIR=0 disables)
     bool pair = true;
 };
@@ -794,7 +804,7 @@ static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s
     cfg.stream = s;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = PAIR ? 2 : p.splits;
+    at[0].val.clusterDim.x = PAIR ? (p.cluster ? 2 * p.splits : 2) : p.splits;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -802,6 +812,33 @@ static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s
     cfg.attrs = at;
     cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT, PAIR, MASK>, p);
+}
+
+// How many clusters of `cs` CTAs (cs / 2 CTA pairs) of the 128-wide pair variant can be resident at once.
+template <bool SPLIT>
+static int co_resident_pair(TcGemm *t, int cs) {
+    using L = SmemLayout<128, SPLIT, true>;
+    int &slot = t->max_pair_clusters[SPLIT ? 1 : 0][cs];
+    if (slot) return slot;
+    if (prepare<128, SPLIT, true>(t) != cudaSuccess) return 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs * 74);
+    cfg.blockDim = dim3(L::THREADS);
+    cfg.dynamicSmemBytes = L::TOTAL;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (void *)tc_gemm_kernel<128, SPLIT, true, false>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = -1;
+    }
+    slot = n;
+    return n;
 }
 
 template <int BN>
@@ -818,22 +855,34 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     // CTA pairs for large unsplit GEMMs: a 256 x 128 tile per pair halves B's per-SM operand traffic.
     // Pair MMAs also cost ~65 cycles with fresh operand tiles where a 1-CTA MMA of any N <= 128 costs ~89
     // (tools/mma_rate.cu, profiles/round2_tcgen05_rates.md); the dgrad pairs too (measured 84.0 -> 81.6 us at
-    // M = 8192, 44.4 -> 43.1 at 4096).  Development knobs: MTX_TC_PAIR_MASK=0 unpairs the dgrad;
-    // MTX_TC_PAIR_SPLIT=1 lets a weight gradient too small to fill the pairs split K through global partials
-    // (measured no faster than the DSMEM cluster fold: off).
+    // M = 8192, 44.4 -> 43.1 at 4096).  Development knob MTX_TC_PAIR_MASK=0 unpairs the dgrad.  A weight gradient
+    // too small to fill the pairs splits K over the pairs of one cluster, folded through DSMEM (below).
     static const bool pair_mask = !getenv("MTX_TC_PAIR_MASK") || atoi(getenv("MTX_TC_PAIR_MASK"));
-    static const bool pair_split = getenv("MTX_TC_PAIR_SPLIT") && atoi(getenv("MTX_TC_PAIR_SPLIT"));
+    static const int pair_split_env = getenv("MTX_TC_PAIR_SPLIT") ? atoi(getenv("MTX_TC_PAIR_SPLIT")) : -1;
     const int64_t ptiles = (int64_t)((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
     int pair_splits = 1;
     bool pair = t->pair && (g.epi != EPI_MASK || pair_mask) && BN == 128 && N % 64 == 0 && M > BM;
+    bool pair_cluster = false;
     if (pair && !(plan.splits == 1 && ptiles * 2 >= sms / 2)) {
         pair = false;
         const int kb = (K + BK - 1) / BK;
-        if (pair_split && g.epi == EPI_STORE && g.partial && M >= 2 * BM) {
-            const int sp = (int)std::min<int64_t>(std::max(1, kb / 8), std::max<int64_t>(1, (sms / 2) / ptiles));
+        // default: the long weight gradients (K >= 8192: 87.1 -> 84.9 us at 1024 x 1024 x 8192; no gain at
+        // K <= 4096, tools/gemm3x_bench.py); MTX_TC_PAIR_SPLIT=0/1 forces it off/on
+        const bool pair_split = pair_split_env >= 0 ? pair_split_env != 0 : kb >= 256;
+        if (pair_split && g.epi == EPI_STORE && M >= 2 * BM) {
+            // a weight gradient too small to fill the pairs: split K over S pairs of one cluster (2S CTAs),
+            // folded through distributed shared memory like the 1-CTA cluster plan
+            const int sp = (int)std::min<int64_t>(std::min(4, std::max(1, kb / 8)), std::max<int64_t>(1, (sms / 2) / ptiles));
             if (sp > 1 && ptiles * sp * 8 >= (int64_t)(sms / 2) * 6) {
-                pair = true;
-                pair_splits = sp;
+                const int nc = g.tf32x3 ? co_resident_pair<true>(t, 2 * sp) : co_resident_pair<false>(t, 2 * sp);
+                if (t->cluster && nc >= ptiles) {
+                    pair = true;
+                    pair_splits = sp;
+                    pair_cluster = true;
+                } else if (g.partial) {
+                    pair = true;  // split-K through global partials
+                    pair_splits = sp;
+                }
             }
         }
     }
@@ -866,7 +915,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     const int tiles = p.tiles_m * p.tiles_n;
     int splits = pair ? pair_splits : plan.splits;
     // split-K fold through DSMEM when the tile's splits fit one cluster and all clusters are co-resident
-    bool cluster = false;
+    bool cluster = pair_cluster;
     if (splits > 1 && splits <= 8 && t->cluster && !pair) {
         const int per = (p.kb_total + splits - 1) / splits;
         const int sp = (p.kb_total + per - 1) / per;
@@ -896,7 +945,7 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     p.ldc = g.ldc;
     p.partial = g.partial;
     const int total = tiles * splits;
-    const int grid = cluster ? total : pair ? 2 * std::min(total, sms / 2) : std::min(total, sms);
+    const int grid = cluster ? (pair ? 2 * total : total) : pair ? 2 * std::min(total, sms / 2) : std::min(total, sms);
     const char *kind = g.epi == EPI_MASK ? "dgrad" : (g.ta ? "wgrad" : "fwd");
     char name[96];
     snprintf(name, sizeof name, "gemm_tc%s_%s[M=%d,N=%d,K=%d,splits=%d,cluster=%d,pair=%d,bn=%d]", g.tf32x3 ? "3x" : "",
