@@ -7,7 +7,7 @@ import mtx_synth as S
 import paper_1704_04560_b200 as P
 from paper_1704_04560_b200 import mtx
 
-rep = P.Replica(dict(S.CONFIGS["cfg4"], B=1024), precision=P.MTX_TF32)
+rep = P.Replica(dict(S.CONFIGS["cfg4"], B=1024), precision=P.MTX_3XTF32)
 shapes = [(8192, 1024, 1024, 0, 0, 1), (8192, 1024, 1024, 0, 1, 3), (1024, 1024, 8192, 1, 0, 0),
           (8192, 1024, 28, 0, 0, 1), (512, 512, 784, 0, 0, 1), (784, 512, 512, 1, 0, 0), (4096, 4096, 4096, 0, 0, 1)]
 torch.backends.cuda.matmul.allow_tf32 = True

@@ -9,7 +9,7 @@ import mtx_synth as S
 import paper_1704_04560_b200 as P
 from paper_1704_04560_b200 import mtx
 
-rep = P.Replica(dict(S.CONFIGS["cfg4"]), precision=P.MTX_TF32)  # full-size: split-K partial room
+rep = P.Replica(dict(S.CONFIGS["cfg4"]), precision=P.MTX_3XTF32)  # full-size: split-K partial room
 SHAPES = {  # (M, N, K, ta, tb, epi)
     "cfg2_fwd1": (512, 512, 784, 0, 0, 1), "cfg2_fwd2": (512, 512, 512, 0, 0, 1),
     "cfg2_dgrad": (512, 512, 512, 0, 1, 3), "cfg2_wgrad1": (784, 512, 512, 1, 0, 0),
