@@ -72,6 +72,7 @@ struct TcParams {
     float *C_hi, *C_lo;  // optional hi/lo planes of the output (for the next 3xTF32 GEMM)
     int M, N, K;
     int a_mn, b_mn;      // operand majorness (1 = MN-major)
+    int a_3d, b_3d;      // MN-major operand described by a 3-D tensor map (32-element chunks stacked in one box)
     int tiles_m, tiles_n, splits, kb_total, kb_per_split;
     int epi;
     const float *bias;
@@ -237,6 +238,24 @@ __device__ __forceinline__ void umma_commit_pair_elect(uint32_t bar, uint16_t ma
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_elect(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1,
+                                                  int c2) {
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n}\n" ::"r"(
+            dst),
+        "l"((uint64_t)map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair_elect(uint32_t dst, const CUtensorMap *map, uint32_t bar_cluster, int c0,
+                                                       int c1, int c2) {
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n}\n" ::"r"(
+            dst),
+        "l"((uint64_t)map), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1) {
     asm volatile(
@@ -435,14 +454,24 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                             if (PAIR) tma_load_2d_pair_elect(dst, map, fbc, c0, c1);
                             else tma_load_2d_elect(dst, map, fb, c0, c1);
                         };
+                        // MN-major 3-D map: (32-element chunk, K row, chunk index) -> the chunks of a tile land
+                        // BK * 128 B apart, the MN-major SWIZZLE_128B_BASE32B layout, in one TMA operation
+                        auto load3 = [&](uint32_t dst, const CUtensorMap *map, int k_row, int chunk) {
+                            if (PAIR) tma_load_3d_pair_elect(dst, map, fbc, 0, k_row, chunk);
+                            else tma_load_3d_elect(dst, map, fb, 0, k_row, chunk);
+                        };
                         if (!p.a_mn) {
                             load(pa, ma, k0, (int)(row0 + m0));
+                        } else if (p.a_3d) {
+                            load3(pa, ma, (int)(row0 + k0), m0 / 32);
                         } else {
 #pragma unroll
                             for (int j = 0; j < BM / 32; j++) load(pa + j * 4096, ma, m0 + 32 * j, (int)(row0 + k0));
                         }
                         if (!p.b_mn) {
                             load(pb, mb, k0, n0);
+                        } else if (p.b_3d) {
+                            load3(pb, mb, k0, n0 / 32);
                         } else {
 #pragma unroll
                             for (int j = 0; j < B_COLS / 32; j++) load(pb + j * 4096, mb, n0 + 32 * j, k0);
@@ -655,6 +684,21 @@ bool make_map(EncodeTiled enc, CUtensorMap *m, const float *ptr, int64_t rows, i
                      mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// MN-major operand [rows][cols] (row pitch ld) as a 3-D map: dim0 = 32 elements of a 128-B chunk, dim1 = rows
+// (the K index), dim2 = cols / 32 chunks (stride 128 B); box {32, BK, chunks}.  Needs cols % 32 == 0: chunks never
+// run past a row (the 2-D map's zero fill is what covers a ragged cols).
+bool make_map_mn3d(EncodeTiled enc, CUtensorMap *m, const float *ptr, int64_t rows, int64_t cols, int64_t ld, int chunks) {
+    if (cols % 32 || ld % 4) return false;
+    cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)(cols / 32)};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 4, 128};
+    cuuint32_t box[3] = {32, (cuuint32_t)BK, (cuuint32_t)chunks};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)ptr, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
@@ -894,11 +938,17 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     // spans the whole wrap-extended buffer (rows are offset on the device by a_win + a_base).
     const int64_t a_rows_total = g.a_rows_total;
     bool ok;
+    // MN-major operands with whole 32-element chunks take the 3-D map (one TMA operation per operand tile)
+    static const bool mn3d = !getenv("MTX_TC_MN3D") || atoi(getenv("MTX_TC_MN3D"));
+    p.a_3d = (mn3d && g.ta && M % 32 == 0 && g.lda % 4 == 0) ? 1 : 0;
+    p.b_3d = (mn3d && !g.tb && N % 32 == 0 && g.ldb % 4 == 0 && BN % 32 == 0) ? 1 : 0;
     auto map_a = [&](CUtensorMap *m, const float *ptr) {
+        if (p.a_3d) return make_map_mn3d(t->encode, m, ptr, g.arow.win ? a_rows_total : K, M, g.lda, BM / 32);
         return !g.ta ? make_map(t->encode, m, ptr, g.arow.win ? a_rows_total : M, K, g.lda, BM, false)
                      : make_map(t->encode, m, ptr, g.arow.win ? a_rows_total : K, M, g.lda, BK, true);
     };
     auto map_b = [&](CUtensorMap *m, const float *ptr) {
+        if (p.b_3d) return make_map_mn3d(t->encode, m, ptr, K, N, g.ldb, (pair ? BN / 2 : BN) / 32);
         return g.tb ? make_map(t->encode, m, ptr, N, K, g.ldb, pair ? BN / 2 : BN, false)   // [N][K], K-major
                     : make_map(t->encode, m, ptr, K, N, g.ldb, BK, true);   // [K][N], MN-major
     };
