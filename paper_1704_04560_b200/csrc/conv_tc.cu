@@ -104,9 +104,12 @@ struct CtSmem {
     static constexpr uint32_t A_BUF = 2 * A_PLANE;      // hi + lo
     static constexpr uint32_t B_PLANE = NCOL * 128;
     static constexpr uint32_t A_OFF = 0, B_OFF = 2 * A_BUF;  // two A buffers (gather of tile i+1 || MMA of tile i)
-    static constexpr uint32_t Y_OFF = B_OFF + 2 * B_PLANE;
     static constexpr int YS = NCOL + 1;  // padded Y' row (conflict-free row-per-lane writes)
-    static constexpr uint32_t BAR_OFF = Y_OFF + YROWS * YS * 4;
+    // Y' of tile i lives in tile i's A buffer when it fits (its MMAs are complete when Y' is written, and the
+    // buffer is refilled only after tile i's epilogue): fewer bytes per CTA, more CTAs per SM
+    static constexpr bool Y_IN_A = (uint32_t)YROWS * YS * 4 <= A_BUF;
+    static constexpr uint32_t Y_OFF = B_OFF + 2 * B_PLANE;
+    static constexpr uint32_t BAR_OFF = Y_OFF + (Y_IN_A ? 0u : (uint32_t)YROWS * YS * 4);
     static constexpr uint32_t TOTAL = BAR_OFF + 64 + 1024;  // + 2 mbarriers, tmem slot, alignment slack
     static constexpr uint32_t ACC_COLS = NCOL <= 32 ? 32 : NCOL <= 64 ? 64 : NCOL <= 128 ? 128 : 256;
     static constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;  // two accumulators
@@ -220,6 +223,7 @@ __device__ __forceinline__ void ct_pipeline(int units, WFN wfn, GATHER gather, E
         mbar_wait(bar0 + 8 * buf, (phases >> buf) & 1);
         phases ^= 1u << buf;
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (L::Y_IN_A) sY = (float *)(sm + L::A_OFF + buf * L::A_BUF);
         {  // warp w reads TMEM lane quarter w % 4 (rows 32*(w%4) ..), 16-column chunks c = w / 4, w / 4 + 2, ...
             const int q = (tid >> 5) & 3, ch = tid >> 7, row = 32 * q + (tid & 31);
 #pragma unroll
