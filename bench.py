@@ -109,6 +109,8 @@ def kernel_work(name: str):
     kind, args = m.group(1), dict(kv.split("=") for kv in m.group(2).split(","))
     a = {k: int(v) for k, v in args.items()}
     if kind.startswith("gemm"):
+        if kind.startswith("gemm_tc3xf16"):  # 3 fp16 MMAs per product (3xF16 split): vs a third of the f16 peak
+            return "flop", 2 * a["M"] * a["N"] * a["K"], "tensor3xf16"
         if kind.startswith("gemm_tc3x"):  # 3 tf32 MMAs per product: tensor work is 3x the algorithmic flops
             return "flop", 2 * a["M"] * a["N"] * a["K"], "tensor3x"
         tensor = kind.startswith("gemm_tc")
@@ -178,6 +180,10 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
         achieved = per_launch_work / per_launch_s / 1e12
         peak, unit = pk["bf16_tflops"] * TF32_PER_BF16 / 3, "TFLOP/s"
         top["bound"] = "tensor"
+    elif top["bound"] == "tensor3xf16":  # fp32-equivalent flops vs one third of the f16 (= bf16) peak
+        achieved = per_launch_work / per_launch_s / 1e12
+        peak, unit = pk["bf16_tflops"] / 3, "TFLOP/s"
+        top["bound"] = "tensor"
     else:  # fp32 CUDA-core FMA peak at the clock observed under load
         achieved = per_launch_work / per_launch_s / 1e12
         clk = sm_mhz or pk.get("sm_max_mhz", 1965.0)
@@ -189,8 +195,9 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
     bn = re.search(r"bn=(\d+)", longest)
     bn = bn.group(1) if bn else "128"
     pr = re.search(r"pair=(\d)", longest)
-    tpl = f"{bn}, {{}}, {pr.group(1) if pr else 0}, {1 if '_dgrad' in longest else 0}"  # <BN, 3x, PAIR, MASK>
-    ncu_kernel = {"gemm_tc3x": f"tc_gemm_kernel<{tpl.format(1)}>", "gemm_tc": f"tc_gemm_kernel<{tpl.format(0)}>",
+    tpl = f"{bn}, {{}}, {pr.group(1) if pr else 0}, {1 if '_dgrad' in longest else 0}, {{}}"  # <BN, 3x, PAIR, MASK, F16>
+    ncu_kernel = {"gemm_tc3xf16": f"tc_gemm_kernel<{tpl.format(1, 1)}>", "gemm_tc3x": f"tc_gemm_kernel<{tpl.format(1, 0)}>",
+                  "gemm_tc": f"tc_gemm_kernel<{tpl.format(0, 0)}>",
                   "avg_update": "avg_update_kernel<1>", "fused_avg_update": "fused_avg_update_kernel", "head_softmax_xent": "head_kernel",
                   "colsum": "colsum_kernel", "splitk_reduce": "splitk_reduce_kernel", "conv_bwd": "conv_bwd_kernel",
                   "conv_fwd": "conv_fwd_kernel"}
@@ -209,7 +216,10 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
     return {"kernel": top_name, "bound": top["bound"], "achieved": round(achieved, 3), "peak": round(peak, 1),
             "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
             "peak_kind": {"GB/s": "measured copy" if top["bound"] == "hbm" else "measured NVLink peer copy per direction",
-                          "TFLOP/s": "measured bf16 burst x tf32/bf16 nominal ratio" + (" / 3 (3xTF32)" if top_name.startswith("gemm_tc3x") else "")}.get(unit),
+                          "TFLOP/s": ("measured bf16 burst (= f16 dense) / 3 (3xF16: three f16 MMAs per product)"
+                                      if top_name.startswith("gemm_tc3xf16") else
+                                      "measured bf16 burst x tf32/bf16 nominal ratio" +
+                                      (" / 3 (3xTF32)" if top_name.startswith("gemm_tc3x") else ""))}.get(unit),
             "work_per_launch": per_launch_work, "launch_us": round(per_launch_s * 1e6, 3),
             "share_of_kernel_time": round(top["ms"] / total, 3),
             "launch_overhead_us_subtracted": round(over_ms * 1e3, 3),
@@ -286,7 +296,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     # cfg4 (the largest config; the north_star's scaling target is quoted on it)
     ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
-    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "3xtf32"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "3xtf32", "3xf16"])
     ap.add_argument("--impl", default="mtx", choices=["mtx", "reference"])
     ap.add_argument("--bucket-mb", type=float, default=1.0)
     ap.add_argument("--reduce", default="fused", choices=["nccl", "ordered", "fused", "layerwise", "zero1"],
@@ -336,7 +346,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     tc_ok = "tcgen05" in mtx.mtx_build_info()
-    prec = {"fp32": P.MTX_FP32, "3xtf32": P.MTX_3XTF32}.get(
+    prec = {"fp32": P.MTX_FP32, "3xtf32": P.MTX_3XTF32, "3xf16": P.MTX_3XF16}.get(
         args.precision, P.MTX_3XTF32 if tc_ok else P.MTX_FP32)
     uid = P.nccl_uid_broadcast(rank, world)
     X, y = S.dataset(cfg)
@@ -463,7 +473,8 @@ def main():
         line = {"metric": metric, "value": round(value, 1), "unit": "samples/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 5),
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": {P.MTX_TF32: "tf32", P.MTX_3XTF32: "f32 (3xtf32 tensor cores)"}.get(prec, "f32"),
+                "dtype": {P.MTX_TF32: "tf32", P.MTX_3XTF32: "f32 (3xtf32 tensor cores)",
+                          P.MTX_3XF16: "f32 (3xf16 scaled split, tensor cores)"}.get(prec, "f32"),
                 "data": "synthetic",
                 "config": run_config(args, cfg, world), "engine": mtx.mtx_build_info(),
                 "per_rank_ms": [round(t, 3) for t in t_all], "final_loss": loss,

@@ -76,8 +76,14 @@ typedef enum { MTX_MLP = 0, MTX_CNN = 1 } mtx_model_kind;
  *  MTX_3XTF32: tcgen05 with each operand split into its TF32 part and a TF32 residual,
  *              3 MMAs per k-step (big.small + small.big + big.big): fp32-accurate, gated
  *              at 1e-5 like MTX_FP32.
+ *  MTX_3XF16:  the same 3-product split with fp16 parts (fp16 has TF32's 11-bit significand) and one
+ *              power-of-two scale per tensor that maps the tensor into fp16's exponent range
+ *              (x = s (hi + lo), undone exactly in the consuming GEMM's epilogue): fp32-accurate,
+ *              gated at 1e-5; kind::f16 MMAs take 16 k per instruction where kind::tf32 takes 8, and
+ *              the planes move half the bytes.  Scales come from exact maxima (parameters, inputs)
+ *              or from a-priori bounds of each GEMM output, so no value overflows.
  * Reductions across ranks, the average and the update are fp32 in all modes. */
-typedef enum { MTX_FP32 = 0, MTX_TF32 = 1, MTX_3XTF32 = 2 } mtx_precision;
+typedef enum { MTX_FP32 = 0, MTX_TF32 = 1, MTX_3XTF32 = 2, MTX_3XF16 = 3 } mtx_precision;
 
 /* How the gradient allreduce-sum is computed (reading A2).
  *  MTX_REDUCE_NCCL:    ncclAllReduce(sum) per bucket on a comm stream -- NCCL's order
@@ -278,7 +284,8 @@ mtx_status mtx_read_timing(mtx_ctx *ctx, char *names_buf, uint64_t names_len, do
 /* Diagnostic: one local contraction through a chosen engine (0 = SIMT fp32, 1 =
  * tcgen05 TF32, 2 = tcgen05 3xTF32 -- A and B are split into hi/lo planes in library-owned
  * scratch first; 3 = tcgen05 3xTF32 on the planes of the previous engine-2 call, which must
- * have had the same A, B, shape and layout: times the contraction alone), exactly as the step issues it -- C[M,N] = op(A) op(B) with
+ * have had the same A, B, shape and layout: times the contraction alone; 4 / 5 = the same pair for
+ * tcgen05 3xF16, MTX_3XF16 contexts only), exactly as the step issues it -- C[M,N] = op(A) op(B) with
  * epilogue epi (0 store, 1 +bias then ReLU, 2 +bias, 3 x [mask > 0]); ta/tb as
  * in the step's forward (0,0), dgrad (0,1) and wgrad (1,0) layouts.  Device
  * pointers, row-major fp32, leading dimensions in elements.  Used by the

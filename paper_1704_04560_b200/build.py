@@ -45,21 +45,32 @@ def build(force: bool = False, verbose: bool = False) -> str:
     deps = sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
                   + [os.path.join(ROOT, "include", "mtx.h")])
     dep_mtime = max(os.path.getmtime(d) for d in deps)
-    objs, rebuilt = [], False
+    objs, todo = [], []
     for s in srcs:
         o = os.path.join(OBJ, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
         if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), dep_mtime):
-            cmd = [NVCC, *_flags(inc), "-c", s, "-o", o]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            with open(o + ".log", "w") as f:
-                f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-            if r.returncode != 0:
-                sys.stderr.write(r.stdout + r.stderr)
-                raise RuntimeError(f"nvcc failed on {s}")
-            if verbose:
-                print(r.stderr)
-            rebuilt = True
+            todo.append((s, o))
+
+    def compile_one(so):
+        s, o = so
+        cmd = [NVCC, *_flags(inc), "-c", s, "-o", o]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        with open(o + ".log", "w") as f:
+            f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        return s, r
+
+    # the translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, todo))
+    for s, r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {s}")
+        if verbose:
+            print(r.stderr)
+    rebuilt = bool(todo)
     if rebuilt or force or not os.path.exists(LIB):
         tmp = LIB + f".tmp{os.getpid()}"
         cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", libdir, "-l:libnccl.so.2",

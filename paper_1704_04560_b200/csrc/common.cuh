@@ -1,5 +1,6 @@
 // common.cuh -- internal helpers of libmtx (product path; independent of oracle/).
 #pragma once
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -38,6 +39,37 @@ MTX_DEVI void split_tf32(float x, float &hi, float &lo) {
     const uint32_t h = rne_tf32_bits(__float_as_uint(x));
     hi = __uint_as_float(h);
     lo = __uint_as_float(rne_tf32_bits(__float_as_uint(x - hi)));
+}
+
+// 3xF16 operand planes: x = s * (hi + lo) with s = 2^e a per-tensor power of two,
+// hi = rn_f16(x / s), lo = rn_f16(x / s - hi).  fp16 has TF32's 11-bit significand, so hi + lo carries
+// x to ~2^-22 relative exactly like the 3xTF32 planes; the power-of-two scale only moves the exponent
+// into fp16's range and is undone exactly in the consuming GEMM's epilogue.  One slot per tensor:
+//   amax  -- max |x| of the tensor's current values (exact when written by quantize_f16; accumulated
+//            with atomicMax by GEMM / head epilogues, zeroed once per step)
+//   scale -- s, written by the tensor's producer before any consumer runs
+struct TScale {
+    float amax;
+    float scale;
+    unsigned pad[2];
+};
+// s = 2^e with bound < 2^(e + 15): every |x| <= bound maps to |x / s| < 32768 (fp16 max 65504).
+MTX_DEVI float f16_scale_for(float bound) {
+    if (!(bound > 0.f) || bound > 3.0e38f) return 1.f;  // zero, NaN, inf: the flag path reports it
+    const int e = (int)((__float_as_uint(bound) >> 23) & 0xFFu) - 127;  // floor(log2 bound) (normal)
+    int se = e + 1 - 15;
+    se = se < -126 ? -126 : (se > 127 ? 127 : se);
+    return __uint_as_float((uint32_t)(se + 127) << 23);
+}
+// hi/lo of y = x * inv_s (exact: inv_s is a power of two); y - hi is exact in fp32
+MTX_DEVI void split_f16(float x, float inv_s, uint16_t &hi, uint16_t &lo) {
+    const float y = x * inv_s;
+    const float h = __half2float(__float2half_rn(y));
+    hi = __half_as_ushort(__float2half_rn(y));
+    lo = __half_as_ushort(__float2half_rn(y - h));
+}
+MTX_DEVI void amax_atomic(float *slot, float v) {  // v >= 0 (non-negative floats order like their bits)
+    atomicMax((unsigned *)slot, __float_as_uint(v));
 }
 
 // Shared-memory mbarriers (completion tracking of TMA / bulk copies and tcgen05 commits).

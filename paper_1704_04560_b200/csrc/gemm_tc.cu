@@ -30,21 +30,28 @@
 namespace mtx {
 namespace {
 
-constexpr int BM = 128, BK = 32;
+#ifndef MTX_F16_CHUNK
+#define MTX_F16_CHUNK 4
+#endif
+// BK: k-block in fp32 (TF32) elements; a k-block row is 128 B in both element types (BKH = 64 fp16)
+constexpr int BM = 128, BK = 32, BKH = 64;
 
 // Shared-memory plan per variant.  SPLIT (3xTF32) stages two planes of each operand tile: hi =
 // rne_tf32(x) and lo = rne_tf32(x - hi), written once by the tensor's producer.
-template <int BN, bool SPLIT, bool PAIR = false>
+// F16 (3xF16): the same two planes in fp16 with a per-tensor power-of-two scale (common.cuh): a k-block
+// of 64 fp16 elements occupies the bytes of 32 fp32 ones, so the byte plan is identical.
+template <int BN, bool SPLIT, bool PAIR = false, bool F16 = false>
 struct SmemLayout {
     // warps 0 TMA, 1 MMA, 2 TMEM alloc, 3 spare, 4-11 epilogue
     static constexpr int THREADS = 384;
     // k-blocks accumulated in TMEM before the epilogue warps promote the partial into fp32
-    // registers (the tensor core's internal accumulation truncates)
-    static constexpr int CHUNK = SPLIT ? 4 : 8;
-    static constexpr uint32_t A_BYTES = BM * BK * 4;
+    // registers (the tensor core's internal accumulation truncates): K = 128
+    // elements per promotion in both split modes
+    static constexpr int CHUNK = F16 ? MTX_F16_CHUNK : SPLIT ? 4 : 8;
+    static constexpr uint32_t A_BYTES = BM * 128;
     // PAIR (cta_group::2): the CTA pair computes a 256 x BN tile; each CTA holds its 128 rows of A and
     // half of B's BN columns (the MMA reads both halves; measured by tools/tc_pair_probe.cu)
-    static constexpr uint32_t B_BYTES = (PAIR ? BN / 2 : BN) * BK * 4;
+    static constexpr uint32_t B_BYTES = (PAIR ? BN / 2 : BN) * 128;
     // stage: [A][B] (hi planes) followed, for 3xTF32, by [A_lo][B_lo] at RAW_BYTES
     static constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;
     static constexpr uint32_t B_OFF = A_BYTES;
@@ -86,6 +93,13 @@ struct TcParams {
     int dbg;               // development only (MTX_TC_DBG): 1 skip epilogue stores, 2 skip TMA loads
     int cluster;           // 1: the splits of a tile form one thread-block cluster and are folded
                            // through distributed shared memory (no partial buffer, no fold launch)
+    // 3xF16: operand scale slots (the sum is multiplied by s_A * s_B, exact) and the output planes
+    const TScale *tsA, *tsB;
+    F16Out fo;
+    // dgrad: the ReLU mask as a bitmask [M][mbits_ld words] (written by the forward epilogue) instead of
+    // the fp32 activation
+    const uint32_t *mbits;
+    int64_t mbits_ld;
 };
 
 // Work unit t -> (k-split z, output tile r).  Cluster mode: the splits of a tile are consecutive
@@ -103,6 +117,10 @@ __device__ __forceinline__ void unit_of(const TcParams &p, int t, int tiles_mn, 
 // ReLU-mask values mask[m][n..n+3] (dgrad epilogue): loaded ahead of the stores they gate, so a
 // warp's mask loads are in flight together instead of one HBM round trip per store.
 __device__ __forceinline__ float4 load_mask(const TcParams &p, int m, int n) {
+    if (p.mbits) {  // bits n..n+3 of the row's word n / 32 (n % 4 == 0; bits past N are 0)
+        const uint32_t w = __ldg(p.mbits + (int64_t)m * p.mbits_ld + (n >> 5)) >> (n & 31);
+        return make_float4((float)(w & 1u), (float)((w >> 1) & 1u), (float)((w >> 2) & 1u), (float)((w >> 3) & 1u));
+    }
     const float *mk = p.mask + (int64_t)m * p.ldm + n;
     if (n + 3 < p.N) return __ldg((const float4 *)mk);
     float mv[4];
@@ -113,8 +131,8 @@ __device__ __forceinline__ float4 load_mask(const TcParams &p, int m, int n) {
 // The fused epilogue on 4 consecutive outputs C[m][n..n+3] (coalesced across a warp): bias (+ReLU)
 // or ReLU mask (mkv, from load_mask), the fp32 store and, for a 3xTF32 consumer, the hi/lo planes.
 // MASK: compile-time dgrad variant (EPI_MASK); otherwise bias (+ReLU) or a plain store.
-template <bool MASK>
-__device__ __forceinline__ void epi_store(const TcParams &p, int m, int n, float4 sv, float4 mkv) {
+template <bool MASK, bool F16>
+__device__ __forceinline__ float4 epi_store(const TcParams &p, int m, int n, float4 sv, float4 mkv, float inv_so, float &amx) {
     const bool vec4 = n + 3 < p.N;
     float o[4] = {sv.x, sv.y, sv.z, sv.w};
     if constexpr (MASK) {
@@ -131,9 +149,31 @@ __device__ __forceinline__ void epi_store(const TcParams &p, int m, int n, float
             }
     }
     const int64_t off = (int64_t)m * p.ldc + n;
-    if (vec4) *(float4 *)(p.C + off) = make_float4(o[0], o[1], o[2], o[3]);
-    else for (int e = 0; e < 4 && n + e < p.N; e++) p.C[off + e] = o[e];
-    if (p.C_hi) {  // hi/lo planes for the consuming 3xTF32 GEMM
+    if (p.C && !(F16 && p.fo.skip_f32 && p.splits == 1)) {
+        if (vec4) *(float4 *)(p.C + off) = make_float4(o[0], o[1], o[2], o[3]);
+        else for (int e = 0; e < 4 && n + e < p.N; e++) p.C[off + e] = o[e];
+    }
+    if (F16) {  // fp16 hi/lo planes (scale from the output bound) for the consuming 3xF16 GEMM
+        if (p.fo.h) {
+            uint16_t hi[4], lo[4];
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const float x = n + e < p.N ? o[e] : 0.f;
+                split_f16(x, inv_so, hi[e], lo[e]);
+                amx = fmaxf(amx, fabsf(x));
+            }
+            const int64_t po = (int64_t)m * p.fo.ld + n;
+            if (vec4) {
+                *(uint2 *)(p.fo.h + po) = make_uint2(hi[0] | ((uint32_t)hi[1] << 16), hi[2] | ((uint32_t)hi[3] << 16));
+                *(uint2 *)(p.fo.l + po) = make_uint2(lo[0] | ((uint32_t)lo[1] << 16), lo[2] | ((uint32_t)lo[3] << 16));
+            } else {
+                for (int e = 0; e < 4 && n + e < p.N; e++) {
+                    p.fo.h[po + e] = __ushort_as_half(hi[e]);
+                    p.fo.l[po + e] = __ushort_as_half(lo[e]);
+                }
+            }
+        }
+    } else if (p.C_hi) {  // hi/lo planes for the consuming 3xTF32 GEMM
         float hi[4], lo[4];
 #pragma unroll
         for (int e = 0; e < 4; e++) split_tf32(o[e], hi[e], lo[e]);
@@ -147,6 +187,7 @@ __device__ __forceinline__ void epi_store(const TcParams &p, int m, int n, float
             }
         }
     }
+    return make_float4(o[0], n + 1 < p.N ? o[1] : 0.f, n + 2 < p.N ? o[2] : 0.f, n + 3 < p.N ? o[3] : 0.f);
 }
 
 // Cluster split-K: the fp32 partial tile [BM][BN] of a CTA lives at the start of its (then idle)
@@ -199,6 +240,22 @@ __device__ __forceinline__ void umma_tf32_elect(uint32_t d_tmem, uint64_t adesc,
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// kind::f16 (fp16 operands, fp32 accumulator): K = 16 per instruction, same issue cost as kind::tf32's K = 8
+__device__ __forceinline__ void umma_f16_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_f16_pair_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                    uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+        " @e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
     asm volatile(
         "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
@@ -237,7 +294,9 @@ __device__ __forceinline__ void umma_commit_pair_elect(uint32_t bar, uint16_t ma
         : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+    // default semantics (release at CTA scope), as CUTLASS arrives on a peer CTA's barrier: ".release.cluster" compiles to
+    // MEMBAR.ALL.GPU, which made every TMEM hand-off wait for the epilogue's outstanding global stores (ncu)
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 __device__ __forceinline__ void tma_load_3d_elect(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1,
                                                   int c2) {
@@ -299,6 +358,9 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 //   MN-major: SWIZZLE_128B_BASE32B (type 1, the only MN-major layout tf32 accepts) -- 128-B rows
 //             of 32 M/N elements, 32-B chunks XOR row%4; 4-row K groups at SBO = 512 B, 32-element
 //             M/N groups at LBO = BK * 128 B.  k-step of 8 = +1024 B.
+//   fp16 (3xF16): K-major as above (64 elements per 128-B row, k-step of 16 = +32 B); MN-major
+//             SWIZZLE_128B (type 2) -- 128-B rows of 64 M/N elements, 16-B chunks XOR row%8; 8-row K
+//             groups at SBO = 1024 B, 64-element M/N groups at LBO = BKH * 128 B.  k-step of 16 = +2048 B.
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes,
                                               uint32_t layout_type) {
     uint64_t d = 0;
@@ -310,17 +372,18 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes,
     return d;
 }
 
-// Instruction descriptor: D fp32, A/B tf32, majors, N>>3, M>>4 (kind::tf32, dense).
-__host__ __device__ constexpr uint32_t instr_desc(int M, int N, int a_mn, int b_mn) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// Instruction descriptor: D fp32, A/B tf32 (format 2, kind::tf32) or f16 (format 0, kind::f16), majors,
+// N>>3, M>>4 (dense).
+__host__ __device__ constexpr uint32_t instr_desc(int M, int N, int a_mn, int b_mn, bool f16 = false) {
+    return (1u << 4) | ((f16 ? 0u : 2u) << 7) | ((f16 ? 0u : 2u) << 10) | ((uint32_t)a_mn << 15) |
+           ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 // PAIR: the cluster holds the S pairs of a tile's splits (cluster rank = 2 * split + rank in the pair); the CTAs
 // holding the same 128-row half (rank in the pair pr) fold that half: CTA (z, pr) rows [z*BM/S, (z+1)*BM/S) of
 // it, reading cluster ranks 2u + pr.
-template <int BN, bool MASK, bool PAIR>
-__device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base) {
+template <int BN, bool MASK, bool PAIR, bool F16>
+__device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base, float inv_so, float &amx) {
     int z, r;
     uint32_t crank = 0;
     if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
@@ -345,13 +408,16 @@ __device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base) {
             if (u < S) {
                 sum.x += v[u].x; sum.y += v[u].y; sum.z += v[u].z; sum.w += v[u].w;
             }
-        epi_store<MASK>(p, m, n, sum, MASK ? load_mask(p, m, n) : make_float4(0.f, 0.f, 0.f, 0.f));
+        epi_store<MASK, F16>(p, m, n, sum, MASK ? load_mask(p, m, n) : make_float4(0.f, 0.f, 0.f, 0.f), inv_so, amx);
     }
 }
 
-template <int BN, bool SPLIT, bool PAIR, bool MASK>
+template <int BN, bool SPLIT, bool PAIR, bool MASK, bool F16>
 __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
-    using L = SmemLayout<BN, SPLIT, PAIR>;
+    using L = SmemLayout<BN, SPLIT, PAIR, F16>;
+    constexpr int KB = F16 ? BKH : BK;        // elements per k-block (one 128-B row)
+    constexpr int CH = F16 ? 64 : 32;         // MN-major: elements per 128-B chunk along M/N
+    constexpr uint32_t CHB = (uint32_t)KB * 128;  // bytes between MN-major chunks of a stage
     constexpr int STAGES = L::STAGES;
     extern __shared__ uint8_t smem_raw[];
     // SWIZZLE_128B atoms need 1024-B aligned stage buffers
@@ -445,7 +511,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                         continue;
                     }
                     if (leader) mbar_expect_tx_elect(fb, PAIR ? 2 * L::STAGE_BYTES : L::STAGE_BYTES);
-                    const int k0 = kb * BK;
+                    const int k0 = kb * KB;
 #pragma unroll
                     for (int plane = 0; plane < (SPLIT ? 2 : 1); plane++) {  // hi into the raw region, lo after it
                         const CUtensorMap *ma = plane ? &p.ta_lo : &p.ta, *mb = plane ? &p.tb_lo : &p.tb;
@@ -463,18 +529,18 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                         if (!p.a_mn) {
                             load(pa, ma, k0, (int)(row0 + m0));
                         } else if (p.a_3d) {
-                            load3(pa, ma, (int)(row0 + k0), m0 / 32);
+                            load3(pa, ma, (int)(row0 + k0), m0 / CH);
                         } else {
 #pragma unroll
-                            for (int j = 0; j < BM / 32; j++) load(pa + j * 4096, ma, m0 + 32 * j, (int)(row0 + k0));
+                            for (int j = 0; j < BM / CH; j++) load(pa + j * CHB, ma, m0 + CH * j, (int)(row0 + k0));
                         }
                         if (!p.b_mn) {
                             load(pb, mb, k0, n0);
                         } else if (p.b_3d) {
-                            load3(pb, mb, k0, n0 / 32);
+                            load3(pb, mb, k0, n0 / CH);
                         } else {
 #pragma unroll
-                            for (int j = 0; j < B_COLS / 32; j++) load(pb + j * 4096, mb, n0 + 32 * j, k0);
+                            for (int j = 0; j < B_COLS / CH; j++) load(pb + j * CHB, mb, n0 + CH * j, k0);
                         }
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -487,10 +553,12 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
         // the epilogue.  Descriptors: built once per k-block, advanced by a constant per 8-element k-step
         // (K-major: 32 B inside the 128-B swizzled row; MN-major: two 4-row K groups = 1024 B).
         {
-            const uint32_t idesc = instr_desc(TILE_M, BN, p.a_mn, p.b_mn);
-            const uint64_t a_hi = p.a_mn ? smem_desc(0, BK * 128, 512, 1) : smem_desc(0, 16, 1024, 2);
-            const uint64_t b_hi = p.b_mn ? smem_desc(0, BK * 128, 512, 1) : smem_desc(0, 16, 1024, 2);
-            const uint32_t a_step = p.a_mn ? (1024 >> 4) : (32 >> 4), b_step = p.b_mn ? (1024 >> 4) : (32 >> 4);
+            const uint32_t idesc = instr_desc(TILE_M, BN, p.a_mn, p.b_mn, F16);
+            const uint64_t mn_desc = F16 ? smem_desc(0, BKH * 128, 1024, 2) : smem_desc(0, BK * 128, 512, 1);
+            const uint64_t a_hi = p.a_mn ? mn_desc : smem_desc(0, 16, 1024, 2);
+            const uint64_t b_hi = p.b_mn ? mn_desc : smem_desc(0, 16, 1024, 2);
+            constexpr uint32_t MN_STEP = (F16 ? 2048 : 1024) >> 4;  // one MMA's K rows in an MN-major tile
+            const uint32_t a_step = p.a_mn ? MN_STEP : (32 >> 4), b_step = p.b_mn ? MN_STEP : (32 >> 4);
             constexpr uint64_t LO = L::RAW_BYTES >> 4;  // hi plane -> lo plane of the same operand tile
             int stage = 0;
             uint32_t phase = 0;
@@ -511,15 +579,20 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                         const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::B_OFF;
                         const uint64_t ad0 = a_hi | ((sa >> 4) & 0x3FFF), bd0 = b_hi | ((sb >> 4) & 0x3FFF);
 #pragma unroll
-                        for (int kk = 0; kk < BK / 8; kk++) {
+                        for (int kk = 0; kk < 4; kk++) {  // 4 MMAs of K = 8 (tf32) / 16 (f16) per k-block
                             const uint64_t ad = ad0 + kk * a_step, bd = bd0 + kk * b_step;
                             const uint32_t acc0 = (kb > c0 || kk > 0) ? 1u : 0u;
                             auto mma = [&](uint64_t x, uint64_t y, uint32_t acc) {
-                                if (PAIR) umma_tf32_pair_elect(d_tmem, x, y, idesc, acc);
-                                else umma_tf32_elect(d_tmem, x, y, idesc, acc);
+                                if (F16) {
+                                    if (PAIR) umma_f16_pair_elect(d_tmem, x, y, idesc, acc);
+                                    else umma_f16_elect(d_tmem, x, y, idesc, acc);
+                                } else {
+                                    if (PAIR) umma_tf32_pair_elect(d_tmem, x, y, idesc, acc);
+                                    else umma_tf32_elect(d_tmem, x, y, idesc, acc);
+                                }
                             };
                             if (SPLIT) {
-                                // 3xTF32: hi.lo + lo.hi + hi.hi (hi = rne_tf32(x), lo = rne_tf32(x - hi))
+                                // 3xTF32 / 3xF16: hi.lo + lo.hi + hi.hi (hi = rn(x), lo = rn(x - hi))
                                 mma(ad, bd + LO, acc0);
                                 mma(ad + LO, bd, 1u);
                                 mma(ad, bd, 1u);
@@ -547,6 +620,18 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
         const int q = warp & 3, h = (warp - 4) >> 2;
         int buf = 0;
         uint32_t buf_phase = 0;
+        // 3xF16: the sum of scaled operands times s_A * s_B (powers of two: exact), and the output planes'
+        // scale from their bound (every CTA computes the same value; one thread publishes it)
+        float fa = 1.f, fb = 1.f, inv_so = 1.f, amx = 0.f;
+        if (F16) {
+            fa = p.tsA->scale;  // applied one after the other: s_A * s_B alone may leave fp32's range
+            fb = p.tsB->scale;
+            if (p.fo.h) {
+                const float so = f16out_scale(p.fo);
+                inv_so = 1.f / so;
+                if (blockIdx.x == 0 && threadIdx.x == 128) p.fo.ts->scale = so;
+            }
+        }
         MTX_UNITS(t) {
             int z, r;
             unit_of(p, t, tiles_mn, z, r);
@@ -581,6 +666,10 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                 }
                 if (++buf == NBUF) { buf = 0; buf_phase ^= 1; }
             }
+            if (F16) {
+#pragma unroll
+                for (int j = 0; j < HALF; j++) acc[j] = (acc[j] * fa) * fb;
+            }
             if (p.cluster) {  // partial tile -> own smem; folded across the cluster below
                 const int row = 32 * q + lane;
 #pragma unroll
@@ -597,8 +686,12 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
             float *stg = (float *)(smem + L::EPI_OFF) + (warp - 4) * 32 * 32;
             const int jj = lane % CPR, rl = lane / CPR;
             auto swz = [](int row, int chunk) { return (chunk ^ (row / (8 / CPR))) & (CPR - 1); };
+            // 3xF16 lean outputs (direct path only): the forward's ReLU bitmask, the dgrad's per-32-row column sums
+            const bool want_bits = F16 && p.fo.bits && p.splits == 1;
+            const bool want_cols = F16 && p.fo.colpart && p.splits == 1;
 #pragma unroll
             for (int c = 0; c < HALF / SW; c++) {
+                float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int j = 0; j < CPR; j++)
                     *(float4 *)(stg + lane * SW + 4 * swz(lane, j)) =
@@ -625,21 +718,52 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                         const int r = it * RPI + rl;
                         const int m = m0 + 32 * q + r;
                         const float4 sv = *(const float4 *)(stg + r * SW + 4 * swz(r, jj));
-                        if (m >= p.M || n >= p.N || (p.dbg & 1)) continue;
-                        if (p.splits > 1) {  // split-K partial (folded with the epilogue by splitk_reduce)
+                        const bool ok = m < p.M && n < p.N && !(p.dbg & 1);
+                        if (ok && p.splits > 1) {  // split-K partial (folded with the epilogue by splitk_reduce)
                             float *dst = p.partial + ((int64_t)z * p.M + m) * p.N + n;
                             if (n + 3 < p.N) *(float4 *)dst = sv;
                             else {
                                 const float o[4] = {sv.x, sv.y, sv.z, sv.w};
                                 for (int e = 0; e < 4 && n + e < p.N; e++) dst[e] = o[e];
                             }
-                            continue;
                         }
-                        epi_store<MASK>(p, m, n, sv, mk[u]);
+                        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (ok && p.splits == 1) o = epi_store<MASK, F16>(p, m, n, sv, mk[u], inv_so, amx);
+                        if (want_bits) {  // the 8 lanes of a row hold its 32 columns: OR their nibbles into one word
+                            uint32_t w = ((o.x > 0.f) | ((o.y > 0.f) << 1) | ((o.z > 0.f) << 2) | ((o.w > 0.f) << 3))
+                                         << (4 * jj);
+                            w |= __shfl_xor_sync(0xffffffffu, w, 1);
+                            w |= __shfl_xor_sync(0xffffffffu, w, 2);
+                            w |= __shfl_xor_sync(0xffffffffu, w, 4);
+                            if (jj == 0 && m < p.M && n < p.N) p.fo.bits[(int64_t)m * p.fo.bits_ld + (n >> 5)] = w;
+                        }
+                        if (want_cols) { cs.x += o.x; cs.y += o.y; cs.z += o.z; cs.w += o.w; }
+                    }
+                }
+                if (want_cols) {  // rows of this warp's quarter, in a fixed tree over the lanes of a column group
+#pragma unroll
+                    for (int o = 8; o < 32; o <<= 1) {
+                        cs.x += __shfl_xor_sync(0xffffffffu, cs.x, o);
+                        cs.y += __shfl_xor_sync(0xffffffffu, cs.y, o);
+                        cs.z += __shfl_xor_sync(0xffffffffu, cs.z, o);
+                        cs.w += __shfl_xor_sync(0xffffffffu, cs.w, o);
+                    }
+                    if (rl == 0 && n < p.N && m0 + 32 * q < p.M) {
+                        float *dst = p.fo.colpart + (int64_t)((m0 + 32 * q) >> 5) * p.N + n;
+                        if (n + 3 < p.N) *(float4 *)dst = cs;
+                        else {
+                            const float v[4] = {cs.x, cs.y, cs.z, cs.w};
+                            for (int e = 0; e < 4 && n + e < p.N; e++) dst[e] = v[e];
+                        }
                     }
                 }
                 __syncwarp();
             }
+        }
+        if (F16 && p.fo.h && !p.cluster) {  // amax of the planes written (the next consumer's bound)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+            if (lane == 0) amax_atomic(&p.fo.ts->amax, amx);
         }
     }
 #undef MTX_UNITS
@@ -648,7 +772,16 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
         // [z*BM/S, (z+1)*BM/S) over the splits in ascending order (deterministic) and stores them
         // with the fused epilogue; the second barrier keeps every CTA's smem alive until read
         cluster_sync_all();
-        if (warp >= 4 && warp < 12) cluster_fold<BN, MASK, PAIR>(p, smem_u32(smem));
+        if (warp >= 4 && warp < 12) {
+            float inv_so = 1.f, amx = 0.f;
+            if (F16 && p.fo.h) inv_so = 1.f / f16out_scale(p.fo);
+            cluster_fold<BN, MASK, PAIR, F16>(p, smem_u32(smem), inv_so, amx);
+            if (F16 && p.fo.h) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+                if (lane == 0) amax_atomic(&p.fo.ts->amax, amx);
+            }
+        }
         cluster_sync_all();
     }
     tc_fence_before();
@@ -673,15 +806,18 @@ typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, 
 // Row-major fp32 matrix [rows][cols] (row pitch ld elements), box = 32 cols x box_rows.
 // K-major operands use the 128-B swizzle (16-B atoms), MN-major ones the 128-B swizzle with
 // 32-B atoms, matching the UMMA descriptors above.
-bool make_map(EncodeTiled enc, CUtensorMap *m, const float *ptr, int64_t rows, int64_t cols, int64_t ld,
-              int box_rows, bool mn_major) {
+// f16: fp16 planes, box = 64 cols (128 B) x box_rows, the plain 128-B swizzle for both majors.
+bool make_map(EncodeTiled enc, CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
+              int box_rows, bool mn_major, bool f16 = false) {
+    const int esz = f16 ? 2 : 4;
+    if ((ld * esz) % 16) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-    cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * esz};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)ptr, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+    CUresult r = enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)ptr, dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     (mn_major && !f16) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -690,14 +826,18 @@ bool make_map(EncodeTiled enc, CUtensorMap *m, const float *ptr, int64_t rows, i
 // MN-major operand [rows][cols] (row pitch ld) as a 3-D map: dim0 = 32 elements of a 128-B chunk, dim1 = rows
 // (the K index), dim2 = cols / 32 chunks (stride 128 B); box {32, BK, chunks}.  Needs cols % 32 == 0: chunks never
 // run past a row (the 2-D map's zero fill is what covers a ragged cols).
-bool make_map_mn3d(EncodeTiled enc, CUtensorMap *m, const float *ptr, int64_t rows, int64_t cols, int64_t ld, int chunks) {
-    if (cols % 32 || ld % 4) return false;
-    cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)(cols / 32)};
-    cuuint64_t strides[2] = {(cuuint64_t)ld * 4, 128};
-    cuuint32_t box[3] = {32, (cuuint32_t)BK, (cuuint32_t)chunks};
+// f16: chunks of 64 fp16 elements (128 B), box {64, BKH, chunks}, the plain 128-B swizzle.
+bool make_map_mn3d(EncodeTiled enc, CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, int64_t ld, int chunks,
+                   bool f16 = false) {
+    const int esz = f16 ? 2 : 4, ce = 128 / esz;
+    if (cols % ce || (ld * esz) % 16) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)ce, (cuuint64_t)rows, (cuuint64_t)(cols / ce)};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * esz, 128};
+    cuuint32_t box[3] = {(cuuint32_t)ce, (cuuint32_t)(f16 ? BKH : BK), (cuuint32_t)chunks};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)ptr, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+    CUresult r = enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)ptr, dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     f16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -707,12 +847,12 @@ bool make_map_mn3d(EncodeTiled enc, CUtensorMap *m, const float *ptr, int64_t ro
 struct TcGemm {
     EncodeTiled encode = nullptr;
     int sms = 148;
-    bool attr_set[32] = {};
+    bool attr_set[64] = {};
     // split-K folded through distributed shared memory (MTX_TC_CLUSTER=0 disables: global partials
     // + splitk_reduce launch)
     bool cluster = true;
-    int max_clusters[2][3][9] = {};  // [SPLIT][BN 128/64/32][cluster size]: co-resident clusters (0 = unknown)
-    int max_pair_clusters[2][9] = {};  // [SPLIT][cluster size] for the 128-wide pair variant
+    int max_clusters[3][3][9] = {};  // [1x / 3xTF32 / 3xF16][BN 128/64/32][cluster size]: co-resident clusters (0 = unknown)
+    int max_pair_clusters[3][9] = {};  // [1x / 3xTF32 / 3xF16][cluster size] for the 128-wide pair variant
     // CTA-pair (cta_group::2) 256 x 128 tiles for large GEMMs (MTX_TC_PAIR=0 disables)
     bool pair = true;
 };
@@ -724,17 +864,18 @@ bool tc_available() { return true; }
 // N tile (128, 64, 32) whose tiles x K-splits reach 3/4 of the SMs with >= 4 k-blocks per split
 // (wide tiles keep the operand re-reads from L2 low; splits fill the SMs, their fold is one light
 // launch).  Store-bound single-k-block GEMMs use 64-wide tiles.
-TcPlan tc_plan(int sms, int M, int N, int K) {
+TcPlan tc_plan(int sms, int M, int N, int K, bool f16) {
     TcPlan pl;
     const int tm = (M + BM - 1) / BM;
-    const int kb = (K + BK - 1) / BK;
-    const int max_split = std::max(1, kb / 4);
+    const int kb = (K + (f16 ? BKH : BK) - 1) / (f16 ? BKH : BK);
+    const int max_split = std::max(1, kb / (f16 ? 2 : 4));  // >= 128 elements of K per split
     pl.bn = 128;
     pl.splits = 1;
     if (tm * ((N + 127) / 128) * 2 >= sms) {
         if (kb <= 2 && N >= 64) pl.bn = 64;
     } else {
         for (int bn : {128, 64, 32}) {
+            if (f16 && bn == 32) break;  // an MN-major fp16 operand tile is whole 64-element chunks
             const int tiles = tm * ((N + bn - 1) / bn);
             const int s = std::max(1, std::min(max_split, sms / tiles));
             pl.bn = bn;
@@ -747,13 +888,15 @@ TcPlan tc_plan(int sms, int M, int N, int K) {
     // development overrides for plan sweeps (tools/gemm_plan_sweep.py), read on every call
     if (const char *e = getenv("MTX_TC_BN")) {
         const int v = atoi(e);
-        if (v == 32 || v == 64 || v == 128) pl.bn = v;
+        if ((v == 32 && !f16) || v == 64 || v == 128) pl.bn = v;
     }
     if (const char *e = getenv("MTX_TC_SPLITS")) pl.splits = std::max(1, std::min(atoi(e), kb));
     return pl;
 }
 
-int tc_choose_splits(int sms, int M, int N, int K) { return tc_plan(sms, M, N, K).splits; }
+int tc_choose_splits(int sms, int M, int N, int K) {
+    return std::max(tc_plan(sms, M, N, K, false).splits, tc_plan(sms, M, N, K, true).splits);
+}
 
 TcGemm *tc_create(int device) {
     TcGemm *t = new TcGemm();
@@ -788,18 +931,26 @@ bool tc_supports(TcGemm *t, const GemmDesc &g) {
     if (g.lda % 4 || g.ldb % 4 || g.ldc % 4 || !al16(g.A) || !al16(g.B) || !al16(g.C)) return false;
     if (g.epi == EPI_MASK && (g.ldm % 4 || !al16(g.mask))) return false;
     // dataset operand with the sample dimension along K: its k-blocks must not run into the next rank's rows
-    if (g.ta && g.arow.win && g.K % BK) return false;
+    if (g.ta && g.arow.win && g.K % (g.f16x3 ? BKH : BK)) return false;
     if (g.tf32x3 && !(g.A_hi && g.A_lo && g.B_hi && g.B_lo)) return false;  // 3xTF32 consumes producer planes
+    if (g.f16x3) {  // 3xF16: producer planes with 16-B row pitches and their scale slots
+        if (!(g.A_h && g.A_l && g.B_h && g.B_l && g.tsA && g.tsB)) return false;
+        if (g.lda_p % 8 || g.ldb_p % 8 || !al16(g.A_h) || !al16(g.A_l) || !al16(g.B_h) || !al16(g.B_l)) return false;
+        if (g.C_h && (g.ldc_p % 4 || !g.tsC || ((uintptr_t)g.C_h & 7) || ((uintptr_t)g.C_l & 7))) return false;
+        if (g.N < 64 && !g.tb) return false;  // an MN-major B tile is whole 64-element chunks
+    }
     if (g.arow.win && g.a_rows_total <= 0) return false;
     return true;
 }
 
-template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false>
+// variant: 0 = 1xTF32, 1 = 3xTF32, 2 = 3xF16
+template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false>
 static cudaError_t prepare(TcGemm *t) {
-    using L = SmemLayout<BN, SPLIT, PAIR>;
-    const int slot = (SPLIT ? 1 : 0) + 2 * (BN == 128 ? 0 : BN == 64 ? 1 : 2) + (PAIR ? 8 : 0) + (MASK ? 16 : 0);
+    using L = SmemLayout<BN, SPLIT, PAIR, F16>;
+    const int slot = (SPLIT ? 1 : 0) + 2 * (BN == 128 ? 0 : BN == 64 ? 1 : 2) + (PAIR ? 8 : 0) + (MASK ? 16 : 0) +
+                     (F16 ? 32 : 0);
     if (!t->attr_set[slot]) {
-        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT, PAIR, MASK>,
+        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
         if (e != cudaSuccess) return e;
         t->attr_set[slot] = true;
@@ -808,12 +959,12 @@ static cudaError_t prepare(TcGemm *t) {
 }
 
 // How many clusters of `cs` CTAs of this variant can be resident at once (cached).
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, bool F16>
 static int co_resident_clusters(TcGemm *t, int cs) {
-    using L = SmemLayout<BN, SPLIT>;
-    int &slot = t->max_clusters[SPLIT ? 1 : 0][BN == 128 ? 0 : BN == 64 ? 1 : 2][cs];
+    using L = SmemLayout<BN, SPLIT, false, F16>;
+    int &slot = t->max_clusters[F16 ? 2 : SPLIT ? 1 : 0][BN == 128 ? 0 : BN == 64 ? 1 : 2][cs];
     if (slot) return slot;
-    if (prepare<BN, SPLIT>(t) != cudaSuccess) return 0;
+    if (prepare<BN, SPLIT, false, false, F16>(t) != cudaSuccess) return 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs * 148);
     cfg.blockDim = dim3(L::THREADS);
@@ -826,7 +977,7 @@ static int co_resident_clusters(TcGemm *t, int cs) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, (void *)tc_gemm_kernel<BN, SPLIT, false, false>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, (void *)tc_gemm_kernel<BN, SPLIT, false, false, F16>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         n = -1;  // query failed: never use the cluster path for this variant
     }
@@ -834,13 +985,13 @@ static int co_resident_clusters(TcGemm *t, int cs) {
     return n;
 }
 
-template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false>
+template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false>
 static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s) {
-    using L = SmemLayout<BN, SPLIT, PAIR>;
-    cudaError_t e = prepare<BN, SPLIT, PAIR, MASK>(t);
+    using L = SmemLayout<BN, SPLIT, PAIR, F16>;
+    cudaError_t e = prepare<BN, SPLIT, PAIR, MASK, F16>(t);
     if (e != cudaSuccess) return e;
     if (!p.cluster && !PAIR)
-        return launch_pdl(tc_gemm_kernel<BN, SPLIT, PAIR, MASK>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
+        return launch_pdl(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(L::THREADS);
@@ -855,16 +1006,16 @@ static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s
     at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT, PAIR, MASK>, p);
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16>, p);
 }
 
 // How many clusters of `cs` CTAs (cs / 2 CTA pairs) of the 128-wide pair variant can be resident at once.
-template <bool SPLIT>
+template <bool SPLIT, bool F16>
 static int co_resident_pair(TcGemm *t, int cs) {
-    using L = SmemLayout<128, SPLIT, true>;
-    int &slot = t->max_pair_clusters[SPLIT ? 1 : 0][cs];
+    using L = SmemLayout<128, SPLIT, true, F16>;
+    int &slot = t->max_pair_clusters[F16 ? 2 : SPLIT ? 1 : 0][cs];
     if (slot) return slot;
-    if (prepare<128, SPLIT, true>(t) != cudaSuccess) return 0;
+    if (prepare<128, SPLIT, true, false, F16>(t) != cudaSuccess) return 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs * 74);
     cfg.blockDim = dim3(L::THREADS);
@@ -877,7 +1028,7 @@ static int co_resident_pair(TcGemm *t, int cs) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, (void *)tc_gemm_kernel<128, SPLIT, true, false>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, (void *)tc_gemm_kernel<128, SPLIT, true, false, F16>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         n = -1;
     }
@@ -886,15 +1037,45 @@ static int co_resident_pair(TcGemm *t, int cs) {
 }
 
 template <int BN>
-static int co_resident(TcGemm *t, bool split, int cs) {
-    return split ? co_resident_clusters<BN, true>(t, cs) : co_resident_clusters<BN, false>(t, cs);
+static int co_resident(TcGemm *t, int variant, int cs) {
+    return variant == 2 ? co_resident_clusters<BN, true, true>(t, cs)
+         : variant == 1 ? co_resident_clusters<BN, true, false>(t, cs)
+                        : co_resident_clusters<BN, false, false>(t, cs);
+}
+static int co_resident_pair_v(TcGemm *t, int variant, int cs) {
+    return variant == 2 ? co_resident_pair<true, true>(t, cs)
+         : variant == 1 ? co_resident_pair<true, false>(t, cs)
+                        : co_resident_pair<false, false>(t, cs);
 }
 
-cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h) {
+// One instantiation per (variant, BN, PAIR, MASK) the planner can pick.
+template <bool SPLIT, bool F16>
+static cudaError_t launch_variant(TcGemm *t, const TcParams &p, int grid, cudaStream_t s, int BN, bool pair, bool mask) {
+    if (pair && mask) return launch<128, SPLIT, true, true, F16>(t, p, grid, s);
+    if (pair) return launch<128, SPLIT, true, false, F16>(t, p, grid, s);
+    if (mask) {
+        if (BN == 128) return launch<128, SPLIT, false, true, F16>(t, p, grid, s);
+        if (BN == 64) return launch<64, SPLIT, false, true, F16>(t, p, grid, s);
+        if constexpr (!F16) return launch<32, SPLIT, false, true, F16>(t, p, grid, s);
+        return cudaErrorInvalidValue;
+    }
+    if (BN == 128) return launch<128, SPLIT, false, false, F16>(t, p, grid, s);
+    if (BN == 64) return launch<64, SPLIT, false, false, F16>(t, p, grid, s);
+    if constexpr (!F16) return launch<32, SPLIT, false, false, F16>(t, p, grid, s);
+    return cudaErrorInvalidValue;
+}
+
+// launch == false: only the plan -- *splits_out = the K-splits the launch would use (1: the direct epilogue,
+// which alone writes the 3xF16 lean outputs)
+static cudaError_t tc_gemm_impl(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h, bool launch,
+                                int *splits_out) {
     const int M = g.aug ? g.M - 1 : g.M;  // the bias row of an augmented wgrad is a column sum (below)
     const int N = g.N, K = g.K;
     const int sms = g.sm_budget > 0 ? std::min(g.sm_budget, t->sms) : t->sms;
-    const TcPlan plan = tc_plan(sms, M, N, K);
+    const bool f16 = g.f16x3 != 0;
+    const int variant = f16 ? 2 : g.tf32x3 ? 1 : 0;
+    const int KBE = f16 ? BKH : BK;  // elements per k-block
+    const TcPlan plan = tc_plan(sms, M, N, K, f16);
     const int BN = plan.bn;
     // CTA pairs for large unsplit GEMMs: a 256 x 128 tile per pair halves B's per-SM operand traffic.
     // Pair MMAs also cost ~65 cycles with fresh operand tiles where a 1-CTA MMA of any N <= 128 costs ~89
@@ -909,16 +1090,16 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     bool pair_cluster = false;
     if (pair && !(plan.splits == 1 && ptiles * 2 >= sms / 2)) {
         pair = false;
-        const int kb = (K + BK - 1) / BK;
+        const int kb = (K + KBE - 1) / KBE;
         // default: the long weight gradients (K >= 8192: 87.1 -> 84.9 us at 1024 x 1024 x 8192; no gain at
         // K <= 4096, tools/gemm3x_bench.py); MTX_TC_PAIR_SPLIT=0/1 forces it off/on
-        const bool pair_split = pair_split_env >= 0 ? pair_split_env != 0 : kb >= 256;
+        const bool pair_split = pair_split_env >= 0 ? pair_split_env != 0 : kb * KBE >= 8192;
         if (pair_split && g.epi == EPI_STORE && M >= 2 * BM) {
             // a weight gradient too small to fill the pairs: split K over S pairs of one cluster (2S CTAs),
             // folded through distributed shared memory like the 1-CTA cluster plan
-            const int sp = (int)std::min<int64_t>(std::min(4, std::max(1, kb / 8)), std::max<int64_t>(1, (sms / 2) / ptiles));
+            const int sp = (int)std::min<int64_t>(std::min(4, std::max(1, kb * KBE / 256)), std::max<int64_t>(1, (sms / 2) / ptiles));
             if (sp > 1 && ptiles * sp * 8 >= (int64_t)(sms / 2) * 6) {
-                const int nc = g.tf32x3 ? co_resident_pair<true>(t, 2 * sp) : co_resident_pair<false>(t, 2 * sp);
+                const int nc = co_resident_pair_v(t, variant, 2 * sp);
                 if (t->cluster && nc >= ptiles) {
                     pair = true;
                     pair_splits = sp;
@@ -940,28 +1121,53 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     bool ok;
     // MN-major operands with whole 32-element chunks take the 3-D map (one TMA operation per operand tile)
     static const bool mn3d = !getenv("MTX_TC_MN3D") || atoi(getenv("MTX_TC_MN3D"));
-    p.a_3d = (mn3d && g.ta && M % 32 == 0 && g.lda % 4 == 0) ? 1 : 0;
-    p.b_3d = (mn3d && !g.tb && N % 32 == 0 && g.ldb % 4 == 0 && BN % 32 == 0) ? 1 : 0;
-    auto map_a = [&](CUtensorMap *m, const float *ptr) {
-        if (p.a_3d) return make_map_mn3d(t->encode, m, ptr, g.arow.win ? a_rows_total : K, M, g.lda, BM / 32);
-        return !g.ta ? make_map(t->encode, m, ptr, g.arow.win ? a_rows_total : M, K, g.lda, BM, false)
-                     : make_map(t->encode, m, ptr, g.arow.win ? a_rows_total : K, M, g.lda, BK, true);
+    // operand row pitches (3xF16: the planes' own pitch) and elements per MN-major chunk
+    const int64_t lda = f16 ? g.lda_p : g.lda, ldb = f16 ? g.ldb_p : g.ldb;
+    const int CHE = f16 ? 64 : 32;
+    p.a_3d = (mn3d && g.ta && M % CHE == 0 && lda % 4 == 0) ? 1 : 0;
+    p.b_3d = (mn3d && !g.tb && N % CHE == 0 && ldb % 4 == 0 && BN % CHE == 0 && (!pair || (BN / 2) % CHE == 0)) ? 1 : 0;
+    auto map_a = [&](CUtensorMap *m, const void *ptr) {
+        if (p.a_3d) return make_map_mn3d(t->encode, m, ptr, g.arow.win ? a_rows_total : K, M, lda, BM / CHE, f16);
+        return !g.ta ? make_map(t->encode, m, ptr, g.arow.win ? a_rows_total : M, K, lda, BM, false, f16)
+                     : make_map(t->encode, m, ptr, g.arow.win ? a_rows_total : K, M, lda, KBE, true, f16);
     };
-    auto map_b = [&](CUtensorMap *m, const float *ptr) {
-        if (p.b_3d) return make_map_mn3d(t->encode, m, ptr, K, N, g.ldb, (pair ? BN / 2 : BN) / 32);
-        return g.tb ? make_map(t->encode, m, ptr, N, K, g.ldb, pair ? BN / 2 : BN, false)   // [N][K], K-major
-                    : make_map(t->encode, m, ptr, K, N, g.ldb, BK, true);   // [K][N], MN-major
+    auto map_b = [&](CUtensorMap *m, const void *ptr) {
+        if (p.b_3d) return make_map_mn3d(t->encode, m, ptr, K, N, ldb, (pair ? BN / 2 : BN) / CHE, f16);
+        return g.tb ? make_map(t->encode, m, ptr, N, K, ldb, pair ? BN / 2 : BN, false, f16)   // [N][K], K-major
+                    : make_map(t->encode, m, ptr, K, N, ldb, KBE, true, f16);   // [K][N], MN-major
     };
-    if (g.tf32x3) ok = map_a(&p.ta, g.A_hi) && map_a(&p.ta_lo, g.A_lo) && map_b(&p.tb, g.B_hi) && map_b(&p.tb_lo, g.B_lo);
+    if (f16) ok = map_a(&p.ta, g.A_h) && map_a(&p.ta_lo, g.A_l) && map_b(&p.tb, g.B_h) && map_b(&p.tb_lo, g.B_l);
+    else if (g.tf32x3) ok = map_a(&p.ta, g.A_hi) && map_a(&p.ta_lo, g.A_lo) && map_b(&p.tb, g.B_hi) && map_b(&p.tb_lo, g.B_lo);
     else ok = map_a(&p.ta, g.A) && map_b(&p.tb, g.B);
     if (!ok) return cudaErrorInvalidValue;
     p.C_hi = g.C_hi;
     p.C_lo = g.C_lo;
+    if (f16) {
+        p.tsA = g.tsA;
+        p.tsB = g.tsB;
+        if (g.C_h) {
+            p.fo.h = g.C_h;
+            p.fo.l = g.C_l;
+            p.fo.ld = g.ldc_p;
+            p.fo.ts = g.tsC;
+            p.fo.a = g.tsA;
+            p.fo.b = g.tsB;
+            p.fo.k = g.bnd_k;
+            p.fo.bias = g.bnd_bias;
+        }
+        // lean outputs (direct epilogue only; the caller checks tc_direct first)
+        p.fo.skip_f32 = g.skip_c32;
+        p.fo.bits = g.relu_bits;
+        p.fo.bits_ld = g.relu_bits_ld;
+        p.fo.colpart = g.colpart;
+        p.mbits = g.mask_bits;
+        p.mbits_ld = g.mask_bits_ld;
+    }
     p.a_win = g.arow.win;
     p.a_base = g.arow.base;
     p.tiles_m = pair ? (M + 2 * BM - 1) / (2 * BM) : (M + BM - 1) / BM;
     p.tiles_n = (N + BN - 1) / BN;
-    p.kb_total = (K + BK - 1) / BK;
+    p.kb_total = (K + KBE - 1) / KBE;
     const int tiles = p.tiles_m * p.tiles_n;
     int splits = pair ? pair_splits : plan.splits;
     // split-K fold through DSMEM when the tile's splits fit one cluster and all clusters are co-resident
@@ -969,9 +1175,9 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     if (splits > 1 && splits <= 8 && t->cluster && !pair) {
         const int per = (p.kb_total + splits - 1) / splits;
         const int sp = (p.kb_total + per - 1) / per;
-        const int nc = BN == 128 ? co_resident<128>(t, g.tf32x3, sp)
-                     : BN == 64  ? co_resident<64>(t, g.tf32x3, sp)
-                                 : co_resident<32>(t, g.tf32x3, sp);
+        const int nc = BN == 128 ? co_resident<128>(t, variant, sp)
+                     : BN == 64  ? co_resident<64>(t, variant, sp)
+                                 : co_resident<32>(t, variant, sp);
         if (sp > 1 && nc >= tiles) {
             cluster = true;
             splits = sp;
@@ -986,6 +1192,8 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     if (splits == 1) cluster = false;
     p.splits = splits;
     p.cluster = cluster ? 1 : 0;
+    if (splits_out) *splits_out = splits;
+    if (!launch) return cudaSuccess;
     if (const char *k = getenv("MTX_TC_DBG")) p.dbg = atoi(k);  // development timing knob
     p.epi = g.epi;
     p.bias = g.bias;
@@ -998,29 +1206,34 @@ cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h)
     const int grid = cluster ? (pair ? 2 * total : total) : pair ? 2 * std::min(total, sms / 2) : std::min(total, sms);
     const char *kind = g.epi == EPI_MASK ? "dgrad" : (g.ta ? "wgrad" : "fwd");
     char name[96];
-    snprintf(name, sizeof name, "gemm_tc%s_%s[M=%d,N=%d,K=%d,splits=%d,cluster=%d,pair=%d,bn=%d]", g.tf32x3 ? "3x" : "",
+    snprintf(name, sizeof name, "gemm_tc%s_%s[M=%d,N=%d,K=%d,splits=%d,cluster=%d,pair=%d,bn=%d]",
+             f16 ? "3xf16" : g.tf32x3 ? "3x" : "",
              kind, M, N, K, splits, cluster ? 1 : 0, pair ? 1 : 0, BN);
     if (h) h->before(name, s);
     cudaError_t e;
-    const bool mask = g.epi == EPI_MASK;  // dgrad: the masked-epilogue instantiation (never paired)
-    if (pair && mask) e = g.tf32x3 ? launch<128, true, true, true>(t, p, grid, s) : launch<128, false, true, true>(t, p, grid, s);
-    else if (pair) e = g.tf32x3 ? launch<128, true, true>(t, p, grid, s) : launch<128, false, true>(t, p, grid, s);
-    else if (mask) {
-        if (BN == 128) e = g.tf32x3 ? launch<128, true, false, true>(t, p, grid, s) : launch<128, false, false, true>(t, p, grid, s);
-        else if (BN == 64) e = g.tf32x3 ? launch<64, true, false, true>(t, p, grid, s) : launch<64, false, false, true>(t, p, grid, s);
-        else e = g.tf32x3 ? launch<32, true, false, true>(t, p, grid, s) : launch<32, false, false, true>(t, p, grid, s);
-    } else if (BN == 128) e = g.tf32x3 ? launch<128, true>(t, p, grid, s) : launch<128, false>(t, p, grid, s);
-    else if (BN == 64) e = g.tf32x3 ? launch<64, true>(t, p, grid, s) : launch<64, false>(t, p, grid, s);
-    else e = g.tf32x3 ? launch<32, true>(t, p, grid, s) : launch<32, false>(t, p, grid, s);
+    const bool mask = g.epi == EPI_MASK;  // dgrad: the masked-epilogue instantiation
+    e = variant == 2 ? launch_variant<true, true>(t, p, grid, s, BN, pair, mask)
+      : variant == 1 ? launch_variant<true, false>(t, p, grid, s, BN, pair, mask)
+                     : launch_variant<false, false>(t, p, grid, s, BN, pair, mask);
     if (h) h->after(name, s);
     if (e != cudaSuccess) return e;
     if (splits > 1 && !cluster) {  // fold with the epilogue in a separate kernel
-        e = splitk_reduce(g.partial, splits, M, N, g.C, g.ldc, s, h, g.epi, g.bias, g.mask, g.ldm, g.C_hi, g.C_lo);
+        e = splitk_reduce(g.partial, splits, M, N, g.C, g.ldc, s, h, g.epi, g.bias, g.mask, g.ldm, g.C_hi, g.C_lo, p.fo,
+                          g.mask_bits, g.mask_bits_ld);
         if (e != cudaSuccess) return e;
     }
     if (g.aug && !g.colsum_external)  // bias gradient row: db[n] = sum_k B[k][n]  (the ones row of augmented A)
         e = colsum(g.B, K, N, g.ldb, g.C + (int64_t)M * g.ldc, g.partial, g.partial_cap, g.counters + 256, s, h);
     return e;
+}
+
+cudaError_t tc_gemm(TcGemm *t, const GemmDesc &g, cudaStream_t s, LaunchHook *h) {
+    return tc_gemm_impl(t, g, s, h, true, nullptr);
+}
+
+bool tc_direct(TcGemm *t, const GemmDesc &g) {
+    int splits = 0;
+    return tc_gemm_impl(t, g, nullptr, nullptr, false, &splits) == cudaSuccess && splits == 1;
 }
 
 }  // namespace mtx

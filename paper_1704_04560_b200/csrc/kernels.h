@@ -42,6 +42,28 @@ struct GemmDesc {
     const float *A_hi = nullptr, *A_lo = nullptr, *B_hi = nullptr, *B_lo = nullptr;
     float *C_hi = nullptr, *C_lo = nullptr;
     unsigned *counters = nullptr;  // tensor-core split-K fixup: >= 256 per-tile counters, zeroed
+    // 3xF16 (f16x3): fp16 operand planes (row pitch *_pld elements, a multiple of 8), their per-tensor
+    // scale slots, and optionally the output's planes + slot; the output's scale is set from the bound
+    // bnd_k * amax(A) * amax(B) (+ amax(B) when bnd_bias: the bias lives in the same parameter buffer)
+    int f16x3 = 0;
+    const __half *A_h = nullptr, *A_l = nullptr, *B_h = nullptr, *B_l = nullptr;
+    int64_t lda_p = 0, ldb_p = 0;
+    const TScale *tsA = nullptr, *tsB = nullptr;
+    __half *C_h = nullptr, *C_l = nullptr;
+    int64_t ldc_p = 0;
+    TScale *tsC = nullptr;
+    float bnd_k = 0.f;
+    int bnd_bias = 0;
+    // 3xF16 lean outputs (direct epilogue only, tc_direct): skip the fp32 C; the forward's ReLU bitmask
+    // [M][relu_bits_ld words] (bit n % 32 of word n / 32 = [C > 0]); the dgrad's per-32-row column sums
+    // colpart[ceil(M/32)][N] (the bias gradient of the layer whose dZ this is, folded later).  Input side:
+    // mask_bits replaces the fp32 mask of a dgrad.
+    int skip_c32 = 0;
+    uint32_t *relu_bits = nullptr;
+    int64_t relu_bits_ld = 0;
+    float *colpart = nullptr;
+    const uint32_t *mask_bits = nullptr;
+    int64_t mask_bits_ld = 0;
 };
 
 // Launch-site hook: the API layer brackets every launch with it (timing/counting).
@@ -61,22 +83,65 @@ constexpr int COLSUM_MAX_GROUPS = 64;  // N <= 8192
 cudaError_t colsum(const float *X, int K, int N, int64_t ld, float *out, float *partial, int64_t partial_cap,
                    unsigned *ticket, cudaStream_t s, LaunchHook *h);
 
+// 3xF16 output planes of a producer kernel: scale from the bound k * amax(a) * amax(b) (+ amax(b) with a
+// bias), amax of the written values accumulated into ts->amax.
+struct F16Out {
+    __half *h = nullptr, *l = nullptr;
+    int64_t ld = 0;
+    TScale *ts = nullptr;
+    const TScale *a = nullptr, *b = nullptr;
+    float k = 0.f;
+    int bias = 0;
+    // lean outputs (GemmDesc: skip_c32 / relu_bits / colpart); the head: colpart per CTA, skip_f32
+    int skip_f32 = 0;
+    uint32_t *bits = nullptr;
+    int64_t bits_ld = 0;
+    float *colpart = nullptr;
+};
+MTX_DEVI float f16out_scale(const F16Out &o) {
+    const float bb = o.b ? o.b->amax : 1.f;
+    return f16_scale_for(o.k * o.a->amax * bb + (o.bias ? bb : 0.f));
+}
+
 // C[m][n] = epi(sum_{z ascending} partial[z][m][n])  (deterministic split-K fold + GEMM epilogue)
 cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float *C, int64_t ldc, cudaStream_t s,
                           LaunchHook *h, int epi = EPI_STORE, const float *bias = nullptr,
                           const float *mask = nullptr, int64_t ldm = 0, float *C_hi = nullptr,
-                          float *C_lo = nullptr);
+                          float *C_lo = nullptr, F16Out fo = F16Out(), const uint32_t *mbits = nullptr,
+                          int64_t mbits_ld = 0);
 
 // hi/lo 3xTF32 planes of x[n] (n % 4 == 0, 16-B aligned; rows of x need not be contiguous: a
 // [rows][cols] block with leading dimension ld)
 cudaError_t split_planes(const float *x, int64_t rows, int64_t cols, int64_t ld, float *hi, float *lo, cudaStream_t s,
                          LaunchHook *h);
 
+// 3xF16 planes of one tensor (common.cuh TScale): a [rows][cols] fp32 block (pitch ld) -> fp16 hi/lo
+// planes (pitch pld, a multiple of 8; columns cols..pld-1 are left as they are).
+struct QSeg {
+    const float *x;
+    int64_t rows, cols, ld;
+    __half *hi, *lo;
+    int64_t pld;
+};
+constexpr int QSEG_MAX = 8;
+constexpr int QUANT_SCRATCH_FLOATS = 1024 + 4;  // per-CTA maxima + the grid barrier words
+// One grid-synchronous launch: amax = max |x| over [amax_x, amax_x + amax_n) (every element of the
+// tensor's storage, e.g. the whole flat parameter buffer incl. biases) or, if amax_x is null, over the
+// segments; s = f16_scale_for(amax); ts->amax / ts->scale written; then the planes of every segment.
+// zero_ts[0..n_zero): per-step slots whose amax is reset (their producers accumulate it next step).
+// scratch: QUANT_SCRATCH_FLOATS floats, zero on first use, private to one stream.
+cudaError_t quantize_f16(const QSeg *segs, int nseg, const float *amax_x, int64_t amax_n, TScale *ts, TScale *zero_ts,
+                         int n_zero, float *scratch, cudaStream_t s, LaunchHook *h);
+
 // Narrow weight gradient (N <= 16, e.g. the classifier layer): dWb[k][j] = sum_i A[i][k] dZ[i][j]
 // for k < K_in, plus (aug) the bias row dWb[K_in][j] = sum_i dZ[i][j].  Thread per k, rows split
 // over blocks, blocked fp32 sums, ascending fold.  A's row offset: arow (dataset operand).
 // out[j] = sum_{p ascending per lane, fixed shuffle tree} partial[p][j], j < n: deterministic fold of
 // per-block partials (one warp per output).
+// out[j] = sum_p partial[p][j] for j < n (partial pitch n): 32 columns x 8 part-slices per CTA, each slice
+// summed in ascending p, the slices in a fixed tree (deterministic); coalesced over j.  The bias gradient
+// from the 3xF16 lean column partials.
+cudaError_t colpart_fold(const float *partial, int parts, int n, float *out, cudaStream_t s, LaunchHook *h);
 cudaError_t fold_partials(const float *partial, int parts, int n, float *out, cudaStream_t s, LaunchHook *h);
 cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *dZ, int rows, int K_in, int N,
                          float *dWb, float *partial, int64_t partial_cap, unsigned *ticket, cudaStream_t s,
@@ -88,10 +153,13 @@ cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *
 // (per-block partials folded in block order by the last block; ticket must be 0
 // on entry and is re-armed on exit; loss_part holds >= 1024 floats).  dp_hi/dp_lo
 // (nullable): 3xTF32 planes of dprev for the consuming tensor-core GEMMs.
+// fo (3xF16): fp16 planes of dprev, scale from the bound |dprev| <= 2 inv_b max|W_L| (fo.k = 2 inv_b, fo.a =
+// the parameters' slot, fo.b = null): sum_j |softmax_j - onehot_j| <= 2.  fo.colpart: per-CTA column sums
+// of dprev [*colpart_rows][d] (the bias gradient of layer L-1); fo.skip_f32: dprev's fp32 copy not written.
 cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, const float *Wb, const int32_t *labels,
                        RowSel lrow, float inv_b, float *dZL, float *dprev, float *dp_hi, float *dp_lo,
                        float *loss_rows, float *loss_part, unsigned *ticket, float *loss_out, cudaStream_t s,
-                       LaunchHook *h);
+                       LaunchHook *h, F16Out fo = F16Out(), int *colpart_rows = nullptr);
 
 // out = sum_{i ascending in a fixed tree} v[i] (one block; deterministic).
 cudaError_t reduce_sum(const float *v, int n, float *out, cudaStream_t s, LaunchHook *h);

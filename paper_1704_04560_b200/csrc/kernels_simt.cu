@@ -140,8 +140,11 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(GemmDesc g) {
 // bias (+ReLU) for forward GEMMs, the ReLU mask for dgrad, plain store otherwise.
 __global__ void splitk_reduce_kernel(const float *__restrict__ partial, int splits, int M, int N, float *C,
                                      int64_t ldc, int epi, const float *__restrict__ bias,
-                                     const float *__restrict__ mask, int64_t ldm, float *C_hi, float *C_lo) {
+                                     const float *__restrict__ mask, int64_t ldm, float *C_hi, float *C_lo, F16Out fo,
+                                     const uint32_t *__restrict__ mbits, int64_t mbits_ld) {
     pdl_wait();
+    const float inv_so = fo.h ? 1.f / f16out_scale(fo) : 1.f;
+    float amx = 0.f;
     const int64_t total = (int64_t)M * N;
     // 4 consecutive elements per thread (float4 when the row holds them), splits loaded 8 at a time
     const int64_t n4 = (total + 3) / 4;
@@ -178,10 +181,22 @@ __global__ void splitk_reduce_kernel(const float *__restrict__ partial, int spli
             float r = s[c];
             if (epi == EPI_BIAS_RELU) r = fmaxf(r + bias[n], 0.f);
             else if (epi == EPI_BIAS) r = r + bias[n];
+            else if (epi == EPI_MASK && mbits) r = ((mbits[m * mbits_ld + (n >> 5)] >> (n & 31)) & 1u) ? r : 0.f;
             else if (epi == EPI_MASK) r = mask[m * ldm + n] > 0.f ? r : 0.f;
-            C[m * ldc + n] = r;
+            if (C) C[m * ldc + n] = r;
             if (C_hi) split_tf32(r, C_hi[m * ldc + n], C_lo[m * ldc + n]);
+            if (fo.h) {
+                uint16_t hh, ll;
+                split_f16(r, inv_so, hh, ll);
+                fo.h[m * fo.ld + n] = __ushort_as_half(hh);
+                fo.l[m * fo.ld + n] = __ushort_as_half(ll);
+                amx = fmaxf(amx, fabsf(r));
+            }
         }
+    }
+    if (fo.h) {
+        for (int o = 16; o > 0; o >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+        if ((threadIdx.x & 31) == 0) amax_atomic(&fo.ts->amax, amx);
     }
 }
 
@@ -217,14 +232,14 @@ cudaError_t gemm_simt(const GemmDesc &g, cudaStream_t s, LaunchHook *h) {
 
 cudaError_t splitk_reduce(const float *partial, int splits, int M, int N, float *C, int64_t ldc, cudaStream_t s,
                           LaunchHook *h, int epi, const float *bias, const float *mask, int64_t ldm, float *C_hi,
-                          float *C_lo) {
+                          float *C_lo, F16Out fo, const uint32_t *mbits, int64_t mbits_ld) {
     int64_t total = (int64_t)M * N;
     unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total / 4 + 255) / 256, 148 * 8));
     char rn[80];
     snprintf(rn, sizeof rn, "splitk_reduce[M=%d,N=%d,splits=%d,epi=%d]", M, N, splits, epi);
     if (h) h->before(rn, s);
     launch_pdl(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, s, partial, splits, M, N, C, ldc, epi, bias, mask, ldm,
-               C_hi, C_lo);
+               C_hi, C_lo, fo, mbits, mbits_ld);
     if (h) h->after(rn, s);
     return cudaGetLastError();
 }
@@ -258,6 +273,143 @@ cudaError_t split_planes(const float *x, int64_t rows, int64_t cols, int64_t ld,
     snprintf(name, sizeof name, "split_planes[n=%lld]", (long long)(rows * cols));
     if (h) h->before(name, s);
     launch_pdl(split_planes_kernel, dim3(blocks), dim3(256), 0, s, x, rows, cols, ld, hi, lo);
+    if (h) h->after(name, s);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ 3xF16 operand planes
+namespace {
+struct QArgs {
+    QSeg seg[QSEG_MAX];
+    int nseg;
+    const float *ax;
+    int64_t an;
+    TScale *ts, *zero_ts;
+    int n_zero;
+    float *scratch;  // [0, 1024): per-CTA maxima; then the grid barrier's arrival count and generation
+};
+constexpr int Q_T = 512;
+
+__device__ __forceinline__ float block_max(float v, float *red) {
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < Q_T / 32 ? red[threadIdx.x] : 0.f;
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    v = red[0];
+    __syncthreads();
+    return v;
+}
+
+// Grid-synchronous (every CTA resident: grid <= SM count): phase 1 max |x|, barrier, phase 2 planes.
+__global__ void __launch_bounds__(Q_T) quantize_f16_kernel(const __grid_constant__ QArgs a) {
+    pdl_wait();
+    __shared__ float red[Q_T / 32];
+    unsigned *bar = (unsigned *)(a.scratch + 1024);
+    const int64_t tid = blockIdx.x * (int64_t)Q_T + threadIdx.x, nth = (int64_t)gridDim.x * Q_T;
+    float m = 0.f;
+    if (a.ax) {
+        const bool v4 = ((uintptr_t)a.ax & 15) == 0;
+        const int64_t n4 = v4 ? a.an / 4 : 0;
+        for (int64_t i = tid; i < n4; i += nth) {
+            const float4 v = __ldg((const float4 *)a.ax + i);
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
+        for (int64_t i = 4 * n4 + tid; i < a.an; i += nth) m = fmaxf(m, fabsf(__ldg(a.ax + i)));
+    } else {
+        for (int q = 0; q < a.nseg; q++) {
+            const QSeg &g = a.seg[q];
+            for (int64_t i = tid; i < g.rows * g.cols; i += nth)
+                m = fmaxf(m, fabsf(__ldg(g.x + (i / g.cols) * g.ld + i % g.cols)));
+        }
+    }
+    m = block_max(m, red);
+    if (threadIdx.x == 0) {
+        const unsigned gen0 = atomicAdd(bar + 1, 0u);  // before arriving: the generation cannot move yet
+        a.scratch[blockIdx.x] = m;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            bar[0] = 0u;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (atomicAdd(bar + 1, 0u) == gen0) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    m = 0.f;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += Q_T) m = fmaxf(m, __ldcg(a.scratch + i));
+    const float amax = block_max(m, red);
+    const float sc = f16_scale_for(amax), inv = 1.f / sc;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.ts->amax = amax;
+        a.ts->scale = sc;
+        for (int i = 0; i < a.n_zero; i++) a.zero_ts[i].amax = 0.f;
+    }
+    for (int q = 0; q < a.nseg; q++) {
+        const QSeg &g = a.seg[q];
+        const bool v4 = g.cols % 4 == 0 && g.ld % 4 == 0 && g.pld % 4 == 0 && ((uintptr_t)g.x & 15) == 0 &&
+                        ((uintptr_t)g.hi & 7) == 0 && ((uintptr_t)g.lo & 7) == 0;
+        if (v4) {
+            const int64_t c4 = g.cols / 4, tot = g.rows * c4;
+            for (int64_t i = tid; i < tot; i += nth) {
+                const int64_t r = i / c4, c = 4 * (i % c4);
+                const float4 v = __ldg((const float4 *)(g.x + r * g.ld + c));
+                uint16_t h[4], l[4];
+                split_f16(v.x, inv, h[0], l[0]);
+                split_f16(v.y, inv, h[1], l[1]);
+                split_f16(v.z, inv, h[2], l[2]);
+                split_f16(v.w, inv, h[3], l[3]);
+                *(uint2 *)(g.hi + r * g.pld + c) = make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
+                *(uint2 *)(g.lo + r * g.pld + c) = make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
+            }
+        } else {
+            for (int64_t i = tid; i < g.rows * g.cols; i += nth) {
+                const int64_t r = i / g.cols, c = i % g.cols;
+                uint16_t h, l;
+                split_f16(__ldg(g.x + r * g.ld + c), inv, h, l);
+                g.hi[r * g.pld + c] = __ushort_as_half(h);
+                g.lo[r * g.pld + c] = __ushort_as_half(l);
+            }
+        }
+    }
+}
+}  // namespace
+
+cudaError_t quantize_f16(const QSeg *segs, int nseg, const float *amax_x, int64_t amax_n, TScale *ts, TScale *zero_ts,
+                         int n_zero, float *scratch, cudaStream_t s, LaunchHook *h) {
+    if (nseg < 0 || nseg > QSEG_MAX || !ts || !scratch) return cudaErrorInvalidValue;
+    QArgs a{};
+    int64_t work = 0;
+    for (int q = 0; q < nseg; q++) {
+        a.seg[q] = segs[q];
+        work += segs[q].rows * segs[q].cols;
+    }
+    a.nseg = nseg;
+    a.ax = amax_x;
+    a.an = amax_n;
+    a.ts = ts;
+    a.zero_ts = zero_ts;
+    a.n_zero = n_zero;
+    a.scratch = scratch;
+    work = std::max(work, amax_x ? amax_n : 0);
+    static int sms = [] {
+        int d = 0, n = 148;
+        cudaGetDevice(&d);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+        return n;
+    }();
+    // one CTA per SM at most: the barrier needs every CTA resident (1024 maxima slots)
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>({(work / 4 + Q_T - 1) / Q_T, sms, 1024}));
+    char name[64];
+    snprintf(name, sizeof name, "quantize_f16[n=%lld]", (long long)work);
+    if (h) h->before(name, s);
+    launch_pdl(quantize_f16_kernel, dim3(blocks), dim3(Q_T), 0, s, a);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }
@@ -328,6 +480,46 @@ __global__ void __launch_bounds__(256) fold_partials_kernel(const float *__restr
     if (lane == 0) out[j] = s;
 }
 }  // namespace
+
+namespace {
+// 32 columns x 32 part-slices per CTA; slice ty sums parts ty, ty + 32, ... (8 loads in flight), the 32 slices
+// are folded by a fixed tree (deterministic)
+__global__ void __launch_bounds__(1024) colpart_fold_kernel(const float *__restrict__ partial, int parts, int n,
+                                                              float *__restrict__ out) {
+    pdl_wait();
+    __shared__ float red[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int j = blockIdx.x * 32 + tx;
+    float v = 0.f;
+    if (j < n) {
+        int p = ty;
+        for (; p + 7 * 32 < parts; p += 8 * 32) {
+            float x[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) x[u] = __ldg(partial + (int64_t)(p + 32 * u) * n + j);
+#pragma unroll
+            for (int u = 0; u < 8; u++) v += x[u];
+        }
+        for (; p < parts; p += 32) v += __ldg(partial + (int64_t)p * n + j);
+    }
+    red[ty][tx] = v;
+    __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) {
+        if (ty < o) red[ty][tx] += red[ty + o][tx];
+        __syncthreads();
+    }
+    if (ty == 0 && j < n) out[j] = red[0][tx];
+}
+}  // namespace
+
+cudaError_t colpart_fold(const float *partial, int parts, int n, float *out, cudaStream_t s, LaunchHook *h) {
+    char name[64];
+    snprintf(name, sizeof name, "colpart_fold[parts=%d,n=%d]", parts, n);
+    if (h) h->before(name, s);
+    launch_pdl(colpart_fold_kernel, dim3(cdiv(n, 32)), dim3(1024), 0, s, partial, parts, n, out);
+    if (h) h->after(name, s);
+    return cudaGetLastError();
+}
 
 cudaError_t fold_partials(const float *partial, int parts, int n, float *out, cudaStream_t s, LaunchHook *h) {
     char name[64];
@@ -501,8 +693,11 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
                                                              float *__restrict__ dprev, float *__restrict__ dp_hi,
                                                              float *__restrict__ dp_lo, float *__restrict__ loss_rows,
                                                              float *__restrict__ loss_part, unsigned *ticket,
-                                                             float *__restrict__ loss_out) {
+                                                             float *__restrict__ loss_out, F16Out fo) {
     pdl_wait();
+    const float inv_so = fo.h ? 1.f / f16out_scale(fo) : 1.f;
+    if (fo.h && blockIdx.x == 0 && threadIdx.x == 0) fo.ts->scale = 1.f / inv_so;
+    float amx = 0.f;
     // HEAD_MAXC 2 and 10 are exact class counts (HIGGS, MNIST/CIFAR-10): the class loops compile
     // without predicates; the other instances take C at run time
     constexpr bool EXACT = HEAD_MAXC == 2 || HEAD_MAXC == 10;
@@ -556,6 +751,9 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
     }
     __syncthreads();
     float wloss = 0.f;  // this warp's rows, in row order
+    float hcs[NV][4];  // 3xF16 lean: this lane's column sums of dprev over the warp's rows
+#pragma unroll
+    for (int t = 0; t < NV; t++) hcs[t][0] = hcs[t][1] = hcs[t][2] = hcs[t][3] = 0.f;
     for (int i = i_first; i < rows; i += gridDim.x * HEAD_WARPS) {
         if (i != i_first) load_row(i);
         float z[HEAD_MAXC];
@@ -625,13 +823,37 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
                     }
 #pragma unroll
                 for (int u = 0; u < 4; u++) o[u] = av[t][u] > 0.f ? o[u] : 0.f;
+                if (fo.colpart) {
+#pragma unroll
+                    for (int u = 0; u < 4; u++) hcs[t][u] += k + u < d ? o[u] : 0.f;
+                }
                 float oh[4], ol[4];
                 if (dp_hi) {
 #pragma unroll
                     for (int u = 0; u < 4; u++) split_tf32(o[u], oh[u], ol[u]);
                 }
                 const int64_t off = (int64_t)i * d + k;
-                if (VEC && k + 3 < d) {
+                if (fo.h) {
+                    const int64_t po = (int64_t)i * fo.ld + k;
+                    uint16_t hh[4], ll[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        split_f16(k + u < d ? o[u] : 0.f, inv_so, hh[u], ll[u]);
+                        amx = fmaxf(amx, k + u < d ? fabsf(o[u]) : 0.f);
+                    }
+                    if (VEC && k + 3 < d) {
+                        *(uint2 *)(fo.h + po) = make_uint2(hh[0] | ((uint32_t)hh[1] << 16), hh[2] | ((uint32_t)hh[3] << 16));
+                        *(uint2 *)(fo.l + po) = make_uint2(ll[0] | ((uint32_t)ll[1] << 16), ll[2] | ((uint32_t)ll[3] << 16));
+                    } else {
+                        for (int u = 0; u < 4; u++)
+                            if (k + u < d) {
+                                fo.h[po + u] = __ushort_as_half(hh[u]);
+                                fo.l[po + u] = __ushort_as_half(ll[u]);
+                            }
+                    }
+                }
+                if (fo.skip_f32) {
+                } else if (VEC && k + 3 < d) {
                     *(float4 *)(dprev + off) = make_float4(o[0], o[1], o[2], o[3]);
                     if (dp_hi) {
                         *(float4 *)(dp_hi + off) = make_float4(oh[0], oh[1], oh[2], oh[3]);
@@ -646,6 +868,24 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
                         }
                 }
             }
+        }
+    }
+    if (fo.h) {
+        for (int o = 16; o > 0; o >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
+        if (lane == 0) amax_atomic(&fo.ts->amax, amx);
+    }
+    if (fo.colpart) {  // per-CTA column sums: the warps' sums in warp order (deterministic)
+        float *csm = sWt + (size_t)dp * C;
+#pragma unroll
+        for (int t = 0; t < NV; t++) {
+            const int k = 4 * lane + 128 * t;
+            if (k < dp) *(float4 *)(csm + warp * dp + k) = make_float4(hcs[t][0], hcs[t][1], hcs[t][2], hcs[t][3]);
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < d; k += HEAD_WARPS * 32) {
+            float v = 0.f;
+            for (int w = 0; w < HEAD_WARPS; w++) v += csm[w * dp + k];
+            fo.colpart[(int64_t)blockIdx.x * d + k] = v;
         }
     }
     // loss: warp sums -> block sum (warp order) -> per-block partial; the last block folds the
@@ -682,26 +922,32 @@ template <int NV, bool VEC, int CM, int W>
 cudaError_t launch_head(unsigned blocks, size_t smem, cudaStream_t s, int rows, int d, int C, const float *A, RowSel arow,
                         const float *Wb, const int32_t *labels, RowSel lrow, float inv_b, float *dZL, float *dprev,
                         float *dp_hi, float *dp_lo, float *loss_rows, float *loss_part, unsigned *ticket,
-                        float *loss_out) {
+                        float *loss_out, F16Out fo) {
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(head_kernel<NV, VEC, CM, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     return launch_pdl(head_kernel<NV, VEC, CM, W>, dim3(blocks), dim3(W * 32), smem, s, rows, d, C, A, arow, Wb,
-                      labels, lrow, inv_b, dZL, dprev, dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out);
+                      labels, lrow, inv_b, dZL, dprev, dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out, fo);
 }
 }  // namespace
 
 cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, const float *Wb, const int32_t *labels,
                        RowSel lrow, float inv_b, float *dZL, float *dprev, float *dp_hi, float *dp_lo,
                        float *loss_rows, float *loss_part, unsigned *ticket, float *loss_out, cudaStream_t s,
-                       LaunchHook *h) {
+                       LaunchHook *h, F16Out fo, int *colpart_rows) {
     if (C > 16 || C < 1 || d > 1024) return cudaErrorInvalidValue;
-    const size_t smem = sizeof(float) * (size_t)((d + 1 + 3) & ~3) * C;
     // enough rows per block that the block count stays <= 1024 (loss partial slots)
     int hw = rows > 2048 ? 2 : 8;
     if (const char *e = getenv("MTX_HEAD_WARPS")) hw = atoi(e) == 4 ? 4 : atoi(e) == 2 ? 2 : 8;  // development knob
-    const unsigned blocks = std::min<unsigned>(cdiv(rows, hw), 1024u);
+    // column sums (3xF16 lean: the bias gradient of layer L-1) are one row per CTA: 8 warps and <= 256 CTAs
+    // keep those rows few (the same 2048 warps in flight as 2-warp CTAs x 1024 at cfg4)
+    if (fo.colpart) hw = 8;
+    const size_t dpad = (size_t)((d + 1 + 3) & ~3);
+    // W_L staged transposed; + one row of column sums per warp
+    const size_t smem = sizeof(float) * dpad * (C + (fo.colpart ? hw : 0));
+    const unsigned blocks = std::min<unsigned>(cdiv(rows, hw), fo.colpart ? 256u : 1024u);
+    if (colpart_rows) *colpart_rows = (int)blocks;
     const bool vec = (d % 4 == 0) && ((uintptr_t)A % 16 == 0) && (dprev == nullptr || (uintptr_t)dprev % 16 == 0) &&
                      (dp_hi == nullptr || ((uintptr_t)dp_hi % 16 == 0 && (uintptr_t)dp_lo % 16 == 0));
     char name[80];
@@ -710,9 +956,9 @@ cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, cons
     cudaError_t e;
 #define HEAD_CASE4(NVv, CMv, Wv)                                                                               \
     e = vec ? launch_head<NVv, true, CMv, Wv>(blocks, smem, s, rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL,   \
-                                              dprev, dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out)     \
+                                              dprev, dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out, fo) \
             : launch_head<NVv, false, CMv, Wv>(blocks, smem, s, rows, d, C, A, arow, Wb, labels, lrow, inv_b, dZL,  \
-                                               dprev, dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out)
+                                               dprev, dp_hi, dp_lo, loss_rows, loss_part, ticket, loss_out, fo)
 #define HEAD_CASE3(NVv, CMv)          \
     if (hw == 2) {                    \
         HEAD_CASE4(NVv, CMv, 2);      \

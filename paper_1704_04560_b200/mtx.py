@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libmtx.so")
 STATUS = ["MTX_OK", "MTX_ERR_INVALID_ARG", "MTX_ERR_STATE", "MTX_ERR_SHAPE", "MTX_ERR_CUDA", "MTX_ERR_NCCL",
           "MTX_ERR_NUMERIC", "MTX_ERR_PROTOCOL", "MTX_ERR_OOM", "MTX_ERR_UNSUPPORTED"]
 MTX_MLP, MTX_CNN = 0, 1
-MTX_FP32, MTX_TF32, MTX_3XTF32 = 0, 1, 2
+MTX_FP32, MTX_TF32, MTX_3XTF32, MTX_3XF16 = 0, 1, 2, 3
 MTX_REDUCE_NCCL, MTX_REDUCE_ORDERED, MTX_REDUCE_FUSED, MTX_REDUCE_LAYERWISE, MTX_REDUCE_ZERO1 = 0, 1, 2, 3, 4
 MTX_BUF_PARAMS, MTX_BUF_VELOCITY, MTX_BUF_GRADS = 0, 1, 2
 

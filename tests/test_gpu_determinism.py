@@ -20,7 +20,7 @@ import paper_1704_04560_b200 as P  # noqa: E402
 from paper_1704_04560_b200 import mtx  # noqa: E402
 
 TC = "tcgen05" in mtx.mtx_build_info()
-PRECS = [P.MTX_FP32] + ([P.MTX_3XTF32] if TC else [])
+PRECS = [P.MTX_FP32] + ([P.MTX_3XTF32, P.MTX_3XF16] if TC else [])
 
 
 def _trajectory(cfg, X, y, prec, steps):
@@ -53,7 +53,8 @@ def test_step_bitwise_repeatable(name, prec):
 @pytest.mark.skipif(not TC, reason="tcgen05 engine not built")
 @pytest.mark.parametrize("shape", [(8192, 1024, 1024, 0, 0, 1), (8192, 1024, 1024, 0, 1, 3), (1024, 1024, 8192, 1, 0, 0),
                                    (784, 512, 512, 1, 0, 0), (512, 512, 784, 0, 0, 1), (28, 1024, 8192, 1, 0, 0)])
-def test_gemm_bitwise_repeatable(shape):
+@pytest.mark.parametrize("engine", [2, 4])
+def test_gemm_bitwise_repeatable(shape, engine):
     M, N, K, ta, tb, epi = shape
     rng = np.random.default_rng(M + N + K)
     A = torch.from_numpy(rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)).cuda()
@@ -62,12 +63,12 @@ def test_gemm_bitwise_repeatable(shape):
     mask = torch.from_numpy(np.maximum(rng.standard_normal((M, N)), 0).astype(np.float32)).cuda()
     outs = []
     for _ in range(3):
-        r = P.Replica(dict(S.CONFIGS["cfg4"], B=1024), precision=P.MTX_3XTF32)
+        r = P.Replica(dict(S.CONFIGS["cfg4"], B=1024), precision=P.MTX_3XTF32 if engine == 2 else P.MTX_3XF16)
         try:
             C = torch.full((M, N), np.nan, device="cuda")
             torch.cuda.synchronize()
             for _ in range(2):  # the second call reuses the first one's split-K tickets / scratch
-                mtx.mtx_debug_gemm(r.ctx, 2, M, N, K, ta, tb, epi, A.data_ptr(), M if ta else K, B.data_ptr(),
+                mtx.mtx_debug_gemm(r.ctx, engine, M, N, K, ta, tb, epi, A.data_ptr(), M if ta else K, B.data_ptr(),
                                    K if tb else N, C.data_ptr(), N, bias.data_ptr(), mask.data_ptr(), N, r.s)
             r.sync()
             outs.append(C.cpu().numpy().tobytes())

@@ -77,6 +77,48 @@ def test_gemm_layouts(rep, engine, layout, shape):
     assert maxrel(C, ref) <= 1e-5 * max(1.0, np.sqrt(K / 1024)), maxrel(C, ref)
 
 
+@pytest.fixture(scope="module")
+def rep16():
+    r = P.Replica(dict(S.CONFIGS["cfg4"], B=1024), precision=P.MTX_3XF16)
+    yield r
+    r.close()
+
+
+@pytest.mark.skipif(not TC, reason="tcgen05 engine not built")
+@pytest.mark.parametrize("layout", [(0, 0, 1), (0, 0, 2), (0, 1, 3), (1, 0, 0)])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_gemm_layouts_3xf16(rep16, layout, shape):
+    """3xF16 engine (diagnostic engine 4: A and B quantized to fp16 hi/lo planes with one power-of-two
+    scale per operand, then kind::f16 MMAs): the fp32 tier against the float64 definition."""
+    ta, tb, epi = layout
+    M, N, K = shape
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    C, ref = _run(rep16, 4, M, N, K, ta, tb, epi, rng)
+    assert not np.isnan(C).any()
+    assert maxrel(C, ref) <= 1e-5 * max(1.0, np.sqrt(K / 1024)), maxrel(C, ref)
+
+
+@pytest.mark.skipif(not TC, reason="tcgen05 engine not built")
+@pytest.mark.parametrize("scales", [(1e-7, 3e4), (2.0 ** 40, 2.0 ** -60), (1e-20, 1e-8)])
+def test_gemm_3xf16_exponent_range(rep16, scales):
+    """The per-tensor power-of-two scale carries operands far outside fp16's range (|x| up to 2^40, down to
+    1e-20) through the fp16 planes: the result keeps the fp32 tier."""
+    M, N, K = 1000, 384, 520
+    rng = np.random.default_rng(7)
+    sa, sb = scales
+    A = (rng.standard_normal((M, K)) * sa).astype(np.float32)
+    B = (rng.standard_normal((K, N)) * sb).astype(np.float32)
+    d = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    Ad, Bd = d(A), d(B)
+    Cd = torch.full((M, N), np.nan, device="cuda")
+    torch.cuda.synchronize()
+    mtx.mtx_debug_gemm(rep16.ctx, 4, M, N, K, 0, 0, 0, Ad.data_ptr(), K, Bd.data_ptr(), N, Cd.data_ptr(), N,
+                       None, None, 0, rep16.s)
+    rep16.sync()
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    assert maxrel(Cd.cpu().numpy(), ref) <= 1e-5
+
+
 def _tf32_trunc(x: np.ndarray) -> np.ndarray:
     """fp32 -> TF32 by truncating the low 13 mantissa bits: how tcgen05 kind::tf32 consumes fp32
     shared-memory operands (reading A12, measured with tools/tc_probe.cu)."""

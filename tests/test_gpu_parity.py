@@ -24,7 +24,7 @@ if not torch.cuda.is_available():
 import paper_1704_04560_b200 as P  # noqa: E402  (loads libmtx.so; raises if missing)
 from paper_1704_04560_b200 import mtx  # noqa: E402
 
-PRECISIONS = [P.MTX_FP32] + ([P.MTX_3XTF32] if "tcgen05" in mtx.mtx_build_info() else [])
+PRECISIONS = [P.MTX_FP32] + ([P.MTX_3XTF32, P.MTX_3XF16] if "tcgen05" in mtx.mtx_build_info() else [])
 
 
 def small_cfg(name, **kw):
@@ -215,9 +215,10 @@ def test_ragged_mlp_one_step(precision):
     _check_step(cfg, X, y, precision, 4, start)
 
 
+@pytest.mark.parametrize("precision", PRECISIONS[1:] or PRECISIONS)
 @pytest.mark.parametrize("C,d,B", [(10, 71, 75), (2, 71, 75), (10, 64, 2100), (2, 33, 2100), (1, 40, 75),
                                    (5, 130, 75), (16, 129, 75)])
-def test_head_class_counts(C, d, B):
+def test_head_class_counts(C, d, B, precision):
     """The fused head's instances: exact C = 2 / 10 (HIGGS, MNIST/CIFAR), generic C <= 4 / <= 16,
     vector and scalar (d % 4 != 0) row loads, and the > 2048-row launch shape; B is ragged."""
     cfg = dict(kind="mlp", dims=[24, d, C], data="mnist", n=B + 50, B=B, lr=0.05, mu=0.9)
@@ -225,7 +226,7 @@ def test_head_class_counts(C, d, B):
     X = rng.standard_normal((B + 50, 24)).astype(np.float32)
     y = rng.integers(0, C, B + 50).astype(np.int32)
     start = oracle.init_params(oracle.Net.from_cfg(cfg), 42)
-    _check_step(cfg, X, y, P.MTX_3XTF32, 1, start)
+    _check_step(cfg, X, y, precision, 1, start)
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
