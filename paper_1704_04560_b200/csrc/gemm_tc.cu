@@ -119,7 +119,7 @@ __device__ __forceinline__ void unit_of(const TcParams &p, int t, int tiles_mn, 
 __device__ __forceinline__ float4 load_mask(const TcParams &p, int m, int n) {
     if (p.mbits) {  // bits n..n+3 of the row's word n / 32 (n % 4 == 0; bits past N are 0)
         const uint32_t w = __ldg(p.mbits + (int64_t)m * p.mbits_ld + (n >> 5)) >> (n & 31);
-        return make_float4((float)(w & 1u), (float)((w >> 1) & 1u), (float)((w >> 2) & 1u), (float)((w >> 3) & 1u));
+        return make_float4((w & 1u) ? 1.f : 0.f, (w & 2u) ? 1.f : 0.f, (w & 4u) ? 1.f : 0.f, (w & 8u) ? 1.f : 0.f);
     }
     const float *mk = p.mask + (int64_t)m * p.ldm + n;
     if (n + 3 < p.N) return __ldg((const float4 *)mk);
@@ -131,8 +131,18 @@ __device__ __forceinline__ float4 load_mask(const TcParams &p, int m, int n) {
 // The fused epilogue on 4 consecutive outputs C[m][n..n+3] (coalesced across a warp): bias (+ReLU)
 // or ReLU mask (mkv, from load_mask), the fp32 store and, for a 3xTF32 consumer, the hi/lo planes.
 // MASK: compile-time dgrad variant (EPI_MASK); otherwise bias (+ReLU) or a plain store.
+// bias[n..n+3] (zero past N): loaded once per staged sub-tile column group, not per row
+__device__ __forceinline__ float4 load_bias(const TcParams &p, int n) {
+    if (!(p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) || n >= p.N) return make_float4(0.f, 0.f, 0.f, 0.f);
+    if (n + 3 < p.N && ((uintptr_t)(p.bias + n) & 15) == 0) return __ldg((const float4 *)(p.bias + n));
+    float b[4];
+    for (int e = 0; e < 4; e++) b[e] = n + e < p.N ? __ldg(p.bias + n + e) : 0.f;
+    return make_float4(b[0], b[1], b[2], b[3]);
+}
+
 template <bool MASK, bool F16>
-__device__ __forceinline__ float4 epi_store(const TcParams &p, int m, int n, float4 sv, float4 mkv, float inv_so, float &amx) {
+__device__ __forceinline__ float4 epi_store(const TcParams &p, int m, int n, float4 sv, float4 mkv, float inv_so, float &amx,
+                                            float4 bz) {
     const bool vec4 = n + 3 < p.N;
     float o[4] = {sv.x, sv.y, sv.z, sv.w};
     if constexpr (MASK) {
@@ -141,10 +151,11 @@ __device__ __forceinline__ float4 epi_store(const TcParams &p, int m, int n, flo
         for (int e = 0; e < 4; e++)
             if (!(mv[e] > 0.f)) o[e] = 0.f;
     } else if (p.epi == EPI_BIAS_RELU || p.epi == EPI_BIAS) {
+        const float bv[4] = {bz.x, bz.y, bz.z, bz.w};
 #pragma unroll
         for (int e = 0; e < 4; e++)
             if (n + e < p.N) {
-                o[e] += __ldg(p.bias + n + e);
+                o[e] += bv[e];
                 if (p.epi == EPI_BIAS_RELU) o[e] = fmaxf(o[e], 0.f);
             }
     }
@@ -155,21 +166,31 @@ __device__ __forceinline__ float4 epi_store(const TcParams &p, int m, int n, flo
     }
     if (F16) {  // fp16 hi/lo planes (scale from the output bound) for the consuming 3xF16 GEMM
         if (p.fo.h) {
-            uint16_t hi[4], lo[4];
+            float x[4];
 #pragma unroll
             for (int e = 0; e < 4; e++) {
-                const float x = n + e < p.N ? o[e] : 0.f;
-                split_f16(x, inv_so, hi[e], lo[e]);
-                amx = fmaxf(amx, fabsf(x));
+                x[e] = n + e < p.N ? o[e] : 0.f;
+                amx = fmaxf(amx, fabsf(x[e]));
+            }
+            // two elements per conversion (cvt.rn.f16x2.f32); same rounding as split_f16
+            __half2 h2[2], l2[2];
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const float2 y = make_float2(x[2 * e] * inv_so, x[2 * e + 1] * inv_so);
+                h2[e] = __float22half2_rn(y);
+                const float2 hf = __half22float2(h2[e]);
+                l2[e] = __float22half2_rn(make_float2(y.x - hf.x, y.y - hf.y));
             }
             const int64_t po = (int64_t)m * p.fo.ld + n;
             if (vec4) {
-                *(uint2 *)(p.fo.h + po) = make_uint2(hi[0] | ((uint32_t)hi[1] << 16), hi[2] | ((uint32_t)hi[3] << 16));
-                *(uint2 *)(p.fo.l + po) = make_uint2(lo[0] | ((uint32_t)lo[1] << 16), lo[2] | ((uint32_t)lo[3] << 16));
+                *(uint2 *)(p.fo.h + po) = make_uint2(*(uint32_t *)&h2[0], *(uint32_t *)&h2[1]);
+                *(uint2 *)(p.fo.l + po) = make_uint2(*(uint32_t *)&l2[0], *(uint32_t *)&l2[1]);
             } else {
+                const __half hh[4] = {__low2half(h2[0]), __high2half(h2[0]), __low2half(h2[1]), __high2half(h2[1])};
+                const __half ll[4] = {__low2half(l2[0]), __high2half(l2[0]), __low2half(l2[1]), __high2half(l2[1])};
                 for (int e = 0; e < 4 && n + e < p.N; e++) {
-                    p.fo.h[po + e] = __ushort_as_half(hi[e]);
-                    p.fo.l[po + e] = __ushort_as_half(lo[e]);
+                    p.fo.h[po + e] = hh[e];
+                    p.fo.l[po + e] = ll[e];
                 }
             }
         }
@@ -408,7 +429,8 @@ __device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base, floa
             if (u < S) {
                 sum.x += v[u].x; sum.y += v[u].y; sum.z += v[u].z; sum.w += v[u].w;
             }
-        epi_store<MASK, F16>(p, m, n, sum, MASK ? load_mask(p, m, n) : make_float4(0.f, 0.f, 0.f, 0.f), inv_so, amx);
+        epi_store<MASK, F16>(p, m, n, sum, MASK ? load_mask(p, m, n) : make_float4(0.f, 0.f, 0.f, 0.f), inv_so, amx,
+                             load_bias(p, n));
     }
 }
 
@@ -699,8 +721,10 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                                     acc[SW * c + 4 * j + 3]);
                 __syncwarp();
                 const int n = n0 + SW * c + 4 * jj;
+                const float4 bz = MASK ? make_float4(0.f, 0.f, 0.f, 0.f) : load_bias(p, n);
                 constexpr int ITS = 32 / RPI;  // row groups of the sub-tile
-                constexpr int G4 = MASK ? 4 : 1;  // dgrad: 4 groups' mask loads in flight together
+                // dgrad: the groups' mask loads in flight together (4 fp32 masks, or all 8 words of a bitmask)
+                constexpr int G4 = MASK ? (F16 ? ITS : 4) : 1;
 #pragma unroll
                 for (int it0 = 0; it0 < ITS; it0 += G4) {
                     float4 mk[G4];
@@ -728,7 +752,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                             }
                         }
                         float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-                        if (ok && p.splits == 1) o = epi_store<MASK, F16>(p, m, n, sv, mk[u], inv_so, amx);
+                        if (ok && p.splits == 1) o = epi_store<MASK, F16>(p, m, n, sv, mk[u], inv_so, amx, bz);
                         if (want_bits) {  // the 8 lanes of a row hold its 32 columns: OR their nibbles into one word
                             uint32_t w = ((o.x > 0.f) | ((o.y > 0.f) << 1) | ((o.z > 0.f) << 2) | ((o.w > 0.f) << 3))
                                          << (4 * jj);

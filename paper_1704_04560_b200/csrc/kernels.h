@@ -130,8 +130,10 @@ constexpr int QUANT_SCRATCH_FLOATS = 1024 + 4;  // per-CTA maxima + the grid bar
 // segments; s = f16_scale_for(amax); ts->amax / ts->scale written; then the planes of every segment.
 // zero_ts[0..n_zero): per-step slots whose amax is reset (their producers accumulate it next step).
 // scratch: QUANT_SCRATCH_FLOATS floats, zero on first use, private to one stream.
+// pre_parts > 0: scratch[0, pre_parts) already holds per-CTA maxima from the producing launch (avg_update's
+// amax_part): no max pass and no grid barrier.
 cudaError_t quantize_f16(const QSeg *segs, int nseg, const float *amax_x, int64_t amax_n, TScale *ts, TScale *zero_ts,
-                         int n_zero, float *scratch, cudaStream_t s, LaunchHook *h);
+                         int n_zero, float *scratch, cudaStream_t s, LaunchHook *h, int pre_parts = 0);
 
 // Narrow weight gradient (N <= 16, e.g. the classifier layer): dWb[k][j] = sum_i A[i][k] dZ[i][j]
 // for k < K_in, plus (aug) the bias row dWb[K_in][j] = sum_i dZ[i][j].  Thread per k, rows split
@@ -169,9 +171,11 @@ cudaError_t reduce_sum(const float *v, int n, float *out, cudaStream_t s, Launch
 // flag |= 1 on a non-finite gbar.  If win != nullptr, thread 0 advances the
 // window start: *win = (*win + B) mod n_data.  whi / wlo (nullable): also write the 3xTF32 hi/lo
 // planes of the updated w (rne_tf32 split, as split_planes).
+// amax_part (nullable, >= 1024 floats): per-CTA max |w| of the updated weights, *nparts of them (3xF16: the
+// next planes' scale without re-reading w for it).
 cudaError_t avg_update(float *G, float *w, float *v, int64_t n, float invP, float lr, float mu, int *flag,
                        int64_t *win, int64_t B, int64_t n_data, cudaStream_t s, LaunchHook *h, float *whi = nullptr,
-                       float *wlo = nullptr);
+                       float *wlo = nullptr, float *amax_part = nullptr, int *nparts = nullptr);
 
 // Ordered reduce (test mode): G[e] = ((g_0[e] + g_1[e]) + ...) + g_{P-1}[e], g_r at gathered + r*stride.
 cudaError_t ordered_fold(const float *gathered, int P, int64_t stride, int64_t n, float *G, cudaStream_t s,

@@ -287,6 +287,7 @@ struct QArgs {
     TScale *ts, *zero_ts;
     int n_zero;
     float *scratch;  // [0, 1024): per-CTA maxima; then the grid barrier's arrival count and generation
+    int pre_parts;   // > 0: scratch[0, pre_parts) already holds the maxima (written by the producer launch)
 };
 constexpr int Q_T = 512;
 
@@ -312,7 +313,8 @@ __global__ void __launch_bounds__(Q_T) quantize_f16_kernel(const __grid_constant
     unsigned *bar = (unsigned *)(a.scratch + 1024);
     const int64_t tid = blockIdx.x * (int64_t)Q_T + threadIdx.x, nth = (int64_t)gridDim.x * Q_T;
     float m = 0.f;
-    if (a.ax) {
+    if (a.pre_parts > 0) {
+    } else if (a.ax) {
         const bool v4 = ((uintptr_t)a.ax & 15) == 0;
         const int64_t n4 = v4 ? a.an / 4 : 0;
         for (int64_t i = tid; i < n4; i += nth) {
@@ -327,8 +329,8 @@ __global__ void __launch_bounds__(Q_T) quantize_f16_kernel(const __grid_constant
                 m = fmaxf(m, fabsf(__ldg(g.x + (i / g.cols) * g.ld + i % g.cols)));
         }
     }
-    m = block_max(m, red);
-    if (threadIdx.x == 0) {
+    if (a.pre_parts <= 0) m = block_max(m, red);
+    if (a.pre_parts <= 0 && threadIdx.x == 0) {
         const unsigned gen0 = atomicAdd(bar + 1, 0u);  // before arriving: the generation cannot move yet
         a.scratch[blockIdx.x] = m;
         __threadfence();
@@ -343,7 +345,8 @@ __global__ void __launch_bounds__(Q_T) quantize_f16_kernel(const __grid_constant
     }
     __syncthreads();
     m = 0.f;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += Q_T) m = fmaxf(m, __ldcg(a.scratch + i));
+    const int parts = a.pre_parts > 0 ? a.pre_parts : (int)gridDim.x;
+    for (int i = threadIdx.x; i < parts; i += Q_T) m = fmaxf(m, __ldcg(a.scratch + i));
     const float amax = block_max(m, red);
     const float sc = f16_scale_for(amax), inv = 1.f / sc;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -355,10 +358,11 @@ __global__ void __launch_bounds__(Q_T) quantize_f16_kernel(const __grid_constant
         const QSeg &g = a.seg[q];
         const bool v4 = g.cols % 4 == 0 && g.ld % 4 == 0 && g.pld % 4 == 0 && ((uintptr_t)g.x & 15) == 0 &&
                         ((uintptr_t)g.hi & 7) == 0 && ((uintptr_t)g.lo & 7) == 0;
-        if (v4) {
-            const int64_t c4 = g.cols / 4, tot = g.rows * c4;
-            for (int64_t i = tid; i < tot; i += nth) {
-                const int64_t r = i / c4, c = 4 * (i % c4);
+        if (v4 && g.rows * (g.cols / 4) < (1ll << 31)) {  // 32-bit index math (a 64-bit division per group was the cost)
+            const unsigned c4 = (unsigned)(g.cols / 4), tot = (unsigned)(g.rows * c4);
+            for (unsigned i = (unsigned)tid; i < tot; i += (unsigned)nth) {
+                const unsigned rq = i / c4;
+                const int64_t r = rq, c = 4 * (int64_t)(i - rq * c4);
                 const float4 v = __ldg((const float4 *)(g.x + r * g.ld + c));
                 uint16_t h[4], l[4];
                 split_f16(v.x, inv, h[0], l[0]);
@@ -382,7 +386,7 @@ __global__ void __launch_bounds__(Q_T) quantize_f16_kernel(const __grid_constant
 }  // namespace
 
 cudaError_t quantize_f16(const QSeg *segs, int nseg, const float *amax_x, int64_t amax_n, TScale *ts, TScale *zero_ts,
-                         int n_zero, float *scratch, cudaStream_t s, LaunchHook *h) {
+                         int n_zero, float *scratch, cudaStream_t s, LaunchHook *h, int pre_parts) {
     if (nseg < 0 || nseg > QSEG_MAX || !ts || !scratch) return cudaErrorInvalidValue;
     QArgs a{};
     int64_t work = 0;
@@ -397,7 +401,8 @@ cudaError_t quantize_f16(const QSeg *segs, int nseg, const float *amax_x, int64_
     a.zero_ts = zero_ts;
     a.n_zero = n_zero;
     a.scratch = scratch;
-    work = std::max(work, amax_x ? amax_n : 0);
+    a.pre_parts = pre_parts;
+    work = std::max(work, amax_x && pre_parts <= 0 ? amax_n : 0);
     static int sms = [] {
         int d = 0, n = 148;
         cudaGetDevice(&d);
@@ -1028,9 +1033,10 @@ __global__ void __launch_bounds__(UPD_T) avg_update_kernel(const float4 *__restr
                                                          float4 *__restrict__ v, int64_t n4, float invP, float lr,
                                                          float mu, int *flag, int64_t *win, int64_t B,
                                                          int64_t n_data, int tail, float4 *__restrict__ whi,
-                                                         float4 *__restrict__ wlo) {
+                                                         float4 *__restrict__ wlo, float *__restrict__ amax_part) {
     pdl_wait();
     bool bad = false;
+    float wmax = 0.f;  // 3xF16: max |w| of this CTA's updated weights (the next planes' scale)
     const int64_t stride = (int64_t)gridDim.x * UPD_T * UPD_U;
     for (int64_t base = (int64_t)blockIdx.x * UPD_T * UPD_U + threadIdx.x; base < n4; base += stride) {
         float4 g[UPD_U], wv[UPD_U], vv[UPD_U];
@@ -1061,6 +1067,7 @@ __global__ void __launch_bounds__(UPD_T) avg_update_kernel(const float4 *__restr
             }
             __stcs(w + i, wv[u]);
             if (HAS_V) __stcs(v + i, vv[u]);
+            if (amax_part) wmax = fmaxf(wmax, fmaxf(fmaxf(fabsf(pw[0]), fabsf(pw[1])), fmaxf(fabsf(pw[2]), fabsf(pw[3]))));
             if (whi) {  // 3xTF32: the next step's hi/lo planes of the updated weights
                 float hi[4], lo[4];
 #pragma unroll
@@ -1082,28 +1089,42 @@ __global__ void __launch_bounds__(UPD_T) avg_update_kernel(const float4 *__restr
             ws[i] = __fmaf_rn(-lr, gb, ws[i]);
         }
         if (whi) split_tf32(ws[i], ((float *)whi)[i], ((float *)wlo)[i]);
+        wmax = fmaxf(wmax, fabsf(ws[i]));
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0 && flag) atomicOr(flag, 1);
+    if (amax_part) {  // per-CTA maximum (the quantize launch that follows folds them: no re-read of w for its max)
+        __shared__ float red[UPD_T / 32];
+        for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = wmax;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int k = 1; k < UPD_T / 32; k++) wmax = fmaxf(wmax, red[k]);
+            amax_part[blockIdx.x] = wmax;
+        }
+    }
     if (win && blockIdx.x == 0 && threadIdx.x == 0) *win = (*win + B) % n_data;
 }
 }  // namespace
 
 cudaError_t avg_update(float *G, float *w, float *v, int64_t n, float invP, float lr, float mu, int *flag,
                        int64_t *win, int64_t B, int64_t n_data, cudaStream_t s, LaunchHook *h, float *whi,
-                       float *wlo) {
+                       float *wlo, float *amax_part, int *nparts) {
     int64_t n4 = n / 4;
     int tail = (int)(n - 4 * n4);
     int64_t need = (n4 + UPD_T * UPD_U - 1) / (UPD_T * UPD_U);
-    unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, 148 * 8));
+    // at most 1024 CTAs when they leave per-CTA maxima (the quantize scratch's slots)
+    unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, amax_part ? 1024 : 148 * 8));
+    if (nparts) *nparts = (int)blocks;
     char name[64];
     snprintf(name, sizeof name, "avg_update[n=%lld,v=%d,planes=%d]", (long long)n, v ? 1 : 0, whi ? 1 : 0);
     if (h) h->before(name, s);
     if (v)
         launch_pdl(avg_update_kernel<true>, dim3(blocks), dim3(UPD_T), 0, s, (const float4 *)G, (float4 *)w, (float4 *)v,
-                   n4, invP, lr, mu, flag, win, B, n_data, tail, (float4 *)whi, (float4 *)wlo);
+                   n4, invP, lr, mu, flag, win, B, n_data, tail, (float4 *)whi, (float4 *)wlo, amax_part);
     else
         launch_pdl(avg_update_kernel<false>, dim3(blocks), dim3(UPD_T), 0, s, (const float4 *)G, (float4 *)w,
-                   (float4 *)nullptr, n4, invP, lr, mu, flag, win, B, n_data, tail, (float4 *)whi, (float4 *)wlo);
+                   (float4 *)nullptr, n4, invP, lr, mu, flag, win, B, n_data, tail, (float4 *)whi, (float4 *)wlo,
+                   amax_part);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }

@@ -601,12 +601,13 @@ mtx_status quantize_buffer(mtx_ctx *c, const float *buf, int64_t rows, int64_t c
 }
 // 3xF16 parameter planes (one scale over the whole flat buffer, biases included: it bounds every bias
 // read by the forward epilogues); resets the per-step slots' amax (their producers run after this)
-mtx_status quantize_params(mtx_ctx *c, int scr, cudaStream_t s, LaunchHook *h) {
+// pre_parts > 0: the update launch just before left that many per-CTA maxima of the new parameters in qscr[scr]
+mtx_status quantize_params(mtx_ctx *c, int scr, cudaStream_t s, LaunchHook *h, int pre_parts = 0) {
     const int n = (int)c->param_segs.size();
     for (int i = 0; i < std::max(n, 1); i += QSEG_MAX)
         CK(quantize_f16(c->param_segs.data() + i, std::min(QSEG_MAX, n - i), c->params, c->N_pad,
                         c->tsl + mtx_ctx::TS_PARAMS, c->tsl + mtx_ctx::TS_STEP, c->n_ts - mtx_ctx::TS_STEP,
-                        c->qscr[scr], s, h));
+                        c->qscr[scr], s, h, pre_parts));
     return MTX_OK;
 }
 
@@ -1058,11 +1059,16 @@ struct Runner {
             if (mtx_status st = grads_ready(s)) return st;
             // 3xTF32: the update also writes the next step's weight planes (no split at step start)
             float *whi = c->params_hi ? c->params_hi + bkt.lo : nullptr, *wlo = c->params_lo ? c->params_lo + bkt.lo : nullptr;
+            // 3xF16 with one bucket (always at P = 1): the update leaves per-CTA maxima of the new parameters for
+            // the planes' scale (no separate max pass over w)
+            const bool fuse_max = c->f16 && last && bkt.lo == 0 && upd_hi == c->N_pad;
+            int nparts = 0;
             cudaError_t e = avg_update(c->grads + bkt.lo, c->params + bkt.lo, vel_or_null(bkt.lo), upd_hi - bkt.lo,
-                                       invP, c->opt.lr, c->opt.momentum, c->flag, win, c->B, c->n_data, s, h, whi, wlo);
+                                       invP, c->opt.lr, c->opt.momentum, c->flag, win, c->B, c->n_data, s, h, whi, wlo,
+                                       fuse_max ? c->qscr[0] : nullptr, &nparts);
             if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "update: %s", cudaGetErrorString(e));
             // 3xF16: the next step's parameter planes (one scale over the updated buffer)
-            if (c->f16 && last) return quantize_params(c, 0, s, h);
+            if (c->f16 && last) return quantize_params(c, 0, s, h, fuse_max ? nparts : 0);
             return MTX_OK;
         }
         if (mtx_status st = grads_ready(c->comm_s)) return st;

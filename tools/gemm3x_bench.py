@@ -21,7 +21,8 @@ rep = P.Replica(dict(S.CONFIGS["cfg4"], B=1024), precision=P.MTX_3XF16 if F16 el
 E0, E1 = (4, 5) if F16 else (2, 3)
 shapes = [(8192, 1024, 1024, 0, 0, 1), (8192, 1024, 1024, 0, 1, 3), (1024, 1024, 8192, 1, 0, 0),
           (4096, 1024, 1024, 0, 0, 1), (4096, 1024, 1024, 0, 1, 3), (1024, 1024, 4096, 1, 0, 0),
-          (2048, 1024, 1024, 0, 0, 1), (2048, 1024, 1024, 0, 1, 3), (1024, 1024, 2048, 1, 0, 0)]
+          (2048, 1024, 1024, 0, 0, 1), (2048, 1024, 1024, 0, 1, 3), (1024, 1024, 2048, 1, 0, 0),
+          (8192, 1024, 28, 0, 0, 1), (28, 1024, 8192, 1, 0, 0)]
 only = os.environ.get("SHAPES")
 for i, (M, N, K, ta, tb, epi) in enumerate(shapes):
     if only and str(i) not in only.split(","):
