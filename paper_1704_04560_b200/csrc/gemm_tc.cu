@@ -661,6 +661,21 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
             const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
             float acc[HALF];
             bool first = true;
+            // 3xF16 dgrad with a ReLU bitmask: this tile's mask words are loaded before its accumulation (their
+            // L2 latency hides behind the MMAs instead of stalling the store phase).  Word k of the rl group
+            // (8 lanes) = (sub-tile k / 8, row group k % 8); lane jj holds words 2 jj and 2 jj + 1.
+            constexpr bool PRE_BITS = F16 && MASK && HALF == 64;
+            uint32_t mw0 = 0, mw1 = 0;
+            if (PRE_BITS && p.mbits && p.splits == 1) {
+                const int rl8 = (lane & 31) >> 3, j8 = lane & 7;
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    const int k = 2 * j8 + e, m = m0 + 32 * q + (k % 8) * 4 + rl8, nc = n0 + 32 * (k / 8);
+                    uint32_t w = 0;
+                    if (m < p.M && nc < p.N) w = __ldg(p.mbits + (int64_t)m * p.mbits_ld + (nc >> 5));
+                    if (e == 0) mw0 = w; else mw1 = w;
+                }
+            }
             for (int c0 = kb0; c0 < kb1; c0 += L::CHUNK) {
                 mbar_wait(tfull0 + 8 * buf, buf_phase);
                 tc_fence_after();
@@ -731,6 +746,13 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
 #pragma unroll
                     for (int u = 0; u < G4; u++) {
                         const int m = m0 + 32 * q + (it0 + u) * RPI + rl;
+                        if (PRE_BITS && p.mbits) {  // the preloaded word of (sub-tile c, row group it0 + u)
+                            const int k = 8 * c + it0 + u;
+                            const uint32_t w = __shfl_sync(0xffffffffu, (k & 1) ? mw1 : mw0, rl * 8 + (k >> 1)) >> (n & 31);
+                            mk[u] = make_float4((w & 1u) ? 1.f : 0.f, (w & 2u) ? 1.f : 0.f, (w & 4u) ? 1.f : 0.f,
+                                                (w & 8u) ? 1.f : 0.f);
+                            continue;
+                        }
                         mk[u] = (MASK && p.splits == 1 && it0 + u < ITS && m < p.M && n < p.N)
                                     ? load_mask(p, m, n)
                                     : make_float4(0.f, 0.f, 0.f, 0.f);

@@ -102,7 +102,7 @@ def main():
         report["checks"].append("allreduce_avg dyadic bit-exact")
 
         # ---- the training step, DP(P) vs oracle DP(P)
-        precisions = [P.MTX_FP32] + ([P.MTX_3XTF32] if "tcgen05" in mtx.mtx_build_info() else [])
+        precisions = [P.MTX_FP32] + ([P.MTX_3XTF32, P.MTX_3XF16] if "tcgen05" in mtx.mtx_build_info() else [])
         for prec in precisions:
             tol, gtol = TOL[prec], GRAD_TOL[prec]
             for name, B, steps in (("cfg1", 64, 5), ("cfg2", 512, 3), ("cfg3", 64, 2)):
@@ -178,7 +178,7 @@ def main():
         report["checks"].append(f"layerwise and zero1 steps vs oracle at P={world}")
 
         # ---- FUSED (NVLink peer-memory reduce + update) is bit-exact with ORDERED (same rank-ordered fold)
-        for prec in ([P.MTX_FP32, P.MTX_3XTF32] if "tcgen05" in mtx.mtx_build_info() else [P.MTX_FP32]):
+        for prec in ([P.MTX_FP32, P.MTX_3XTF32, P.MTX_3XF16] if "tcgen05" in mtx.mtx_build_info() else [P.MTX_FP32]):
             for name, B, n in (("cfg1", 64, 1000), ("cfg2", 512, 4096)):
                 cfg = dict(S.CONFIGS[name], B=B)
                 X, y = S.mnist_like(1, n)
