@@ -726,6 +726,75 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
             // 3xF16 lean outputs (direct path only): the forward's ReLU bitmask, the dgrad's per-32-row column sums
             const bool want_bits = F16 && p.fo.bits && p.splits == 1;
             const bool want_cols = F16 && p.fo.colpart && p.splits == 1;
+            // 3xF16 lean fast path: a whole 32-row x 64-column piece in range, planes only (no fp32 copy, no split-K),
+            // forward (bias + ReLU [+ bits]) or dgrad (bitmask [+ column sums]): no per-element bounds or mode tests
+            if constexpr (F16 && HALF == 64) {
+                const bool fast = p.splits == 1 && p.fo.h && p.fo.skip_f32 && !(p.dbg & 1) && m0 + 32 * q + 32 <= p.M &&
+                                  n0 + HALF <= p.N && (MASK ? (p.mbits != nullptr)
+                                                            : (p.epi == EPI_BIAS_RELU && ((uintptr_t)p.bias & 15) == 0));
+                if (fast) {
+#pragma unroll
+                    for (int c = 0; c < 2; c++) {
+#pragma unroll
+                        for (int j = 0; j < 8; j++)
+                            *(float4 *)(stg + lane * 32 + 4 * swz(lane, j)) =
+                                make_float4(acc[32 * c + 4 * j], acc[32 * c + 4 * j + 1], acc[32 * c + 4 * j + 2],
+                                            acc[32 * c + 4 * j + 3]);
+                        __syncwarp();
+                        const int n = n0 + 32 * c + 4 * jj;
+                        const float4 bz = MASK ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg((const float4 *)(p.bias + n));
+                        float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                        for (int it = 0; it < 8; it++) {
+                            const int r = it * 4 + rl, m = m0 + 32 * q + r;
+                            const float4 sv = *(const float4 *)(stg + r * 32 + 4 * swz(r, jj));
+                            float x[4] = {sv.x, sv.y, sv.z, sv.w};
+                            if constexpr (MASK) {
+                                const int k = 8 * c + it;
+                                const uint32_t w = __shfl_sync(0xffffffffu, (k & 1) ? mw1 : mw0, rl * 8 + (k >> 1)) >> (4 * jj);
+#pragma unroll
+                                for (int e = 0; e < 4; e++) x[e] = ((w >> e) & 1u) ? x[e] : 0.f;
+                            } else {
+                                x[0] = fmaxf(x[0] + bz.x, 0.f); x[1] = fmaxf(x[1] + bz.y, 0.f);
+                                x[2] = fmaxf(x[2] + bz.z, 0.f); x[3] = fmaxf(x[3] + bz.w, 0.f);
+                            }
+                            amx = fmaxf(amx, fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3]))));
+                            __half2 h2[2], l2[2];
+#pragma unroll
+                            for (int e = 0; e < 2; e++) {
+                                const float2 y = make_float2(x[2 * e] * inv_so, x[2 * e + 1] * inv_so);
+                                h2[e] = __float22half2_rn(y);
+                                const float2 hf = __half22float2(h2[e]);
+                                l2[e] = __float22half2_rn(make_float2(y.x - hf.x, y.y - hf.y));
+                            }
+                            const int64_t po = (int64_t)m * p.fo.ld + n;
+                            *(uint2 *)(p.fo.h + po) = make_uint2(*(uint32_t *)&h2[0], *(uint32_t *)&h2[1]);
+                            *(uint2 *)(p.fo.l + po) = make_uint2(*(uint32_t *)&l2[0], *(uint32_t *)&l2[1]);
+                            if (!MASK && p.fo.bits) {  // the row's 32 columns sit in its 8 lanes: OR the nibbles
+                                uint32_t w = ((x[0] > 0.f) | ((x[1] > 0.f) << 1) | ((x[2] > 0.f) << 2) | ((x[3] > 0.f) << 3))
+                                             << (4 * jj);
+                                w |= __shfl_xor_sync(0xffffffffu, w, 1);
+                                w |= __shfl_xor_sync(0xffffffffu, w, 2);
+                                w |= __shfl_xor_sync(0xffffffffu, w, 4);
+                                if (jj == 0) p.fo.bits[(int64_t)m * p.fo.bits_ld + (n >> 5)] = w;
+                            }
+                            if (MASK) { cs.x += x[0]; cs.y += x[1]; cs.z += x[2]; cs.w += x[3]; }
+                        }
+                        if (MASK && p.fo.colpart) {  // the warp's 32 rows, fixed tree over the lanes of a column group
+#pragma unroll
+                            for (int o = 8; o < 32; o <<= 1) {
+                                cs.x += __shfl_xor_sync(0xffffffffu, cs.x, o);
+                                cs.y += __shfl_xor_sync(0xffffffffu, cs.y, o);
+                                cs.z += __shfl_xor_sync(0xffffffffu, cs.z, o);
+                                cs.w += __shfl_xor_sync(0xffffffffu, cs.w, o);
+                            }
+                            if (rl == 0) *(float4 *)(p.fo.colpart + (int64_t)((m0 + 32 * q) >> 5) * p.N + n) = cs;
+                        }
+                        __syncwarp();
+                    }
+                    continue;
+                }
+            }
 #pragma unroll
             for (int c = 0; c < HALF / SW; c++) {
                 float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -806,10 +875,17 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                 __syncwarp();
             }
         }
-        if (F16 && p.fo.h && !p.cluster) {  // amax of the planes written (the next consumer's bound)
+        if (F16 && p.fo.h && !p.cluster) {  // amax of the planes written (the next consumer's bound): one atomic per CTA
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
-            if (lane == 0) amax_atomic(&p.fo.ts->amax, amx);
+            float *red = (float *)(smem + L::EPI_OFF);  // the staging area is free once the last tile is stored
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (lane == 0) red[warp - 4] = amx;
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (warp == 4 && lane == 0) {
+                for (int k = 1; k < 8; k++) amx = fmaxf(amx, red[k]);
+                amax_atomic(&p.fo.ts->amax, amx);
+            }
         }
     }
 #undef MTX_UNITS

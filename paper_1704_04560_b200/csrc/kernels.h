@@ -130,10 +130,11 @@ constexpr int QUANT_SCRATCH_FLOATS = 1024 + 4;  // per-CTA maxima + the grid bar
 // segments; s = f16_scale_for(amax); ts->amax / ts->scale written; then the planes of every segment.
 // zero_ts[0..n_zero): per-step slots whose amax is reset (their producers accumulate it next step).
 // scratch: QUANT_SCRATCH_FLOATS floats, zero on first use, private to one stream.
-// pre_parts > 0: scratch[0, pre_parts) already holds per-CTA maxima from the producing launch (avg_update's
-// amax_part): no max pass and no grid barrier.
+// pre_parts > 0: pre[0, pre_parts) already holds per-CTA maxima from the producing launch(es) (avg_update's
+// amax_part, the fused update's per-rank arrays): no max pass and no grid barrier.
 cudaError_t quantize_f16(const QSeg *segs, int nseg, const float *amax_x, int64_t amax_n, TScale *ts, TScale *zero_ts,
-                         int n_zero, float *scratch, cudaStream_t s, LaunchHook *h, int pre_parts = 0);
+                         int n_zero, float *scratch, cudaStream_t s, LaunchHook *h, int pre_parts = 0,
+                         const float *pre = nullptr);
 
 // Narrow weight gradient (N <= 16, e.g. the classifier layer): dWb[k][j] = sum_i A[i][k] dZ[i][j]
 // for k < K_in, plus (aug) the bias row dWb[K_in][j] = sum_i dZ[i][j].  Thread per k, rows split
@@ -162,6 +163,13 @@ cudaError_t head_fused(int rows, int d, int C, const float *A, RowSel arow, cons
                        RowSel lrow, float inv_b, float *dZL, float *dprev, float *dp_hi, float *dp_lo,
                        float *loss_rows, float *loss_part, unsigned *ticket, float *loss_out, cudaStream_t s,
                        LaunchHook *h, F16Out fo = F16Out(), int *colpart_rows = nullptr);
+
+// Forward of a layer with K <= 64 on the CUDA cores (kernels_smallk.cu): C = act(A W + b), fp32 FMA in ascending
+// k, with the 3xF16 producer outputs of fo (planes + amax, ReLU bits, skip_f32).  A's rows start at arow.
+bool fwd_smallk_supported(int M, int N, int K, int64_t ldc, int64_t pld);
+cudaError_t fwd_smallk(int M, int N, int K, const float *A, int64_t lda, RowSel arow, const float *W, int64_t ldw,
+                       const float *bias, bool relu, float *C, int64_t ldc, const F16Out &fo, cudaStream_t s,
+                       LaunchHook *h);
 
 // out = sum_{i ascending in a fixed tree} v[i] (one block; deterministic).
 cudaError_t reduce_sum(const float *v, int n, float *out, cudaStream_t s, LaunchHook *h);

@@ -287,7 +287,8 @@ struct QArgs {
     TScale *ts, *zero_ts;
     int n_zero;
     float *scratch;  // [0, 1024): per-CTA maxima; then the grid barrier's arrival count and generation
-    int pre_parts;   // > 0: scratch[0, pre_parts) already holds the maxima (written by the producer launch)
+    int pre_parts;   // > 0: pre[0, pre_parts) already holds the maxima (written by the producer launch)
+    const float *pre;
 };
 constexpr int Q_T = 512;
 
@@ -346,7 +347,8 @@ __global__ void __launch_bounds__(Q_T) quantize_f16_kernel(const __grid_constant
     __syncthreads();
     m = 0.f;
     const int parts = a.pre_parts > 0 ? a.pre_parts : (int)gridDim.x;
-    for (int i = threadIdx.x; i < parts; i += Q_T) m = fmaxf(m, __ldcg(a.scratch + i));
+    const float *src = a.pre_parts > 0 ? a.pre : a.scratch;
+    for (int i = threadIdx.x; i < parts; i += Q_T) m = fmaxf(m, __ldcg(src + i));
     const float amax = block_max(m, red);
     const float sc = f16_scale_for(amax), inv = 1.f / sc;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -386,7 +388,7 @@ __global__ void __launch_bounds__(Q_T) quantize_f16_kernel(const __grid_constant
 }  // namespace
 
 cudaError_t quantize_f16(const QSeg *segs, int nseg, const float *amax_x, int64_t amax_n, TScale *ts, TScale *zero_ts,
-                         int n_zero, float *scratch, cudaStream_t s, LaunchHook *h, int pre_parts) {
+                         int n_zero, float *scratch, cudaStream_t s, LaunchHook *h, int pre_parts, const float *pre) {
     if (nseg < 0 || nseg > QSEG_MAX || !ts || !scratch) return cudaErrorInvalidValue;
     QArgs a{};
     int64_t work = 0;
@@ -402,6 +404,7 @@ cudaError_t quantize_f16(const QSeg *segs, int nseg, const float *amax_x, int64_
     a.n_zero = n_zero;
     a.scratch = scratch;
     a.pre_parts = pre_parts;
+    a.pre = pre ? pre : scratch;
     work = std::max(work, amax_x && pre_parts <= 0 ? amax_n : 0);
     static int sms = [] {
         int d = 0, n = 148;
@@ -875,9 +878,15 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
             }
         }
     }
-    if (fo.h) {
+    if (fo.h) {  // one atomic per CTA
         for (int o = 16; o > 0; o >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
-        if (lane == 0) amax_atomic(&fo.ts->amax, amx);
+        if (lane == 0) swl[warp] = amx;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < HEAD_WARPS; w++) amx = fmaxf(amx, swl[w]);
+            amax_atomic(&fo.ts->amax, amx);
+        }
+        __syncthreads();
     }
     if (fo.colpart) {  // per-CTA column sums: the warps' sums in warp order (deterministic)
         float *csm = sWt + (size_t)dp * C;

@@ -143,6 +143,10 @@ struct mtx_ctx {
     int n_ts = TS_STEP;
     float *qscr[2] = {nullptr, nullptr};
     std::vector<QSeg> param_segs;
+    // per-CTA max |w| of the last update: [0, 1024) at P = 1 (avg_update), [rank][148] at P > 1 (the fused update
+    // writes its slots in every replica); the parameter quantize folds them instead of re-reading w
+    float *wmax = nullptr;
+    int wmax_parts = 0;  // entries valid right now (0: none -- the quantize takes its own max)
     __half *data_h = nullptr;  // the dataset's planes (inside the dataset buffer)
     // 3xF16 lean MLP outputs: abits[l] = A_l's ReLU mask as bits [b][(d_l + 31) / 32] (A_l's fp32
     // copy is then not written), colp[l] = dZ_l's column partial sums [colp_rows][d_l] (dZ_l's fp32 copy not
@@ -517,6 +521,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     TScale *tsl = f16 ? (TScale *)take(sizeof(TScale) * mtx_ctx::TS_MAX) : nullptr;
     float *qs0 = f16 ? (float *)take(4 * QUANT_SCRATCH_FLOATS) : nullptr;
     float *qs1 = f16 ? (float *)take(4 * QUANT_SCRATCH_FLOATS) : nullptr;
+    float *wmx = f16 ? (float *)take(4 * MAX_PEERS * 1024) : nullptr;
     if (f16 && n_ts > mtx_ctx::TS_DBG) return UINT64_MAX / 2;  // more per-step tensors than slots (never for these models)
     if (assign) {
         c->f16 = f16;
@@ -527,6 +532,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         c->n_ts = n_ts;
         c->qscr[0] = qs0;
         c->qscr[1] = qs1;
+        c->wmax = wmx;
         size_t k = 0;
         for (auto &pr : planes)
             if (pr.h) pr.ts = tsl + slot_of[k++];
@@ -599,6 +605,9 @@ mtx_status quantize_buffer(mtx_ctx *c, const float *buf, int64_t rows, int64_t c
     CK(quantize_f16(&q, 1, nullptr, 0, v.ts, nullptr, 0, c->qscr[scr], s, h));
     return MTX_OK;
 }
+bool fused_overlap();
+// 3xF16 at P > 1 with the one-launch fused update: it leaves the per-rank maxima of the updated weights
+bool wmax_fused(const mtx_ctx *c) { return c->f16 && c->world > 1 && c->fused && c->wmax && !fused_overlap(); }
 // 3xF16 parameter planes (one scale over the whole flat buffer, biases included: it bounds every bias
 // read by the forward epilogues); resets the per-step slots' amax (their producers run after this)
 // pre_parts > 0: the update launch just before left that many per-CTA maxima of the new parameters in qscr[scr]
@@ -607,7 +616,7 @@ mtx_status quantize_params(mtx_ctx *c, int scr, cudaStream_t s, LaunchHook *h, i
     for (int i = 0; i < std::max(n, 1); i += QSEG_MAX)
         CK(quantize_f16(c->param_segs.data() + i, std::min(QSEG_MAX, n - i), c->params, c->N_pad,
                         c->tsl + mtx_ctx::TS_PARAMS, c->tsl + mtx_ctx::TS_STEP, c->n_ts - mtx_ctx::TS_STEP,
-                        c->qscr[scr], s, h, pre_parts));
+                        c->qscr[scr], s, h, pre_parts, c->wmax));
     return MTX_OK;
 }
 
@@ -765,6 +774,23 @@ struct Runner {
                 g.bnd_k = (float)g.K;
                 g.bnd_bias = (g.epi == EPI_BIAS_RELU || g.epi == EPI_BIAS) ? 1 : 0;
             }
+        }
+        // 3xF16 forward with a short contraction (cfg4's 28 input features): CUDA cores, all epilogue work spread
+        // over many CTAs per SM (kernels_smallk.cu; the tensor-core tile is one k-block of pure epilogue)
+        if (c->f16 && c_planes && g.epi == EPI_BIAS_RELU && !g.ta && !g.tb && !g.aug &&
+            fwd_smallk_supported(g.M, g.N, g.K, g.ldc, cv.pld) && !getenv("MTX_NO_SMALLK")) {
+            F16Out fo;
+            fo.h = cv.h; fo.l = cv.l; fo.ld = cv.pld; fo.ts = cv.ts;
+            fo.a = g.tsA; fo.b = g.tsB; fo.k = (float)g.K; fo.bias = 1;
+            if (ln && ln->bits) {
+                fo.bits = ln->bits;
+                fo.bits_ld = ln->bits_ld;
+                fo.skip_f32 = 1;
+                ln->done = true;
+            }
+            e = fwd_smallk(g.M, g.N, g.K, g.A, g.lda, g.arow, g.B, g.ldb, g.bias, true, g.C, g.ldc, fo, s, h);
+            if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "fwd_smallk: %s", cudaGetErrorString(e));
+            return MTX_OK;
         }
         if (c->opt.precision != MTX_FP32 && c->tc && tc_supports(c->tc, g)) {
             if (ln && c_planes && tc_direct(c->tc, g)) {  // 3xF16 lean outputs instead of the fp32 copy
@@ -1047,7 +1073,8 @@ struct Runner {
             const bool has_loss = ov ? bkt.hi > c->N_pad : true;
             cudaError_t e = fused_bucket_update(c->pp, c->world, c->rank, ov ? bi : 0, c->stepctr, lo, hi, c->opt.lr,
                                                 c->opt.momentum, c->opt.momentum != 0.f, c->flag, win, c->B, c->n_data,
-                                                has_loss ? c->N_pad : -1, ov ? comm_sms() : 148, cs, h);
+                                                has_loss ? c->N_pad : -1, ov ? comm_sms() : 148, cs, h,
+                                                c->f16 && !ov);
             if (e == cudaSuccess && last)
                 e = peer_barrier_step(c->pp, c->world, c->rank, c->epoch, c->flag, c->stepctr, cs, h);
             if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "fused update: %s", cudaGetErrorString(e));
@@ -1065,7 +1092,7 @@ struct Runner {
             int nparts = 0;
             cudaError_t e = avg_update(c->grads + bkt.lo, c->params + bkt.lo, vel_or_null(bkt.lo), upd_hi - bkt.lo,
                                        invP, c->opt.lr, c->opt.momentum, c->flag, win, c->B, c->n_data, s, h, whi, wlo,
-                                       fuse_max ? c->qscr[0] : nullptr, &nparts);
+                                       fuse_max ? c->wmax : nullptr, &nparts);
             if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "update: %s", cudaGetErrorString(e));
             // 3xF16: the next step's parameter planes (one scale over the updated buffer)
             if (c->f16 && last) return quantize_params(c, 0, s, h, fuse_max ? nparts : 0);
@@ -1124,8 +1151,9 @@ struct Runner {
                 CK(split_planes(sx, c->b, c->d0, c->d0, (float *)xh, (float *)xl, s, h));
         }
         if (c->f16) {  // 3xF16: same, with the per-tensor scales (P = 1: the previous update wrote the parameters')
+            // P > 1 with the fused update: its per-rank maxima of the new weights give the scale directly
             if (c->world > 1)
-                if (mtx_status st = quantize_params(c, 0, s, h)) return st;
+                if (mtx_status st = quantize_params(c, 0, s, h, wmax_fused(c) ? c->world * 148 : 0)) return st;
             if (staged)
                 if (mtx_status st = quantize_buffer(c, sx, c->b, c->d0, c->d0, 0, s, h)) return st;
         }
@@ -1372,7 +1400,14 @@ mtx_status assemble_shards(mtx_ctx *c) {
 // 3xTF32: hi/lo planes of the parameters after a change outside the step (init, broadcast,
 // mtx_set_buffer); at P = 1 the step itself relies on them being current.
 mtx_status refresh_param_planes(mtx_ctx *c, cudaStream_t s) {
-    if (c->f16) return quantize_params(c, 1, s, nullptr);
+    if (c->f16) {
+        if (mtx_status st = quantize_params(c, 1, s, nullptr)) return st;
+        if (wmax_fused(c)) {  // seed the fused update's maxima with the exact max (the next step's quantize folds them)
+            CK(cudaMemsetAsync(c->wmax, 0, 4 * (size_t)c->world * 148, s));
+            CK(cudaMemcpyAsync(c->wmax, &c->tsl[mtx_ctx::TS_PARAMS].amax, 4, cudaMemcpyDeviceToDevice, s));
+        }
+        return MTX_OK;
+    }
     if (!c->params_hi) return MTX_OK;
     CK(split_planes(c->params, 1, c->N_pad, c->N_pad, c->params_hi, c->params_lo, s, nullptr));
     return MTX_OK;
@@ -1434,6 +1469,7 @@ mtx_status map_peers(mtx_ctx *c) {
         c->pp.v[r] = (float *)(ws_r + rel(c->vel));
         c->pp.flags[r] = (uint64_t *)(ws_r + rel(c->flags));
         c->pp.bflags[r] = (uint64_t *)(ws_r + rel(c->bflags));
+        c->pp.wmax[r] = c->wmax ? (float *)(ws_r + rel(c->wmax)) : nullptr;
     }
     c->fused = true;
     return MTX_OK;

@@ -83,9 +83,11 @@ template <bool HAS_V>
 __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, int rank, int bucket,
                                                          const uint64_t *stepctr, int64_t lo4, int64_t hi4, float invP,
                                                          float lr, float mu, int *flag, int64_t *win, int64_t B,
-                                                         int64_t n_data, int64_t loss_idx) {
+                                                         int64_t n_data, int64_t loss_idx, int track_wmax) {
     pdl_wait();
     __shared__ int go;
+    __shared__ float red[16];
+    float wmax = 0.f;
     const uint64_t epoch = *(volatile const uint64_t *)stepctr + 1;
     if (threadIdx.x == 0) {
         go = 0;
@@ -143,9 +145,20 @@ __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, i
                 if (q < P) __stcg((float4 *)pp.w[q] + i, w);
             if (HAS_V) __stcg((float4 *)pp.v[rank] + i, v);
             __stcg((float4 *)pp.G[rank] + i, G);
+            wmax = fmaxf(wmax, fmaxf(fmaxf(fabsf(w.x), fabsf(w.y)), fmaxf(fabsf(w.z), fabsf(w.w))));
         }
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+    if (track_wmax) {  // this CTA's max |w| into slot [rank][CTA] of every replica's array (3xF16 planes' scale)
+        for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = wmax;
+        __syncthreads();
+        if (threadIdx.x < P) {
+            float m = red[0];
+            for (int k = 1; k < (int)(blockDim.x >> 5); k++) m = fmaxf(m, red[k]);
+            pp.wmax[threadIdx.x][rank * gridDim.x + blockIdx.x] = m;
+        }
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (loss_idx >= 0) {  // every rank folds all ranks' local loss sums itself (same order, same bits)
             float L = __ldcv(pp.g[0] + loss_idx);
@@ -250,7 +263,8 @@ cudaError_t peer_barrier_step(const PeerPtrs &pp, int P, int rank, uint64_t *epo
 
 cudaError_t fused_bucket_update(const PeerPtrs &pp, int P, int rank, int bucket, const uint64_t *stepctr, int64_t lo,
                                 int64_t hi, float lr, float mu, bool has_v, int *flag, int64_t *win, int64_t B,
-                                int64_t n_data, int64_t loss_idx, int ctas, cudaStream_t s, LaunchHook *h) {
+                                int64_t n_data, int64_t loss_idx, int ctas, cudaStream_t s, LaunchHook *h,
+                                bool track_wmax) {
     if (P > MAX_PEERS || bucket >= MAX_BUCKETS || lo % 4 || hi % 4) return cudaErrorInvalidValue;
     int64_t a, b;
     bucket_share(lo, hi, P, rank, a, b);
@@ -260,7 +274,7 @@ cudaError_t fused_bucket_update(const PeerPtrs &pp, int P, int rank, int bucket,
     const float invP = 1.0f / (float)P;
     auto kern = has_v ? fused_bucket_kernel<true> : fused_bucket_kernel<false>;
     launch_pdl(kern, dim3(std::max(1, ctas)), dim3(512), 0, s, pp, P, rank, bucket, stepctr, a / 4, b / 4, invP, lr, mu,
-               flag, win, B, n_data, loss_idx);
+               flag, win, B, n_data, loss_idx, (track_wmax && pp.wmax[0]) ? 1 : 0);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }

@@ -19,6 +19,8 @@ struct PeerPtrs {
     float *G[MAX_PEERS];
     uint64_t *flags[MAX_PEERS];  // per-rank arrival epochs, indexed by source rank
     uint64_t *bflags[MAX_PEERS]; // per-rank "bucket ready" epochs, [bucket][source rank] (MAX_BUCKETS x MAX_PEERS)
+    float *wmax[MAX_PEERS];      // 3xF16: per-rank arrays of per-CTA max |w| of the updated weights, [rank][CTA]
+                                 // (null: not tracked); the next step's parameter quantize folds them
 };
 
 constexpr int MAX_BUCKETS = 64;
@@ -40,7 +42,8 @@ cudaError_t peer_barrier(const PeerPtrs &pp, int P, int rank, uint64_t *epoch_ct
 // window start advances (the step's last bucket).  `ctas` CTAs (the SMs the backward GEMMs leave free).
 cudaError_t fused_bucket_update(const PeerPtrs &pp, int P, int rank, int bucket, const uint64_t *stepctr, int64_t lo,
                                 int64_t hi, float lr, float mu, bool has_v, int *flag, int64_t *win, int64_t B,
-                                int64_t n_data, int64_t loss_idx, int ctas, cudaStream_t s, LaunchHook *h);
+                                int64_t n_data, int64_t loss_idx, int ctas, cudaStream_t s, LaunchHook *h,
+                                bool track_wmax = false);
 // The rank's share of bucket [lo, hi) (float indices, multiples of 4): [lo + 4*(n4*r/P), lo + 4*(n4*(r+1)/P)).
 inline void bucket_share(int64_t lo, int64_t hi, int P, int r, int64_t &a, int64_t &b) {
     const int64_t n4 = (hi - lo) / 4;

@@ -166,6 +166,10 @@ int main(int argc, char **argv) {
         run<1, 0>(128, R, 4);
         run<1, 0>(256, R, 4);
         run<1, 0>(64, R, 4);
+        run<1, 1>(128, R, 4);  // kind::f16 pairs (the 3xF16 engine's tile)
+        run<1, 1>(256, R, 4);
+        run<0, 1>(128, R, 4);
+        run<0, 1>(64, R, 4);
         return 0;
     }
     for (int N : {64, 128, 256}) {
