@@ -100,6 +100,8 @@ struct TcParams {
     // the fp32 activation
     const uint32_t *mbits;
     int64_t mbits_ld;
+    int pf;  // producer: L2 prefetch distance in k-blocks (0: off)
+    int mc;  // PAIR: 4-CTA clusters of two pairs on adjacent N tiles; each A plane is loaded once and multicast
 };
 
 // Work unit t -> (k-split z, output tile r).  Cluster mode: the splits of a tile are consecutive
@@ -299,6 +301,17 @@ __device__ __forceinline__ void tma_load_2d_pair_elect(uint32_t dst, const CUten
         "l"((uint64_t)map), "r"(bar_cluster), "r"(c0), "r"(c1)
         : "memory");
 }
+// CTA pair load multicast to the CTAs of `mask` (same smem offset in each; each destination pair's leader barrier
+// counts the bytes): the A tile shared by the two pairs of a 4-CTA cluster (3xF16 multicast plan)
+__device__ __forceinline__ void tma_load_2d_pair_mc_elect(uint32_t dst, const CUtensorMap *map, uint32_t bar_cluster, int c0,
+                                                          int c1, uint16_t mask) {
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;\n}\n" ::"r"(
+            dst),
+        "l"((uint64_t)map), "r"(bar_cluster), "r"(c0), "r"(c1), "h"(mask)
+        : "memory");
+}
 __device__ __forceinline__ void umma_tf32_pair_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                                      uint32_t accumulate) {
     asm volatile(
@@ -335,6 +348,21 @@ __device__ __forceinline__ void tma_load_3d_pair_elect(uint32_t dst, const CUten
         " @e cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n}\n" ::"r"(
             dst),
         "l"((uint64_t)map), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+// L2 prefetch of a future operand tile (no smem, no barrier): the ring only holds STAGES k-blocks, fewer than an HBM
+// round trip's worth of MMAs when the operand was evicted from L2 since its producer wrote it
+__device__ __forceinline__ void tma_prefetch_2d_elect(const CUtensorMap *map, int c0, int c1) {
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n}\n" ::"l"((uint64_t)map), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d_elect(const CUtensorMap *map, int c0, int c1, int c2) {
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n}\n" ::"l"((uint64_t)map), "r"(c0),
+        "r"(c1), "r"(c2)
         : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1) {
@@ -452,6 +480,16 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                    tempty0 = tfull0 + 8 * NBUF;
     uint32_t *tmem_slot = (uint32_t *)(smem + L::BAR_OFF + 224);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // development (MTX_TC_DBG & 4): %globaltimer at the phases of CTA 0 and the last CTA, printed at exit
+    __shared__ uint64_t dts[8];
+    auto stamp = [&](int i) {
+        if (p.dbg & 4) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            dts[i] = t;
+        }
+    };
+    if (threadIdx.x == 0) stamp(0);
     uint32_t crank = 0;  // PAIR: cluster rank; pairs are cluster ranks (2j, 2j + 1) -- a cluster holds one pair,
                          // or the S pairs of a tile's K splits (p.cluster)
     if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
@@ -468,7 +506,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
         }
         for (int s = 0; s < STAGES; s++) {
             mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, (PAIR && p.mc) ? 2 : 1);  // multicast: a slot is free once both pairs consumed it
         }
         for (int a = 0; a < NBUF; a++) {
             mbar_init(tfull0 + 8 * a, 1);
@@ -496,6 +534,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_wait();  // prologue above overlaps the previous kernel's tail (programmatic launch)
+    if (threadIdx.x == 0) stamp(1);
 
     const int tiles_mn = p.tiles_m * p.tiles_n;
     const int total = tiles_mn * p.splits;
@@ -522,6 +561,25 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                 const int m0 = (r / p.tiles_n) * TILE_M + m_off, n0 = (r % p.tiles_n) * BN + nb_off;
                 const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
                 for (int kb = kb0; kb < kb1; kb++) {
+                    if (p.pf && kb + p.pf < kb1 && !(p.dbg & 2)) {  // k-block kb + pf into L2 (both planes, A and B)
+                        const int kp = (kb + p.pf) * KB;
+#pragma unroll
+                        for (int plane = 0; plane < (SPLIT ? 2 : 1); plane++) {
+                            const CUtensorMap *ma = plane ? &p.ta_lo : &p.ta, *mb = plane ? &p.tb_lo : &p.tb;
+                            if (!p.a_mn) tma_prefetch_2d_elect(ma, kp, (int)(row0 + m0));
+                            else if (p.a_3d) tma_prefetch_3d_elect(ma, 0, (int)(row0 + kp), m0 / CH);
+                            else {
+#pragma unroll
+                                for (int j = 0; j < BM / CH; j++) tma_prefetch_2d_elect(ma, m0 + CH * j, (int)(row0 + kp));
+                            }
+                            if (!p.b_mn) tma_prefetch_2d_elect(mb, kp, n0);
+                            else if (p.b_3d) tma_prefetch_3d_elect(mb, 0, kp, n0 / CH);
+                            else {
+#pragma unroll
+                                for (int j = 0; j < B_COLS / CH; j++) tma_prefetch_2d_elect(mb, n0 + CH * j, kp);
+                            }
+                        }
+                    }
                     mbar_wait(empty0 + 8 * stage, phase ^ 1);
                     const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::B_OFF;
                     const uint32_t fb = full0 + 8 * stage;
@@ -548,7 +606,13 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                             if (PAIR) tma_load_3d_pair_elect(dst, map, fbc, 0, k_row, chunk);
                             else tma_load_3d_elect(dst, map, fb, 0, k_row, chunk);
                         };
-                        if (!p.a_mn) {
+                        if (PAIR && p.mc && !p.a_mn) {
+                            // the cluster's two pairs share A's rows: pair 0 loads the hi plane, pair 1 the lo plane, each
+                            // multicast to the same-rank CTA of both pairs
+                            if ((int)((crank >> 1) & 1) == plane)
+                                tma_load_2d_pair_mc_elect(pa, ma, fbc, k0, (int)(row0 + m0),
+                                                          (uint16_t)((1u << rank) | (1u << (rank + 2))));
+                        } else if (!p.a_mn) {
                             load(pa, ma, k0, (int)(row0 + m0));
                         } else if (p.a_3d) {
                             load3(pa, ma, (int)(row0 + k0), m0 / CH);
@@ -586,18 +650,25 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
             uint32_t phase = 0;
             int buf = 0;
             uint32_t buf_phase = 0;
+            long long wait_te = 0, wait_full = 0;  // development (MTX_TC_DBG & 4): MMA-warp stall cycles
             MTX_UNITS(t) {
                 int z, r;
                 unit_of(p, t, tiles_mn, z, r);
                 const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
                 for (int c0 = kb0; c0 < kb1; c0 += L::CHUNK) {
                     const int c1 = min(kb1, c0 + L::CHUNK);
+                    long long w0 = (p.dbg & 4) ? clock64() : 0;
                     mbar_wait(tempty0 + 8 * buf, buf_phase ^ 1);
+                    if (p.dbg & 4) wait_te += clock64() - w0;
                     tc_fence_after();
                     const uint32_t d_tmem = tmem_base + buf * L::ACC_COLS;
                     for (int kb = c0; kb < c1; kb++) {
+                        long long w1 = (p.dbg & 4) ? clock64() : 0;
                         mbar_wait(full0 + 8 * stage, phase);
+                        if ((p.dbg & 4) && !(kb == kb0 && t == (PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x)))
+                            wait_full += clock64() - w1;
                         tc_fence_after();
+                        if (lane == 0 && kb == kb0 && t == (PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x)) stamp(2);
                         const uint32_t sa = sbase + stage * L::STAGE_BYTES, sb = sa + L::B_OFF;
                         const uint64_t ad0 = a_hi | ((sa >> 4) & 0x3FFF), bd0 = b_hi | ((sb >> 4) & 0x3FFF);
 #pragma unroll
@@ -623,7 +694,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                             }
                         }
                         // frees the smem slot (of both CTAs of a pair) when these MMAs retire
-                        if (PAIR) umma_commit_pair_elect(empty0 + 8 * stage, pair_mask);
+                        if (PAIR) umma_commit_pair_elect(empty0 + 8 * stage, p.mc ? (uint16_t)0xF : pair_mask);
                         else umma_commit_elect(empty0 + 8 * stage);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -631,8 +702,12 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                     if (PAIR) umma_commit_pair_elect(tfull0 + 8 * buf, pair_mask);
                     else umma_commit_elect(tfull0 + 8 * buf);
                     if (++buf == NBUF) { buf = 0; buf_phase ^= 1; }
+                    if (lane == 0) stamp(3);
                 }
             }
+            if ((p.dbg & 4) && lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 2))
+                printf("tcmma cta %d: wait_tempty %.2f us, wait_full %.2f us (after the first k-block)\n", blockIdx.x,
+                       wait_te / 1965.0, wait_full / 1965.0);
         }
     } else if (warp >= 4 && warp < 12) {
         // ================= epilogue: 8 warps; warp -> (TMEM lane quarter q, column half h).  Each
@@ -695,6 +770,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                         acc[CW * c + j] = first ? __uint_as_float(v[j]) : __fadd_rn(acc[CW * c + j], __uint_as_float(v[j]));
                 }
                 first = false;
+                if (warp == 4 && lane == 0) stamp(4);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {  // accumulator buffer drained (PAIR: on the leader, which issues into it)
@@ -729,7 +805,10 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
             // 3xF16 lean fast path: a whole 32-row x 64-column piece in range, planes only (no fp32 copy, no split-K),
             // forward (bias + ReLU [+ bits]) or dgrad (bitmask [+ column sums]): no per-element bounds or mode tests
             if constexpr (F16 && HALF == 64) {
-                const bool fast = p.splits == 1 && p.fo.h && p.fo.skip_f32 && !(p.dbg & 1) && m0 + 32 * q + 32 <= p.M &&
+                // output: the fp16 planes alone (lean), or the fp32 copy alone (a layer the SIMT head consumes)
+                const bool planes = p.fo.h != nullptr;
+                const bool fast = p.splits == 1 && (planes ? p.fo.skip_f32 : (p.C && (p.ldc & 3) == 0 && !p.C_hi)) &&
+                                  !(p.dbg & 1) && m0 + 32 * q + 32 <= p.M &&
                                   n0 + HALF <= p.N && (MASK ? (p.mbits != nullptr)
                                                             : (p.epi == EPI_BIAS_RELU && ((uintptr_t)p.bias & 15) == 0));
                 if (fast) {
@@ -758,18 +837,22 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                                 x[0] = fmaxf(x[0] + bz.x, 0.f); x[1] = fmaxf(x[1] + bz.y, 0.f);
                                 x[2] = fmaxf(x[2] + bz.z, 0.f); x[3] = fmaxf(x[3] + bz.w, 0.f);
                             }
-                            amx = fmaxf(amx, fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3]))));
-                            __half2 h2[2], l2[2];
+                            if (planes) {
+                                amx = fmaxf(amx, fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3]))));
+                                __half2 h2[2], l2[2];
 #pragma unroll
-                            for (int e = 0; e < 2; e++) {
-                                const float2 y = make_float2(x[2 * e] * inv_so, x[2 * e + 1] * inv_so);
-                                h2[e] = __float22half2_rn(y);
-                                const float2 hf = __half22float2(h2[e]);
-                                l2[e] = __float22half2_rn(make_float2(y.x - hf.x, y.y - hf.y));
+                                for (int e = 0; e < 2; e++) {
+                                    const float2 y = make_float2(x[2 * e] * inv_so, x[2 * e + 1] * inv_so);
+                                    h2[e] = __float22half2_rn(y);
+                                    const float2 hf = __half22float2(h2[e]);
+                                    l2[e] = __float22half2_rn(make_float2(y.x - hf.x, y.y - hf.y));
+                                }
+                                const int64_t po = (int64_t)m * p.fo.ld + n;
+                                *(uint2 *)(p.fo.h + po) = make_uint2(*(uint32_t *)&h2[0], *(uint32_t *)&h2[1]);
+                                *(uint2 *)(p.fo.l + po) = make_uint2(*(uint32_t *)&l2[0], *(uint32_t *)&l2[1]);
+                            } else {
+                                *(float4 *)(p.C + (int64_t)m * p.ldc + n) = make_float4(x[0], x[1], x[2], x[3]);
                             }
-                            const int64_t po = (int64_t)m * p.fo.ld + n;
-                            *(uint2 *)(p.fo.h + po) = make_uint2(*(uint32_t *)&h2[0], *(uint32_t *)&h2[1]);
-                            *(uint2 *)(p.fo.l + po) = make_uint2(*(uint32_t *)&l2[0], *(uint32_t *)&l2[1]);
                             if (!MASK && p.fo.bits) {  // the row's 32 columns sit in its 8 lanes: OR the nibbles
                                 uint32_t w = ((x[0] > 0.f) | ((x[1] > 0.f) << 1) | ((x[2] > 0.f) << 2) | ((x[3] > 0.f) << 3))
                                              << (4 * jj);
@@ -889,6 +972,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
         }
     }
 #undef MTX_UNITS
+    if (warp == 4 && lane == 0) stamp(5);
     if (p.cluster) {
         // every CTA of the cluster holds its split's partial tile: CTA z folds rows
         // [z*BM/S, (z+1)*BM/S) over the splits in ascending order (deterministic) and stores them
@@ -908,6 +992,13 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) {
+        stamp(6);
+        if ((p.dbg & 4) && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+            printf("tcts cta %d/%d t0 %llu: pdl %.2f first_full %.2f last_commit %.2f last_drain %.2f stores_done %.2f exit %.2f us\n",
+                   blockIdx.x, gridDim.x, (unsigned long long)dts[0], (dts[1] - dts[0]) * 1e-3, (dts[2] - dts[0]) * 1e-3,
+                   (dts[3] - dts[0]) * 1e-3, (dts[4] - dts[0]) * 1e-3, (dts[5] - dts[0]) * 1e-3, (dts[6] - dts[0]) * 1e-3);
+    }
     if (PAIR) cluster_sync_all();  // both CTAs done with the pair's TMEM and barriers
     if (warp == 2) {
         tc_fence_after();
@@ -1121,7 +1212,7 @@ static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s
     cfg.stream = s;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = PAIR ? (p.cluster ? 2 * p.splits : 2) : p.splits;
+    at[0].val.clusterDim.x = PAIR ? (p.cluster ? 2 * p.splits : p.mc ? 4 : 2) : p.splits;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1317,6 +1408,9 @@ static cudaError_t tc_gemm_impl(TcGemm *t, const GemmDesc &g, cudaStream_t s, La
     if (splits_out) *splits_out = splits;
     if (!launch) return cudaSuccess;
     if (const char *k = getenv("MTX_TC_DBG")) p.dbg = atoi(k);  // development timing knob
+    // L2 prefetch distance: one ring ahead of the loads (development knob MTX_TC_PF: 0 disables, n = distance)
+    static const int pf_env = getenv("MTX_TC_PF") ? atoi(getenv("MTX_TC_PF")) : -1;
+    p.pf = pf_env >= 0 ? pf_env : 0;  // measured slower at 4 and 8 (cfg4 506 -> 635 / 608 us/step): off
     p.epi = g.epi;
     p.bias = g.bias;
     p.mask = g.mask;
@@ -1325,12 +1419,24 @@ static cudaError_t tc_gemm_impl(TcGemm *t, const GemmDesc &g, cudaStream_t s, La
     p.ldc = g.ldc;
     p.partial = g.partial;
     const int total = tiles * splits;
-    const int grid = cluster ? (pair ? 2 * total : total) : pair ? 2 * std::min(total, sms / 2) : std::min(total, sms);
+    int grid = cluster ? (pair ? 2 * total : total) : pair ? 2 * std::min(total, sms / 2) : std::min(total, sms);
+    // 3xF16 CTA pairs, unsplit, K-major A, an even number of N tiles: clusters of two pairs on adjacent N tiles load
+    // each A plane once and multicast it (a third less L2 -> SM traffic).  Development knob MTX_TC_MC=1: measured no
+    // faster (cfg4 forward 44.5 -> 45.8 us) -- the MMA phase is bound by shared-memory bandwidth (TMA writes ~62 B/clk
+    // + MMA operand reads ~92 B/clk per SM against 128 B/clk), not by L2 delivery
+    static const int mc_env = getenv("MTX_TC_MC") ? atoi(getenv("MTX_TC_MC")) : 0;
+    if (f16 && pair && !cluster && splits == 1 && !p.a_mn && p.tiles_n % 2 == 0 && sms >= t->sms && mc_env == 1) {
+        const int nc = co_resident_pair_v(t, variant, 4);
+        if (nc >= 2) {
+            p.mc = 1;
+            grid = 4 * std::min(nc, total / 2);
+        }
+    }
     const char *kind = g.epi == EPI_MASK ? "dgrad" : (g.ta ? "wgrad" : "fwd");
     char name[96];
-    snprintf(name, sizeof name, "gemm_tc%s_%s[M=%d,N=%d,K=%d,splits=%d,cluster=%d,pair=%d,bn=%d]",
+    snprintf(name, sizeof name, "gemm_tc%s_%s[M=%d,N=%d,K=%d,splits=%d,cluster=%d,pair=%d,bn=%d%s]",
              f16 ? "3xf16" : g.tf32x3 ? "3x" : "",
-             kind, M, N, K, splits, cluster ? 1 : 0, pair ? 1 : 0, BN);
+             kind, M, N, K, splits, cluster ? 1 : 0, pair ? 1 : 0, BN, p.mc ? ",mc=1" : "");
     if (h) h->before(name, s);
     cudaError_t e;
     const bool mask = g.epi == EPI_MASK;  // dgrad: the masked-epilogue instantiation
