@@ -79,7 +79,7 @@ __device__ __forceinline__ bool wait_flags(const uint64_t *mine, int P, uint64_t
     return true;
 }
 
-template <bool HAS_V>
+template <bool HAS_V, int U, int PM>  // PM: peers the arrays hold (P <= PM)
 __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, int rank, int bucket,
                                                          const uint64_t *stepctr, int64_t lo4, int64_t hi4, float invP,
                                                          float lr, float mu, int *flag, int64_t *win, int64_t B,
@@ -102,27 +102,28 @@ __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, i
     __syncthreads();
     if (!go) return;  // a peer timed out: load and store nothing (the context is poisoned at the next sync)
     bool bad = false;
-    // two float4 per peer per thread in flight (2P loads), ascending-rank fold, update, w to every replica
+    // U float4 per peer per thread in flight (U*P loads over NVLink: the kernel is latency-bound on them), then the
+    // ascending-rank fold, the update and w to every replica
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i0 = lo4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < hi4; i0 += 2 * stride) {
-        const int64_t i1 = i0 + stride;
-        const bool two = i1 < hi4;
-        float4 g0[MAX_PEERS], g1[MAX_PEERS];
+    for (int64_t i0 = lo4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < hi4; i0 += U * stride) {
+        float4 gq[U][PM];
 #pragma unroll
-        for (int q = 0; q < MAX_PEERS; q++)
-            if (q < P) {
-                g0[q] = __ldcv((const float4 *)pp.g[q] + i0);
-                if (two) g1[q] = __ldcv((const float4 *)pp.g[q] + i1);
-            }
+        for (int u = 0; u < U; u++) {
+            const int64_t iu = i0 + u * stride;
+            if (iu >= hi4) break;
 #pragma unroll
-        for (int u = 0; u < 2; u++) {
-            if (u == 1 && !two) break;
-            const int64_t i = u ? i1 : i0;
-            float4 G = u ? g1[0] : g0[0];
+            for (int q = 0; q < PM; q++)
+                if (q < P) gq[u][q] = __ldcv((const float4 *)pp.g[q] + iu);
+        }
 #pragma unroll
-            for (int q = 1; q < MAX_PEERS; q++)
+        for (int u = 0; u < U; u++) {
+            const int64_t i = i0 + u * stride;
+            if (i >= hi4) break;
+            float4 G = gq[u][0];
+#pragma unroll
+            for (int q = 1; q < PM; q++)
                 if (q < P) {
-                    const float4 x = u ? g1[q] : g0[q];
+                    const float4 x = gq[u][q];
                     G.x = __fadd_rn(G.x, x.x); G.y = __fadd_rn(G.y, x.y);
                     G.z = __fadd_rn(G.z, x.z); G.w = __fadd_rn(G.w, x.w);
                 }
@@ -231,8 +232,10 @@ cudaError_t p2p_preload() {
     // issued while a peer barrier spins on this GPU (mtx_debug_reduce's simulated ranks) would deadlock
     cudaFuncAttributes a;
     cudaError_t e = cudaFuncGetAttributes(&a, (const void *)peer_barrier_kernel);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<true>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<true, 2, MAX_PEERS>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<false, 2, MAX_PEERS>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<true, 4, 4>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<false, 4, 4>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_avg_update_kernel<true>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_avg_update_kernel<false>);
     return e;
@@ -272,7 +275,9 @@ cudaError_t fused_bucket_update(const PeerPtrs &pp, int P, int rank, int bucket,
     snprintf(name, sizeof name, "fused_avg_update[n=%lld,P=%d,v=%d]", (long long)(hi - lo), P, has_v ? 1 : 0);
     if (h) h->before(name, s);
     const float invP = 1.0f / (float)P;
-    auto kern = has_v ? fused_bucket_kernel<true> : fused_bucket_kernel<false>;
+    // 4 float4 per peer in flight up to P = 4 (16 loads per thread), 2 beyond (register budget)
+    auto kern = P <= 4 ? (has_v ? fused_bucket_kernel<true, 4, 4> : fused_bucket_kernel<false, 4, 4>)
+                       : (has_v ? fused_bucket_kernel<true, 2, MAX_PEERS> : fused_bucket_kernel<false, 2, MAX_PEERS>);
     launch_pdl(kern, dim3(std::max(1, ctas)), dim3(512), 0, s, pp, P, rank, bucket, stepctr, a / 4, b / 4, invP, lr, mu,
                flag, win, B, n_data, loss_idx, (track_wmax && pp.wmax[0]) ? 1 : 0);
     if (h) h->after(name, s);
