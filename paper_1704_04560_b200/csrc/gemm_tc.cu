@@ -535,6 +535,10 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
     const uint32_t tmem_base = *tmem_slot;
     pdl_wait();  // prologue above overlaps the previous kernel's tail (programmatic launch)
     if (threadIdx.x == 0) stamp(1);
+    // 256-wide pair tiles: 128 promoted accumulators per epilogue thread.  The producer / MMA / allocator warpgroup
+    // hands registers to the two epilogue warpgroups (128 x 56 + 256 x 224 <= 64 K); each role's code follows its
+    // setmaxnreg so the compiler allocates that region within the new budget
+    constexpr bool REGS = BN == 256;
 
     const int tiles_mn = p.tiles_m * p.tiles_n;
     const int total = tiles_mn * p.splits;
@@ -547,6 +551,8 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
     const int m_off = PAIR ? BM * (int)rank : 0;    // this CTA's rows within the unit
     const int nb_off = PAIR ? B_COLS * (int)rank : 0;
 
+    if (warp < 4) {
+    if constexpr (REGS) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
     if (warp == 0) {
         // ================= TMA producer (the whole warp runs the loop; one elected lane issues)
         {
@@ -709,7 +715,9 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                 printf("tcmma cta %d: wait_tempty %.2f us, wait_full %.2f us (after the first k-block)\n", blockIdx.x,
                        wait_te / 1965.0, wait_full / 1965.0);
         }
-    } else if (warp >= 4 && warp < 12) {
+    }
+    } else {
+        if constexpr (REGS) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
         // ================= epilogue: 8 warps; warp -> (TMEM lane quarter q, column half h).  Each
         // chunk partial is read from TMEM and added into fp32 registers (IEEE round-to-nearest);
         // after the tile's last chunk the fused epilogue writes the row segment to global memory.
@@ -739,16 +747,20 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
             // 3xF16 dgrad with a ReLU bitmask: this tile's mask words are loaded before its accumulation (their
             // L2 latency hides behind the MMAs instead of stalling the store phase).  Word k of the rl group
             // (8 lanes) = (sub-tile k / 8, row group k % 8); lane jj holds words 2 jj and 2 jj + 1.
-            constexpr bool PRE_BITS = F16 && MASK && HALF == 64;
-            uint32_t mw0 = 0, mw1 = 0;
+            // (HALF = 128: 4 sub-tiles, words 4 jj .. 4 jj + 3)
+            constexpr bool PRE_BITS = F16 && MASK && (HALF == 64 || HALF == 128);
+            constexpr int NW = HALF / 32;  // mask words per lane
+            uint32_t mw[NW > 0 ? NW : 1];
+#pragma unroll
+            for (int e = 0; e < NW; e++) mw[e] = 0;
             if (PRE_BITS && p.mbits && p.splits == 1) {
                 const int rl8 = (lane & 31) >> 3, j8 = lane & 7;
 #pragma unroll
-                for (int e = 0; e < 2; e++) {
-                    const int k = 2 * j8 + e, m = m0 + 32 * q + (k % 8) * 4 + rl8, nc = n0 + 32 * (k / 8);
+                for (int e = 0; e < NW; e++) {
+                    const int k = NW * j8 + e, m = m0 + 32 * q + (k % 8) * 4 + rl8, nc = n0 + 32 * (k / 8);
                     uint32_t w = 0;
                     if (m < p.M && nc < p.N) w = __ldg(p.mbits + (int64_t)m * p.mbits_ld + (nc >> 5));
-                    if (e == 0) mw0 = w; else mw1 = w;
+                    mw[e] = w;
                 }
             }
             for (int c0 = kb0; c0 < kb1; c0 += L::CHUNK) {
@@ -804,7 +816,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
             const bool want_cols = F16 && p.fo.colpart && p.splits == 1;
             // 3xF16 lean fast path: a whole 32-row x 64-column piece in range, planes only (no fp32 copy, no split-K),
             // forward (bias + ReLU [+ bits]) or dgrad (bitmask [+ column sums]): no per-element bounds or mode tests
-            if constexpr (F16 && HALF == 64) {
+            if constexpr (F16 && (HALF == 64 || HALF == 128)) {
                 // output: the fp16 planes alone (lean), or the fp32 copy alone (a layer the SIMT head consumes)
                 const bool planes = p.fo.h != nullptr;
                 const bool fast = p.splits == 1 && (planes ? p.fo.skip_f32 : (p.C && (p.ldc & 3) == 0 && !p.C_hi)) &&
@@ -813,7 +825,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                                                             : (p.epi == EPI_BIAS_RELU && ((uintptr_t)p.bias & 15) == 0));
                 if (fast) {
 #pragma unroll
-                    for (int c = 0; c < 2; c++) {
+                    for (int c = 0; c < HALF / 32; c++) {
 #pragma unroll
                         for (int j = 0; j < 8; j++)
                             *(float4 *)(stg + lane * 32 + 4 * swz(lane, j)) =
@@ -830,7 +842,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                             float x[4] = {sv.x, sv.y, sv.z, sv.w};
                             if constexpr (MASK) {
                                 const int k = 8 * c + it;
-                                const uint32_t w = __shfl_sync(0xffffffffu, (k & 1) ? mw1 : mw0, rl * 8 + (k >> 1)) >> (4 * jj);
+                                const uint32_t w = __shfl_sync(0xffffffffu, mw[k % NW], rl * 8 + k / NW) >> (4 * jj);
 #pragma unroll
                                 for (int e = 0; e < 4; e++) x[e] = ((w >> e) & 1u) ? x[e] : 0.f;
                             } else {
@@ -900,7 +912,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                         const int m = m0 + 32 * q + (it0 + u) * RPI + rl;
                         if (PRE_BITS && p.mbits) {  // the preloaded word of (sub-tile c, row group it0 + u)
                             const int k = 8 * c + it0 + u;
-                            const uint32_t w = __shfl_sync(0xffffffffu, (k & 1) ? mw1 : mw0, rl * 8 + (k >> 1)) >> (n & 31);
+                            const uint32_t w = __shfl_sync(0xffffffffu, mw[k % NW], rl * 8 + k / NW) >> (n & 31);
                             mk[u] = make_float4((w & 1u) ? 1.f : 0.f, (w & 2u) ? 1.f : 0.f, (w & 4u) ? 1.f : 0.f,
                                                 (w & 8u) ? 1.f : 0.f);
                             continue;
@@ -1160,8 +1172,8 @@ bool tc_supports(TcGemm *t, const GemmDesc &g) {
 template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false>
 static cudaError_t prepare(TcGemm *t) {
     using L = SmemLayout<BN, SPLIT, PAIR, F16>;
-    const int slot = (SPLIT ? 1 : 0) + 2 * (BN == 128 ? 0 : BN == 64 ? 1 : 2) + (PAIR ? 8 : 0) + (MASK ? 16 : 0) +
-                     (F16 ? 32 : 0);
+    const int slot = (SPLIT ? 1 : 0) + 2 * (BN == 128 ? 0 : BN == 64 ? 1 : BN == 32 ? 2 : 3) + (PAIR ? 8 : 0) +
+                     (MASK ? 16 : 0) + (F16 ? 32 : 0);
     if (!t->attr_set[slot]) {
         cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
@@ -1264,6 +1276,10 @@ static int co_resident_pair_v(TcGemm *t, int variant, int cs) {
 // One instantiation per (variant, BN, PAIR, MASK) the planner can pick.
 template <bool SPLIT, bool F16>
 static cudaError_t launch_variant(TcGemm *t, const TcParams &p, int grid, cudaStream_t s, int BN, bool pair, bool mask) {
+    if constexpr (F16) {
+        if (pair && BN == 256)
+            return mask ? launch<256, SPLIT, true, true, F16>(t, p, grid, s) : launch<256, SPLIT, true, false, F16>(t, p, grid, s);
+    }
     if (pair && mask) return launch<128, SPLIT, true, true, F16>(t, p, grid, s);
     if (pair) return launch<128, SPLIT, true, false, F16>(t, p, grid, s);
     if (mask) {
@@ -1289,7 +1305,7 @@ static cudaError_t tc_gemm_impl(TcGemm *t, const GemmDesc &g, cudaStream_t s, La
     const int variant = f16 ? 2 : g.tf32x3 ? 1 : 0;
     const int KBE = f16 ? BKH : BK;  // elements per k-block
     const TcPlan plan = tc_plan(sms, M, N, K, f16);
-    const int BN = plan.bn;
+    int BN = plan.bn;
     // CTA pairs for large unsplit GEMMs: a 256 x 128 tile per pair halves B's per-SM operand traffic.
     // Pair MMAs also cost ~65 cycles with fresh operand tiles where a 1-CTA MMA of any N <= 128 costs ~89
     // (tools/mma_rate.cu, profiles/round2_tcgen05_rates.md); the dgrad pairs too (measured 84.0 -> 81.6 us at
@@ -1324,6 +1340,15 @@ static cudaError_t tc_gemm_impl(TcGemm *t, const GemmDesc &g, cudaStream_t s, La
             }
         }
     }
+    // 3xF16 unsplit pairs with enough 256-wide tiles to fill the SMs: 256 x 256 pair tiles (N = 256 MMAs).  Half the
+    // B bytes per flop: each 64 KB stage carries 2x the MMA time of a 48 KB one, so the 3-deep ring covers the L2/HBM
+    // latency the 4-deep 128-wide ring did not (the MMA phase waited on operands ~20 % of the time)
+    // Development knob MTX_TC_BN256=1: correct, measured slower (cfg4 forward 47.5 -> 51.4 us, dgrad 44.8 -> 46.8: 1.73
+    // rounds of 256-wide tiles run as 2, and each tile's store phase doubles behind a 2-deep TMEM ring)
+    static const int bn256_env = getenv("MTX_TC_BN256") ? atoi(getenv("MTX_TC_BN256")) : 0;
+    if (f16 && pair && !pair_cluster && pair_splits == 1 && BN == 128 && N % 256 == 0 && bn256_env == 1 &&
+        (int64_t)((M + 2 * BM - 1) / (2 * BM)) * (N / 256) * 2 >= sms)
+        BN = 256;
     TcParams p{};
     p.M = M; p.N = N; p.K = K;
     p.a_mn = g.ta ? 1 : 0;
