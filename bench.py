@@ -346,9 +346,9 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     tc_ok = "tcgen05" in mtx.mtx_build_info()
-    # auto: the fastest fp32-tier tensor-core mode measured for the workload: 3xF16 everywhere but
-    # cfg2, whose small latency-bound GEMMs run faster as 3xTF32
-    auto = (P.MTX_3XTF32 if args.config == "cfg2" else P.MTX_3XF16) if tc_ok else P.MTX_FP32
+    # auto: the fastest fp32-tier tensor-core mode measured for the workload: 3xF16 for cfg4's large
+    # GEMMs; 3xTF32 for the small latency-bound ones of cfg1-3 (the 3xF16 parameter quantize does not pay there)
+    auto = (P.MTX_3XF16 if args.config == "cfg4" else P.MTX_3XTF32) if tc_ok else P.MTX_FP32
     prec = {"fp32": P.MTX_FP32, "3xtf32": P.MTX_3XTF32, "3xf16": P.MTX_3XF16}.get(args.precision, auto)
     uid = P.nccl_uid_broadcast(rank, world)
     X, y = S.dataset(cfg)

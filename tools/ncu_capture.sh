@@ -7,5 +7,5 @@ tag=$1; shift
 cmd="python bench.py $* --no-cpu-baseline"
 $cmd > gpurun_out/ncu_plain_$tag.json 2> gpurun_out/ncu_plain_$tag.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$tag.csv $cmd > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k "regex:tc_gemm_kernel|avg_update|head_kernel|gemm_simt|conv_|colsum" -s 40 -c 6 -o gpurun_out/prof_$tag $cmd > gpurun_out/ncu_full_$tag.log 2>&1
+ncu --set full --clock-control none --import-source on -k "regex:tc_gemm_kernel|avg_update|head_kernel|gemm_simt|conv_|colsum|fwd_smallk|quantize_f16|wgrad_narrow" -s 40 -c 12 -o gpurun_out/prof_$tag $cmd > gpurun_out/ncu_full_$tag.log 2>&1
 echo "ncu done $tag"
