@@ -544,7 +544,9 @@ cudaError_t wgrad_narrow(const float *A, int64_t lda, RowSel arow, const float *
     (void)ticket;
     if (N > NW_MAXN) return cudaErrorInvalidValue;
     const int kb = (K_in + 1 + NW_T - 1) / NW_T;
-    int splits = std::max(1, std::min((4 * 148 + kb - 1) / kb, (rows + 31) / 32));
+    // ~8 CTAs of 4 warps per SM: each thread keeps 32 rows of loads in flight, so the bytes in flight (and the
+    // bandwidth of this load-bound kernel) scale with the CTAs resident (4 per SM: 3.2 TB/s at cfg4)
+    int splits = std::max(1, std::min((8 * 148 + kb - 1) / kb, (rows + 31) / 32));
     while (splits > 1 && (int64_t)splits * (K_in + 1) * N > partial_cap) splits--;
     const int rows_per = (rows + splits - 1) / splits;
     splits = (rows + rows_per - 1) / rows_per;
@@ -720,22 +722,23 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
     const float *Abase = A + arow.row0() * (int64_t)d;
     const int32_t *lab = labels + lrow.row0();
     float av[NV][4];
-    auto load_row = [&](int i) {  // features 4*lane + 128*t .. +3 of row i, all loads in flight
+    // features 4*lane + 128*t .. +3 of row i into dst, all loads in flight
+    auto load_row = [&](int i, float (&dst)[NV][4]) {
         const float *a = Abase + (int64_t)i * d;
 #pragma unroll
         for (int t = 0; t < NV; t++) {
             const int k = 4 * lane + 128 * t;
             if (VEC && k + 3 < d) {
                 const float4 v = __ldg((const float4 *)(a + k));
-                av[t][0] = v.x; av[t][1] = v.y; av[t][2] = v.z; av[t][3] = v.w;
+                dst[t][0] = v.x; dst[t][1] = v.y; dst[t][2] = v.z; dst[t][3] = v.w;
             } else {
 #pragma unroll
-                for (int u = 0; u < 4; u++) av[t][u] = (k + u < d) ? __ldg(a + k + u) : 0.f;
+                for (int u = 0; u < 4; u++) dst[t][u] = (k + u < d) ? __ldg(a + k + u) : 0.f;
             }
         }
     };
     const int i_first = blockIdx.x * HEAD_WARPS + warp;
-    if (i_first < rows) load_row(i_first);  // in flight while W_L is staged
+    if (i_first < rows) load_row(i_first, av);  // in flight while W_L is staged
     // row k of W_L (C weights; k == d is the bias row) -> column k of sWt, k in [d+1, dp) zeroed:
     // R rows per thread in flight, consecutive k across the warp (conflict-free stores), no
     // index division (it cost ~700 instructions per warp when it was e -> (e % C, e / C))
@@ -763,7 +766,7 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32) head_kernel(int rows, int d, 
 #pragma unroll
     for (int t = 0; t < NV; t++) hcs[t][0] = hcs[t][1] = hcs[t][2] = hcs[t][3] = 0.f;
     for (int i = i_first; i < rows; i += gridDim.x * HEAD_WARPS) {
-        if (i != i_first) load_row(i);
+        if (i != i_first) load_row(i, av);
         float z[HEAD_MAXC];
 #pragma unroll
         for (int j = 0; j < HEAD_MAXC; j++) z[j] = 0.f;
