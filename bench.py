@@ -142,7 +142,7 @@ def kernel_work(name: str):
 
 
 def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: str):
-    """Dominant kernel class (by total device time) -> achieved / peak.
+    """Dominant kernel launch (one kernel at one shape/plan, by total device time per step) -> achieved / peak.
 
     Each kernel's event pair inside the timing graph also spans the graph's per-node launch
     latency; the timing graph brackets an empty kernel the same way ("launch_overhead") and that
@@ -161,9 +161,20 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
             g["work"] += w[1] * cnt
             g["unit"], g["bound"] = w[0], w[2]
     total = sum(g["ms"] for g in groups.values())
-    # kernels without algorithmic work (peer_barrier: a cross-GPU wait) are not roofline candidates
-    worked = {k: g for k, g in groups.items() if g["bound"]} or groups
-    top_name, top = max(worked.items(), key=lambda kv: kv[1]["ms"])
+    # the dominant LAUNCH (kernel + shape): a class mixes shapes whose rates differ (cfg4's 28-row weight gradient
+    # runs the same kernel as the 1024-row ones at a fraction of the rate); kernels without algorithmic work
+    # (peer_barrier: a cross-GPU wait) are not roofline candidates
+    launches = {}
+    for name, (ms, cnt) in timing.items():
+        w = kernel_work(name)
+        if w:
+            launches[name] = {"ms": ms, "cnt": cnt, "work": w[1] * cnt, "unit": w[0], "bound": w[2]}
+    if launches:
+        top_launch, top = max(launches.items(), key=lambda kv: kv[1]["ms"])
+        top_name = top_launch.split("[")[0]
+    else:
+        top_name, top = max(groups.items(), key=lambda kv: kv[1]["ms"])
+        top_launch = top_name
     per_launch_s = top["ms"] / 1e3 / top["cnt"]
     per_launch_work = top["work"] / top["cnt"]
     # every kernel of the timing pass runs alone (serialised graph): the burst peaks apply
@@ -191,7 +202,7 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
     # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
     # (profiles/ncu_traffic.json, written by tools/ncu_summary.py), averaged over its captured launches
     # the tensor-core GEMM's template is <N tile, 3xTF32>: take the N tile of the group's longest launch
-    longest = max((kv for kv in timing.items() if kv[0].split("[")[0] == top_name), key=lambda kv: kv[1][0])[0]
+    longest = top_launch
     bn = re.search(r"bn=(\d+)", longest)
     bn = bn.group(1) if bn else "128"
     pr = re.search(r"pair=(\d)", longest)
@@ -213,7 +224,8 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
             meta = tj.get("_meta", {}).get(config, {})
             traffic_src = f"profiles/ncu_traffic.json [{hit}] from {meta.get('capture', 'ncu --set full')}" \
                           f" at commit {meta.get('commit', '?')}"
-    return {"kernel": top_name, "bound": top["bound"], "achieved": round(achieved, 3), "peak": round(peak, 1),
+    return {"kernel": top_name, "launch": top_launch, "bound": top["bound"], "achieved": round(achieved, 3),
+            "peak": round(peak, 1),
             "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
             "peak_kind": {"GB/s": "measured copy" if top["bound"] == "hbm" else "measured NVLink peer copy per direction",
                           "TFLOP/s": ("measured bf16 burst (= f16 dense) / 3 (3xF16: three f16 MMAs per product)"
@@ -221,7 +233,7 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
                                       "measured bf16 burst x tf32/bf16 nominal ratio" +
                                       (" / 3 (3xTF32)" if top_name.startswith("gemm_tc3x") else ""))}.get(unit),
             "work_per_launch": per_launch_work, "launch_us": round(per_launch_s * 1e6, 3),
-            "share_of_kernel_time": round(top["ms"] / total, 3),
+            "share_of_kernel_time": round(top["ms"] / total, 3),  # this launch shape's share of the step's kernel time
             "launch_overhead_us_subtracted": round(over_ms * 1e3, 3),
             "breakdown_us_per_step": {k: round(g["ms"] * 1e3 / steps, 2) for k, g in
                                       sorted(groups.items(), key=lambda kv: -kv[1]["ms"])},

@@ -171,6 +171,14 @@ cudaError_t fwd_smallk(int M, int N, int K, const float *A, int64_t lda, RowSel 
                        const float *bias, bool relu, float *C, int64_t ldc, const F16Out &fo, cudaStream_t s,
                        LaunchHook *h);
 
+// Weight gradient of a layer with K_in <= 32 input features (cfg4's first layer) on the CUDA cores:
+// dW[k][n] = sum_i X[i][k] dZ[i][n] (rows of X from xrow), dZ fp32 or its 3xF16 planes (dzh/dzl, pitch lddz, slot
+// dzs); per-CTA partials (<= partial_cap floats) folded in order into dW [K_in][N] (the bias row is separate).
+bool wgrad_smallm_supported(int K_in, int N);
+cudaError_t wgrad_smallm(int rows, int K_in, int N, const float *X, int64_t ldx, RowSel xrow, const float *dZ,
+                         const __half *dzh, const __half *dzl, int64_t lddz, const TScale *dzs, float *dW, float *partial,
+                         int64_t partial_cap, cudaStream_t s, LaunchHook *h);
+
 // out = sum_{i ascending in a fixed tree} v[i] (one block; deterministic).
 cudaError_t reduce_sum(const float *v, int n, float *out, cudaStream_t s, LaunchHook *h);
 

@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(Q_T) quantize_f16_kernel(const __grid_constant
     } else if (a.ax) {
         const bool v4 = ((uintptr_t)a.ax & 15) == 0;
         const int64_t n4 = v4 ? a.an / 4 : 0;
+#pragma unroll 4
         for (int64_t i = tid; i < n4; i += nth) {
             const float4 v = __ldg((const float4 *)a.ax + i);
             m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
@@ -362,17 +363,32 @@ __global__ void __launch_bounds__(Q_T) quantize_f16_kernel(const __grid_constant
                         ((uintptr_t)g.hi & 7) == 0 && ((uintptr_t)g.lo & 7) == 0;
         if (v4 && g.rows * (g.cols / 4) < (1ll << 31)) {  // 32-bit index math (a 64-bit division per group was the cost)
             const unsigned c4 = (unsigned)(g.cols / 4), tot = (unsigned)(g.rows * c4);
-            for (unsigned i = (unsigned)tid; i < tot; i += (unsigned)nth) {
-                const unsigned rq = i / c4;
-                const int64_t r = rq, c = 4 * (int64_t)(i - rq * c4);
-                const float4 v = __ldg((const float4 *)(g.x + r * g.ld + c));
-                uint16_t h[4], l[4];
-                split_f16(v.x, inv, h[0], l[0]);
-                split_f16(v.y, inv, h[1], l[1]);
-                split_f16(v.z, inv, h[2], l[2]);
-                split_f16(v.w, inv, h[3], l[3]);
-                *(uint2 *)(g.hi + r * g.pld + c) = make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
-                *(uint2 *)(g.lo + r * g.pld + c) = make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
+            // 4 groups per thread per iteration, all 4 loads issued first (one load in flight per thread left this
+            // pass latency-bound: 12 us for cfg4's 12.7 MB of parameters)
+            constexpr int QU = 4;
+            for (unsigned i0 = (unsigned)tid; i0 < tot; i0 += QU * (unsigned)nth) {
+                float4 v[QU];
+                int64_t ro[QU], co[QU];
+#pragma unroll
+                for (int u = 0; u < QU; u++) {
+                    const unsigned i = i0 + u * (unsigned)nth;
+                    const unsigned rq = i / c4;
+                    ro[u] = rq;
+                    co[u] = 4 * (int64_t)(i - rq * c4);
+                    if (i < tot) v[u] = __ldg((const float4 *)(g.x + ro[u] * g.ld + co[u]));
+                }
+#pragma unroll
+                for (int u = 0; u < QU; u++) {
+                    if (i0 + u * (unsigned)nth >= tot) break;
+                    uint16_t h[4], l[4];
+                    split_f16(v[u].x, inv, h[0], l[0]);
+                    split_f16(v[u].y, inv, h[1], l[1]);
+                    split_f16(v[u].z, inv, h[2], l[2]);
+                    split_f16(v[u].w, inv, h[3], l[3]);
+                    const int64_t r = ro[u], c = co[u];
+                    *(uint2 *)(g.hi + r * g.pld + c) = make_uint2(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16));
+                    *(uint2 *)(g.lo + r * g.pld + c) = make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
+                }
             }
         } else {
             for (int64_t i = tid; i < g.rows * g.cols; i += nth) {

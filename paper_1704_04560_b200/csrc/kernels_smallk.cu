@@ -8,6 +8,8 @@
 // fp32 FMAs in ascending k (a K-term chain: the fp32 tier), ~6 us of FMA issue at this shape.
 #include <stdio.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace mtx {
@@ -174,6 +176,118 @@ cudaError_t fwd_smallk(int M, int N, int K, const float *A, int64_t lda, RowSel 
     launch_pdl(kern, grid, dim3(SK_T), smem, s, M, N, K, A, lda, arow, W, ldw, bias, relu ? 1 : 0, C, ldc, fo);
     if (h) h->after(name, s);
     return cudaGetLastError();
+}
+
+}  // namespace mtx
+
+// ------------------------------------------------------------------ weight gradient of a short-K_in layer
+// dW[k][n] = sum_i X[i][k] dZ[i][n] for k < K_in <= 32 (cfg4's first layer: 28 features, K = b samples): the
+// tensor-core tile would be 28 useful rows of 128.  CUDA cores: a CTA owns 128 columns and a contiguous row range;
+// 32-row chunks of dZ (fp32, or rebuilt exactly from its 3xF16 planes: s * (hi + lo) is exact in fp32) and of X are
+// staged in shared memory; thread (cg, kg) accumulates k = 4 kg .. 4 kg + 3 x n = 4 cg .. 4 cg + 3 over the rows in
+// ascending order.  Per-CTA partials [split][K_in * N], folded in split order (colpart_fold): deterministic.
+namespace mtx {
+namespace {
+constexpr int WS_N = 128, WS_R = 32, WS_T = 256;
+
+__global__ void __launch_bounds__(WS_T) wgrad_smallm_kernel(int rows, int K_in, int N, const float *__restrict__ X,
+                                                           int64_t ldx, RowSel xrow, const float *__restrict__ dZ,
+                                                           const __half *__restrict__ dzh, const __half *__restrict__ dzl,
+                                                           int64_t lddz, const TScale *dzs, int rows_per,
+                                                           float *__restrict__ partial) {
+    pdl_wait();
+    __shared__ __align__(16) float sz[WS_R][WS_N];
+    __shared__ __align__(16) float sx[WS_R][33];
+    const int n0 = blockIdx.x * WS_N, r0 = blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
+    const int cg = threadIdx.x & 31, kg = threadIdx.x >> 5;  // 32 column groups x 8 k groups
+    const float s = dzh ? dzs->scale : 1.f;
+    const float *Xb = X + xrow.row0() * ldx;
+    float acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) acc[a][b] = 0.f;
+    for (int i0 = r0; i0 < r1; i0 += WS_R) {
+        const int nr = min(WS_R, r1 - i0);
+        // stage dZ rows (4 columns per thread-iteration) and X rows (unrolled: all of a thread's loads in flight)
+#pragma unroll
+        for (int e = threadIdx.x; e < WS_R * (WS_N / 4); e += WS_T) {
+            const int r = e / (WS_N / 4), c4 = 4 * (e % (WS_N / 4)), n = n0 + c4;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (r < nr && n + 3 < N) {
+                const int64_t off = (int64_t)(i0 + r) * lddz + n;
+                if (dzh) {
+                    const uint2 h = __ldg((const uint2 *)(dzh + off)), l = __ldg((const uint2 *)(dzl + off));
+                    const float2 h0 = __half22float2(*(const __half2 *)&h.x), h1 = __half22float2(*(const __half2 *)&h.y);
+                    const float2 l0 = __half22float2(*(const __half2 *)&l.x), l1 = __half22float2(*(const __half2 *)&l.y);
+                    v = make_float4((h0.x + l0.x) * s, (h0.y + l0.y) * s, (h1.x + l1.x) * s, (h1.y + l1.y) * s);
+                } else {
+                    v = __ldg((const float4 *)(dZ + off));
+                }
+            } else if (r < nr) {
+                float t[4];
+                for (int u = 0; u < 4; u++) {
+                    t[u] = 0.f;
+                    if (n + u < N) {
+                        const int64_t off = (int64_t)(i0 + r) * lddz + n + u;
+                        t[u] = dzh ? (__half2float(dzh[off]) + __half2float(dzl[off])) * s : dZ[off];
+                    }
+                }
+                v = make_float4(t[0], t[1], t[2], t[3]);
+            }
+            *(float4 *)&sz[r][c4] = v;
+        }
+#pragma unroll
+        for (int e = threadIdx.x; e < WS_R * 32; e += WS_T) {
+            const int r = e >> 5, k = e & 31;
+            sx[r][k] = (r < nr && k < K_in) ? __ldg(Xb + (int64_t)(i0 + r) * ldx + k) : 0.f;
+        }
+        __syncthreads();
+        for (int r = 0; r < nr; r++) {
+            const float4 z = *(const float4 *)&sz[r][4 * cg];
+            const float zz[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+            for (int a = 0; a < 4; a++) {
+                const float x = sx[r][4 * kg + a];
+#pragma unroll
+                for (int b = 0; b < 4; b++) acc[a][b] = __fmaf_rn(x, zz[b], acc[a][b]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+        const int k = 4 * kg + a;
+        if (k >= K_in) continue;
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const int n = n0 + 4 * cg + b;
+            if (n < N) partial[(int64_t)blockIdx.y * K_in * N + (int64_t)k * N + n] = acc[a][b];
+        }
+    }
+}
+}  // namespace
+
+bool wgrad_smallm_supported(int K_in, int N) { return K_in >= 1 && K_in <= 32 && N >= 1; }
+
+cudaError_t wgrad_smallm(int rows, int K_in, int N, const float *X, int64_t ldx, RowSel xrow, const float *dZ,
+                         const __half *dzh, const __half *dzl, int64_t lddz, const TScale *dzs, float *dW, float *partial,
+                         int64_t partial_cap, cudaStream_t s, LaunchHook *h) {
+    const int nb = (N + WS_N - 1) / WS_N;
+    int splits = std::max(1, std::min((3 * 148 + nb - 1) / nb, (rows + WS_R - 1) / WS_R));
+    while (splits > 1 && (int64_t)splits * K_in * N > partial_cap) splits--;
+    int rows_per = (rows + splits - 1) / splits;
+    rows_per = (rows_per + WS_R - 1) / WS_R * WS_R;
+    splits = (rows + rows_per - 1) / rows_per;
+    char name[80];
+    snprintf(name, sizeof name, "wgrad_smallm[M=%d,N=%d,K=%d,splits=%d]", K_in, N, rows, splits);
+    if (h) h->before(name, s);
+    launch_pdl(wgrad_smallm_kernel, dim3(nb, splits), dim3(WS_T), 0, s, rows, K_in, N, X, ldx, xrow, dZ, dzh, dzl, lddz,
+               dzs, rows_per, partial);
+    if (h) h->after(name, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return colpart_fold(partial, splits, K_in * N, dW, s, h);
 }
 
 }  // namespace mtx

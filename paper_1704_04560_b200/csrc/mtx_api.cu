@@ -606,6 +606,12 @@ mtx_status quantize_buffer(mtx_ctx *c, const float *buf, int64_t rows, int64_t c
     return MTX_OK;
 }
 bool fused_overlap();
+// Development knob MTX_SMALLM=1: the CUDA-core weight gradient of a <= 32-input layer (kernels_smallk.cu) instead of
+// the tensor-core split-K GEMM (measured slower at cfg4: 34 + 6 us against 26 + 2)
+bool smallm_on() {
+    static const bool v = getenv("MTX_SMALLM") && atoi(getenv("MTX_SMALLM")) == 1;
+    return v;
+}
 // 3xF16 at P > 1 with the one-launch fused update: it leaves the per-rank maxima of the updated weights
 bool wmax_fused(const mtx_ctx *c) { return c->f16 && c->world > 1 && c->fused && c->wmax && !fused_overlap(); }
 // 3xF16 parameter planes (one scale over the whole flat buffer, biases included: it bounds every bias
@@ -878,6 +884,20 @@ struct Runner {
             cudaError_t e = wgrad_narrow(A, L.rows_w, arow, dZ, (int)c->b, L.rows_w, L.cols, c->grads + L.pad_off,
                                          part(), c->partial_floats, ctrs() + 254, s, h);
             if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "wgrad_narrow: %s", cudaGetErrorString(e));
+            return MTX_OK;
+        }
+        PlaneView zv;
+        if (c->f16 && wgrad_smallm_supported(L.rows_w, L.cols) && plane_view(c, dZ, &zv) && smallm_on()) {
+            // 3xF16, a layer with <= 32 inputs (cfg4's first): CUDA cores from dZ's planes (kernels_smallk.cu); the
+            // bias row from the column partials of the (lean) dZ, else its column sums
+            cudaError_t e = wgrad_smallm((int)c->b, L.rows_w, L.cols, A, L.rows_w, arow, dZ, zv.h, zv.l, zv.pld, zv.ts,
+                                         c->grads + L.pad_off, part(), c->partial_floats, s, h);
+            if (e == cudaSuccess) {
+                float *db = c->grads + L.pad_off + (int64_t)L.rows_w * L.cols;
+                e = dz_cp ? colpart_fold(dz_cp, dz_cp_rows, L.cols, db, s, h)
+                          : colsum(dZ, (int)c->b, L.cols, L.cols, db, part(), c->partial_floats, ctrs() + 256, s, h);
+            }
+            if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "wgrad_smallm: %s", cudaGetErrorString(e));
             return MTX_OK;
         }
         bias_cp = dz_cp;
