@@ -83,8 +83,10 @@ template <bool HAS_V, int U, int PM>  // PM: peers the arrays hold (P <= PM)
 __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, int rank, int bucket,
                                                          const uint64_t *stepctr, int64_t lo4, int64_t hi4, float invP,
                                                          float lr, float mu, int *flag, int64_t *win, int64_t B,
-                                                         int64_t n_data, int64_t loss_idx, int track_wmax) {
+                                                         int64_t n_data, int64_t loss_idx, int track_wmax, int dbg_ts) {
     pdl_wait();
+    uint64_t t_in = 0, t_go = 0;
+    if (dbg_ts && threadIdx.x == 0) t_in = globaltimer();
     __shared__ int go;
     __shared__ float red[16];
     float wmax = 0.f;
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, i
     }
     __syncthreads();
     if (!go) return;  // a peer timed out: load and store nothing (the context is poisoned at the next sync)
+    if (dbg_ts && threadIdx.x == 0) t_go = globaltimer();
     bool bad = false;
     // U float4 per peer per thread in flight (U*P loads over NVLink: the kernel is latency-bound on them), then the
     // ascending-rank fold, the update and w to every replica
@@ -167,6 +170,12 @@ __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, i
             pp.G[rank][loss_idx + 1] = L;
         }
         if (win) *win = (*win + B) % n_data;
+    }
+    if (dbg_ts) {  // development (MTX_FUSED_TS=1): flag wait vs reduction work of CTAs 0 and the last
+        __syncthreads();
+        if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+            printf("fusedts rank %d cta %d: wait %.2f us, work %.2f us\n", rank, blockIdx.x, (t_go - t_in) * 1e-3,
+                   (globaltimer() - t_go) * 1e-3);
     }
 }
 
@@ -275,11 +284,12 @@ cudaError_t fused_bucket_update(const PeerPtrs &pp, int P, int rank, int bucket,
     snprintf(name, sizeof name, "fused_avg_update[n=%lld,P=%d,v=%d]", (long long)(hi - lo), P, has_v ? 1 : 0);
     if (h) h->before(name, s);
     const float invP = 1.0f / (float)P;
+    static const int dbg_ts = getenv("MTX_FUSED_TS") ? atoi(getenv("MTX_FUSED_TS")) : 0;
     // 4 float4 per peer in flight up to P = 4 (16 loads per thread), 2 beyond (register budget)
     auto kern = P <= 4 ? (has_v ? fused_bucket_kernel<true, 4, 4> : fused_bucket_kernel<false, 4, 4>)
                        : (has_v ? fused_bucket_kernel<true, 2, MAX_PEERS> : fused_bucket_kernel<false, 2, MAX_PEERS>);
     launch_pdl(kern, dim3(std::max(1, ctas)), dim3(512), 0, s, pp, P, rank, bucket, stepctr, a / 4, b / 4, invP, lr, mu,
-               flag, win, B, n_data, loss_idx, (track_wmax && pp.wmax[0]) ? 1 : 0);
+               flag, win, B, n_data, loss_idx, (track_wmax && pp.wmax[0]) ? 1 : 0, dbg_ts);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }
