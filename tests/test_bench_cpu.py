@@ -61,6 +61,21 @@ def test_roofline_skips_kernels_without_work():
     assert "peer_barrier" in r["breakdown_us_per_step"]
 
 
+def test_roofline_takes_the_dominant_launch_not_the_class():
+    """cfg4's 28-row weight gradient shares the kernel class with the 1024-row ones at a fraction of their rate:
+    the roofline is the launch (kernel + shape) with the most device time, rated on its own work."""
+    b = _bench()
+    big = "gemm_tc3xf16_wgrad[M=1024,N=1024,K=8192,splits=2,cluster=1,pair=1,bn=128]"
+    small = "gemm_tc3xf16_wgrad[M=28,N=1024,K=8192,splits=16,cluster=0,pair=0,bn=128]"
+    timing = {big: (3.0, 60), small: (0.52, 20),
+              "gemm_tc3xf16_fwd[M=8192,N=1024,K=1024,splits=1,cluster=0,pair=1,bn=128]": (2.8, 60)}
+    pk = {"hbm_gbs": 6550.0, "bf16_tflops": 1650.0, "bf16_tflops_sustained": 1500.0}
+    r = b.roofline(timing, pk, 1965.0, 20, "cfg4")
+    assert r["launch"] == big and r["kernel"] == "gemm_tc3xf16_wgrad" and r["bound"] == "tensor"
+    assert abs(r["achieved"] - 2 * 1024 * 1024 * 8192 / (3.0e-3 / 60) / 1e12) < 1e-3
+    assert abs(r["peak"] - 1650.0 / 3) < 0.1  # three f16 MMAs per product against the f16 (= bf16) dense peak
+
+
 def test_reference_arm_prints_one_json_line():
     """`--impl reference` times the oracle on host cores and prints the contract's line, alone on stdout."""
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
