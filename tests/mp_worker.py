@@ -105,10 +105,15 @@ def main():
         precisions = [P.MTX_FP32] + ([P.MTX_3XTF32, P.MTX_3XF16] if "tcgen05" in mtx.mtx_build_info() else [])
         for prec in precisions:
             tol, gtol = TOL[prec], GRAD_TOL[prec]
-            for name, B, steps in (("cfg1", 64, 5), ("cfg2", 512, 3), ("cfg3", 64, 2)):
+            runs = [("cfg1", 64, 5), ("cfg2", 512, 3), ("cfg3", 64, 2)]
+            if prec == P.MTX_3XF16:  # cfg4's shape: the 28-feature CUDA-core forward, lean outputs, fused maxima
+                runs.append(("cfg4", 512, 2))
+            for name, B, steps in runs:
                 cfg = dict(S.CONFIGS[name], B=B)
                 if name == "cfg3":
                     X, y = S.cifar_like(1, 300)
+                elif name == "cfg4":
+                    X, y = S.higgs_like(1, 2048)
                 else:
                     X, y = S.mnist_like(1, 1000 if name == "cfg1" else 4096)
                 gpu = run_model(rank, world, cfg, X, y, steps, prec)
@@ -179,9 +184,11 @@ def main():
 
         # ---- FUSED (NVLink peer-memory reduce + update) is bit-exact with ORDERED (same rank-ordered fold)
         for prec in ([P.MTX_FP32, P.MTX_3XTF32, P.MTX_3XF16] if "tcgen05" in mtx.mtx_build_info() else [P.MTX_FP32]):
-            for name, B, n in (("cfg1", 64, 1000), ("cfg2", 512, 4096)):
+            # 3xF16 + cfg4's shape: the fused update's per-rank maxima give the same parameter planes as ORDERED's
+            # own max pass
+            for name, B, n in (("cfg1", 64, 1000), ("cfg2", 512, 4096)) + ((("cfg4", 512, 2048),) if prec == P.MTX_3XF16 else ()):
                 cfg = dict(S.CONFIGS[name], B=B)
-                X, y = S.mnist_like(1, n)
+                X, y = S.higgs_like(1, n) if name == "cfg4" else S.mnist_like(1, n)
                 a = run_model(rank, world, cfg, X, y, 3, prec, P.MTX_REDUCE_ORDERED)
                 b = run_model(rank, world, cfg, X, y, 3, prec, P.MTX_REDUCE_FUSED)
                 for t, ((la, Ga, wa, va), (lb, Gb, wb, vb)) in enumerate(zip(a, b)):
