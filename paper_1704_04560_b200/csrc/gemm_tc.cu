@@ -101,6 +101,7 @@ struct TcParams {
     const uint32_t *mbits;
     int64_t mbits_ld;
     int pf;  // producer: L2 prefetch distance in k-blocks (0: off)
+    int pfb; // before the PDL wait: L2 prefetch of the CTA's first B k-blocks (forward / dgrad: the weights)
     int mc;  // PAIR: 4-CTA clusters of two pairs on adjacent N tiles; each A plane is loaded once and multicast
 };
 
@@ -533,6 +534,26 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
     if (PAIR) cluster_sync_all();  // the peer's barriers exist before any TMA / arrive targets them
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Before waiting on the previous kernel: pull this CTA's first B k-blocks into L2.  B of a forward / dgrad is the
+    // weights (written steps ago); a prefetch is only a hint (L2 is coherent), so it is safe whatever produced B.
+    if (warp == 0 && !(p.dbg & 2) && p.pfb) {
+        int z0, r0;
+        const int t0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+        if (t0 < p.tiles_m * p.tiles_n * p.splits) {
+            unit_of(p, t0, p.tiles_m * p.tiles_n, z0, r0);
+            const int n0 = (r0 % p.tiles_n) * BN + (PAIR ? (BN / 2) * (int)(crank & 1) : 0);
+            const int kb0 = z0 * p.kb_per_split, kb1 = min(p.kb_total, kb0 + min(p.kb_per_split, L::STAGES));
+            constexpr int KBP = F16 ? BKH : BK, CHP = F16 ? 64 : 32;
+            for (int kb = kb0; kb < kb1; kb++) {
+#pragma unroll
+                for (int plane = 0; plane < (SPLIT ? 2 : 1); plane++) {
+                    const CUtensorMap *mb = plane ? &p.tb_lo : &p.tb;
+                    if (!p.b_mn) tma_prefetch_2d_elect(mb, kb * KBP, n0);
+                    else if (p.b_3d) tma_prefetch_3d_elect(mb, 0, kb * KBP, n0 / CHP);
+                }
+            }
+        }
+    }
     pdl_wait();  // prologue above overlaps the previous kernel's tail (programmatic launch)
     if (threadIdx.x == 0) stamp(1);
     // 256-wide pair tiles: 128 promoted accumulators per epilogue thread.  The producer / MMA / allocator warpgroup
@@ -1436,6 +1457,9 @@ static cudaError_t tc_gemm_impl(TcGemm *t, const GemmDesc &g, cudaStream_t s, La
     // L2 prefetch distance: one ring ahead of the loads (development knob MTX_TC_PF: 0 disables, n = distance)
     static const int pf_env = getenv("MTX_TC_PF") ? atoi(getenv("MTX_TC_PF")) : -1;
     p.pf = pf_env >= 0 ? pf_env : 0;  // measured slower at 4 and 8 (cfg4 506 -> 635 / 608 us/step): off
+    // development knob MTX_TC_PFB=1: measured slightly slower (cfg4 525.3 -> 529.5 us/step)
+    static const int pfb_env = getenv("MTX_TC_PFB") ? atoi(getenv("MTX_TC_PFB")) : 0;
+    p.pfb = (pfb_env && !g.ta) ? 1 : 0;  // forward / dgrad (B = weights); a weight gradient's B is the fresh dZ
     p.epi = g.epi;
     p.bias = g.bias;
     p.mask = g.mask;
