@@ -215,6 +215,19 @@ def test_ragged_mlp_one_step(precision):
     _check_step(cfg, X, y, precision, 4, start)
 
 
+@pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("dims,B", [([20, 72, 96, 3], 75), ([28, 200, 136, 2], 300)])
+def test_short_input_mlp_ragged(precision, dims, B):
+    """A <= 64-feature input layer feeding tensor-core GEMMs (3xF16: the CUDA-core fwd_smallk forward with planes and
+    ReLU bits) with ragged rows and a ragged last column block, and the lean hidden tensors after it."""
+    cfg = dict(kind="mlp", dims=dims, data="higgs", n=B + 200, B=B, lr=0.05, mu=0.9)
+    rng = np.random.default_rng(sum(dims) + B)
+    X = rng.standard_normal((B + 200, dims[0])).astype(np.float32)
+    y = rng.integers(0, dims[-1], B + 200).astype(np.int32)
+    start = oracle.init_params(oracle.Net.from_cfg(cfg), 42)
+    _check_step(cfg, X, y, precision, 3, start)
+
+
 @pytest.mark.parametrize("precision", PRECISIONS[1:] or PRECISIONS)
 @pytest.mark.parametrize("C,d,B", [(10, 71, 75), (2, 71, 75), (10, 64, 2100), (2, 33, 2100), (1, 40, 75),
                                    (5, 130, 75), (16, 129, 75)])
