@@ -131,6 +131,8 @@ def kernel_work(name: str):
     if kind == "fused_avg_update":  # NVLink-bound: per direction per GPU, the P-1 peers'
         # gradients of the owned n/P slice come in and the P-1 peers' updated w slices are stored in
         P = a["P"]
+        if a.get("push"):  # push protocol: the peers' gradients already landed locally (copy engines, during the
+            return "byte", 4 * (a["n"] // P) * (P - 1), "nvlink"  # backward); only the w slices go out
         return "byte", 8 * (a["n"] // P) * (P - 1), "nvlink"
     if kind == "head_softmax_xent":  # read A rows, write dZ_{L-1} (and dZ_L, loss)
         return "byte", 4 * a["rows"] * (a["d"] * (1 + a["dgrad"]) + a["C"] + 1), "hbm"

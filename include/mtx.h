@@ -301,15 +301,20 @@ mtx_status mtx_debug_gemm(mtx_ctx *ctx, int32_t engine, int32_t M, int32_t N, in
  *  g[q], G[q]: device buffers of n + 32 floats per simulated rank q (the local gradient g_q with its
  *              loss sum at index n; G_q receives the reduced sum); w[q], v[q]: n floats (v may be NULL
  *              when momentum == 0).  n % 4 == 0, 16-byte aligned; all borrowed, updated in place.
- *  mode MTX_REDUCE_FUSED:   the product's peer-memory protocol -- per simulated rank, on P concurrent
- *              streams: peer_barrier, fused_avg_update of the rank's owned slice (ascending-rank fold,
- *              x fl(1/P), momentum update, w stored to every replica; v_q and G_q written on slice q
- *              only; the folded loss to G_q[n + 1]), peer_barrier.
+ *  mode MTX_REDUCE_FUSED:   the product's peer-memory protocol (pull) -- per simulated rank, on P
+ *              concurrent streams: the fused kernel (publish "ready", wait for every rank, ascending-rank
+ *              fold of the owned slice over the ranks' g, x fl(1/P), momentum update, w stored to every
+ *              replica; v_q and G_q written on slice q only; the folded loss to G_q[n + 1]), peer_barrier.
+ *  mode MTX_REDUCE_FUSED | MTX_DEBUG_REDUCE_PUSH: the push protocol (the default of a P > 1 FUSED
+ *              step): each rank's copy-engine copies of g into every owner's landing area + its
+ *              "landed" flags, then the same fused kernel reading the owned slice's gradients from the
+ *              landing area, peer_barrier.  Same results, bit for bit.
  *  mode MTX_REDUCE_ORDERED: every simulated rank folds all g_q in ascending rank order into G_r
  *              (the loss slot included) and updates its own (w_r, v_r) with x fl(1/P).
  *  other modes: MTX_ERR_UNSUPPORTED (their sum is NCCL's arithmetic on P GPUs).
  * Asynchronous on `stream`; a non-finite average sets the numeric flag (MTX_ERR_NUMERIC at the next
  * synchronising call). */
+#define MTX_DEBUG_REDUCE_PUSH 0x100
 mtx_status mtx_debug_reduce(mtx_ctx *ctx, int32_t mode, int32_t P, void *const *g, void *const *w, void *const *v,
                             void *const *G, uint64_t n, float lr, float momentum, void *stream);
 

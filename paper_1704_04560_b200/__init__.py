@@ -11,7 +11,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import mtx
-from .mtx import (MTX_3XF16, MTX_3XTF32, MTX_BUF_GRADS, MTX_BUF_PARAMS, MTX_BUF_VELOCITY, MTX_FP32,  # noqa: F401
+from .mtx import (MTX_3XF16, MTX_3XTF32, MTX_BUF_GRADS, MTX_DEBUG_REDUCE_PUSH, MTX_BUF_PARAMS, MTX_BUF_VELOCITY, MTX_FP32,  # noqa: F401
                   MTX_REDUCE_FUSED, MTX_REDUCE_LAYERWISE, MTX_REDUCE_NCCL, MTX_REDUCE_ORDERED, MTX_REDUCE_ZERO1,
                   MTX_TF32, MtxError)
 

@@ -30,6 +30,12 @@
 namespace mtx {
 namespace {
 
+// Phase timestamps and MMA-warp stall counters (MTX_TC_DBG & 4) exist only in a trace build (-DMTX_TRACE=1): their
+// printf gave every GEMM variant a stack frame and cost the small latency-bound GEMMs ~2-4 us per launch (cfg2)
+#ifndef MTX_TRACE
+#define MTX_TRACE 0
+#endif
+constexpr bool TRACE = MTX_TRACE != 0;
 #ifndef MTX_F16_CHUNK
 #define MTX_F16_CHUNK 4
 #endif
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
     // development (MTX_TC_DBG & 4): %globaltimer at the phases of CTA 0 and the last CTA, printed at exit
     __shared__ uint64_t dts[8];
     auto stamp = [&](int i) {
-        if (p.dbg & 4) {
+        if (TRACE && (p.dbg & 4)) {
             uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             dts[i] = t;
@@ -684,15 +690,15 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                 const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
                 for (int c0 = kb0; c0 < kb1; c0 += L::CHUNK) {
                     const int c1 = min(kb1, c0 + L::CHUNK);
-                    long long w0 = (p.dbg & 4) ? clock64() : 0;
+                    long long w0 = (TRACE && (p.dbg & 4)) ? clock64() : 0;
                     mbar_wait(tempty0 + 8 * buf, buf_phase ^ 1);
-                    if (p.dbg & 4) wait_te += clock64() - w0;
+                    if (TRACE && (p.dbg & 4)) wait_te += clock64() - w0;
                     tc_fence_after();
                     const uint32_t d_tmem = tmem_base + buf * L::ACC_COLS;
                     for (int kb = c0; kb < c1; kb++) {
-                        long long w1 = (p.dbg & 4) ? clock64() : 0;
+                        long long w1 = (TRACE && (p.dbg & 4)) ? clock64() : 0;
                         mbar_wait(full0 + 8 * stage, phase);
-                        if ((p.dbg & 4) && !(kb == kb0 && t == (PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x)))
+                        if ((TRACE && (p.dbg & 4)) && !(kb == kb0 && t == (PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x)))
                             wait_full += clock64() - w1;
                         tc_fence_after();
                         if (lane == 0 && kb == kb0 && t == (PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x)) stamp(2);
@@ -732,7 +738,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                     if (lane == 0) stamp(3);
                 }
             }
-            if ((p.dbg & 4) && lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 2))
+            if ((TRACE && (p.dbg & 4)) && lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 2))
                 printf("tcmma cta %d: wait_tempty %.2f us, wait_full %.2f us (after the first k-block)\n", blockIdx.x,
                        wait_te / 1965.0, wait_full / 1965.0);
         }
@@ -1027,7 +1033,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
     __syncthreads();
     if (threadIdx.x == 0) {
         stamp(6);
-        if ((p.dbg & 4) && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+        if ((TRACE && (p.dbg & 4)) && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
             printf("tcts cta %d/%d t0 %llu: pdl %.2f first_full %.2f last_commit %.2f last_drain %.2f stores_done %.2f exit %.2f us\n",
                    blockIdx.x, gridDim.x, (unsigned long long)dts[0], (dts[1] - dts[0]) * 1e-3, (dts[2] - dts[0]) * 1e-3,
                    (dts[3] - dts[0]) * 1e-3, (dts[4] - dts[0]) * 1e-3, (dts[5] - dts[0]) * 1e-3, (dts[6] - dts[0]) * 1e-3);

@@ -119,6 +119,7 @@ struct mtx_ctx {
     uint64_t ws_bytes = 0;
     float *params = nullptr, *vel = nullptr, *grads = nullptr, *gather = nullptr;
     float *gred = nullptr;  // MTX_REDUCE_FUSED: reduced sum G (+ loss slot), sharded by owner
+    float *stage = nullptr; // MTX_REDUCE_FUSED push protocol: landing area [source rank][N_pad / P] of this rank's share
     // the buffer holding the reduced gradient sum G and the loss slot after a step
     float *gsum() const { return gred ? gred : grads; }
     int64_t loss_at() const { return N_pad + (gred ? 1 : 0); }
@@ -416,6 +417,8 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
     // FUSED: the reduced sum G lives in its own buffer, never written by the backward, so a peer can read
     // this rank's G slice (mtx_get_buffer) while this rank already computes the next step's local g
     float *gred = (c->world > 1 && c->opt.reduce == MTX_REDUCE_FUSED) ? (float *)take(4 * (c->N_pad + LOSS_SLOT)) : nullptr;
+    float *stage = (c->world > 1 && c->opt.reduce == MTX_REDUCE_FUSED)
+                       ? (float *)take(4 * c->world * stage_pitch(c->N_pad, c->world)) : nullptr;
     std::vector<float *> acts, fcA, dzs, colp;
     std::vector<uint32_t *> abits;
     int64_t colp_rows = 0;
@@ -540,7 +543,7 @@ uint64_t carve(mtx_ctx *c, uint8_t *base, bool assign) {
         for (auto &pr : planes)
             if (pr.h && pr.ts == tsl + mtx_ctx::TS_PARAMS)
                 c->param_segs.push_back({pr.base, pr.rows, pr.cols, pr.ld, pr.h, pr.l, pr.pld});
-        c->params = params; c->vel = vel; c->grads = grads; c->gather = gather; c->gred = gred;
+        c->params = params; c->vel = vel; c->grads = grads; c->gather = gather; c->gred = gred; c->stage = stage;
         c->acts = acts; c->fcA = fcA; c->dzs = dzs; c->lanes = lanes;
         c->convP = cP; c->convDP = cDP; c->convArg = cArg;
         c->dz[0] = dz0; c->dz[1] = dz1; c->dzL = dzL; c->loss_rows = loss_rows;
@@ -634,6 +637,17 @@ mtx_status quantize_params(mtx_ctx *c, int scr, cudaStream_t s, LaunchHook *h, i
 // launch after the backward, so off by default.
 bool fused_overlap() {
     static const bool v = getenv("MTX_FUSED_OVERLAP") && atoi(getenv("MTX_FUSED_OVERLAP"));
+    return v;
+}
+// MTX_REDUCE_FUSED at P > 1, push protocol (MTX_FUSED_PUSH=1; default off): as each gradient bucket completes in the
+// backward, the copy engines write its slice of every owner's share into that owner's landing area (cudaMemcpyAsync to
+// the peer mapping on the comm stream: NVLink traffic overlapping the rest of the backward with no SMs taken from its
+// GEMMs); after the last bucket push_done publishes "landed", and the one fused launch reads the P gradients of its
+// share from local memory, folds them in ascending rank order and updates.  Bit-identical to the pull kernel; its
+// work drops (cfg4 P = 4: 7-20 us instead of 20-27 us) but the step does not get faster (291.5 vs 286.7 us at P = 4,
+// 355 vs 352 at P = 2): rank skew, not the reduction's work, sets the wait.
+bool fused_push() {
+    static const bool v = getenv("MTX_FUSED_PUSH") && atoi(getenv("MTX_FUSED_PUSH")) != 0;
     return v;
 }
 int comm_sms() {
@@ -1085,6 +1099,28 @@ struct Runner {
             // fused_overlap(): per bucket on the comm stream, overlapping the rest of the backward on SMs the
             // backward GEMMs leave free -- measured slower, kept as an ablation.
             const bool ov = fused_overlap();
+            const bool push = !ov && fused_push() && c->stage;
+            if (push) {
+                // this bucket's gradients into every owner's landing area (own share: read in place), on the comm
+                // stream after the backward work that wrote them
+                if (mtx_status st = grads_ready(c->comm_s)) return st;
+                const int P = c->world;
+                cudaError_t e = push_bucket(c->pp, P, c->rank, c->N_pad, bkt.lo, std::min<int64_t>(bkt.hi, c->N_pad),
+                                            c->grads, c->comm_s);
+                if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "gradient push: %s", cudaGetErrorString(e));
+                if (!last) return MTX_OK;
+                e = push_done(c->pp, P, c->rank, c->stepctr, c->comm_s, h);
+                if (e == cudaSuccess) e = cudaEventRecord(c->ev_join, c->comm_s);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(s, c->ev_join, 0);
+                int64_t *win = !staged ? c->win : nullptr;
+                if (e == cudaSuccess)
+                    e = fused_bucket_update(c->pp, P, c->rank, 0, c->stepctr, 0, c->N_pad, c->opt.lr, c->opt.momentum,
+                                            c->opt.momentum != 0.f, c->flag, win, c->B, c->n_data, c->N_pad, 148, s, h,
+                                            c->f16, true);
+                if (e == cudaSuccess) e = peer_barrier_step(c->pp, P, c->rank, c->epoch, c->flag, c->stepctr, s, h);
+                if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "fused push update: %s", cudaGetErrorString(e));
+                return MTX_OK;
+            }
             if (!ov && !last) return MTX_OK;
             const cudaStream_t cs = ov ? c->comm_s : s;
             if (mtx_status st = grads_ready(cs)) return st;
@@ -1490,6 +1526,7 @@ mtx_status map_peers(mtx_ctx *c) {
         c->pp.flags[r] = (uint64_t *)(ws_r + rel(c->flags));
         c->pp.bflags[r] = (uint64_t *)(ws_r + rel(c->bflags));
         c->pp.wmax[r] = c->wmax ? (float *)(ws_r + rel(c->wmax)) : nullptr;
+        c->pp.stage[r] = c->stage ? (float *)(ws_r + rel(c->stage)) : nullptr;
     }
     c->fused = true;
     return MTX_OK;
@@ -2111,41 +2148,74 @@ mtx_status mtx_debug_reduce(mtx_ctx *c, int32_t mode, int32_t P, void *const *g,
         }
         return MTX_OK;
     }
-    if (mode != MTX_REDUCE_FUSED) return fail(c, MTX_ERR_UNSUPPORTED, "mode %d is NCCL arithmetic (needs P GPUs)", mode);
-    // FUSED: the product protocol with P simulated ranks on P concurrent streams of this GPU -- per rank
-    // peer_barrier -> fused_avg_update (owned slice: rank-ordered fold, x fl(1/P), update, w to every
-    // replica) -> peer_barrier, with PeerPtrs pointing at the P local buffer sets and per-rank flag arrays
+    const bool push = mode == (MTX_REDUCE_FUSED | MTX_DEBUG_REDUCE_PUSH);
+    if (mode != MTX_REDUCE_FUSED && !push)
+        return fail(c, MTX_ERR_UNSUPPORTED, "mode %d is NCCL arithmetic (needs P GPUs)", mode);
+    // FUSED: the product protocol with P simulated ranks on P concurrent streams of this GPU, PeerPtrs pointing at
+    // the P local buffer sets and per-rank flag arrays / step counters.
+    //   pull (the kernel of a P > 1 step with MTX_FUSED_PUSH=0): fused_bucket_update over [0, n) -- publish "ready",
+    //        wait for every rank's flag, fold the owned slice over the peers' g in ascending rank order, x fl(1/P),
+    //        update, w to every replica, v and G on the owned slice -- then peer_barrier
+    //   push (MTX_DEBUG_REDUCE_PUSH, the default P > 1 step protocol): push_bucket (copies of g into every owner's
+    //        landing area) + push_done, then the same kernel reading its share's gradients from the landing area
+    constexpr int64_t SYNC_U64 = MAX_PEERS * MAX_PEERS + MAX_PEERS + MAX_PEERS * MAX_BUCKETS * MAX_PEERS + MAX_PEERS;
     PeerPtrs pp{};
     if (!c->dbg_sync) {
-        CK(cudaMalloc(&c->dbg_sync, 8 * (MAX_PEERS * MAX_PEERS + MAX_PEERS)));  // zeroed on `s` below
+        CK(cudaMalloc(&c->dbg_sync, 8 * SYNC_U64));  // zeroed on `s` below
         for (int q = 0; q < MAX_PEERS; q++) {
             CK(cudaStreamCreateWithFlags(&c->dbg_streams[q], cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&c->dbg_ev_join[q], cudaEventDisableTiming));
         }
         CK(cudaEventCreateWithFlags(&c->dbg_ev, cudaEventDisableTiming));
     }
+    uint64_t *epochs = c->dbg_sync + MAX_PEERS * MAX_PEERS, *bfl = epochs + MAX_PEERS,
+             *stepctrs = bfl + MAX_PEERS * MAX_BUCKETS * MAX_PEERS;
+    const int64_t pitch = stage_pitch((int64_t)n, P);
+    if (push && (int64_t)P * P * pitch > c->dbg_floats) {  // the P landing areas (P x pitch floats each), debug scratch
+        CK(cudaStreamSynchronize(s));
+        if (c->dbg_planes) cudaFree(c->dbg_planes);
+        c->dbg_planes = nullptr;
+        c->dbg_floats = 0;
+        CK(cudaMalloc(&c->dbg_planes, 4 * P * P * pitch));
+        c->dbg_floats = P * P * pitch;
+    }
+    if (push) c->dbg_key[0] = c->dbg_key[1] = nullptr;  // the scratch no longer holds engine-2 planes
     for (int q = 0; q < P; q++) {
         pp.g[q] = (float *)g[q];
         pp.G[q] = (float *)G[q];
         pp.w[q] = (float *)w[q];
         pp.v[q] = has_v ? (float *)v[q] : nullptr;
         pp.flags[q] = c->dbg_sync + MAX_PEERS * q;
+        pp.bflags[q] = bfl + MAX_BUCKETS * MAX_PEERS * q;
+        pp.stage[q] = push ? c->dbg_planes + P * pitch * q : nullptr;
     }
     // fresh epochs for every call (each call is a new "world")
-    CK(cudaMemsetAsync(c->dbg_sync, 0, 8 * (MAX_PEERS * MAX_PEERS + MAX_PEERS), s));
+    CK(cudaMemsetAsync(c->dbg_sync, 0, 8 * SYNC_U64, s));
     CK(cudaEventRecord(c->dbg_ev, s));
     CK(p2p_preload());
-    // issue phase by phase over the ranks, so every rank's barrier is enqueued before anything waits on it
-    for (int phase = 0; phase < 3; phase++)
+    // pull: every rank's kernel spins until all P have published, so all P must be resident at once -- 128 / P CTAs
+    // each; push: the kernels start after every rank's push_done (stream events), the product's 148 CTAs
+    const int ctas = push ? 148 : std::max(1, 128 / P);
+    // issue phase by phase over the ranks, so everything a rank waits on is enqueued before the wait
+    for (int phase = 0; phase < 4; phase++)
         for (int r = 0; r < P; r++) {
             cudaStream_t sr = c->dbg_streams[r];
-            uint64_t *epoch = c->dbg_sync + MAX_PEERS * MAX_PEERS + r;
-            if (phase == 0) CK(cudaStreamWaitEvent(sr, c->dbg_ev, 0));
-            if (phase == 1)
-                CK(fused_avg_update(pp, P, r, (int64_t)n, lr, momentum, has_v, c->flag, nullptr, 0, 1, sr, nullptr,
-                                    false));
-            else
-                CK(peer_barrier(pp, P, r, epoch, c->flag, sr, nullptr, false));
+            if (phase == 0) {
+                CK(cudaStreamWaitEvent(sr, c->dbg_ev, 0));
+                if (push) {
+                    CK(push_bucket(pp, P, r, (int64_t)n, 0, (int64_t)n, (const float *)g[r], sr));
+                    CK(push_done(pp, P, r, stepctrs + r, sr, nullptr));
+                    CK(cudaEventRecord(c->dbg_ev_join[r], sr));
+                }
+            } else if (phase == 1) {
+                if (push)
+                    for (int q = 0; q < P; q++) CK(cudaStreamWaitEvent(sr, c->dbg_ev_join[q], 0));
+            } else if (phase == 2) {
+                CK(fused_bucket_update(pp, P, r, 0, stepctrs + r, 0, (int64_t)n, lr, momentum, has_v, c->flag, nullptr,
+                                       0, 1, (int64_t)n, ctas, sr, nullptr, false, push));
+            } else {
+                CK(peer_barrier(pp, P, r, epochs + r, c->flag, sr, nullptr, false));
+            }
         }
     for (int r = 0; r < P; r++) {
         CK(cudaEventRecord(c->dbg_ev_join[r], c->dbg_streams[r]));

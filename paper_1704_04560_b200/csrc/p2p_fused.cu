@@ -18,6 +18,10 @@
 
 #include "p2p_fused.h"
 
+#ifndef MTX_TRACE
+#define MTX_TRACE 0
+#endif
+
 namespace mtx {
 namespace {
 
@@ -83,7 +87,8 @@ template <bool HAS_V, int U, int PM>  // PM: peers the arrays hold (P <= PM)
 __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, int rank, int bucket,
                                                          const uint64_t *stepctr, int64_t lo4, int64_t hi4, float invP,
                                                          float lr, float mu, int *flag, int64_t *win, int64_t B,
-                                                         int64_t n_data, int64_t loss_idx, int track_wmax, int dbg_ts) {
+                                                         int64_t n_data, int64_t loss_idx, int track_wmax, int dbg_ts,
+                                                         int64_t share4) {
     pdl_wait();
     uint64_t t_in = 0, t_go = 0;
     if (dbg_ts && threadIdx.x == 0) t_in = globaltimer();
@@ -91,14 +96,16 @@ __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, i
     __shared__ float red[16];
     float wmax = 0.f;
     const uint64_t epoch = *(volatile const uint64_t *)stepctr + 1;
+    // push protocol (share4 > 0): the peers' gradients of this share sit in the local landing area
+    const float4 *stage4 = share4 > 0 ? (const float4 *)pp.stage[rank] : nullptr;
     if (threadIdx.x == 0) {
         go = 0;
         if (!(*(volatile int *)flag & 2)) {
-            if (blockIdx.x == 0) {  // publish "my bucket is ready" in every peer's flag array
+            if (!stage4 && blockIdx.x == 0) {  // publish "my bucket is ready" in every peer's flag array
                 __threadfence_system();
                 for (int q = 0; q < P; q++) st_release_sys(pp.bflags[q] + bucket * MAX_PEERS + rank, epoch);
             }
-            go = wait_flags(pp.bflags[rank] + bucket * MAX_PEERS, P, epoch, flag) ? 1 : 0;
+            go = wait_flags(pp.bflags[rank] + (stage4 ? PUSH_SLOT : bucket) * MAX_PEERS, P, epoch, flag) ? 1 : 0;
         }
     }
     __syncthreads();
@@ -116,7 +123,10 @@ __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, i
             if (iu >= hi4) break;
 #pragma unroll
             for (int q = 0; q < PM; q++)
-                if (q < P) gq[u][q] = __ldcv((const float4 *)pp.g[q] + iu);
+                if (q < P) {
+                    if (stage4 && q != rank) gq[u][q] = __ldcv(stage4 + q * share4 + (iu - lo4));
+                    else gq[u][q] = __ldcv((const float4 *)pp.g[q] + iu);
+                }
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -171,7 +181,7 @@ __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, i
         }
         if (win) *win = (*win + B) % n_data;
     }
-    if (dbg_ts) {  // development (MTX_FUSED_TS=1): flag wait vs reduction work of CTAs 0 and the last
+    if (MTX_TRACE && dbg_ts) {  // development (trace build -DMTX_TRACE=1) (MTX_FUSED_TS=1): flag wait vs reduction work of CTAs 0 and the last
         __syncthreads();
         if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
             printf("fusedts rank %d cta %d: wait %.2f us, work %.2f us\n", rank, blockIdx.x, (t_go - t_in) * 1e-3,
@@ -179,62 +189,41 @@ __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, i
     }
 }
 
-template <bool HAS_V>
-__global__ void __launch_bounds__(256) fused_avg_update_kernel(PeerPtrs pp, int P, int rank, int64_t lo4, int64_t hi4,
-                                                             float invP, float lr, float mu, int *flag, int64_t *win,
-                                                             int64_t B, int64_t n_data, int64_t loss_idx) {
+__global__ void push_done_kernel(PeerPtrs pp, int P, int rank, const uint64_t *stepctr) {
     pdl_wait();
-    // a peer barrier timed out: peer gradients may be partly written -- load and store nothing
-    if (*(volatile int *)flag & 2) return;
-    bool bad = false;
-    for (int64_t i = lo4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi4;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        float4 g[8];
-#pragma unroll
-        for (int q = 0; q < 8; q++)
-            if (q < P) g[q] = __ldcv((const float4 *)pp.g[q] + i);  // peer loads bypass stale caches
-        float4 G = g[0];
-#pragma unroll
-        for (int q = 1; q < 8; q++)
-            if (q < P) {  // ascending-rank left fold
-                G.x = __fadd_rn(G.x, g[q].x); G.y = __fadd_rn(G.y, g[q].y);
-                G.z = __fadd_rn(G.z, g[q].z); G.w = __fadd_rn(G.w, g[q].w);
-            }
-        const float4 w0 = ((const float4 *)pp.w[rank])[i];
-        float4 w = w0, v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (HAS_V) v = ((const float4 *)pp.v[rank])[i];
-        float gb[4] = {G.x * invP, G.y * invP, G.z * invP, G.w * invP};
-        float *pw = &w.x, *pv = &v.x;
-#pragma unroll
-        for (int c = 0; c < 4; c++) {
-            bad |= !isfinite(gb[c]);
-            if (HAS_V) {
-                pv[c] = __fmaf_rn(mu, pv[c], gb[c]);
-                pw[c] = __fmaf_rn(-lr, pv[c], pw[c]);
-            } else {
-                pw[c] = __fmaf_rn(-lr, gb[c], pw[c]);
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < 8; q++)  // the updated weights go to every replica (local store for q == rank)
-            if (q < P) __stcg((float4 *)pp.w[q] + i, w);
-        // velocity and the reduced gradient stay with their owner (sharded optimizer state, ZeRO-1
-        // style): only the owner reads them in the next step; mtx_get_buffer / mtx_param_digest
-        // assemble the full buffers from the peers' mapped workspaces on demand
-        if (HAS_V) __stcg((float4 *)pp.v[rank] + i, v);
-        __stcg((float4 *)pp.G[rank] + i, G);
-    }
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        // the loss slot: every rank folds all ranks' local loss sums itself (same order, same bits)
-        float L = __ldcv(pp.g[0] + loss_idx);
-        for (int q = 1; q < P; q++) L = __fadd_rn(L, __ldcv(pp.g[q] + loss_idx));
-        pp.G[rank][loss_idx + 1] = L;  // slot 0 keeps this rank's local sum (peers may still read it)
-        if (win) *win = (*win + B) % n_data;
-    }
+    const uint64_t epoch = *(volatile const uint64_t *)stepctr + 1;
+    __threadfence_system();
+    const int q = threadIdx.x;
+    if (q < P) st_release_sys(pp.bflags[q] + PUSH_SLOT * MAX_PEERS + rank, epoch);
 }
 
 }  // namespace
+
+cudaError_t push_bucket(const PeerPtrs &pp, int P, int rank, int64_t n, int64_t lo, int64_t hi, const float *g,
+                        cudaStream_t s) {
+    if (lo % 4 || hi % 4 || n % 4) return cudaErrorInvalidValue;
+    const int64_t pitch = stage_pitch(n, P);
+    for (int k = 1; k < P; k++) {  // rank + 1 first: at any moment the ranks' copies go to different owners
+        const int q = (rank + k) % P;
+        int64_t a, b;
+        bucket_share(0, n, P, q, a, b);
+        const int64_t x = std::max(lo, a), y = std::min(hi, b);
+        if (x < y) {
+            cudaError_t e = cudaMemcpyAsync(pp.stage[q] + pitch * rank + (x - a), g + x, 4 * (y - x), cudaMemcpyDefault, s);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
+}
+
+cudaError_t push_done(const PeerPtrs &pp, int P, int rank, const uint64_t *stepctr, cudaStream_t s, LaunchHook *h) {
+    char name[32];
+    snprintf(name, sizeof name, "push_done[P=%d]", P);
+    if (h) h->before(name, s);
+    push_done_kernel<<<1, 32, 0, s>>>(pp, P, rank, stepctr);
+    if (h) h->after(name, s);
+    return cudaGetLastError();
+}
 
 cudaError_t p2p_preload() {
     // CUDA 12 loads kernels lazily at their first launch, and loading waits for the device: a first launch
@@ -245,8 +234,7 @@ cudaError_t p2p_preload() {
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<false, 2, MAX_PEERS>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<true, 4, 4>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<false, 4, 4>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_avg_update_kernel<true>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_avg_update_kernel<false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)push_done_kernel);
     return e;
 }
 
@@ -276,12 +264,16 @@ cudaError_t peer_barrier_step(const PeerPtrs &pp, int P, int rank, uint64_t *epo
 cudaError_t fused_bucket_update(const PeerPtrs &pp, int P, int rank, int bucket, const uint64_t *stepctr, int64_t lo,
                                 int64_t hi, float lr, float mu, bool has_v, int *flag, int64_t *win, int64_t B,
                                 int64_t n_data, int64_t loss_idx, int ctas, cudaStream_t s, LaunchHook *h,
-                                bool track_wmax) {
+                                bool track_wmax, bool from_stage) {
     if (P > MAX_PEERS || bucket >= MAX_BUCKETS || lo % 4 || hi % 4) return cudaErrorInvalidValue;
     int64_t a, b;
     bucket_share(lo, hi, P, rank, a, b);
+    // push protocol: the landing area's row pitch is the longest share
+    if (from_stage && (lo != 0 || !pp.stage[rank])) return cudaErrorInvalidValue;
+    const int64_t share4 = from_stage ? stage_pitch(hi, P) / 4 : 0;
     char name[96];
-    snprintf(name, sizeof name, "fused_avg_update[n=%lld,P=%d,v=%d]", (long long)(hi - lo), P, has_v ? 1 : 0);
+    snprintf(name, sizeof name, "fused_avg_update[n=%lld,P=%d,v=%d%s]", (long long)(hi - lo), P, has_v ? 1 : 0,
+             from_stage ? ",push=1" : "");
     if (h) h->before(name, s);
     const float invP = 1.0f / (float)P;
     static const int dbg_ts = getenv("MTX_FUSED_TS") ? atoi(getenv("MTX_FUSED_TS")) : 0;
@@ -289,28 +281,7 @@ cudaError_t fused_bucket_update(const PeerPtrs &pp, int P, int rank, int bucket,
     auto kern = P <= 4 ? (has_v ? fused_bucket_kernel<true, 4, 4> : fused_bucket_kernel<false, 4, 4>)
                        : (has_v ? fused_bucket_kernel<true, 2, MAX_PEERS> : fused_bucket_kernel<false, 2, MAX_PEERS>);
     launch_pdl(kern, dim3(std::max(1, ctas)), dim3(512), 0, s, pp, P, rank, bucket, stepctr, a / 4, b / 4, invP, lr, mu,
-               flag, win, B, n_data, loss_idx, (track_wmax && pp.wmax[0]) ? 1 : 0, dbg_ts);
-    if (h) h->after(name, s);
-    return cudaGetLastError();
-}
-
-cudaError_t fused_avg_update(const PeerPtrs &pp, int P, int rank, int64_t n_pad, float lr, float mu, bool has_v,
-                             int *flag, int64_t *win, int64_t B, int64_t n_data, cudaStream_t s, LaunchHook *h,
-                             bool pdl) {
-    if (P > 8 || n_pad % 4) return cudaErrorInvalidValue;
-    const int64_t n4 = n_pad / 4;
-    const int64_t lo4 = n4 * rank / P, hi4 = n4 * (rank + 1) / P;
-    const int64_t mine = hi4 - lo4;
-    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((mine + 255) / 256, 148 * 4));
-    char name[96];
-    snprintf(name, sizeof name, "fused_avg_update[n=%lld,P=%d,v=%d]", (long long)n_pad, P, has_v ? 1 : 0);
-    if (h) h->before(name, s);
-    const float invP = 1.0f / (float)P;
-    auto kern = has_v ? fused_avg_update_kernel<true> : fused_avg_update_kernel<false>;
-    if (pdl)
-        launch_pdl(kern, dim3(blocks), dim3(256), 0, s, pp, P, rank, lo4, hi4, invP, lr, mu, flag, win, B, n_data, n_pad);
-    else
-        kern<<<blocks, 256, 0, s>>>(pp, P, rank, lo4, hi4, invP, lr, mu, flag, win, B, n_data, n_pad);
+               flag, win, B, n_data, loss_idx, (track_wmax && pp.wmax[0]) ? 1 : 0, dbg_ts, share4);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }

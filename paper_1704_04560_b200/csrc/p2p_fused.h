@@ -21,9 +21,13 @@ struct PeerPtrs {
     uint64_t *bflags[MAX_PEERS]; // per-rank "bucket ready" epochs, [bucket][source rank] (MAX_BUCKETS x MAX_PEERS)
     float *wmax[MAX_PEERS];      // 3xF16: per-rank arrays of per-CTA max |w| of the updated weights, [rank][CTA]
                                  // (null: not tracked); the next step's parameter quantize folds them
+    float *stage[MAX_PEERS];     // push protocol: per-rank landing area [source rank][share length] of the gradients of
+                                 // the rank's own share, written by the peers' copy engines during the backward
 };
 
 constexpr int MAX_BUCKETS = 64;
+// bflags slot of the push protocol's "all my gradient pushes have landed" epochs ([PUSH_SLOT][source rank])
+constexpr int PUSH_SLOT = MAX_BUCKETS - 1;
 
 // Loads the kernels of this file (CUDA lazy loading would otherwise load them at their first launch).
 cudaError_t p2p_preload();
@@ -40,10 +44,22 @@ cudaError_t peer_barrier(const PeerPtrs &pp, int P, int rank, uint64_t *epoch_ct
 // x fl(1/P) and the momentum update and stores w into every replica (v and G stay with the owner).
 // loss_idx >= 0: this bucket carries the loss slot (folded into slot loss_idx + 1); win != nullptr: the
 // window start advances (the step's last bucket).  `ctas` CTAs (the SMs the backward GEMMs leave free).
+// from_stage (push protocol, one launch over the whole buffer): the peers' gradients of this rank's share are read
+// from its own landing area pp.stage[rank] ([source rank][share]) instead of over NVLink, and the kernel waits for the
+// peers' PUSH_SLOT flags (set by push_done) instead of publishing and waiting for bucket flags.
 cudaError_t fused_bucket_update(const PeerPtrs &pp, int P, int rank, int bucket, const uint64_t *stepctr, int64_t lo,
                                 int64_t hi, float lr, float mu, bool has_v, int *flag, int64_t *win, int64_t B,
                                 int64_t n_data, int64_t loss_idx, int ctas, cudaStream_t s, LaunchHook *h,
-                                bool track_wmax = false);
+                                bool track_wmax = false, bool from_stage = false);
+// Push protocol landing-area row pitch (floats) for a buffer of n floats: the longest share of [0, n)
+inline int64_t stage_pitch(int64_t n, int P) { return 4 * ((n / 4 + P - 1) / P); }
+// Push protocol: copy-engine copies (cudaMemcpyAsync on s) of this rank's gradients g[lo, hi) into every other owner's
+// landing area, pp.stage[q] + pitch * rank + (offset in q's share of [0, n)).
+cudaError_t push_bucket(const PeerPtrs &pp, int P, int rank, int64_t n, int64_t lo, int64_t hi, const float *g,
+                        cudaStream_t s);
+// Push protocol: after this rank's copies of its gradients into every owner's landing area (stream-ordered before this
+// launch), publish "pushes landed at epoch *stepctr + 1" in every rank's PUSH_SLOT flags (system-scope release).
+cudaError_t push_done(const PeerPtrs &pp, int P, int rank, const uint64_t *stepctr, cudaStream_t s, LaunchHook *h);
 // The rank's share of bucket [lo, hi) (float indices, multiples of 4): [lo + 4*(n4*r/P), lo + 4*(n4*(r+1)/P)).
 inline void bucket_share(int64_t lo, int64_t hi, int P, int r, int64_t &a, int64_t &b) {
     const int64_t n4 = (hi - lo) / 4;
@@ -53,11 +69,5 @@ inline void bucket_share(int64_t lo, int64_t hi, int P, int r, int64_t &a, int64
 // Final barrier of a step: as peer_barrier, then (stepctr != nullptr) advances the step counter.
 cudaError_t peer_barrier_step(const PeerPtrs &pp, int P, int rank, uint64_t *epoch_ctr, int *errflag, uint64_t *stepctr,
                               cudaStream_t s, LaunchHook *h);
-
-// Rank-ordered reduce of the owned slice + fused average/momentum update, results published to
-// every replica; loss slot n_pad folded by every rank into slot n_pad + 1.
-cudaError_t fused_avg_update(const PeerPtrs &pp, int P, int rank, int64_t n_pad, float lr, float mu, bool has_v,
-                             int *flag, int64_t *win, int64_t B, int64_t n_data, cudaStream_t s, LaunchHook *h,
-                             bool pdl = true);
 
 }  // namespace mtx

@@ -22,6 +22,7 @@ MTX_MLP, MTX_CNN = 0, 1
 MTX_FP32, MTX_TF32, MTX_3XTF32, MTX_3XF16 = 0, 1, 2, 3
 MTX_REDUCE_NCCL, MTX_REDUCE_ORDERED, MTX_REDUCE_FUSED, MTX_REDUCE_LAYERWISE, MTX_REDUCE_ZERO1 = 0, 1, 2, 3, 4
 MTX_BUF_PARAMS, MTX_BUF_VELOCITY, MTX_BUF_GRADS = 0, 1, 2
+MTX_DEBUG_REDUCE_PUSH = 0x100  # mtx_debug_reduce: FUSED with the push protocol
 
 
 class MtxError(RuntimeError):

@@ -77,7 +77,9 @@ def test_gemm_bitwise_repeatable(shape, engine):
     assert outs[1] == outs[0] and outs[2] == outs[0]
 
 
-def test_fused_protocol_bitwise_repeatable():
+@pytest.mark.parametrize("proto", ["pull", "push"])
+def test_fused_protocol_bitwise_repeatable(proto):
+    mode = P.MTX_REDUCE_FUSED | (P.MTX_DEBUG_REDUCE_PUSH if proto == "push" else 0)
     n, Pn = (1 << 20) + 4, 8
     g = np.zeros((Pn, n + 32), np.float32)
     for q in range(Pn):
@@ -91,7 +93,7 @@ def test_fused_protocol_bitwise_repeatable():
             gd, wd, vd = [dev(g[q]) for q in range(Pn)], [dev(w) for _ in range(Pn)], [dev(v) for _ in range(Pn)]
             Gd = [torch.zeros(n + 32, device="cuda") for _ in range(Pn)]
             torch.cuda.synchronize()
-            mtx.mtx_debug_reduce(r.ctx, P.MTX_REDUCE_FUSED, Pn, [t.data_ptr() for t in gd], [t.data_ptr() for t in wd],
+            mtx.mtx_debug_reduce(r.ctx, mode, Pn, [t.data_ptr() for t in gd], [t.data_ptr() for t in wd],
                                  [t.data_ptr() for t in vd], [t.data_ptr() for t in Gd], n, 0.01, 0.9, r.s)
             r.sync()
             r.get()

@@ -73,14 +73,20 @@ def _oracle(g, w, v, P_, mu, lr=0.01):
     return G, wo, vo
 
 
-@pytest.mark.parametrize("P_", [2, 4, 8])
+FUSED_MODES = {"pull": P.MTX_REDUCE_FUSED, "push": P.MTX_REDUCE_FUSED | P.MTX_DEBUG_REDUCE_PUSH}
+
+
+@pytest.mark.parametrize("proto", ["pull", "push"])
+@pytest.mark.parametrize("P_", [2, 3, 4, 8])
 @pytest.mark.parametrize("n", [1000, (1 << 20) + 4])
 @pytest.mark.parametrize("mu", [0.9, 0.0])
-def test_fused_protocol_bit_exact(rep, P_, n, mu):
-    """MTX_REDUCE_FUSED: every replica's w equals the oracle's everywhere; each owner's slice of v and G
-    equals the oracle's; the loss slot is the rank-ordered fold on every rank."""
+def test_fused_protocol_bit_exact(rep, P_, n, mu, proto):
+    """MTX_REDUCE_FUSED, both protocols (pull: the kernel loads the peers' g over NVLink; push: the peers' copy
+    engines wrote them into the owner's landing area -- unequal shares when P does not divide n / 4): every
+    replica's w equals the oracle's everywhere; each owner's slice of v and G equals the oracle's; the loss slot
+    is the rank-ordered fold on every rank."""
     g, w, v = _inputs(P_, n)
-    Gs, ws, vs = _run(rep, P.MTX_REDUCE_FUSED, P_, g, w, v, mu)
+    Gs, ws, vs = _run(rep, FUSED_MODES[proto], P_, g, w, v, mu)
     G, wo, vo = _oracle(g, w, v, P_, mu)
     for q in range(P_):
         assert same(ws[q], wo), f"replica {q} w"
@@ -104,12 +110,13 @@ def test_ordered_fold_and_update_bit_exact(rep, P_, n):
         assert same(vs[r], vo), f"rank {r} v"
 
 
-def test_fused_protocol_alexnet_size_p8(rep):
+@pytest.mark.parametrize("proto", ["pull", "push"])
+def test_fused_protocol_alexnet_size_p8(rep, proto):
     """The AlexNet-scale flat buffer (61.1 M parameters) at P = 8, momentum."""
     n = ALEXNET
     P_ = 8
     g, w, v = _inputs(P_, n, seed=5)
-    Gs, ws, vs = _run(rep, P.MTX_REDUCE_FUSED, P_, g, w, v, 0.9)
+    Gs, ws, vs = _run(rep, FUSED_MODES[proto], P_, g, w, v, 0.9)
     G, wo, vo = _oracle(g, w, v, P_, 0.9)
     for q in range(P_):
         assert same(ws[q], wo), f"replica {q} w"

@@ -24,12 +24,13 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_dp_step_multigpu(world, tmp_path):
+@pytest.mark.parametrize("world,proto", [(2, "pull"), (4, "pull"), (2, "push")])
+def test_dp_step_multigpu(world, proto, tmp_path):
+    """proto: the FUSED reduction's pull kernel (default) or the copy-engine push protocol (MTX_FUSED_PUSH=1)."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     rep = tmp_path / "report.json"
-    env = dict(os.environ, MTX_MP_REPORT=str(rep), PYTHONPATH=ROOT)
+    env = dict(os.environ, MTX_MP_REPORT=str(rep), PYTHONPATH=ROOT, MTX_FUSED_PUSH="1" if proto == "push" else "0")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "tests", "mp_worker.py")]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
