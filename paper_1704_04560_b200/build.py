@@ -36,7 +36,8 @@ def nccl_dirs():
 def _flags(inc):
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
                    "-I", inc, "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"] + \
-        (["-DMTX_TRACE=1"] if os.environ.get("MTX_TRACE") == "1" else [])  # development trace build (force=True)
+        (["-DMTX_TRACE=1"] if os.environ.get("MTX_TRACE") == "1" else []) + \
+        (["-DMTX_TC_EXPERIMENTS=1"] if os.environ.get("MTX_TC_EXPERIMENTS") == "1" else [])  # dev builds (force=True)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -36,6 +36,12 @@ namespace {
 #define MTX_TRACE 0
 #endif
 constexpr bool TRACE = MTX_TRACE != 0;
+// Measured-and-rejected engine experiments (L2 prefetch MTX_TC_PF / MTX_TC_PFB, A multicast MTX_TC_MC) exist only in an
+// experiment build (-DMTX_TC_EXPERIMENTS=1): their code, even disabled at run time, slowed the small GEMMs (cfg2)
+#ifndef MTX_TC_EXPERIMENTS
+#define MTX_TC_EXPERIMENTS 0
+#endif
+constexpr bool EXPER = MTX_TC_EXPERIMENTS != 0;
 #ifndef MTX_F16_CHUNK
 #define MTX_F16_CHUNK 4
 #endif
@@ -513,7 +519,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
         }
         for (int s = 0; s < STAGES; s++) {
             mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, (PAIR && p.mc) ? 2 : 1);  // multicast: a slot is free once both pairs consumed it
+            mbar_init(empty0 + 8 * s, (EXPER && PAIR && p.mc) ? 2 : 1);  // multicast: a slot is free once both pairs consumed it
         }
         for (int a = 0; a < NBUF; a++) {
             mbar_init(tfull0 + 8 * a, 1);
@@ -542,7 +548,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
     const uint32_t tmem_base = *tmem_slot;
     // Before waiting on the previous kernel: pull this CTA's first B k-blocks into L2.  B of a forward / dgrad is the
     // weights (written steps ago); a prefetch is only a hint (L2 is coherent), so it is safe whatever produced B.
-    if (warp == 0 && !(p.dbg & 2) && p.pfb) {
+    if (EXPER && warp == 0 && !(p.dbg & 2) && p.pfb) {
         int z0, r0;
         const int t0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
         if (t0 < p.tiles_m * p.tiles_n * p.splits) {
@@ -594,7 +600,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                 const int m0 = (r / p.tiles_n) * TILE_M + m_off, n0 = (r % p.tiles_n) * BN + nb_off;
                 const int kb0 = z * p.kb_per_split, kb1 = min(p.kb_total, kb0 + p.kb_per_split);
                 for (int kb = kb0; kb < kb1; kb++) {
-                    if (p.pf && kb + p.pf < kb1 && !(p.dbg & 2)) {  // k-block kb + pf into L2 (both planes, A and B)
+                    if (EXPER && p.pf && kb + p.pf < kb1 && !(p.dbg & 2)) {  // k-block kb + pf into L2 (both planes, A and B)
                         const int kp = (kb + p.pf) * KB;
 #pragma unroll
                         for (int plane = 0; plane < (SPLIT ? 2 : 1); plane++) {
@@ -639,7 +645,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                             if (PAIR) tma_load_3d_pair_elect(dst, map, fbc, 0, k_row, chunk);
                             else tma_load_3d_elect(dst, map, fb, 0, k_row, chunk);
                         };
-                        if (PAIR && p.mc && !p.a_mn) {
+                        if (EXPER && PAIR && p.mc && !p.a_mn) {
                             // the cluster's two pairs share A's rows: pair 0 loads the hi plane, pair 1 the lo plane, each
                             // multicast to the same-rank CTA of both pairs
                             if ((int)((crank >> 1) & 1) == plane)
@@ -727,7 +733,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                             }
                         }
                         // frees the smem slot (of both CTAs of a pair) when these MMAs retire
-                        if (PAIR) umma_commit_pair_elect(empty0 + 8 * stage, p.mc ? (uint16_t)0xF : pair_mask);
+                        if (PAIR) umma_commit_pair_elect(empty0 + 8 * stage, (EXPER && p.mc) ? (uint16_t)0xF : pair_mask);
                         else umma_commit_elect(empty0 + 8 * stage);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -1462,10 +1468,10 @@ static cudaError_t tc_gemm_impl(TcGemm *t, const GemmDesc &g, cudaStream_t s, La
     if (const char *k = getenv("MTX_TC_DBG")) p.dbg = atoi(k);  // development timing knob
     // L2 prefetch distance: one ring ahead of the loads (development knob MTX_TC_PF: 0 disables, n = distance)
     static const int pf_env = getenv("MTX_TC_PF") ? atoi(getenv("MTX_TC_PF")) : -1;
-    p.pf = pf_env >= 0 ? pf_env : 0;  // measured slower at 4 and 8 (cfg4 506 -> 635 / 608 us/step): off
+    p.pf = (EXPER && pf_env >= 0) ? pf_env : 0;  // measured slower at 4 and 8 (cfg4 506 -> 635 / 608 us/step): off
     // development knob MTX_TC_PFB=1: measured slightly slower (cfg4 525.3 -> 529.5 us/step)
     static const int pfb_env = getenv("MTX_TC_PFB") ? atoi(getenv("MTX_TC_PFB")) : 0;
-    p.pfb = (pfb_env && !g.ta) ? 1 : 0;  // forward / dgrad (B = weights); a weight gradient's B is the fresh dZ
+    p.pfb = (EXPER && pfb_env && !g.ta) ? 1 : 0;  // forward / dgrad (B = weights); a weight gradient's B is the fresh dZ
     p.epi = g.epi;
     p.bias = g.bias;
     p.mask = g.mask;
@@ -1480,7 +1486,7 @@ static cudaError_t tc_gemm_impl(TcGemm *t, const GemmDesc &g, cudaStream_t s, La
     // faster (cfg4 forward 44.5 -> 45.8 us) -- the MMA phase is bound by shared-memory bandwidth (TMA writes ~62 B/clk
     // + MMA operand reads ~92 B/clk per SM against 128 B/clk), not by L2 delivery
     static const int mc_env = getenv("MTX_TC_MC") ? atoi(getenv("MTX_TC_MC")) : 0;
-    if (f16 && pair && !cluster && splits == 1 && !p.a_mn && p.tiles_n % 2 == 0 && sms >= t->sms && mc_env == 1) {
+    if (EXPER && f16 && pair && !cluster && splits == 1 && !p.a_mn && p.tiles_n % 2 == 0 && sms >= t->sms && mc_env == 1) {
         const int nc = co_resident_pair_v(t, variant, 4);
         if (nc >= 2) {
             p.mc = 1;
