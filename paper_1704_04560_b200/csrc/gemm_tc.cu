@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                     const uint32_t fb = full0 + 8 * stage;
                     // PAIR: both CTAs' loads complete on the leader's full barrier, armed by the leader alone
                     const uint32_t fbc = PAIR ? mapa_u32(fb, lead_rank) : fb;
-                    if (p.dbg & 2) {  // development: MMA-only timing
+                    if (EXPER && (p.dbg & 2)) {  // development (experiment build): MMA-only timing
                         if (leader) mbar_arrive_elect(fb);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                         continue;
@@ -853,7 +853,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                 // output: the fp16 planes alone (lean), or the fp32 copy alone (a layer the SIMT head consumes)
                 const bool planes = p.fo.h != nullptr;
                 const bool fast = p.splits == 1 && (planes ? p.fo.skip_f32 : (p.C && (p.ldc & 3) == 0 && !p.C_hi)) &&
-                                  !(p.dbg & 1) && m0 + 32 * q + 32 <= p.M &&
+                                  !(EXPER && (p.dbg & 1)) && m0 + 32 * q + 32 <= p.M &&
                                   n0 + HALF <= p.N && (MASK ? (p.mbits != nullptr)
                                                             : (p.epi == EPI_BIAS_RELU && ((uintptr_t)p.bias & 15) == 0));
                 if (fast) {
@@ -961,7 +961,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                         const int r = it * RPI + rl;
                         const int m = m0 + 32 * q + r;
                         const float4 sv = *(const float4 *)(stg + r * SW + 4 * swz(r, jj));
-                        const bool ok = m < p.M && n < p.N && !(p.dbg & 1);
+                        const bool ok = m < p.M && n < p.N && !(EXPER && (p.dbg & 1));
                         if (ok && p.splits > 1) {  // split-K partial (folded with the epilogue by splitk_reduce)
                             float *dst = p.partial + ((int64_t)z * p.M + m) * p.N + n;
                             if (n + 3 < p.N) *(float4 *)dst = sv;
@@ -1465,7 +1465,7 @@ static cudaError_t tc_gemm_impl(TcGemm *t, const GemmDesc &g, cudaStream_t s, La
     p.cluster = cluster ? 1 : 0;
     if (splits_out) *splits_out = splits;
     if (!launch) return cudaSuccess;
-    if (const char *k = getenv("MTX_TC_DBG")) p.dbg = atoi(k);  // development timing knob
+    if (const char *k = getenv("MTX_TC_DBG")) p.dbg = atoi(k);  // development timing knob (trace / experiment builds)
     // L2 prefetch distance: one ring ahead of the loads (development knob MTX_TC_PF: 0 disables, n = distance)
     static const int pf_env = getenv("MTX_TC_PF") ? atoi(getenv("MTX_TC_PF")) : -1;
     p.pf = (EXPER && pf_env >= 0) ? pf_env : 0;  // measured slower at 4 and 8 (cfg4 506 -> 635 / 608 us/step): off

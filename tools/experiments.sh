@@ -1,9 +1,12 @@
 #!/bin/bash
 # Round-2b A/B measurements behind DESIGN.md §5 / §13 (one B200 unless noted; outputs in gpurun_out/).
 # Usage: bash tools/experiments.sh <name>      e.g. gpurun -- 'bash tools/experiments.sh knobs'
+# The prefetch / multicast knobs and MTX_TC_DBG 1-3 exist only in an experiment build, the phase stamps (MTX_TC_DBG=4,
+# MTX_FUSED_TS) only in a trace build: this script rebuilds with both (MTX_TC_EXPERIMENTS=1 MTX_TRACE=1); rebuild the
+# product library afterwards (build(force=True) without them).
 set -x
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+MTX_TC_EXPERIMENTS=1 MTX_TRACE=1 python -c "from paper_1704_04560_b200 import build as b; b.build(force=True)" > /dev/null 2>&1
 case "$1" in
   knobs)  # GEMM engine knobs on the cfg4 step: L2 prefetch, A multicast, 256-wide pair tiles, CUDA-core first-layer wgrad
     for kv in "" MTX_TC_PF=4 MTX_TC_PF=8 MTX_TC_MC=1 MTX_TC_BN256=1 MTX_SMALLM=1; do
