@@ -608,7 +608,7 @@ mtx_status quantize_buffer(mtx_ctx *c, const float *buf, int64_t rows, int64_t c
     CK(quantize_f16(&q, 1, nullptr, 0, v.ts, nullptr, 0, c->qscr[scr], s, h));
     return MTX_OK;
 }
-bool fused_overlap();
+bool fused_overlap(const mtx_ctx *c);
 // Development knob MTX_SMALLM=1: the CUDA-core weight gradient of a <= 32-input layer (kernels_smallk.cu) instead of
 // the tensor-core split-K GEMM (measured slower at cfg4: 34 + 6 us against 26 + 2)
 bool smallm_on() {
@@ -616,7 +616,7 @@ bool smallm_on() {
     return v;
 }
 // 3xF16 at P > 1 with the one-launch fused update: it leaves the per-rank maxima of the updated weights
-bool wmax_fused(const mtx_ctx *c) { return c->f16 && c->world > 1 && c->fused && c->wmax && !fused_overlap(); }
+bool wmax_fused(const mtx_ctx *c) { return c->f16 && c->world > 1 && c->fused && c->wmax && !fused_overlap(c); }
 // 3xF16 parameter planes (one scale over the whole flat buffer, biases included: it bounds every bias
 // read by the forward epilogues); resets the per-step slots' amax (their producers run after this)
 // pre_parts > 0: the update launch just before left that many per-CTA maxima of the new parameters in qscr[scr]
@@ -633,11 +633,13 @@ mtx_status quantize_params(mtx_ctx *c, int scr, cudaStream_t s, LaunchHook *h, i
 // MTX_REDUCE_FUSED at P > 1, ablation knob MTX_FUSED_OVERLAP=1: the fused reduction runs per bucket on the
 // comm stream while the backward continues, on MTX_COMM_SMS SMs (default 16) that the backward's GEMMs are
 // planned to leave free (a persistent GEMM CTA fills its SM; without a reserve the reduction would queue
-// behind it), the backward then being one chain on the caller's stream.  Measured slower than one fused
-// launch after the backward, so off by default.
-bool fused_overlap() {
-    static const bool v = getenv("MTX_FUSED_OVERLAP") && atoi(getenv("MTX_FUSED_OVERLAP"));
-    return v;
+// behind it), the backward then being one chain on the caller's stream.  Default from P = 4 (MTX_FUSED_OVERLAP=0/1
+// forces it): measured at cfg4 P = 4 263 vs 270 us/step with 16 reserved SMs (at b = 2048 the 1024-wide GEMMs are one
+// tile per CTA pair and leave SMs idle anyway); slower at P = 2 (351 vs 331 us: there the reserve costs the GEMMs
+// more than the ~30 us of reduction it hides) -- DESIGN.md §6.
+bool fused_overlap(const mtx_ctx *c) {
+    static const int v = getenv("MTX_FUSED_OVERLAP") ? atoi(getenv("MTX_FUSED_OVERLAP")) : -1;
+    return v >= 0 ? v != 0 : c->world >= 4;
 }
 // MTX_REDUCE_FUSED at P > 1, push protocol (MTX_FUSED_PUSH=1; default off): as each gradient bucket completes in the
 // backward, the copy engines write its slice of every owner's share into that owner's landing area (cudaMemcpyAsync to
@@ -677,7 +679,7 @@ struct Runner {
     mtx_status on_lane(int ln, F fn) {
         // MTX_REDUCE_FUSED at P > 1: the backward is one chain on the caller's stream, every GEMM planned for the
         // SMs the per-bucket reduction kernels leave free (concurrent side-lane GEMMs would take those SMs too)
-        if (ln <= 0 || ln >= c->lanes || !c->side[ln - 1] || (c->fused && c->world > 1 && fused_overlap())) return fn();
+        if (ln <= 0 || ln >= c->lanes || !c->side[ln - 1] || (c->fused && c->world > 1 && fused_overlap(c))) return fn();
         if (c->hook.enabled) {
             // per-kernel timing pass: serialised on the caller's stream (every kernel timed alone, like
             // ncu's launch list) but with the lane's launch plan -- its SM budget and scratch -- so each
@@ -757,7 +759,7 @@ struct Runner {
     }
 
     mtx_status gemm(GemmDesc g, Lean *ln = nullptr) {
-        if (c->fused && c->world > 1 && fused_overlap() && (g.epi == EPI_MASK || g.ta)) {  // backward GEMM at P > 1
+        if (c->fused && c->world > 1 && fused_overlap(c) && (g.epi == EPI_MASK || g.ta)) {  // backward GEMM at P > 1
             const int avail = 148 - comm_sms();
             g.sm_budget = g.sm_budget > 0 ? std::min(g.sm_budget, avail) : avail;
         }
@@ -832,11 +834,11 @@ struct Runner {
                     return MTX_OK;
                 };
                 mtx_status cs = (c->lanes > mtx_ctx::COLSUM_LANE && !c->hook.enabled &&
-                                 !(c->fused && c->world > 1 && fused_overlap()))
+                                 !(c->fused && c->world > 1 && fused_overlap(c)))
                                     ? on_lane(mtx_ctx::COLSUM_LANE, fold) : fold();
                 if (cs) return cs;
                 g.colsum_external = true;
-            } else if (g.aug && c->lanes > mtx_ctx::COLSUM_LANE && !c->hook.enabled && !(c->fused && c->world > 1 && fused_overlap())) {
+            } else if (g.aug && c->lanes > mtx_ctx::COLSUM_LANE && !c->hook.enabled && !(c->fused && c->world > 1 && fused_overlap(c))) {
                 // the bias row (column sums of B = dZ) runs on its own lane beside the GEMM
                 const GemmDesc gc = g;
                 mtx_status cs = on_lane(mtx_ctx::COLSUM_LANE, [&] {
@@ -1095,10 +1097,10 @@ struct Runner {
             // The averaging operator fused with its collective.  The kernel publishes "gradients ready" to
             // every peer, waits for theirs, folds + updates this rank's share of its range and stores w into
             // every replica; a barrier after the last one makes every replica's w complete before the next
-            // step reads it.  Default: one launch over the whole buffer after the backward, on all SMs.
-            // fused_overlap(): per bucket on the comm stream, overlapping the rest of the backward on SMs the
-            // backward GEMMs leave free -- measured slower, kept as an ablation.
-            const bool ov = fused_overlap();
+            // step reads it.  P <= 3: one launch over the whole buffer after the backward, on all SMs.
+            // fused_overlap() (P >= 4): per bucket on the comm stream, overlapping the rest of the backward on SMs
+            // the backward GEMMs leave free.
+            const bool ov = fused_overlap(c);
             const bool push = !ov && fused_push() && c->stage;
             if (push) {
                 // this bucket's gradients into every owner's landing area (own share: read in place), on the comm
@@ -1436,7 +1438,7 @@ mtx_status assemble_shards(mtx_ctx *c) {
     if (!c->fused || c->world <= 1) return MTX_OK;
     // the fused kernels share out every bucket (overlap ablation) or the whole buffer to the ranks (bucket_share)
     std::vector<std::pair<int64_t, int64_t>> ranges;
-    if (fused_overlap())
+    if (fused_overlap(c))
         for (const Bucket &bk : c->buckets) ranges.push_back({bk.lo, std::min<int64_t>(bk.hi, c->N_pad)});
     else
         ranges.push_back({0, c->N_pad});
