@@ -475,7 +475,9 @@ __device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base, floa
     }
 }
 
-template <int BN, bool SPLIT, bool PAIR, bool MASK, bool F16>
+// FAST (3xF16, 128-wide tiles): the host guarantees every tile takes the whole-tile fast epilogue (no ragged edge,
+// no split-K, planes-only or fp32-only output): the general epilogue and the cluster fold are compiled out of it
+template <int BN, bool SPLIT, bool PAIR, bool MASK, bool F16, bool FAST = false>
 __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
     using L = SmemLayout<BN, SPLIT, PAIR, F16>;
     constexpr int KB = F16 ? BKH : BK;        // elements per k-block (one 128-B row)
@@ -828,7 +830,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
 #pragma unroll
                 for (int j = 0; j < HALF; j++) acc[j] = (acc[j] * fa) * fb;
             }
-            if (p.cluster) {  // partial tile -> own smem; folded across the cluster below
+            if (!FAST && p.cluster) {  // partial tile -> own smem; folded across the cluster below
                 const int row = 32 * q + lane;
 #pragma unroll
                 for (int j = 0; j < HALF / 4; j++)
@@ -852,7 +854,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
             if constexpr (F16 && (HALF == 64 || HALF == 128)) {
                 // output: the fp16 planes alone (lean), or the fp32 copy alone (a layer the SIMT head consumes)
                 const bool planes = p.fo.h != nullptr;
-                const bool fast = p.splits == 1 && (planes ? p.fo.skip_f32 : (p.C && (p.ldc & 3) == 0 && !p.C_hi)) &&
+                const bool fast = FAST || p.splits == 1 && (planes ? p.fo.skip_f32 : (p.C && (p.ldc & 3) == 0 && !p.C_hi)) &&
                                   !(EXPER && (p.dbg & 1)) && m0 + 32 * q + 32 <= p.M &&
                                   n0 + HALF <= p.N && (MASK ? (p.mbits != nullptr)
                                                             : (p.epi == EPI_BIAS_RELU && ((uintptr_t)p.bias & 15) == 0));
@@ -1018,7 +1020,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
     }
 #undef MTX_UNITS
     if (warp == 4 && lane == 0) stamp(5);
-    if (p.cluster) {
+    if (!FAST && p.cluster) {
         // every CTA of the cluster holds its split's partial tile: CTA z folds rows
         // [z*BM/S, (z+1)*BM/S) over the splits in ascending order (deterministic) and stores them
         // with the fused epilogue; the second barrier keeps every CTA's smem alive until read
@@ -1105,7 +1107,7 @@ bool make_map_mn3d(EncodeTiled enc, CUtensorMap *m, const void *ptr, int64_t row
 struct TcGemm {
     EncodeTiled encode = nullptr;
     int sms = 148;
-    bool attr_set[64] = {};
+    bool attr_set[128] = {};
     // split-K folded through distributed shared memory (MTX_TC_CLUSTER=0 disables: global partials
     // + splitk_reduce launch)
     bool cluster = true;
@@ -1202,13 +1204,13 @@ bool tc_supports(TcGemm *t, const GemmDesc &g) {
 }
 
 // variant: 0 = 1xTF32, 1 = 3xTF32, 2 = 3xF16
-template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false>
+template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false, bool FAST = false>
 static cudaError_t prepare(TcGemm *t) {
     using L = SmemLayout<BN, SPLIT, PAIR, F16>;
     const int slot = (SPLIT ? 1 : 0) + 2 * (BN == 128 ? 0 : BN == 64 ? 1 : BN == 32 ? 2 : 3) + (PAIR ? 8 : 0) +
-                     (MASK ? 16 : 0) + (F16 ? 32 : 0);
+                     (MASK ? 16 : 0) + (F16 ? 32 : 0) + (FAST ? 64 : 0);
     if (!t->attr_set[slot]) {
-        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16>,
+        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
         if (e != cudaSuccess) return e;
         t->attr_set[slot] = true;
@@ -1243,13 +1245,13 @@ static int co_resident_clusters(TcGemm *t, int cs) {
     return n;
 }
 
-template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false>
+template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false, bool FAST = false>
 static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s) {
     using L = SmemLayout<BN, SPLIT, PAIR, F16>;
-    cudaError_t e = prepare<BN, SPLIT, PAIR, MASK, F16>(t);
+    cudaError_t e = prepare<BN, SPLIT, PAIR, MASK, F16, FAST>(t);
     if (e != cudaSuccess) return e;
     if (!p.cluster && !PAIR)
-        return launch_pdl(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
+        return launch_pdl(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(L::THREADS);
@@ -1264,7 +1266,7 @@ static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s
     at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16>, p);
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST>, p);
 }
 
 // How many clusters of `cs` CTAs (cs / 2 CTA pairs) of the 128-wide pair variant can be resident at once.
@@ -1308,10 +1310,14 @@ static int co_resident_pair_v(TcGemm *t, int variant, int cs) {
 
 // One instantiation per (variant, BN, PAIR, MASK) the planner can pick.
 template <bool SPLIT, bool F16>
-static cudaError_t launch_variant(TcGemm *t, const TcParams &p, int grid, cudaStream_t s, int BN, bool pair, bool mask) {
+static cudaError_t launch_variant(TcGemm *t, const TcParams &p, int grid, cudaStream_t s, int BN, bool pair, bool mask,
+                                  bool fast) {
     if constexpr (F16) {
         if (pair && BN == 256)
             return mask ? launch<256, SPLIT, true, true, F16>(t, p, grid, s) : launch<256, SPLIT, true, false, F16>(t, p, grid, s);
+        if (fast && pair && BN == 128)  // every tile on the whole-tile fast epilogue
+            return mask ? launch<128, SPLIT, true, true, F16, true>(t, p, grid, s)
+                        : launch<128, SPLIT, true, false, F16, true>(t, p, grid, s);
     }
     if (pair && mask) return launch<128, SPLIT, true, true, F16>(t, p, grid, s);
     if (pair) return launch<128, SPLIT, true, false, F16>(t, p, grid, s);
@@ -1501,9 +1507,13 @@ static cudaError_t tc_gemm_impl(TcGemm *t, const GemmDesc &g, cudaStream_t s, La
     if (h) h->before(name, s);
     cudaError_t e;
     const bool mask = g.epi == EPI_MASK;  // dgrad: the masked-epilogue instantiation
-    e = variant == 2 ? launch_variant<true, true>(t, p, grid, s, BN, pair, mask)
-      : variant == 1 ? launch_variant<true, false>(t, p, grid, s, BN, pair, mask)
-                     : launch_variant<false, false>(t, p, grid, s, BN, pair, mask);
+    // 3xF16: every tile whole and on the fast epilogue (the kernel's `fast` test holds for all of them)
+    const bool fast_all = f16 && splits == 1 && !cluster && !(EXPER && p.dbg) && M % (pair ? 2 * BM : BM) == 0 &&
+                          N % BN == 0 && (p.fo.h ? p.fo.skip_f32 != 0 : (p.C && (p.ldc & 3) == 0 && !p.C_hi)) &&
+                          (mask ? p.mbits != nullptr : (p.epi == EPI_BIAS_RELU && ((uintptr_t)p.bias & 15) == 0));
+    e = variant == 2 ? launch_variant<true, true>(t, p, grid, s, BN, pair, mask, fast_all)
+      : variant == 1 ? launch_variant<true, false>(t, p, grid, s, BN, pair, mask, false)
+                     : launch_variant<false, false>(t, p, grid, s, BN, pair, mask, false);
     if (h) h->after(name, s);
     if (e != cudaSuccess) return e;
     if (splits > 1 && !cluster) {  // fold with the epilogue in a separate kernel
