@@ -476,8 +476,9 @@ __device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base, floa
 }
 
 // FAST (3xF16, 128-wide tiles): the host guarantees every tile takes the whole-tile fast epilogue (no ragged edge,
-// no split-K, planes-only or fp32-only output): the general epilogue and the cluster fold are compiled out of it
-template <int BN, bool SPLIT, bool PAIR, bool MASK, bool F16, bool FAST = false>
+// no split-K, planes-only or fp32-only output): the general epilogue and the cluster fold are compiled out of it.
+// CLU (3xF16 pairs): every launch is a split-K cluster (partials folded through DSMEM): the direct epilogue is out.
+template <int BN, bool SPLIT, bool PAIR, bool MASK, bool F16, bool FAST = false, bool CLU = false>
 __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
     using L = SmemLayout<BN, SPLIT, PAIR, F16>;
     constexpr int KB = F16 ? BKH : BK;        // elements per k-block (one 128-B row)
@@ -830,7 +831,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
 #pragma unroll
                 for (int j = 0; j < HALF; j++) acc[j] = (acc[j] * fa) * fb;
             }
-            if (!FAST && p.cluster) {  // partial tile -> own smem; folded across the cluster below
+            if (CLU || (!FAST && p.cluster)) {  // partial tile -> own smem; folded across the cluster below
                 const int row = 32 * q + lane;
 #pragma unroll
                 for (int j = 0; j < HALF / 4; j++)
@@ -1020,7 +1021,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
     }
 #undef MTX_UNITS
     if (warp == 4 && lane == 0) stamp(5);
-    if (!FAST && p.cluster) {
+    if (CLU || (!FAST && p.cluster)) {
         // every CTA of the cluster holds its split's partial tile: CTA z folds rows
         // [z*BM/S, (z+1)*BM/S) over the splits in ascending order (deterministic) and stores them
         // with the fused epilogue; the second barrier keeps every CTA's smem alive until read
@@ -1107,7 +1108,7 @@ bool make_map_mn3d(EncodeTiled enc, CUtensorMap *m, const void *ptr, int64_t row
 struct TcGemm {
     EncodeTiled encode = nullptr;
     int sms = 148;
-    bool attr_set[128] = {};
+    bool attr_set[256] = {};
     // split-K folded through distributed shared memory (MTX_TC_CLUSTER=0 disables: global partials
     // + splitk_reduce launch)
     bool cluster = true;
@@ -1204,13 +1205,13 @@ bool tc_supports(TcGemm *t, const GemmDesc &g) {
 }
 
 // variant: 0 = 1xTF32, 1 = 3xTF32, 2 = 3xF16
-template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false, bool FAST = false>
+template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false, bool FAST = false, bool CLU = false>
 static cudaError_t prepare(TcGemm *t) {
     using L = SmemLayout<BN, SPLIT, PAIR, F16>;
     const int slot = (SPLIT ? 1 : 0) + 2 * (BN == 128 ? 0 : BN == 64 ? 1 : BN == 32 ? 2 : 3) + (PAIR ? 8 : 0) +
-                     (MASK ? 16 : 0) + (F16 ? 32 : 0) + (FAST ? 64 : 0);
+                     (MASK ? 16 : 0) + (F16 ? 32 : 0) + (FAST ? 64 : 0) + (CLU ? 128 : 0);
     if (!t->attr_set[slot]) {
-        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST>,
+        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST, CLU>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
         if (e != cudaSuccess) return e;
         t->attr_set[slot] = true;
@@ -1245,13 +1246,13 @@ static int co_resident_clusters(TcGemm *t, int cs) {
     return n;
 }
 
-template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false, bool FAST = false>
+template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false, bool FAST = false, bool CLU = false>
 static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s) {
     using L = SmemLayout<BN, SPLIT, PAIR, F16>;
-    cudaError_t e = prepare<BN, SPLIT, PAIR, MASK, F16, FAST>(t);
+    cudaError_t e = prepare<BN, SPLIT, PAIR, MASK, F16, FAST, CLU>(t);
     if (e != cudaSuccess) return e;
     if (!p.cluster && !PAIR)
-        return launch_pdl(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
+        return launch_pdl(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST, CLU>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(L::THREADS);
@@ -1266,7 +1267,7 @@ static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s
     at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST>, p);
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST, CLU>, p);
 }
 
 // How many clusters of `cs` CTAs (cs / 2 CTA pairs) of the 128-wide pair variant can be resident at once.
@@ -1318,6 +1319,8 @@ static cudaError_t launch_variant(TcGemm *t, const TcParams &p, int grid, cudaSt
         if (fast && pair && BN == 128)  // every tile on the whole-tile fast epilogue
             return mask ? launch<128, SPLIT, true, true, F16, true>(t, p, grid, s)
                         : launch<128, SPLIT, true, false, F16, true>(t, p, grid, s);
+        if (p.cluster && pair && BN == 128 && !mask)  // split-K clusters of pairs (the weight gradients)
+            return launch<128, SPLIT, true, false, F16, false, true>(t, p, grid, s);
     }
     if (pair && mask) return launch<128, SPLIT, true, true, F16>(t, p, grid, s);
     if (pair) return launch<128, SPLIT, true, false, F16>(t, p, grid, s);
