@@ -477,8 +477,9 @@ __device__ __noinline__ void cluster_fold(const TcParams &p, uint32_t base, floa
 
 // FAST (3xF16, 128-wide tiles): the host guarantees every tile takes the whole-tile fast epilogue (no ragged edge,
 // no split-K, planes-only or fp32-only output): the general epilogue and the cluster fold are compiled out of it.
-// CLU (3xF16 pairs): every launch is a split-K cluster (partials folded through DSMEM): the direct epilogue is out.
-template <int BN, bool SPLIT, bool PAIR, bool MASK, bool F16, bool FAST = false, bool CLU = false>
+// CLU (3xF16): every launch is a split-K cluster (partials folded through DSMEM): the direct epilogue is out.
+// PART (3xF16): split-K partials to global memory only (folded by splitk_reduce): the output epilogues are out.
+template <int BN, bool SPLIT, bool PAIR, bool MASK, bool F16, bool FAST = false, bool CLU = false, bool PART = false>
 __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
     using L = SmemLayout<BN, SPLIT, PAIR, F16>;
     constexpr int KB = F16 ? BKH : BK;        // elements per k-block (one 128-B row)
@@ -784,7 +785,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
             // L2 latency hides behind the MMAs instead of stalling the store phase).  Word k of the rl group
             // (8 lanes) = (sub-tile k / 8, row group k % 8); lane jj holds words 2 jj and 2 jj + 1.
             // (HALF = 128: 4 sub-tiles, words 4 jj .. 4 jj + 3)
-            constexpr bool PRE_BITS = F16 && MASK && (HALF == 64 || HALF == 128);
+            constexpr bool PRE_BITS = F16 && MASK && !PART && (HALF == 64 || HALF == 128);
             constexpr int NW = HALF / 32;  // mask words per lane
             uint32_t mw[NW > 0 ? NW : 1];
 #pragma unroll
@@ -831,7 +832,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
 #pragma unroll
                 for (int j = 0; j < HALF; j++) acc[j] = (acc[j] * fa) * fb;
             }
-            if (CLU || (!FAST && p.cluster)) {  // partial tile -> own smem; folded across the cluster below
+            if (CLU || (!FAST && !PART && p.cluster)) {  // partial tile -> own smem; folded across the cluster below
                 const int row = 32 * q + lane;
 #pragma unroll
                 for (int j = 0; j < HALF / 4; j++)
@@ -848,11 +849,11 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
             const int jj = lane % CPR, rl = lane / CPR;
             auto swz = [](int row, int chunk) { return (chunk ^ (row / (8 / CPR))) & (CPR - 1); };
             // 3xF16 lean outputs (direct path only): the forward's ReLU bitmask, the dgrad's per-32-row column sums
-            const bool want_bits = F16 && p.fo.bits && p.splits == 1;
-            const bool want_cols = F16 && p.fo.colpart && p.splits == 1;
+            const bool want_bits = F16 && !PART && p.fo.bits && p.splits == 1;
+            const bool want_cols = F16 && !PART && p.fo.colpart && p.splits == 1;
             // 3xF16 lean fast path: a whole 32-row x 64-column piece in range, planes only (no fp32 copy, no split-K),
             // forward (bias + ReLU [+ bits]) or dgrad (bitmask [+ column sums]): no per-element bounds or mode tests
-            if constexpr (F16 && (HALF == 64 || HALF == 128)) {
+            if constexpr (F16 && !PART && (HALF == 64 || HALF == 128)) {
                 // output: the fp16 planes alone (lean), or the fp32 copy alone (a layer the SIMT head consumes)
                 const bool planes = p.fo.h != nullptr;
                 const bool fast = FAST || p.splits == 1 && (planes ? p.fo.skip_f32 : (p.C && (p.ldc & 3) == 0 && !p.C_hi)) &&
@@ -953,7 +954,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                                                 (w & 8u) ? 1.f : 0.f);
                             continue;
                         }
-                        mk[u] = (MASK && p.splits == 1 && it0 + u < ITS && m < p.M && n < p.N)
+                        mk[u] = (MASK && !PART && p.splits == 1 && it0 + u < ITS && m < p.M && n < p.N)
                                     ? load_mask(p, m, n)
                                     : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
@@ -974,7 +975,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                             }
                         }
                         float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-                        if (ok && p.splits == 1) o = epi_store<MASK, F16>(p, m, n, sv, mk[u], inv_so, amx, bz);
+                        if (!PART && ok && p.splits == 1) o = epi_store<MASK, F16>(p, m, n, sv, mk[u], inv_so, amx, bz);
                         if (want_bits) {  // the 8 lanes of a row hold its 32 columns: OR their nibbles into one word
                             uint32_t w = ((o.x > 0.f) | ((o.y > 0.f) << 1) | ((o.z > 0.f) << 2) | ((o.w > 0.f) << 3))
                                          << (4 * jj);
@@ -1006,7 +1007,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
                 __syncwarp();
             }
         }
-        if (F16 && p.fo.h && !p.cluster) {  // amax of the planes written (the next consumer's bound): one atomic per CTA
+        if (F16 && !PART && p.fo.h && !p.cluster) {  // amax of the planes written (the next consumer's bound): one atomic per CTA
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, o));
             float *red = (float *)(smem + L::EPI_OFF);  // the staging area is free once the last tile is stored
@@ -1021,7 +1022,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, SPLIT, PAIR>::THREADS, 1) tc_ge
     }
 #undef MTX_UNITS
     if (warp == 4 && lane == 0) stamp(5);
-    if (CLU || (!FAST && p.cluster)) {
+    if (CLU || (!FAST && !PART && p.cluster)) {
         // every CTA of the cluster holds its split's partial tile: CTA z folds rows
         // [z*BM/S, (z+1)*BM/S) over the splits in ascending order (deterministic) and stores them
         // with the fused epilogue; the second barrier keeps every CTA's smem alive until read
@@ -1108,7 +1109,7 @@ bool make_map_mn3d(EncodeTiled enc, CUtensorMap *m, const void *ptr, int64_t row
 struct TcGemm {
     EncodeTiled encode = nullptr;
     int sms = 148;
-    bool attr_set[256] = {};
+    bool attr_set[512] = {};
     // split-K folded through distributed shared memory (MTX_TC_CLUSTER=0 disables: global partials
     // + splitk_reduce launch)
     bool cluster = true;
@@ -1205,13 +1206,14 @@ bool tc_supports(TcGemm *t, const GemmDesc &g) {
 }
 
 // variant: 0 = 1xTF32, 1 = 3xTF32, 2 = 3xF16
-template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false, bool FAST = false, bool CLU = false>
+template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false, bool FAST = false, bool CLU = false,
+          bool PART = false>
 static cudaError_t prepare(TcGemm *t) {
     using L = SmemLayout<BN, SPLIT, PAIR, F16>;
     const int slot = (SPLIT ? 1 : 0) + 2 * (BN == 128 ? 0 : BN == 64 ? 1 : BN == 32 ? 2 : 3) + (PAIR ? 8 : 0) +
-                     (MASK ? 16 : 0) + (F16 ? 32 : 0) + (FAST ? 64 : 0) + (CLU ? 128 : 0);
+                     (MASK ? 16 : 0) + (F16 ? 32 : 0) + (FAST ? 64 : 0) + (CLU ? 128 : 0) + (PART ? 256 : 0);
     if (!t->attr_set[slot]) {
-        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST, CLU>,
+        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST, CLU, PART>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
         if (e != cudaSuccess) return e;
         t->attr_set[slot] = true;
@@ -1246,13 +1248,15 @@ static int co_resident_clusters(TcGemm *t, int cs) {
     return n;
 }
 
-template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false, bool FAST = false, bool CLU = false>
+template <int BN, bool SPLIT, bool PAIR = false, bool MASK = false, bool F16 = false, bool FAST = false, bool CLU = false,
+          bool PART = false>
 static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s) {
     using L = SmemLayout<BN, SPLIT, PAIR, F16>;
-    cudaError_t e = prepare<BN, SPLIT, PAIR, MASK, F16, FAST, CLU>(t);
+    cudaError_t e = prepare<BN, SPLIT, PAIR, MASK, F16, FAST, CLU, PART>(t);
     if (e != cudaSuccess) return e;
     if (!p.cluster && !PAIR)
-        return launch_pdl(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST, CLU>, dim3(grid), dim3(L::THREADS), L::TOTAL, s, p);
+        return launch_pdl(tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST, CLU, PART>, dim3(grid), dim3(L::THREADS),
+                          L::TOTAL, s, p);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(L::THREADS);
@@ -1267,7 +1271,7 @@ static cudaError_t launch(TcGemm *t, const TcParams &p, int grid, cudaStream_t s
     at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST, CLU>, p);
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, SPLIT, PAIR, MASK, F16, FAST, CLU, PART>, p);
 }
 
 // How many clusters of `cs` CTAs (cs / 2 CTA pairs) of the 128-wide pair variant can be resident at once.
@@ -1319,8 +1323,11 @@ static cudaError_t launch_variant(TcGemm *t, const TcParams &p, int grid, cudaSt
         if (fast && pair && BN == 128)  // every tile on the whole-tile fast epilogue
             return mask ? launch<128, SPLIT, true, true, F16, true>(t, p, grid, s)
                         : launch<128, SPLIT, true, false, F16, true>(t, p, grid, s);
-        if (p.cluster && pair && BN == 128 && !mask)  // split-K clusters of pairs (the weight gradients)
-            return launch<128, SPLIT, true, false, F16, false, true>(t, p, grid, s);
+        if (p.cluster && BN == 128 && !mask)  // split-K clusters (the weight gradients)
+            return pair ? launch<128, SPLIT, true, false, F16, false, true>(t, p, grid, s)
+                        : launch<128, SPLIT, false, false, F16, false, true>(t, p, grid, s);
+        if (p.splits > 1 && !p.cluster && !pair && BN == 128 && !mask)  // split-K partials (narrow weight gradients)
+            return launch<128, SPLIT, false, false, F16, false, false, true>(t, p, grid, s);
     }
     if (pair && mask) return launch<128, SPLIT, true, true, F16>(t, p, grid, s);
     if (pair) return launch<128, SPLIT, true, false, F16>(t, p, grid, s);
