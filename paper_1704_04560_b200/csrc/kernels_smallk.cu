@@ -21,7 +21,10 @@ constexpr int SK_M = 128, SK_N = 128, SK_T = 256;
 // columns 8 tx .. 8 tx + 7.  Outputs: fp32 C (unless fo.skip_f32), fp16 planes + amax (fo.h), ReLU bits (fo.bits).
 // KP: K rounded up (16 / 32 / 64; the k loop is unrolled, A is staged transposed so a thread's 8 rows are two
 // 128-bit shared loads, zero rows past K add nothing).
-template <int KP>
+// KL: k-loop trip count (KP, or K itself when it is a multiple of 4 below KP: cfg4's 28 features skip 4 zero rows).
+// LEAN: the 3xF16 lean forward (bias + ReLU, planes + bits, no fp32 copy, N % 128 == 0): the other output paths and
+// the column-edge tests are compiled out.
+template <int KP, int KL = KP, bool LEAN = false>
 __global__ void __launch_bounds__(SK_T, 2) fwd_smallk_kernel(int M, int N, int K, const float *__restrict__ A, int64_t lda,
                                                            RowSel arow, const float *__restrict__ W, int64_t ldw,
                                                            const float *__restrict__ bias, int relu, float *__restrict__ C,
@@ -73,7 +76,7 @@ __global__ void __launch_bounds__(SK_T, 2) fwd_smallk_kernel(int M, int N, int K
     // unrolled by 8, not fully: the fully unrolled body missed in the instruction cache (ncu: 18 % of the warp
     // samples stalled on no instruction)
 #pragma unroll 8
-    for (int k = 0; k < KP; k++) {
+    for (int k = 0; k < KL; k++) {
         const float4 a0 = *(const float4 *)(As + k * SK_M + 8 * ty), a1 = *(const float4 *)(As + k * SK_M + 8 * ty + 4);
         const float4 b0 = *(const float4 *)(Ws + k * SK_N + 8 * tx), b1 = *(const float4 *)(Ws + k * SK_N + 8 * tx + 4);
         const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
@@ -86,11 +89,12 @@ __global__ void __launch_bounds__(SK_T, 2) fwd_smallk_kernel(int M, int N, int K
     const int nb = n0 + 8 * tx;
     float bz[8];
 #pragma unroll
-    for (int j = 0; j < 8; j++) bz[j] = (bias && nb + j < N) ? __ldg(bias + nb + j) : 0.f;
-    const float inv_so = fo.h ? 1.f / f16out_scale(fo) : 1.f;
-    if (fo.h && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) fo.ts->scale = 1.f / inv_so;
+    for (int j = 0; j < 8; j++) bz[j] = LEAN ? __ldg(bias + nb + j) : (bias && nb + j < N) ? __ldg(bias + nb + j) : 0.f;
+    const bool planes = LEAN || fo.h;
+    const float inv_so = planes ? 1.f / f16out_scale(fo) : 1.f;
+    if (planes && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) fo.ts->scale = 1.f / inv_so;
     float amx = 0.f;
-    const bool full = nb + 7 < N;
+    const bool full = LEAN || nb + 7 < N;
 #pragma unroll  // fully: acc[i][.] must stay in registers
     for (int i = 0; i < 8; i++) {
         const int m = m0 + 8 * ty + i;
@@ -99,8 +103,8 @@ __global__ void __launch_bounds__(SK_T, 2) fwd_smallk_kernel(int M, int N, int K
 #pragma unroll
         for (int j = 0; j < 8; j++) {
             o[j] = acc[i][j] + bz[j];
-            if (relu) o[j] = fmaxf(o[j], 0.f);
-            if (nb + j >= N) o[j] = 0.f;
+            if (LEAN || relu) o[j] = fmaxf(o[j], 0.f);
+            if (!LEAN && nb + j >= N) o[j] = 0.f;
             bits |= (o[j] > 0.f ? 1u : 0u) << j;
             amx = fmaxf(amx, fabsf(o[j]));
         }
@@ -108,9 +112,9 @@ __global__ void __launch_bounds__(SK_T, 2) fwd_smallk_kernel(int M, int N, int K
         uint32_t w = bits << (8 * (tx & 3));
         w |= __shfl_xor_sync(0xffffffffu, w, 1);
         w |= __shfl_xor_sync(0xffffffffu, w, 2);
-        if (m >= M || nb >= N) continue;
-        if (fo.bits && (tx & 3) == 0) fo.bits[(int64_t)m * fo.bits_ld + (nb >> 5)] = w;
-        if (C && !fo.skip_f32) {
+        if (m >= M || (!LEAN && nb >= N)) continue;
+        if ((LEAN || fo.bits) && (tx & 3) == 0) fo.bits[(int64_t)m * fo.bits_ld + (nb >> 5)] = w;
+        if (!LEAN && C && !fo.skip_f32) {
             if (full) {
                 *(float4 *)(C + (int64_t)m * ldc + nb) = make_float4(o[0], o[1], o[2], o[3]);
                 *(float4 *)(C + (int64_t)m * ldc + nb + 4) = make_float4(o[4], o[5], o[6], o[7]);
@@ -118,7 +122,7 @@ __global__ void __launch_bounds__(SK_T, 2) fwd_smallk_kernel(int M, int N, int K
                 for (int j = 0; j < 8 && nb + j < N; j++) C[(int64_t)m * ldc + nb + j] = o[j];
             }
         }
-        if (fo.h) {
+        if (planes) {
             uint32_t hp[4], lp[4];
 #pragma unroll
             for (int e = 0; e < 4; e++) {
@@ -141,7 +145,7 @@ __global__ void __launch_bounds__(SK_T, 2) fwd_smallk_kernel(int M, int N, int K
             }
         }
     }
-    if (fo.h) {  // one atomic per CTA (thousands of warps on one address would serialise)
+    if (planes) {  // one atomic per CTA (thousands of warps on one address would serialise)
         __shared__ float red[SK_T / 32];
         for (int off = 16; off > 0; off >>= 1) amx = fmaxf(amx, __shfl_xor_sync(0xffffffffu, amx, off));
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amx;
@@ -167,6 +171,8 @@ cudaError_t fwd_smallk(int M, int N, int K, const float *A, int64_t lda, RowSel 
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(fwd_smallk_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(fwd_smallk_kernel<64, 64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -174,7 +180,11 @@ cudaError_t fwd_smallk(int M, int N, int K, const float *A, int64_t lda, RowSel 
     snprintf(name, sizeof name, "fwd_smallk[M=%d,N=%d,K=%d]", M, N, K);
     if (h) h->before(name, s);
     const dim3 grid((N + SK_N - 1) / SK_N, (M + SK_M - 1) / SK_M);
-    auto kern = KP == 16 ? fwd_smallk_kernel<16> : KP == 32 ? fwd_smallk_kernel<32> : fwd_smallk_kernel<64>;
+    const bool lean = fo.h && fo.skip_f32 && fo.bits && bias && relu && N % SK_N == 0 && fo.ld % 8 == 0;
+    auto kern = KP == 16 ? (lean ? fwd_smallk_kernel<16, 16, true> : fwd_smallk_kernel<16>)
+              : K == 28  ? (lean ? fwd_smallk_kernel<32, 28, true> : fwd_smallk_kernel<32, 28>)
+              : KP == 32 ? (lean ? fwd_smallk_kernel<32, 32, true> : fwd_smallk_kernel<32>)
+                         : (lean ? fwd_smallk_kernel<64, 64, true> : fwd_smallk_kernel<64>);
     launch_pdl(kern, grid, dim3(SK_T), smem, s, M, N, K, A, lda, arow, W, ldw, bias, relu ? 1 : 0, C, ldc, fo);
     if (h) h->after(name, s);
     return cudaGetLastError();
