@@ -1313,7 +1313,24 @@ static int co_resident_pair_v(TcGemm *t, int variant, int cs) {
                         : co_resident_pair<false, false>(t, cs);
 }
 
-// One instantiation per (variant, BN, PAIR, MASK) the planner can pick.
+// Unpaired tiles of width BN, with or without the dgrad mask, in epilogue mode (FAST, CLU, PART).
+template <bool SPLIT, bool F16, bool FAST, bool CLU, bool PART>
+static cudaError_t launch_unpaired(TcGemm *t, const TcParams &p, int grid, cudaStream_t s, int BN, bool mask) {
+    if (mask) {
+        if (BN == 128) return launch<128, SPLIT, false, true, F16, FAST, CLU, PART>(t, p, grid, s);
+        if (BN == 64) return launch<64, SPLIT, false, true, F16, FAST, CLU, PART>(t, p, grid, s);
+        if constexpr (!F16) return launch<32, SPLIT, false, true, F16, FAST, CLU, PART>(t, p, grid, s);
+        return cudaErrorInvalidValue;
+    }
+    if (BN == 128) return launch<128, SPLIT, false, false, F16, FAST, CLU, PART>(t, p, grid, s);
+    if (BN == 64) return launch<64, SPLIT, false, false, F16, FAST, CLU, PART>(t, p, grid, s);
+    if constexpr (!F16) return launch<32, SPLIT, false, false, F16, FAST, CLU, PART>(t, p, grid, s);
+    return cudaErrorInvalidValue;
+}
+
+// One instantiation per (variant, BN, PAIR, MASK, epilogue mode) the planner can pick.  The split engines (3xTF32,
+// 3xF16) get kernels specialised to the launch's epilogue -- split-K cluster fold only (CLU), split-K partials only
+// (PART), whole-tile fast epilogue only (FAST, 3xF16 pairs): code a launch never runs still cost it time.
 template <bool SPLIT, bool F16>
 static cudaError_t launch_variant(TcGemm *t, const TcParams &p, int grid, cudaStream_t s, int BN, bool pair, bool mask,
                                   bool fast) {
@@ -1323,24 +1340,16 @@ static cudaError_t launch_variant(TcGemm *t, const TcParams &p, int grid, cudaSt
         if (fast && pair && BN == 128)  // every tile on the whole-tile fast epilogue
             return mask ? launch<128, SPLIT, true, true, F16, true>(t, p, grid, s)
                         : launch<128, SPLIT, true, false, F16, true>(t, p, grid, s);
-        if (p.cluster && BN == 128 && !mask)  // split-K clusters (the weight gradients)
-            return pair ? launch<128, SPLIT, true, false, F16, false, true>(t, p, grid, s)
-                        : launch<128, SPLIT, false, false, F16, false, true>(t, p, grid, s);
-        if (p.splits > 1 && !p.cluster && !pair && BN == 128 && !mask)  // split-K partials (narrow weight gradients)
-            return launch<128, SPLIT, false, false, F16, false, false, true>(t, p, grid, s);
+        if (p.cluster && pair && BN == 128 && !mask)  // split-K clusters of pairs (the weight gradients)
+            return launch<128, SPLIT, true, false, F16, false, true>(t, p, grid, s);
+    }
+    if constexpr (SPLIT) {
+        if (p.cluster && !pair) return launch_unpaired<SPLIT, F16, false, true, false>(t, p, grid, s, BN, mask);
+        if (p.splits > 1 && !p.cluster && !pair) return launch_unpaired<SPLIT, F16, false, false, true>(t, p, grid, s, BN, mask);
     }
     if (pair && mask) return launch<128, SPLIT, true, true, F16>(t, p, grid, s);
     if (pair) return launch<128, SPLIT, true, false, F16>(t, p, grid, s);
-    if (mask) {
-        if (BN == 128) return launch<128, SPLIT, false, true, F16>(t, p, grid, s);
-        if (BN == 64) return launch<64, SPLIT, false, true, F16>(t, p, grid, s);
-        if constexpr (!F16) return launch<32, SPLIT, false, true, F16>(t, p, grid, s);
-        return cudaErrorInvalidValue;
-    }
-    if (BN == 128) return launch<128, SPLIT, false, false, F16>(t, p, grid, s);
-    if (BN == 64) return launch<64, SPLIT, false, false, F16>(t, p, grid, s);
-    if constexpr (!F16) return launch<32, SPLIT, false, false, F16>(t, p, grid, s);
-    return cudaErrorInvalidValue;
+    return launch_unpaired<SPLIT, F16, false, false, false>(t, p, grid, s, BN, mask);
 }
 
 // launch == false: only the plan -- *splits_out = the K-splits the launch would use (1: the direct epilogue,
