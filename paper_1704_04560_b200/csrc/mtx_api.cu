@@ -616,7 +616,12 @@ bool smallm_on() {
     return v;
 }
 // 3xF16 at P > 1 with the one-launch fused update: it leaves the per-rank maxima of the updated weights
-bool wmax_fused(const mtx_ctx *c) { return c->f16 && c->world > 1 && c->fused && c->wmax && !fused_overlap(c); }
+int comm_sms();
+// 3xF16 at P > 1: the fused update leaves per-CTA maxima of the new weights (every bucket launch within WMAX_SLOTS)
+bool wmax_fused(const mtx_ctx *c) {
+    return c->f16 && c->world > 1 && c->fused && c->wmax &&
+           (!fused_overlap(c) || (int64_t)c->buckets.size() * comm_sms() <= WMAX_SLOTS);
+}
 // 3xF16 parameter planes (one scale over the whole flat buffer, biases included: it bounds every bias
 // read by the forward epilogues); resets the per-step slots' amax (their producers run after this)
 // pre_parts > 0: the update launch just before left that many per-CTA maxima of the new parameters in qscr[scr]
@@ -1118,7 +1123,7 @@ struct Runner {
                 if (e == cudaSuccess)
                     e = fused_bucket_update(c->pp, P, c->rank, 0, c->stepctr, 0, c->N_pad, c->opt.lr, c->opt.momentum,
                                             c->opt.momentum != 0.f, c->flag, win, c->B, c->n_data, c->N_pad, 148, s, h,
-                                            c->f16, true);
+                                            wmax_fused(c), true);
                 if (e == cudaSuccess) e = peer_barrier_step(c->pp, P, c->rank, c->epoch, c->flag, c->stepctr, s, h);
                 if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "fused push update: %s", cudaGetErrorString(e));
                 return MTX_OK;
@@ -1132,7 +1137,7 @@ struct Runner {
             cudaError_t e = fused_bucket_update(c->pp, c->world, c->rank, ov ? bi : 0, c->stepctr, lo, hi, c->opt.lr,
                                                 c->opt.momentum, c->opt.momentum != 0.f, c->flag, win, c->B, c->n_data,
                                                 has_loss ? c->N_pad : -1, ov ? comm_sms() : 148, cs, h,
-                                                c->f16 && !ov);
+                                                wmax_fused(c));
             if (e == cudaSuccess && last)
                 e = peer_barrier_step(c->pp, c->world, c->rank, c->epoch, c->flag, c->stepctr, cs, h);
             if (e != cudaSuccess) return fail(c, MTX_ERR_CUDA, "fused update: %s", cudaGetErrorString(e));
@@ -1211,7 +1216,7 @@ struct Runner {
         if (c->f16) {  // 3xF16: same, with the per-tensor scales (P = 1: the previous update wrote the parameters')
             // P > 1 with the fused update: its per-rank maxima of the new weights give the scale directly
             if (c->world > 1)
-                if (mtx_status st = quantize_params(c, 0, s, h, wmax_fused(c) ? c->world * 148 : 0)) return st;
+                if (mtx_status st = quantize_params(c, 0, s, h, wmax_fused(c) ? c->world * WMAX_SLOTS : 0)) return st;
             if (staged)
                 if (mtx_status st = quantize_buffer(c, sx, c->b, c->d0, c->d0, 0, s, h)) return st;
         }
@@ -1461,7 +1466,7 @@ mtx_status refresh_param_planes(mtx_ctx *c, cudaStream_t s) {
     if (c->f16) {
         if (mtx_status st = quantize_params(c, 1, s, nullptr)) return st;
         if (wmax_fused(c)) {  // seed the fused update's maxima with the exact max (the next step's quantize folds them)
-            CK(cudaMemsetAsync(c->wmax, 0, 4 * (size_t)c->world * 148, s));
+            CK(cudaMemsetAsync(c->wmax, 0, 4 * (size_t)c->world * WMAX_SLOTS, s));
             CK(cudaMemcpyAsync(c->wmax, &c->tsl[mtx_ctx::TS_PARAMS].amax, 4, cudaMemcpyDeviceToDevice, s));
         }
         return MTX_OK;

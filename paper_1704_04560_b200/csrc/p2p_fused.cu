@@ -163,14 +163,14 @@ __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, i
         }
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
-    if (track_wmax) {  // this CTA's max |w| into slot [rank][CTA] of every replica's array (3xF16 planes' scale)
+    if (track_wmax) {  // this CTA's max |w| into slot [rank][track_wmax - 1 + CTA] of every replica's array (3xF16 scale)
         for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = wmax;
         __syncthreads();
         if (threadIdx.x < P) {
             float m = red[0];
             for (int k = 1; k < (int)(blockDim.x >> 5); k++) m = fmaxf(m, red[k]);
-            pp.wmax[threadIdx.x][rank * gridDim.x + blockIdx.x] = m;
+            pp.wmax[threadIdx.x][rank * WMAX_SLOTS + track_wmax - 1 + blockIdx.x] = m;
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -266,6 +266,7 @@ cudaError_t fused_bucket_update(const PeerPtrs &pp, int P, int rank, int bucket,
                                 int64_t n_data, int64_t loss_idx, int ctas, cudaStream_t s, LaunchHook *h,
                                 bool track_wmax, bool from_stage) {
     if (P > MAX_PEERS || bucket >= MAX_BUCKETS || lo % 4 || hi % 4) return cudaErrorInvalidValue;
+    if (track_wmax && (bucket + 1) * std::max(1, ctas) > WMAX_SLOTS) return cudaErrorInvalidValue;
     int64_t a, b;
     bucket_share(lo, hi, P, rank, a, b);
     // push protocol: the landing area's row pitch is the longest share
@@ -281,7 +282,8 @@ cudaError_t fused_bucket_update(const PeerPtrs &pp, int P, int rank, int bucket,
     auto kern = P <= 4 ? (has_v ? fused_bucket_kernel<true, 4, 4> : fused_bucket_kernel<false, 4, 4>)
                        : (has_v ? fused_bucket_kernel<true, 2, MAX_PEERS> : fused_bucket_kernel<false, 2, MAX_PEERS>);
     launch_pdl(kern, dim3(std::max(1, ctas)), dim3(512), 0, s, pp, P, rank, bucket, stepctr, a / 4, b / 4, invP, lr, mu,
-               flag, win, B, n_data, loss_idx, (track_wmax && pp.wmax[0]) ? 1 : 0, dbg_ts, share4);
+               flag, win, B, n_data, loss_idx, (track_wmax && pp.wmax[0]) ? 1 + bucket * std::max(1, ctas) : 0, dbg_ts,
+               share4);
     if (h) h->after(name, s);
     return cudaGetLastError();
 }

@@ -26,6 +26,9 @@ struct PeerPtrs {
 };
 
 constexpr int MAX_BUCKETS = 64;
+// 3xF16 per-rank maxima of the updated weights: slots [rank][WMAX_SLOTS]; bucket b's launch of `ctas` CTAs writes
+// slots b * ctas .. (b + 1) * ctas - 1 (one launch: 0 .. 147)
+constexpr int WMAX_SLOTS = 148;
 // bflags slot of the push protocol's "all my gradient pushes have landed" epochs ([PUSH_SLOT][source rank])
 constexpr int PUSH_SLOT = MAX_BUCKETS - 1;
 
