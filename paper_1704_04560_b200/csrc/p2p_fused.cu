@@ -83,7 +83,7 @@ __device__ __forceinline__ bool wait_flags(const uint64_t *mine, int P, uint64_t
     return true;
 }
 
-template <bool HAS_V, int U, int PM>  // PM: peers the arrays hold (P <= PM)
+template <bool HAS_V, int U, int PM, bool STAGE>  // PM: peers the arrays hold (P <= PM); STAGE: push protocol
 __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, int rank, int bucket,
                                                          const uint64_t *stepctr, int64_t lo4, int64_t hi4, float invP,
                                                          float lr, float mu, int *flag, int64_t *win, int64_t B,
@@ -91,42 +91,58 @@ __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, i
                                                          int64_t share4) {
     pdl_wait();
     uint64_t t_in = 0, t_go = 0;
-    if (dbg_ts && threadIdx.x == 0) t_in = globaltimer();
+    if (MTX_TRACE && dbg_ts && threadIdx.x == 0) t_in = globaltimer();
     __shared__ int go;
     __shared__ float red[16];
     float wmax = 0.f;
     const uint64_t epoch = *(volatile const uint64_t *)stepctr + 1;
-    // push protocol (share4 > 0): the peers' gradients of this share sit in the local landing area
-    const float4 *stage4 = share4 > 0 ? (const float4 *)pp.stage[rank] : nullptr;
+    // this rank's pointers, picked with constant indices (a run-time index into the parameter arrays would copy them
+    // to local memory)
+    float4 *w_me = nullptr, *v_me = nullptr, *G_me = nullptr;
+    const float4 *stage4 = nullptr;  // push protocol: the peers' gradients of this share in the local landing area
+    const uint64_t *bfl_me = nullptr;
+#pragma unroll
+    for (int q = 0; q < MAX_PEERS; q++)
+        if (q == rank) {
+            w_me = (float4 *)pp.w[q];
+            v_me = (float4 *)pp.v[q];
+            G_me = (float4 *)pp.G[q];
+            if (STAGE) stage4 = (const float4 *)pp.stage[q];
+            bfl_me = pp.bflags[q];
+        }
     if (threadIdx.x == 0) {
         go = 0;
         if (!(*(volatile int *)flag & 2)) {
-            if (!stage4 && blockIdx.x == 0) {  // publish "my bucket is ready" in every peer's flag array
+            if (!STAGE && blockIdx.x == 0) {  // publish "my bucket is ready" in every peer's flag array
                 __threadfence_system();
-                for (int q = 0; q < P; q++) st_release_sys(pp.bflags[q] + bucket * MAX_PEERS + rank, epoch);
+#pragma unroll
+                for (int q = 0; q < MAX_PEERS; q++)
+                    if (q < P) st_release_sys(pp.bflags[q] + bucket * MAX_PEERS + rank, epoch);
             }
-            go = wait_flags(pp.bflags[rank] + (stage4 ? PUSH_SLOT : bucket) * MAX_PEERS, P, epoch, flag) ? 1 : 0;
+            go = wait_flags(bfl_me + (STAGE ? PUSH_SLOT : bucket) * MAX_PEERS, P, epoch, flag) ? 1 : 0;
         }
     }
     __syncthreads();
     if (!go) return;  // a peer timed out: load and store nothing (the context is poisoned at the next sync)
-    if (dbg_ts && threadIdx.x == 0) t_go = globaltimer();
+    if (MTX_TRACE && dbg_ts && threadIdx.x == 0) t_go = globaltimer();
     bool bad = false;
     // U float4 per peer per thread in flight (U*P loads over NVLink: the kernel is latency-bound on them), then the
     // ascending-rank fold, the update and w to every replica
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = lo4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < hi4; i0 += U * stride) {
         float4 gq[U][PM];
+        // predicated, not `break`: a loop exit inside the unrolled loads put gq in local memory (256-B stack frame)
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int64_t iu = i0 + u * stride;
-            if (iu >= hi4) break;
 #pragma unroll
-            for (int q = 0; q < PM; q++)
-                if (q < P) {
-                    if (stage4 && q != rank) gq[u][q] = __ldcv(stage4 + q * share4 + (iu - lo4));
+            for (int q = 0; q < PM; q++) {
+                gq[u][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (q < P && iu < hi4) {
+                    if (STAGE && q != rank) gq[u][q] = __ldcv(stage4 + q * share4 + (iu - lo4));
                     else gq[u][q] = __ldcv((const float4 *)pp.g[q] + iu);
                 }
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -140,8 +156,8 @@ __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, i
                     G.x = __fadd_rn(G.x, x.x); G.y = __fadd_rn(G.y, x.y);
                     G.z = __fadd_rn(G.z, x.z); G.w = __fadd_rn(G.w, x.w);
                 }
-            float4 w = ((const float4 *)pp.w[rank])[i], v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (HAS_V) v = ((const float4 *)pp.v[rank])[i];
+            float4 w = w_me[i], v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (HAS_V) v = v_me[i];
             float gb[4] = {G.x * invP, G.y * invP, G.z * invP, G.w * invP};
             float *pw = &w.x, *pv = &v.x;
 #pragma unroll
@@ -157,8 +173,8 @@ __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, i
 #pragma unroll
             for (int q = 0; q < MAX_PEERS; q++)
                 if (q < P) __stcg((float4 *)pp.w[q] + i, w);
-            if (HAS_V) __stcg((float4 *)pp.v[rank] + i, v);
-            __stcg((float4 *)pp.G[rank] + i, G);
+            if (HAS_V) __stcg(v_me + i, v);
+            __stcg(G_me + i, G);
             wmax = fmaxf(wmax, fmaxf(fmaxf(fabsf(w.x), fabsf(w.y)), fmaxf(fabsf(w.z), fabsf(w.w))));
         }
     }
@@ -167,17 +183,21 @@ __global__ void __launch_bounds__(512) fused_bucket_kernel(PeerPtrs pp, int P, i
         for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = wmax;
         __syncthreads();
-        if (threadIdx.x < P) {
+        if (threadIdx.x == 0) {
             float m = red[0];
             for (int k = 1; k < (int)(blockDim.x >> 5); k++) m = fmaxf(m, red[k]);
-            pp.wmax[threadIdx.x][rank * WMAX_SLOTS + track_wmax - 1 + blockIdx.x] = m;
+#pragma unroll
+            for (int q = 0; q < MAX_PEERS; q++)
+                if (q < P) pp.wmax[q][rank * WMAX_SLOTS + track_wmax - 1 + blockIdx.x] = m;
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (loss_idx >= 0) {  // every rank folds all ranks' local loss sums itself (same order, same bits)
             float L = __ldcv(pp.g[0] + loss_idx);
-            for (int q = 1; q < P; q++) L = __fadd_rn(L, __ldcv(pp.g[q] + loss_idx));
-            pp.G[rank][loss_idx + 1] = L;
+#pragma unroll
+            for (int q = 1; q < MAX_PEERS; q++)
+                if (q < P) L = __fadd_rn(L, __ldcv(pp.g[q] + loss_idx));
+            ((float *)G_me)[loss_idx + 1] = L;
         }
         if (win) *win = (*win + B) % n_data;
     }
@@ -230,10 +250,14 @@ cudaError_t p2p_preload() {
     // issued while a peer barrier spins on this GPU (mtx_debug_reduce's simulated ranks) would deadlock
     cudaFuncAttributes a;
     cudaError_t e = cudaFuncGetAttributes(&a, (const void *)peer_barrier_kernel);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<true, 2, MAX_PEERS>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<false, 2, MAX_PEERS>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<true, 4, 4>);
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<false, 4, 4>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<true, 2, MAX_PEERS, false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<false, 2, MAX_PEERS, false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<true, 4, 4, false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<false, 4, 4, false>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<true, 2, MAX_PEERS, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<false, 2, MAX_PEERS, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<true, 4, 4, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)fused_bucket_kernel<false, 4, 4, true>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)push_done_kernel);
     return e;
 }
@@ -279,8 +303,13 @@ cudaError_t fused_bucket_update(const PeerPtrs &pp, int P, int rank, int bucket,
     const float invP = 1.0f / (float)P;
     static const int dbg_ts = getenv("MTX_FUSED_TS") ? atoi(getenv("MTX_FUSED_TS")) : 0;
     // 4 float4 per peer in flight up to P = 4 (16 loads per thread), 2 beyond (register budget)
-    auto kern = P <= 4 ? (has_v ? fused_bucket_kernel<true, 4, 4> : fused_bucket_kernel<false, 4, 4>)
-                       : (has_v ? fused_bucket_kernel<true, 2, MAX_PEERS> : fused_bucket_kernel<false, 2, MAX_PEERS>);
+    auto kern = from_stage
+                    ? (P <= 4 ? (has_v ? fused_bucket_kernel<true, 4, 4, true> : fused_bucket_kernel<false, 4, 4, true>)
+                              : (has_v ? fused_bucket_kernel<true, 2, MAX_PEERS, true>
+                                       : fused_bucket_kernel<false, 2, MAX_PEERS, true>))
+                    : (P <= 4 ? (has_v ? fused_bucket_kernel<true, 4, 4, false> : fused_bucket_kernel<false, 4, 4, false>)
+                              : (has_v ? fused_bucket_kernel<true, 2, MAX_PEERS, false>
+                                       : fused_bucket_kernel<false, 2, MAX_PEERS, false>));
     launch_pdl(kern, dim3(std::max(1, ctas)), dim3(512), 0, s, pp, P, rank, bucket, stepctr, a / 4, b / 4, invP, lr, mu,
                flag, win, B, n_data, loss_idx, (track_wmax && pp.wmax[0]) ? 1 + bucket * std::max(1, ctas) : 0, dbg_ts,
                share4);
