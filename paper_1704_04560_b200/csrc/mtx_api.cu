@@ -638,13 +638,14 @@ mtx_status quantize_params(mtx_ctx *c, int scr, cudaStream_t s, LaunchHook *h, i
 // MTX_REDUCE_FUSED at P > 1, ablation knob MTX_FUSED_OVERLAP=1: the fused reduction runs per bucket on the
 // comm stream while the backward continues, on MTX_COMM_SMS SMs (default 16) that the backward's GEMMs are
 // planned to leave free (a persistent GEMM CTA fills its SM; without a reserve the reduction would queue
-// behind it), the backward then being one chain on the caller's stream.  Default from P = 4 (MTX_FUSED_OVERLAP=0/1
-// forces it): measured at cfg4 P = 4 263 vs 270 us/step with 16 reserved SMs (at b = 2048 the 1024-wide GEMMs are one
-// tile per CTA pair and leave SMs idle anyway); slower at P = 2 (351 vs 331 us: there the reserve costs the GEMMs
-// more than the ~30 us of reduction it hides) -- DESIGN.md §6.
+// behind it), the backward then being one chain on the caller's stream.  Off by default (MTX_FUSED_OVERLAP=1): it
+// won at cfg4 P = 4 against the round-2c GEMMs of the day (263 vs 270 us/step with 16 reserved SMs), but with the
+// epilogue-mode GEMM kernels one launch after the backward is faster again (251.5 vs 253.4 us; cfg2 P = 4 88 vs
+// 104 us; P = 2 331 vs 351) -- DESIGN.md §6.
 bool fused_overlap(const mtx_ctx *c) {
-    static const int v = getenv("MTX_FUSED_OVERLAP") ? atoi(getenv("MTX_FUSED_OVERLAP")) : -1;
-    return v >= 0 ? v != 0 : c->world >= 4;
+    static const int v = getenv("MTX_FUSED_OVERLAP") ? atoi(getenv("MTX_FUSED_OVERLAP")) : 0;
+    (void)c;
+    return v != 0;
 }
 // MTX_REDUCE_FUSED at P > 1, push protocol (MTX_FUSED_PUSH=1; default off): as each gradient bucket completes in the
 // backward, the copy engines write its slice of every owner's share into that owner's landing area (cudaMemcpyAsync to
@@ -1102,9 +1103,9 @@ struct Runner {
             // The averaging operator fused with its collective.  The kernel publishes "gradients ready" to
             // every peer, waits for theirs, folds + updates this rank's share of its range and stores w into
             // every replica; a barrier after the last one makes every replica's w complete before the next
-            // step reads it.  P <= 3: one launch over the whole buffer after the backward, on all SMs.
-            // fused_overlap() (P >= 4): per bucket on the comm stream, overlapping the rest of the backward on SMs
-            // the backward GEMMs leave free.
+            // step reads it.  Default: one launch over the whole buffer after the backward, on all SMs.
+            // fused_overlap() (MTX_FUSED_OVERLAP=1): per bucket on the comm stream, overlapping the rest of the
+            // backward on SMs the backward GEMMs leave free.
             const bool ov = fused_overlap(c);
             const bool push = !ov && fused_push() && c->stage;
             if (push) {
