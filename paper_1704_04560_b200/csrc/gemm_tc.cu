@@ -1335,8 +1335,12 @@ template <bool SPLIT, bool F16>
 static cudaError_t launch_variant(TcGemm *t, const TcParams &p, int grid, cudaStream_t s, int BN, bool pair, bool mask,
                                   bool fast) {
     if constexpr (F16) {
-        if (pair && BN == 256)
+        if (pair && BN == 256) {
+            if (fast)
+                return mask ? launch<256, SPLIT, true, true, F16, true>(t, p, grid, s)
+                            : launch<256, SPLIT, true, false, F16, true>(t, p, grid, s);
             return mask ? launch<256, SPLIT, true, true, F16>(t, p, grid, s) : launch<256, SPLIT, true, false, F16>(t, p, grid, s);
+        }
         if (fast && pair && BN == 128)  // every tile on the whole-tile fast epilogue
             return mask ? launch<128, SPLIT, true, true, F16, true>(t, p, grid, s)
                         : launch<128, SPLIT, true, false, F16, true>(t, p, grid, s);
@@ -1404,8 +1408,9 @@ static cudaError_t tc_gemm_impl(TcGemm *t, const GemmDesc &g, cudaStream_t s, La
     // Development knob MTX_TC_BN256=1: correct, measured slower (cfg4 forward 47.5 -> 51.4 us, dgrad 44.8 -> 46.8: 1.73
     // rounds of 256-wide tiles run as 2, and each tile's store phase doubles behind a 2-deep TMEM ring)
     static const int bn256_env = getenv("MTX_TC_BN256") ? atoi(getenv("MTX_TC_BN256")) : 0;
-    if (f16 && pair && !pair_cluster && pair_splits == 1 && BN == 128 && N % 256 == 0 && bn256_env == 1 &&
-        (int64_t)((M + 2 * BM - 1) / (2 * BM)) * (N / 256) * 2 >= sms)
+    // MTX_TC_BN256=2: whenever the shape allows (development: with the FAST 256-wide kernel)
+    if (f16 && pair && !pair_cluster && pair_splits == 1 && BN == 128 && N % 256 == 0 &&
+        ((bn256_env == 1 && (int64_t)((M + 2 * BM - 1) / (2 * BM)) * (N / 256) * 2 >= sms) || bn256_env == 2))
         BN = 256;
     TcParams p{};
     p.M = M; p.N = N; p.K = K;
