@@ -208,7 +208,18 @@ def roofline(timing: dict, pk: dict, sm_mhz: float | None, steps: int, config: s
     bn = re.search(r"bn=(\d+)", longest)
     bn = bn.group(1) if bn else "128"
     pr = re.search(r"pair=(\d)", longest)
-    tpl = f"{bn}, {{}}, {pr.group(1) if pr else 0}, {1 if '_dgrad' in longest else 0}, {{}}"  # <BN, 3x, PAIR, MASK, F16>
+    pair = int(pr.group(1)) if pr else 0
+    la = dict(kv.split("=") for kv in re.match(r"\w+\[(.*)\]", longest).group(1).split(",")) if "[" in longest else {}
+    sp, cl = int(la.get("splits", 1)), int(la.get("cluster", 0))
+    f16 = top_name.startswith("gemm_tc3xf16")
+    # epilogue mode of the kernel the launch ran (gemm_tc.cu launch_variant): CLU = split-K cluster, PART = split-K
+    # partials (unpaired), FAST = 3xF16 pair with every tile whole (M % 256, N % 128; lean or fp32-only output)
+    clu = 1 if cl and (not pair or f16) else 0
+    part = 1 if sp > 1 and not cl and not pair else 0
+    fast = 1 if f16 and pair and sp == 1 and not cl and int(la.get("M", 1)) % 256 == 0 and int(la.get("N", 1)) % 128 == 0 \
+        else 0
+    # <BN, 3x, PAIR, MASK, F16, FAST, CLU, PART>
+    tpl = f"{bn}, {{}}, {pair}, {1 if '_dgrad' in longest else 0}, {{}}, {fast}, {clu}, {part}"
     ncu_kernel = {"gemm_tc3xf16": f"tc_gemm_kernel<{tpl.format(1, 1)}>", "gemm_tc3x": f"tc_gemm_kernel<{tpl.format(1, 0)}>",
                   "gemm_tc": f"tc_gemm_kernel<{tpl.format(0, 0)}>",
                   "avg_update": "avg_update_kernel<1>", "fused_avg_update": "fused_avg_update_kernel", "head_softmax_xent": "head_kernel",

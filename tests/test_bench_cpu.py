@@ -74,6 +74,11 @@ def test_roofline_takes_the_dominant_launch_not_the_class():
     assert r["launch"] == big and r["kernel"] == "gemm_tc3xf16_wgrad" and r["bound"] == "tensor"
     assert abs(r["achieved"] - 2 * 1024 * 1024 * 8192 / (3.0e-3 / 60) / 1e12) < 1e-3
     assert abs(r["peak"] - 1650.0 / 3) < 0.1  # three f16 MMAs per product against the f16 (= bf16) dense peak
+    # traffic from the committed ncu capture of the kernel instance this launch ran: the split-K cluster (CLU) pair
+    # kernel <BN, 3x, PAIR, MASK, F16, FAST, CLU, PART>
+    tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    if "cfg4:tc_gemm_kernel<128, 1, 1, 0, 1, 0, 1, 0>" in tj:
+        assert r["traffic"] == tj["cfg4:tc_gemm_kernel<128, 1, 1, 0, 1, 0, 1, 0>"], r["traffic_source"]
 
 
 def test_reference_arm_prints_one_json_line():
